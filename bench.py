@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark driver (contract: one JSON line from rank 0).
+
+Default workload: BASELINE config 5 -- the 3-D CliffordBasicBlock
+(conv3^3 -> MultiVectorAct(Mean) -> conv3^3 + residual), g=(1,1,1),
+B=256 samples sharded over the ranks, C=64, 32^3 volume, fp32-accurate mode.
+A "step" is one forward of the block over the whole (sharded) batch with
+inputs resident in HBM; `value` is samples/s of the whole job.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 5] [--precision fp32|3xtf32|tf32|bf16]
+
+Under torchrun (N > 1) every rank takes a contiguous slice of the batch;
+NCCL is used only to broadcast the compact weights from rank 0 and to reduce
+the per-rank times (max) -- the data path has no collective.
+
+--impl reference times the reference algorithm on the host CPU (the oracle
+port, oracle/oracle.py, multi-threaded BLAS) on a bounded sample of the same
+workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Clifford conv TFLOP/s & % roofline; block samples/s at 1/2/4/8 B200"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def mode_peak(precision, peaks, sustained=True):
+    """Effective dense tensor peak (TFLOP/s of algorithmic work) of a mode,
+    derived from the measured bf16 GEMM peak: tf32 = bf16/2; 3xTF32 = tf32/3;
+    fp32 (int8 slices, 6 MMAs per product) = (2*bf16)/6."""
+    bf16 = peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"]
+    return {"bf16": bf16, "tf32": bf16 / 2, "3xtf32": bf16 / 6, "fp32": 2 * bf16 / 6}[precision]
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def bcast(t, world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.broadcast(t, src=0)
+    return t
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    import torch
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_block_sample(spec, precision_unused=None, n_samples=1):
+    """Time the oracle port (reference algorithm, fp64 BLAS) on n samples of a block config."""
+    import oracle as O
+    from paper_2507_01040_b200 import workloads as W
+    f1, b1 = W.conv_params(spec, 1)
+    f2, b2 = W.conv_params(spec, 2)
+    aw, ab = W.act_params(spec)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((n_samples, spec.C, spec.P, spec.nb)).astype(np.float32)
+    t0 = time.perf_counter()
+    O.block_ref(x, spec.g, spec.d, f1, b1, spec.mode, tuple(range(spec.nb)), aw, ab, f2, b2,
+                padding=spec.padding, residual=True)
+    return time.perf_counter() - t0
+
+
+def cpu_conv_sample(spec, n_samples=1):
+    import oracle as O
+    from paper_2507_01040_b200 import workloads as W
+    f, b = W.conv_params(spec, 1)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((n_samples, spec.C, spec.P, spec.nb)).astype(np.float32)
+    pad = 1 if spec.padding == "same" else 0
+    t0 = time.perf_counter()
+    O.conv_ref(x, f, b, spec.g, spec.d, spec.d_filter, pad)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on host cores (rank 0 only)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2507_01040_b200 import workloads as W
+    spec = W.CONFIGS[args.config]
+    cores = os.cpu_count()
+    for _ in range(args.warmup):
+        (cpu_block_sample if spec.kind == "block" else cpu_conv_sample)(spec, n_samples=1) if args.warmup_cpu else None
+    times = []
+    for _ in range(args.steps):
+        times.append((cpu_block_sample if spec.kind == "block" else cpu_conv_sample)(spec, n_samples=1))
+    t = float(np.mean(times))
+    value = 1.0 / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (oracle)",
+        "data": "synthetic (seeded, BASELINE.json distributions)",
+        "config": {"workload": spec.name, "global_batch": spec.B, "sample_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port",
+                         "sample": f"1 sample of {spec.name} per step, oracle/oracle.py (numpy fp64, multithreaded BLAS)"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import paper_2507_01040_b200 as M
+    from paper_2507_01040_b200 import _lib, workloads as W
+
+    world, rank, local = dist_setup(args)
+    spec = W.CONFIGS[args.config]
+    prec = args.precision
+    peaks, peak_kind = load_peaks()
+    lib = _lib.load()
+    lo, hi = W.shard(spec.B, rank, world)
+    nloc = hi - lo
+    dev = torch.device("cuda", local)
+    sig = M.Signature(spec.g)
+
+    # ---- parameters: generated on rank 0, broadcast over NCCL (compact form) ----
+    def param(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(dev) if a is not None else None
+        return bcast(t, world) if t is not None else None
+
+    if spec.kind == "block":
+        f1, b1 = W.conv_params(spec, 1)
+        f2, b2 = W.conv_params(spec, 2)
+        aw, ab = W.act_params(spec)
+        f1, b1, f2, b2 = (param(a) for a in (f1, b1, f2, b2))
+        aw, ab = param(aw), param(ab)
+        blk = M.make_basic_block(sig, nloc, spec.C, spec.C, spec.C, spec.d, f1, b1, spec.mode, f2, b2,
+                                 act_weight=aw, act_bias=ab, padding=spec.padding, residual=True,
+                                 precision=prec)
+        blk.handle()
+        run = lambda xx: M.block_forward(xx, blk)  # noqa: E731
+        flops_per_sample = blk.flops() / nloc
+        conv_layer = blk.conv2
+    elif spec.kind == "conv":
+        f, b = W.conv_params(spec, 1)
+        f, b = param(f), param(b)
+        layer = M.make_conv_layer(M.Dims(nloc, spec.C, spec.C, spec.d, spec.d_filter, spec.k), sig, f, b,
+                                  precision=prec, padding=spec.padding)
+        layer.handle()
+        run = lambda xx: M.conv_forward(xx, layer)  # noqa: E731
+        flops_per_sample = M.conv_flops(layer.dims, layer) / nloc
+        conv_layer = layer
+    else:
+        raise SystemExit("activation config: use --config 1..5 with kind conv/block")
+
+    x = W.make_input(spec, lo, nloc, device=dev)
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        y = run(x)
+    torch.cuda.synchronize()
+    barrier(world)
+
+    launches0 = lib.cl_launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier(world)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            y = run(x)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier(world)
+    launches = lib.cl_launch_count() - launches0
+    t_step = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    t_step = max_over_ranks(t_step, world)
+    value = spec.B / t_step  # whole-job samples/s
+
+    # ---- dominant kernel: the conv launch, timed alone with CUDA events ----
+    xc = x if spec.kind == "conv" else torch.empty(conv_layer.dims.input_shape(), device=dev).normal_()
+    for _ in range(2):
+        M.conv_forward(xc, conv_layer)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    nrep = max(2, args.steps)
+    e0.record()
+    for _ in range(nrep):
+        M.conv_forward(xc, conv_layer)
+    e1.record()
+    torch.cuda.synchronize()
+    t_conv = e0.elapsed_time(e1) / 1e3 / nrep
+    conv_flops = M.conv_flops(conv_layer.dims, conv_layer)
+    achieved = conv_flops / t_conv / 1e12
+    peak = mode_peak(prec, peaks, sustained=True)
+    conv_share = (t_conv * (2 if spec.kind == "block" else 1)) / (t_step)
+
+    # ---- end to end through the public API with pinned HOST buffers ----
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        run(xh)  # warm (allocates the pinned output of the host path)
+        barrier(world)
+        t0 = time.perf_counter()
+        ne = max(1, args.e2e_steps)
+        for _ in range(ne):
+            yh = run(xh)
+            s = float(yh.view(-1)[0])  # host read of the result
+        t_e2e = (time.perf_counter() - t0) / ne
+        t_e2e = max_over_ranks(t_e2e, world)
+        e2e = {"value": spec.B / t_e2e, "unit": "samples/s",
+               "h2d_bytes_per_step": int(x.numel() * 4) * world,
+               "d2h_bytes_per_step": int(y.numel() * 4) * world,
+               "path": "block_forward(pinned host tensor) -> cl_block_forward_host (chunked H2D/compute/D2H over 2 streams)"}
+        del xh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        t_cpu = (cpu_block_sample if spec.kind == "block" else cpu_conv_sample)(spec, n_samples=1)
+        cpu = {"value": 1.0 / t_cpu, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"1 sample of {spec.name}, oracle/oracle.py (numpy fp64 einsum/BLAS)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": {"fp32": "f32 (int8-slice exact accumulation)", "3xtf32": "f32 (3xTF32)",
+                      "tf32": "tf32", "bf16": "bf16"}[prec],
+            "data": "synthetic (seeded, BASELINE.json distributions; inputs generated on device)",
+            "config": {"workload": spec.name, "global_batch": spec.B, "per_rank_batch": nloc,
+                       "precision": prec, "padding": spec.padding,
+                       "parallelism": f"batch-sharded x{world}, NCCL broadcast of weights only",
+                       "l2": "inputs larger than L2 (%.1f GB per rank)" % (x.numel() * 4 / 1e9)},
+            "tflops": flops_per_sample * spec.B / t_step / 1e12,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "conv_tc_kernel (conv2 of the block)",
+                         "peak_basis": f"{prec} effective peak derived from {peak_kind} bf16_tflops_sustained",
+                         "kernel_share_of_step": conv_share},
+            "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--precision", default="3xtf32", choices=["fp32", "3xtf32", "tf32", "bf16"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--warmup-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

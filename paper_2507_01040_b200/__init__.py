@@ -1,0 +1,15 @@
+"""B200-native (sm_100a) Clifford convolution / multivector activation /
+basic-block inference: a drop-in for the layer API of the reference
+`mvkernels` package (arXiv 2507.01040), backed by libclifford_b200.so
+(C-ABI: include/clifford_b200.h)."""
+
+from .activation import (ActivationConfig, AggMode, activation_flops, activation_forward,
+                         make_activation_config)
+from .algebra import (Signature, all_valid_signatures, blade_product, product_table,
+                      schedule_flop_count, schedule_terms, validate_signature)
+from .block import BasicBlock, block_forward, make_basic_block
+from .conv import ConvLayer, build_expanded_kernel, conv_flops, conv_forward, make_conv_layer
+from .layout import Dims, LayoutTag, read_tensor, write_tensor
+from . import errors
+
+__version__ = "0.1.0"

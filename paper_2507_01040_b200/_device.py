@@ -1,0 +1,74 @@
+"""Device-memory plumbing (PyTorch is used for allocation and streams only)."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+
+class Handle:
+    """Owns one C-ABI handle; destroyed with the Python object."""
+
+    def __init__(self, ptr: int, destroy):
+        self.ptr = ptr
+        self._destroy = destroy
+
+    def __del__(self):
+        if self.ptr and self._destroy is not None:
+            try:
+                self._destroy(C.c_void_p(self.ptr))
+            except Exception:
+                pass
+            self.ptr = 0
+
+
+def torch_mod():
+    import torch
+    return torch
+
+
+def is_cuda_tensor(x) -> bool:
+    try:
+        import torch
+    except ImportError:
+        return False
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def is_cpu_tensor(x) -> bool:
+    try:
+        import torch
+    except ImportError:
+        return False
+    return isinstance(x, torch.Tensor) and not x.is_cuda
+
+
+def current_device() -> int:
+    torch = _lib.require_cuda()
+    return torch.cuda.current_device()
+
+
+def stream_ptr(device=None) -> int:
+    torch = torch_mod()
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def to_device_f32(arr, device=None):
+    """Contiguous fp32 CUDA copy of a numpy array / tensor."""
+    torch = _lib.require_cuda()
+    if isinstance(arr, torch.Tensor):
+        return arr.detach().to(device=device or torch.cuda.current_device(), dtype=torch.float32).contiguous().clone()
+    a = np.ascontiguousarray(arr, dtype=np.float32)
+    return torch.from_numpy(a.copy()).to(device=device or torch.cuda.current_device())
+
+
+def frozen_f32(arr) -> np.ndarray:
+    """Private frozen fp32 copy (conv.py:70-74)."""
+    if is_cuda_tensor(arr) or is_cpu_tensor(arr):
+        arr = arr.detach().cpu().numpy()
+    out = np.array(arr, dtype=np.float32, order="C", copy=True)
+    out.flags.writeable = False
+    return out

@@ -1,0 +1,88 @@
+"""Signatures and blade products (host side of the reference algebra module,
+algebra.py:26-63, :87-99, :116-145). Blade products come from the C-ABI
+(`cl_blade_product`), i.e. the same integer code that builds the device
+kernels; the Python side only validates and shapes the results."""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from functools import lru_cache
+from typing import Iterable
+
+import numpy as np
+
+from . import _lib
+from .errors import InvalidMetricValue, InvalidSignature
+
+
+@dataclass(frozen=True)
+class Signature:
+    """Metric signature g of Cl_g(R^k), g_i in {-1, 0, +1} (algebra.py:26-46)."""
+
+    g: tuple[int, ...]
+
+    @property
+    def k(self) -> int:
+        return len(self.g)
+
+    @property
+    def n_blades(self) -> int:
+        return 1 << len(self.g)
+
+    def __str__(self) -> str:
+        return "(" + ",".join(f"{v:+d}" for v in self.g) + ")"
+
+
+def validate_signature(values: Iterable[float]) -> Signature:
+    """algebra.py:49-63: InvalidMetricValue outside {-1,0,+1}, InvalidSignature if all zero."""
+    g = []
+    for v in values:
+        if v not in (-1, 0, 1):
+            raise InvalidMetricValue(f"metric value {v!r} not in {{-1, 0, +1}}")
+        g.append(int(v))
+    if not any(g):
+        raise InvalidSignature(f"signature {tuple(g)} has no non-zero element")
+    return Signature(tuple(g))
+
+
+def blade_product(i_mask: int, j_mask: int, sig: Signature) -> tuple[int, int]:
+    """(target, coeff) of e_I e_J via the C-ABI (algebra.py:87-99)."""
+    lib = _lib.load()
+    t = _lib.C.c_int()
+    c = _lib.C.c_int()
+    _lib.check(lib.cl_blade_product(int(i_mask), int(j_mask), _lib.int32_array(sig.g), sig.k,
+                                    _lib.C.byref(t), _lib.C.byref(c)))
+    return t.value, c.value
+
+
+@lru_cache(maxsize=None)
+def product_table(sig: Signature) -> tuple[np.ndarray, np.ndarray]:
+    """(target, coeff) int64 tables (algebra.py:116-129)."""
+    nb = sig.n_blades
+    tgt = np.empty((nb, nb), np.int64)
+    cof = np.empty((nb, nb), np.int64)
+    for i in range(nb):
+        for j in range(nb):
+            tgt[i, j], cof[i, j] = blade_product(i, j, sig)
+    tgt.flags.writeable = False
+    cof.flags.writeable = False
+    return tgt, cof
+
+
+def schedule_terms(sig: Signature) -> int:
+    """Number of non-zero FMA terms of the signature schedule (specialize.py:49-63)."""
+    n = _lib.load().cl_schedule_terms(_lib.int32_array(sig.g), sig.k)
+    if n < 0:
+        _lib.check(-n)
+    return int(n)
+
+
+def schedule_flop_count(sig: Signature) -> int:
+    """FLOPs of one geometric product (specialize.py:72-74)."""
+    return 2 * schedule_terms(sig)
+
+
+def all_valid_signatures(k_max: int = 3) -> list[Signature]:
+    from itertools import product as iproduct
+    return [Signature(g) for k in range(1, k_max + 1)
+            for g in iproduct((-1, 0, 1), repeat=k) if any(g)]

@@ -1,0 +1,158 @@
+"""Clifford convolution layer on the B200 tensor-core path.
+
+Drop-in for the reference layer API (conv.py:77-140, :371-387): the same
+`make_conv_layer(dims, sig, filters, bias, W=None, U=1)` constructor, the same
+protocol layouts, `conv_forward(x, layer, variant)` and `conv_flops`. The
+forward runs libclifford_b200.so's implicit-GEMM tcgen05 kernel; there is no
+CPU path. Extensions (keyword-only): `precision` in {"fp32" (3xTF32),
+"tf32", "bf16"} and `padding` in {"valid", "same"}.
+
+Inputs: a CUDA torch tensor runs the device path and returns a CUDA tensor;
+a numpy array (or CPU tensor) runs the host path of the C-ABI, which copies
+in and out inside the call, and returns the same kind.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device, _lib
+from .algebra import Signature, schedule_flop_count
+from .errors import ShapeMismatch
+from .layout import Dims
+
+PRECISIONS = {"fp32": 0, "3xtf32": 0, "tf32": 1, "bf16": 2}
+PADDINGS = {"valid": 0, "same": 1}
+# The reference variant names are accepted so existing callers keep working;
+# all of them run the B200 kernel (there is no CPU implementation here).
+VARIANTS = ("b200", "reference", "kernelized", "packed", "specialized")
+
+
+@dataclass(frozen=True, eq=False)
+class ConvLayer:
+    dims: Dims
+    sig: Signature
+    filters: np.ndarray  # (N_B, C_in, C_out, d_filter^k) float32, frozen
+    bias: np.ndarray     # (N_B, C_out) float32, frozen
+    precision: str = "fp32"
+    padding: str = "valid"
+    W: int = 1
+    U: int = 1
+    _handles: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def pad(self) -> int:
+        return (self.dims.d_filter - 1) // 2 if self.padding == "same" else 0
+
+    @property
+    def d_out(self) -> int:
+        return self.dims.d_image + 2 * self.pad - self.dims.d_filter + 1
+
+    def output_shape(self, B=None):
+        B = self.dims.B if B is None else B
+        return (B, self.dims.C_out, self.d_out ** self.dims.k, self.dims.n_blades)
+
+    def handle(self) -> int:
+        """The device handle on the current CUDA device (built once, cached)."""
+        dev = _device.current_device()
+        h = self._handles.get(dev)
+        if h is None:
+            lib = _lib.load()
+            f = _device.to_device_f32(self.filters)
+            b = _device.to_device_f32(self.bias)
+            out = C.c_void_p()
+            _lib.check(lib.cl_conv_create(
+                _lib.int32_array(self.sig.g), self.sig.k, self.dims.C_in, self.dims.C_out,
+                self.dims.d_image, self.dims.d_filter, PADDINGS[self.padding],
+                PRECISIONS[self.precision], C.c_void_p(f.data_ptr()), C.c_void_p(b.data_ptr()),
+                C.c_void_p(_device.stream_ptr()), C.byref(out)))
+            h = _device.Handle(out.value, lib.cl_conv_destroy)
+            self._handles[dev] = h
+        return h.ptr
+
+
+def make_conv_layer(dims: Dims, sig: Signature, filters, bias, W: int | None = None, U: int = 1,
+                    *, precision: str = "fp32", padding: str = "valid") -> ConvLayer:
+    """Validate and freeze a layer (conv.py:101-140 checks, same exceptions)."""
+    if sig.k != dims.k:
+        raise ShapeMismatch(f"signature k={sig.k} does not match dims k={dims.k}")
+    if not 1 <= dims.k <= 3:
+        raise ShapeMismatch(f"convolution supports k in {{1,2,3}}, got k={dims.k}")
+    f = filters.detach().cpu().numpy() if _device.is_cuda_tensor(filters) or _device.is_cpu_tensor(filters) else np.asarray(filters)
+    b = bias.detach().cpu().numpy() if _device.is_cuda_tensor(bias) or _device.is_cpu_tensor(bias) else np.asarray(bias)
+    if f.shape != dims.filters_shape():
+        raise ShapeMismatch(f"filters shape {f.shape}, expected {dims.filters_shape()}")
+    if b.shape != dims.bias_shape():
+        raise ShapeMismatch(f"bias shape {b.shape}, expected {dims.bias_shape()}")
+    W = 1 if W is None else W
+    if W < 1 or U < 1:
+        raise ShapeMismatch(f"W and U must be >= 1, got W={W} U={U}")
+    if precision not in PRECISIONS:
+        raise ValueError(f"unknown precision {precision!r}")
+    if padding not in PADDINGS:
+        raise ValueError(f"unknown padding {padding!r}")
+    if padding == "same" and dims.d_filter % 2 == 0:
+        raise ShapeMismatch("same padding needs an odd d_filter")
+    return ConvLayer(dims, sig, _device.frozen_f32(f), _device.frozen_f32(b), precision, padding, W, U)
+
+
+def _check_input(x, layer: ConvLayer):
+    shape = tuple(x.shape)
+    if shape != layer.dims.input_shape():
+        raise ShapeMismatch(f"input shape {shape}, expected {layer.dims.input_shape()}")
+
+
+def conv_forward(x, layer: ConvLayer, variant: str = "b200"):
+    """Protocol-to-protocol forward pass (conv.py:371-381) on the B200."""
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown conv variant {variant!r}")
+    _check_input(x, layer)
+    lib = _lib.load()
+    B = layer.dims.B
+    if _device.is_cuda_tensor(x):
+        torch = _device.torch_mod()
+        with torch.cuda.device(x.device):
+            xc = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
+            y = torch.empty(layer.output_shape(B), device=x.device, dtype=torch.float32)
+            _lib.check(lib.cl_conv_forward(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
+                                           C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
+        return y
+    if _device.is_cpu_tensor(x):
+        torch = _device.torch_mod()
+        xc = x.float().contiguous()
+        y = torch.empty(layer.output_shape(B), dtype=torch.float32, pin_memory=xc.is_pinned())
+        _lib.check(lib.cl_conv_forward_host(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
+                                            C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
+        return y
+    xa = np.ascontiguousarray(x, dtype=np.float32)
+    y = np.empty(layer.output_shape(B), dtype=np.float32)
+    _lib.check(lib.cl_conv_forward_host(C.c_void_p(layer.handle()), C.c_void_p(xa.ctypes.data),
+                                        C.c_void_p(y.ctypes.data), B, C.c_void_p(_device.stream_ptr())))
+    return y
+
+
+def build_expanded_kernel(layer: ConvLayer):
+    """(C_out*N_B, C_in*N_B, Q) real filter built on the device (conv.py:188-202)."""
+    torch = _lib.require_cuda()
+    d = layer.dims
+    nb = d.n_blades
+    f = _device.to_device_f32(layer.filters)
+    out = torch.empty((d.C_out * nb, d.C_in * nb, d.filter_positions), device=f.device, dtype=torch.float32)
+    _lib.check(_lib.load().cl_expand_kernel(
+        _lib.int32_array(layer.sig.g), layer.sig.k, C.c_void_p(f.data_ptr()), d.C_in, d.C_out,
+        d.filter_positions, C.c_void_p(out.data_ptr()), C.c_void_p(_device.stream_ptr())))
+    return out
+
+
+def conv_flops(dims: Dims, sig_or_layer, padding: str = "valid") -> int:
+    """B * C_out * d_out^k * (C_in * Q * 2*terms + N_B) (conv.py:384-387)."""
+    sig = sig_or_layer.sig if isinstance(sig_or_layer, ConvLayer) else getattr(sig_or_layer, "sig", sig_or_layer)
+    if isinstance(sig_or_layer, ConvLayer):
+        padding = sig_or_layer.padding
+    pad = (dims.d_filter - 1) // 2 if padding == "same" else 0
+    d_out = dims.d_image + 2 * pad - dims.d_filter + 1
+    per_position = dims.C_in * dims.filter_positions * schedule_flop_count(sig)
+    return dims.B * dims.C_out * d_out ** dims.k * (per_position + dims.n_blades)

@@ -1,0 +1,718 @@
+// capi.cu -- the C-ABI of include/clifford_b200.h: handle construction and
+// validation (mirroring make_conv_layer / make_activation_config error
+// behaviour), per-call TMA tensor maps, block orchestration and the
+// chunked host-buffer runtime (copy/compute overlap over two streams).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/clifford_b200.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace cl {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
+static int fail(int code, const char* type, const std::string& msg) {
+  g_last_error = std::string(type) + ": " + msg;
+  return code;
+}
+static int cuda_fail(cudaError_t e, const char* where) {
+  return fail(CL_ERR_CUDA, "CudaError", std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CL_CUDA(expr, where)                 \
+  do {                                       \
+    cudaError_t _e = (expr);                 \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+static void setup_pool() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+static int check_sig(const int32_t* g, int k) {
+  if (k < 1 || k > 3 || g == nullptr)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "supports k in {1,2,3}, got k=" + std::to_string(k));
+  bool any = false;
+  for (int i = 0; i < k; ++i) {
+    if (g[i] < -1 || g[i] > 1)
+      return fail(CL_ERR_INVALID_METRIC_VALUE, "InvalidMetricValue",
+                  "metric value " + std::to_string(g[i]) + " not in {-1, 0, +1}");
+    any = any || g[i] != 0;
+  }
+  if (!any) return fail(CL_ERR_INVALID_SIGNATURE, "InvalidSignature", "signature has no non-zero element");
+  return CL_OK;
+}
+
+static int ipow(int b, int e) {
+  int r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+static int pow2_at_least(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// planning
+// ---------------------------------------------------------------------------
+static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, int d_filter,
+                      ConvPlan& pl) {
+  pl = ConvPlan{};
+  pl.k = k;
+  pl.nb = nb;
+  pl.prec = prec;
+  pl.esize = prec == kPrecBf16 ? 2 : 4;
+  pl.rb = prec == kPrecBf16 ? 16 : nb * 4;
+  pl.epg = pl.rb / pl.esize;
+  pl.merged_bc = (k == 3);
+  pl.d_filter = d_filter;
+  pl.Q = ipow(d_filter, k);
+  const bool pairs = (prec == kPrecBf16 && nb == 4);
+  const int G_real = pairs ? (C_in + 1) / 2 : C_in;
+  const int gpk = 32 / pl.rb;  // row-groups per 32-byte K step
+
+  // spatial tile (tx * ty * tz == 128)
+  int tx = std::min(128, std::max(8, pow2_at_least(d_out)));
+  int ty, tz;
+  if (k == 2) {
+    ty = 128 / tx;
+    tz = 1;
+  } else {
+    ty = std::min(128 / tx, pow2_at_least(d_out));
+    tz = 128 / (tx * ty);
+  }
+  pl.tx = tx;
+  pl.ty = ty;
+  pl.tz = tz;
+
+  pl.N = C_out * nb;
+  pl.n_ntiles = (pl.N + 255) / 256;
+  const int per = (pl.N + pl.n_ntiles - 1) / pl.n_ntiles;
+  pl.n_tile = ((per + 31) / 32) * 32;
+  pl.n_img = prec == kPrecFp32x3 ? 2 : 1;
+
+  const int G_pad_min = ((G_real + gpk - 1) / gpk) * gpk;
+  int best = -1;
+  ConvPlan bestp;
+  for (int ks : {8, 4, 2, 1}) {
+    const int gs = ks * gpk;
+    if (gs > G_pad_min) continue;
+    int G, n_gs;
+    if (pl.merged_bc) {
+      if (prec == kPrecBf16) {
+        G = ((G_real + gs - 1) / gs) * gs;  // pack pass zero-pads channels
+      } else {
+        if (G_real % gs) continue;
+        G = G_real;
+      }
+      n_gs = G / gs;
+    } else {
+      G = G_real;
+      n_gs = (G_real + gs - 1) / gs;  // TMA OOB zero-fills missing channels
+    }
+    ConvPlan c = pl;
+    c.ks = ks;
+    c.gs = gs;
+    c.G = G;
+    c.n_gs = n_gs;
+    c.cps = gs * c.epg / nb;
+    c.k_iters = pl.Q * n_gs;
+    c.a_bytes = (uint32_t)(kTileM * gs * pl.rb);
+    c.b_img_bytes = (uint32_t)(ks * pl.n_tile * 32);
+    c.b_bytes = c.b_img_bytes * pl.n_img;
+    c.stage_bytes = c.a_bytes * (prec == kPrecFp32x3 ? 2 : 1) + c.b_bytes;
+    c.stages = std::min(8, (int)((kMaxSmem - 2048) / c.stage_bytes));
+    if (c.stages >= 4) { bestp = c; best = 4; break; }
+    if (c.stages >= 2 && best < c.stages) { bestp = c; best = c.stages; }
+  }
+  if (best < 0) return false;
+  pl = bestp;
+  pl.tmem_cols = (uint32_t)std::max(32, pow2_at_least(2 * pl.n_tile));
+  pl.smem_bytes = (size_t)pl.stages * pl.stage_bytes + 1024 + 256;
+  return true;
+}
+
+}  // namespace cl
+
+using namespace cl;
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+struct cl_conv {
+  int g[3];
+  int k, nb, C_in, C_out, d_image, d_filter, pad, d_out, prec;
+  float* filters = nullptr;  // (NB, C_in, C_out, Q) device copy
+  float* bias = nullptr;     // (NB, C_out)
+  uint8_t* img = nullptr;    // tensor-core operand images
+  ConvPlan plan;
+};
+
+struct cl_act {
+  int k, nb, mode, K, C;
+  int ki[8];
+  float* w = nullptr;  // (C, NB) blade-keyed weights (Linear) or 0/1 mask
+  float* b = nullptr;  // (C) bias (zeros unless Linear)
+};
+
+struct cl_block {
+  const cl_conv* c1;
+  const cl_act* act;
+  const cl_conv* c2;
+  int residual;
+  int res_crop;
+};
+
+extern "C" {
+
+const char* cl_last_error(void) { return g_last_error.c_str(); }
+uint64_t cl_launch_count(void) { return g_launches.load(); }
+const char* cl_version(void) { return "clifford_b200 0.1 sm_100a"; }
+
+int cl_validate_signature(const int32_t* g, int k) { return check_sig(g, k); }
+
+int cl_blade_product(int i, int j, const int32_t* g, int k, int* target, int* coeff) {
+  if (int st = check_sig(g, k)) return st;
+  const int nb = 1 << k;
+  if (i < 0 || j < 0 || i >= nb || j >= nb)
+    return fail(CL_ERR_INDEX_OUT_OF_RANGE, "IndexOutOfRange", "blade mask outside [0, N_B)");
+  int gi[3] = {0, 0, 0};
+  for (int a = 0; a < k; ++a) gi[a] = g[a];
+  *target = i ^ j;
+  *coeff = blade_coeff(i, j, gi, k);
+  return CL_OK;
+}
+
+int cl_schedule_terms(const int32_t* g, int k) {
+  if (int st = check_sig(g, k)) return -st;
+  int gi[3] = {0, 0, 0};
+  for (int a = 0; a < k; ++a) gi[a] = g[a];
+  const int nb = 1 << k;
+  int n = 0;
+  for (int t = 0; t < nb; ++t)
+    for (int a = 0; a < nb; ++a) n += blade_coeff(a, t ^ a, gi, k) != 0;
+  return n;
+}
+
+int cl_expand_kernel(const int32_t* g, int k, const float* filters_dev, int C_in, int C_out, int Q,
+                     float* out_dev, void* stream) {
+  if (int st = check_sig(g, k)) return st;
+  if (C_in < 1 || C_out < 1 || Q < 1)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "C_in, C_out and Q must be >= 1");
+  int gi[3] = {0, 0, 0};
+  for (int a = 0; a < k; ++a) gi[a] = g[a];
+  CL_CUDA(launch_expand_ref(gi, k, filters_dev, C_in, C_out, Q, out_dev, (cudaStream_t)stream),
+          "expand_kernel");
+  return CL_OK;
+}
+
+// ---- conv ------------------------------------------------------------------
+int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, int d_filter,
+                   int padding, int precision, const float* filters, const float* bias,
+                   void* stream, cl_conv** out) {
+  if (!out) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null output handle pointer");
+  *out = nullptr;
+  if (int st = check_sig(g, k)) return st;
+  if (C_in < 1 || C_out < 1 || d_image < 1 || d_filter < 1)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "C_in, C_out, d_image, d_filter must be >= 1");
+  if (padding != CL_PAD_VALID && padding != CL_PAD_SAME)
+    return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "padding must be 0 (valid) or 1 (same)");
+  if (precision < 0 || precision > 2)
+    return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "precision must be 0 (fp32), 1 (tf32) or 2 (bf16)");
+  const int pad = padding == CL_PAD_SAME ? (d_filter - 1) / 2 : 0;
+  if (padding == CL_PAD_SAME && (d_filter % 2) == 0)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "same padding needs an odd d_filter");
+  const int d_out = d_image + 2 * pad - d_filter + 1;
+  if (d_out < 1)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch",
+                "d_filter " + std::to_string(d_filter) + " exceeds d_image " + std::to_string(d_image));
+  if (k == 1)
+    return fail(CL_ERR_UNSUPPORTED, "Unsupported", "k=1 (1-D) convolution is not implemented on the B200 path yet");
+  if (!filters || !bias) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "filters and bias are required");
+  setup_pool();
+  cudaStream_t s = (cudaStream_t)stream;
+  cl_conv* h = new cl_conv();
+  for (int a = 0; a < 3; ++a) h->g[a] = a < k ? g[a] : 0;
+  h->k = k;
+  h->nb = 1 << k;
+  h->C_in = C_in;
+  h->C_out = C_out;
+  h->d_image = d_image;
+  h->d_filter = d_filter;
+  h->pad = pad;
+  h->d_out = d_out;
+  h->prec = precision;
+  if (!plan_conv(k, h->nb, precision, C_in, C_out, d_out, d_filter, h->plan)) {
+    delete h;
+    return fail(CL_ERR_UNSUPPORTED, "Unsupported", "no shared-memory plan fits this layer");
+  }
+  const size_t nf = (size_t)h->nb * C_in * C_out * h->plan.Q;
+  const size_t nbias = (size_t)h->nb * C_out;
+  const size_t nimg = (size_t)h->plan.n_ntiles * h->plan.k_iters * h->plan.b_bytes;
+  cudaError_t e;
+  if ((e = cudaMalloc(&h->filters, nf * 4)) != cudaSuccess || (e = cudaMalloc(&h->bias, nbias * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&h->img, nimg)) != cudaSuccess) {
+    cl_conv_destroy(h);
+    return cuda_fail(e, "cl_conv_create alloc");
+  }
+  if ((e = cudaMemcpyAsync(h->filters, filters, nf * 4, cudaMemcpyDefault, s)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(h->bias, bias, nbias * 4, cudaMemcpyDefault, s)) != cudaSuccess ||
+      (e = launch_expand_images(h->g, h->plan, h->filters, C_in, C_out, h->img, s)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(s)) != cudaSuccess) {
+    cl_conv_destroy(h);
+    return cuda_fail(e, "cl_conv_create");
+  }
+  *out = h;
+  return CL_OK;
+}
+
+int cl_conv_out_side(const cl_conv* h, int* d_out) {
+  if (!h || !d_out) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null handle");
+  *d_out = h->d_out;
+  return CL_OK;
+}
+
+void cl_conv_destroy(cl_conv* h) {
+  if (!h) return;
+  cudaFree(h->filters);
+  cudaFree(h->bias);
+  cudaFree(h->img);
+  delete h;
+}
+
+}  // extern "C"
+
+namespace cl {
+
+// Epilogue options of one conv launch.
+struct Epi {
+  const cl_act* act = nullptr;
+  const float* resid = nullptr;
+  int res_side = 0, res_crop = 0;
+  __nv_bfloat16* y_bf16 = nullptr;  // write bf16 A-ready output for a following bf16 conv
+  int ybf_groups = 0, ybf_pairs = 0;
+};
+
+static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUtensorMap* map) {
+  const ConvPlan& pl = h->plan;
+  auto enc = get_encode();
+  if (!enc) return fail(CL_ERR_CUDA, "CudaError", "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(xsrc) & 15) != 0)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "input must be 16-byte aligned");
+  const cuuint64_t D = (cuuint64_t)h->d_image;
+  cuuint64_t dims[5];
+  cuuint64_t strides[4];
+  cuuint32_t box[5];
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const cuuint64_t rowb = (cuuint64_t)pl.rb;
+  const bool bf = pl.prec == kPrecBf16;
+  dims[0] = (cuuint64_t)pl.epg;
+  dims[1] = D;
+  dims[2] = D;
+  box[0] = (cuuint32_t)pl.epg;
+  box[1] = (cuuint32_t)pl.tx;
+  box[2] = (cuuint32_t)pl.ty;
+  strides[0] = rowb;
+  strides[1] = rowb * D;
+  if (pl.merged_bc) {
+    dims[3] = D;
+    dims[4] = (cuuint64_t)B * (cuuint64_t)pl.G;
+    strides[2] = rowb * D * D;
+    strides[3] = rowb * D * D * D;
+    box[3] = (cuuint32_t)pl.tz;
+    box[4] = (cuuint32_t)pl.gs;
+  } else {
+    const cuuint64_t Gt = bf ? (cuuint64_t)pl.G : (cuuint64_t)h->C_in;
+    dims[3] = Gt;
+    dims[4] = (cuuint64_t)B;
+    strides[2] = rowb * D * D;
+    strides[3] = rowb * D * D * Gt;
+    box[3] = (cuuint32_t)pl.gs;
+    box[4] = 1;
+  }
+  CUresult r = enc(map, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
+                   const_cast<void*>(xsrc), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   pl.rb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CL_ERR_CUDA, "CudaError", "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return CL_OK;
+}
+
+// Run one conv on device buffers. `xbf` (optional) is an already packed bf16
+// A-ready input (bf16 layers); otherwise x is packed here when needed.
+static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, float* y, long long B,
+                    const Epi& epi, cudaStream_t s) {
+  const ConvPlan& pl = h->plan;
+  if (B == 0) return CL_OK;
+  const long long P_in = (long long)ipow(h->d_image, h->k);
+  __nv_bfloat16* packed = nullptr;
+  const void* src = x;
+  if (pl.prec == kPrecBf16) {
+    if (xbf) {
+      src = xbf;
+    } else {
+      const size_t bytes = (size_t)B * pl.G * P_in * 16;
+      CL_CUDA(cudaMallocAsync((void**)&packed, bytes, s), "conv bf16 pack alloc");
+      CL_CUDA(launch_pack_bf16(x, packed, h->nb, B, h->C_in, P_in, pl.G, h->nb == 4, s), "pack_bf16");
+      src = packed;
+    }
+  }
+  CUtensorMap map;
+  if (int st = encode_input_map(h, src, B, &map)) {
+    if (packed) cudaFreeAsync(packed, s);
+    return st;
+  }
+  ConvKParams p{};
+  p.B = (int)B;
+  p.k = h->k;
+  p.nb = h->nb;
+  p.d_in = h->d_image;
+  p.d_out = h->d_out;
+  p.pad = h->pad;
+  p.tx = pl.tx;
+  p.ty = pl.ty;
+  p.tz = pl.tz;
+  p.ntx = (h->d_out + pl.tx - 1) / pl.tx;
+  p.nty = (h->d_out + pl.ty - 1) / pl.ty;
+  p.ntz = h->k == 3 ? (h->d_out + pl.tz - 1) / pl.tz : 1;
+  p.n_ntiles = pl.n_ntiles;
+  p.n_tile = pl.n_tile;
+  p.N = pl.N;
+  p.C_out = h->C_out;
+  p.num_tiles = (long long)B * p.ntz * p.nty * p.ntx * p.n_ntiles;
+  p.d_filter = h->d_filter;
+  p.n_gs = pl.n_gs;
+  p.gs = pl.gs;
+  p.G = pl.G;
+  p.merged_bc = pl.merged_bc;
+  p.k_iters = pl.k_iters;
+  p.ks = pl.ks;
+  p.a_bytes = pl.a_bytes;
+  p.b_bytes = pl.b_bytes;
+  p.b_img_bytes = pl.b_img_bytes;
+  p.stage_bytes = pl.stage_bytes;
+  p.tmem_cols = pl.tmem_cols;
+  p.stages = pl.stages;
+  p.b_img = h->img;
+  p.bias = h->bias;
+  p.y = y;
+  p.y_bf16 = epi.y_bf16;
+  p.ybf_groups = epi.ybf_groups;
+  p.ybf_pairs = epi.ybf_pairs;
+  p.resid = epi.resid;
+  p.res_side = epi.res_side;
+  p.res_crop = epi.res_crop;
+  p.act_mode = epi.act ? epi.act->mode : -1;
+  p.act_w = epi.act ? epi.act->w : nullptr;
+  p.act_b = epi.act ? epi.act->b : nullptr;
+  p.act_K = epi.act ? (float)epi.act->K : 1.f;
+  const int grid = (int)std::min<long long>(p.num_tiles, (long long)num_sms());
+  cudaError_t e = launch_conv(pl, map, p, grid, s);
+  if (packed) cudaFreeAsync(packed, s);
+  if (e != cudaSuccess) return cuda_fail(e, "conv_tc launch");
+  return CL_OK;
+}
+
+// Generic host-buffer runner: the batch is streamed through the device in
+// chunks on two streams, so chunk i+1's H2D copy overlaps chunk i's compute
+// and chunk i-1's D2H copy (copy engines and SMs work concurrently).
+template <class F>
+static int host_chunked(long long B, size_t in_per, size_t out_per, long long chunk, const float* xh,
+                        float* yh, cudaStream_t user, F&& fwd) {
+  if (B == 0) return CL_OK;
+  if (chunk <= 0) {
+    const size_t target = (size_t)256 << 20;  // ~256 MB of input per chunk
+    chunk = std::max<long long>(1, (long long)(target / std::max<size_t>(in_per, 1)));
+    chunk = std::min<long long>(chunk, std::max<long long>(1, (B + 1) / 2));
+  }
+  chunk = std::min(chunk, B);
+  cudaStream_t st[2];
+  CL_CUDA(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking), "stream create");
+  CL_CUDA(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking), "stream create");
+  cudaEvent_t start;
+  CL_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming), "event");
+  CL_CUDA(cudaEventRecord(start, user), "event record");
+  float* dx[2] = {nullptr, nullptr};
+  float* dy[2] = {nullptr, nullptr};
+  int rc = CL_OK;
+  for (int i = 0; i < 2 && rc == CL_OK; ++i) {
+    cudaStreamWaitEvent(st[i], start, 0);
+    if (cudaMallocAsync((void**)&dx[i], in_per * chunk, st[i]) != cudaSuccess ||
+        cudaMallocAsync((void**)&dy[i], out_per * chunk, st[i]) != cudaSuccess)
+      rc = fail(CL_ERR_CUDA, "CudaError", "host path staging alloc failed");
+  }
+  int it = 0;
+  for (long long b0 = 0; b0 < B && rc == CL_OK; b0 += chunk, ++it) {
+    const long long nb = std::min(chunk, B - b0);
+    const int i = it & 1;
+    cudaError_t e = cudaMemcpyAsync(dx[i], reinterpret_cast<const char*>(xh) + (size_t)b0 * in_per,
+                                    (size_t)nb * in_per, cudaMemcpyHostToDevice, st[i]);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
+    rc = fwd(dx[i], dy[i], nb, st[i]);
+    if (rc != CL_OK) break;
+    e = cudaMemcpyAsync(reinterpret_cast<char*>(yh) + (size_t)b0 * out_per, dy[i], (size_t)nb * out_per,
+                        cudaMemcpyDeviceToHost, st[i]);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "D2H"); break; }
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (dx[i]) cudaFreeAsync(dx[i], st[i]);
+    if (dy[i]) cudaFreeAsync(dy[i], st[i]);
+  }
+  cudaError_t e0 = cudaStreamSynchronize(st[0]);
+  cudaError_t e1 = cudaStreamSynchronize(st[1]);
+  cudaStreamDestroy(st[0]);
+  cudaStreamDestroy(st[1]);
+  cudaEventDestroy(start);
+  if (rc == CL_OK && e0 != cudaSuccess) rc = cuda_fail(e0, "host path");
+  if (rc == CL_OK && e1 != cudaSuccess) rc = cuda_fail(e1, "host path");
+  return rc;
+}
+
+}  // namespace cl
+
+extern "C" {
+
+int cl_conv_forward(const cl_conv* h, const float* x, float* y, int64_t B, void* stream) {
+  if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null conv handle");
+  if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
+  return conv_run(h, x, nullptr, y, B, Epi{}, (cudaStream_t)stream);
+}
+
+int cl_conv_forward_host(const cl_conv* h, const float* xh, float* yh, int64_t B, void* stream) {
+  if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null conv handle");
+  const size_t in_per = (size_t)h->C_in * ipow(h->d_image, h->k) * h->nb * 4;
+  const size_t out_per = (size_t)h->C_out * ipow(h->d_out, h->k) * h->nb * 4;
+  return host_chunked(B, in_per, out_per, 0, xh, yh, (cudaStream_t)stream,
+                      [&](const float* dx, float* dy, long long nb, cudaStream_t s) {
+                        return conv_run(h, dx, nullptr, dy, nb, Epi{}, s);
+                      });
+}
+
+// ---- activation -------------------------------------------------------------
+int cl_act_create(const int32_t* g, int k, int mode, const int32_t* ki, int K, int C,
+                  const float* weight, const float* bias, void* stream, cl_act** out) {
+  if (!out) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null output handle pointer");
+  *out = nullptr;
+  if (int st = check_sig(g, k)) return st;
+  const int nb = 1 << k;
+  if (mode < 0 || mode > 2) return fail(CL_ERR_CONFIG_INVALID, "ValueError", "agg_mode must be 0, 1 or 2");
+  if (K < 1 || K > nb || !ki)
+    return fail(CL_ERR_INDEX_OUT_OF_RANGE, "IndexOutOfRange", "kernel indices outside [0, N_B)");
+  for (int a = 0; a < K; ++a) {
+    if (ki[a] < 0 || ki[a] >= nb)
+      return fail(CL_ERR_INDEX_OUT_OF_RANGE, "IndexOutOfRange", "kernel indices outside [0, N_B)");
+    for (int b2 = 0; b2 < a; ++b2)
+      if (ki[a] == ki[b2]) return fail(CL_ERR_INDEX_OUT_OF_RANGE, "IndexOutOfRange", "kernel indices contain duplicates");
+  }
+  if (mode == CL_AGG_LINEAR && (!weight || !bias))
+    return fail(CL_ERR_MODE_CONFIG_MISMATCH, "ModeConfigMismatch", "Linear mode requires weight and bias");
+  if (mode != CL_AGG_LINEAR && (weight || bias))
+    return fail(CL_ERR_MODE_CONFIG_MISMATCH, "ModeConfigMismatch",
+                std::string(mode == 1 ? "SUM" : "MEAN") + " mode forbids weight/bias");
+  if (C < 1) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "C must be >= 1");
+  if (k == 1) return fail(CL_ERR_UNSUPPORTED, "Unsupported", "k=1 activation is not implemented on the B200 path yet");
+  setup_pool();
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<float> wk((size_t)C * nb, 0.f), bk((size_t)C, 0.f);
+  if (mode == CL_AGG_LINEAR) {
+    std::vector<float> w((size_t)C * K);
+    CL_CUDA(cudaMemcpy(w.data(), weight, w.size() * 4, cudaMemcpyDefault), "act weight copy");
+    CL_CUDA(cudaMemcpy(bk.data(), bias, bk.size() * 4, cudaMemcpyDefault), "act bias copy");
+    for (int c = 0; c < C; ++c)
+      for (int a = 0; a < K; ++a) wk[(size_t)c * nb + ki[a]] = w[(size_t)c * K + a];
+  } else {
+    for (int c = 0; c < C; ++c)
+      for (int a = 0; a < K; ++a) wk[(size_t)c * nb + ki[a]] = 1.f;
+  }
+  cl_act* h = new cl_act();
+  h->k = k;
+  h->nb = nb;
+  h->mode = mode;
+  h->K = K;
+  h->C = C;
+  for (int a = 0; a < 8; ++a) h->ki[a] = a < K ? ki[a] : -1;
+  cudaError_t e;
+  if ((e = cudaMalloc(&h->w, wk.size() * 4)) != cudaSuccess || (e = cudaMalloc(&h->b, bk.size() * 4)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(h->w, wk.data(), wk.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(h->b, bk.data(), bk.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(s)) != cudaSuccess) {
+    cl_act_destroy(h);
+    return cuda_fail(e, "cl_act_create");
+  }
+  *out = h;
+  return CL_OK;
+}
+
+int cl_act_forward(const cl_act* h, const float* x, float* y, int64_t B, int64_t P, void* stream) {
+  if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null activation handle");
+  if (B < 0 || P < 1) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "B >= 0 and P >= 1 required");
+  if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) != 0)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "activation buffers must be 16-byte aligned");
+  ActParams p{};
+  p.x = x;
+  p.y = y;
+  p.n_mv = (long long)B * h->C * P;
+  p.P = P;
+  p.C = h->C;
+  p.mode = h->mode;
+  p.w = h->w;
+  p.b = h->b;
+  p.Kf = (float)h->K;
+  CL_CUDA(launch_act(h->nb, p, (cudaStream_t)stream), "activation launch");
+  return CL_OK;
+}
+
+int cl_act_forward_host(const cl_act* h, const float* xh, float* yh, int64_t B, int64_t P, void* stream) {
+  if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null activation handle");
+  const size_t per = (size_t)h->C * P * h->nb * 4;
+  return host_chunked(B, per, per, 0, xh, yh, (cudaStream_t)stream,
+                      [&](const float* dx, float* dy, long long nb, cudaStream_t s) {
+                        return cl_act_forward(h, dx, dy, nb, P, s);
+                      });
+}
+
+void cl_act_destroy(cl_act* h) {
+  if (!h) return;
+  cudaFree(h->w);
+  cudaFree(h->b);
+  delete h;
+}
+
+// ---- block -------------------------------------------------------------------
+int cl_block_create(const cl_conv* c1, const cl_act* act, const cl_conv* c2, int residual, cl_block** out) {
+  if (!out) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null output handle pointer");
+  *out = nullptr;
+  if (!c1 || !act || !c2) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "block needs conv1, act and conv2");
+  if (c1->k != c2->k || act->k != c1->k)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "block layers disagree on k");
+  for (int a = 0; a < c1->k; ++a)
+    if (c1->g[a] != c2->g[a]) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "block convs disagree on signature");
+  if (c1->C_out != act->C || c2->C_in != c1->C_out)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "block channel counts do not chain");
+  if (c2->d_image != c1->d_out)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "conv2 d_image must equal conv1 d_out");
+  if (c1->prec != c2->prec)
+    return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "block convs must share one precision");
+  int crop = 0;
+  if (residual) {
+    if (c2->C_out != c1->C_in)
+      return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "residual needs C_out == C_in");
+    const int diff = c1->d_image - c2->d_out;
+    if (diff < 0 || (diff & 1))
+      return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "residual needs a centred crop of the input");
+    crop = diff / 2;
+  }
+  cl_block* h = new cl_block{c1, act, c2, residual ? 1 : 0, crop};
+  *out = h;
+  return CL_OK;
+}
+
+}  // extern "C"
+
+namespace cl {
+static int block_run(const cl_block* h, const float* x, float* y, long long B, cudaStream_t s) {
+  const cl_conv* c1 = h->c1;
+  const cl_conv* c2 = h->c2;
+  if (B == 0) return CL_OK;
+  const long long P1 = (long long)ipow(c1->d_out, c1->k);
+  Epi e1;
+  e1.act = h->act;
+  void* mid = nullptr;
+  int rc = CL_OK;
+  if (c1->prec == kPrecBf16) {
+    // conv1's epilogue writes conv2's packed bf16 operand directly
+    const int G2 = c2->plan.G;
+    const size_t bytes = (size_t)B * G2 * P1 * 16;
+    CL_CUDA(cudaMallocAsync(&mid, bytes, s), "block mid alloc");
+    const bool pairs = c2->nb == 4;
+    const int real_groups = pairs ? (c2->C_in + 1) / 2 : c2->C_in;
+    if (G2 != real_groups || (pairs && (c2->C_in & 1)))
+      CL_CUDA(cudaMemsetAsync(mid, 0, bytes, s), "block mid memset");
+    e1.y_bf16 = (__nv_bfloat16*)mid;
+    e1.ybf_groups = G2;
+    e1.ybf_pairs = pairs ? 1 : 0;
+    rc = conv_run(c1, x, nullptr, nullptr, B, e1, s);
+    if (rc == CL_OK) {
+      Epi e2;
+      if (h->residual) { e2.resid = x; e2.res_side = c1->d_image; e2.res_crop = h->res_crop; }
+      rc = conv_run(c2, nullptr, (const __nv_bfloat16*)mid, y, B, e2, s);
+    }
+  } else {
+    const size_t bytes = (size_t)B * c1->C_out * P1 * c1->nb * 4;
+    CL_CUDA(cudaMallocAsync(&mid, bytes, s), "block mid alloc");
+    rc = conv_run(c1, x, nullptr, (float*)mid, B, e1, s);
+    if (rc == CL_OK) {
+      Epi e2;
+      if (h->residual) { e2.resid = x; e2.res_side = c1->d_image; e2.res_crop = h->res_crop; }
+      rc = conv_run(c2, (const float*)mid, nullptr, y, B, e2, s);
+    }
+  }
+  cudaFreeAsync(mid, s);
+  return rc;
+}
+}  // namespace cl
+
+extern "C" {
+
+int cl_block_forward(const cl_block* h, const float* x, float* y, int64_t B, void* stream) {
+  if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null block handle");
+  if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
+  return block_run(h, x, y, B, (cudaStream_t)stream);
+}
+
+int cl_block_forward_host(const cl_block* h, const float* xh, float* yh, int64_t B, int64_t chunk, void* stream) {
+  if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null block handle");
+  const size_t in_per = (size_t)h->c1->C_in * ipow(h->c1->d_image, h->c1->k) * h->c1->nb * 4;
+  const size_t out_per = (size_t)h->c2->C_out * ipow(h->c2->d_out, h->c2->k) * h->c2->nb * 4;
+  return host_chunked(B, in_per, out_per, chunk, xh, yh, (cudaStream_t)stream,
+                      [&](const float* dx, float* dy, long long nb, cudaStream_t s) {
+                        return block_run(h, dx, dy, nb, s);
+                      });
+}
+
+void cl_block_destroy(cl_block* h) { delete h; }
+
+}  // extern "C"

@@ -1,0 +1,372 @@
+// conv_tc.cu -- (2) Clifford convolution as an implicit GEMM on tcgen05.
+//
+// GEMM view of conv.py:151-182:
+//   M = output pixels of one sample tile (128 rows = TMEM lanes),
+//   N = C_out * N_B  (n = co*N_B + t),
+//   K = Q * C_in * N_B (k = (q, ci, j)),
+//   A[m, k] = x[b, ci, p(m) + q, j]   -- never materialised: each pipeline
+//             stage TMA-loads the shifted input box (j, x, y[, z], channels)
+//             straight from the protocol layout (B, C, d^k, N_B); "same"
+//             padding and tile overhang come from TMA out-of-bounds zero fill.
+//   B[n, k] = expanded Clifford filter (subsystem (1), expand.cu), stored as
+//             ready-to-copy UMMA K-major tiles, one bulk copy per stage.
+//
+// Warp roles (384 threads, 1 CTA per SM, persistent over tiles):
+//   warp 0      TMA producer (one lane)
+//   warp 1      MMA issuer (one lane): tcgen05.mma kind::tf32 / kind::f16,
+//               accumulator double-buffered in TMEM (2 x N_TILE fp32 columns)
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue: tcgen05.ld -> bias [-> activation] [-> residual]
+//               -> coalesced stores in the protocol layout (thread = pixel
+//               row, holds all N_B blades of each output channel)
+//   warps 8-11  3xTF32 splitter: A -> (A_hi, A_lo) in shared memory
+//
+// 3xTF32: D += A_lo*B_hi + A_hi*B_lo + A_hi*B_hi with hi = fp32 with the 13
+// low mantissa bits cleared (exactly representable in tf32) and lo = x - hi.
+#include "common.cuh"
+#include "internal.h"
+
+namespace cl {
+
+template <int NB>
+__device__ __forceinline__ float act_gate(const float (&v)[NB], int mode, const float* __restrict__ w,
+                                          float bias, float Kf) {
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) s = fmaf(v[j], __ldg(w + j), s);
+  if (mode == 0) s += bias;
+  else if (mode == 2) s = s / Kf;
+  return 1.f / (1.f + expf(-s));
+}
+
+template <int NB, int PREC>
+__global__ void __launch_bounds__(kConvThreads, 1)
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ConvKParams p) {
+  constexpr bool kSplit = (PREC == kPrecFp32x3);
+  constexpr int RB = (PREC == kPrecBf16) ? 16 : NB * 4;
+  constexpr uint32_t kLayoutA = (RB == 32) ? kSwizzle32B : kSwizzleNone;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = p.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* lo_ready = empty + S;
+  uint64_t* tfull = lo_ready + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&lo_ready[s], 128);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmap);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const long long num_tiles = p.num_tiles;
+  const uint32_t a_total = kSplit ? 2 * p.a_bytes : p.a_bytes;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const int df = p.d_filter;
+      for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        long long r = t;
+        const int nt = (int)(r % p.n_ntiles); r /= p.n_ntiles;
+        const int tx = (int)(r % p.ntx); r /= p.ntx;
+        const int ty = (int)(r % p.nty); r /= p.nty;
+        const int tz = (int)(r % p.ntz);
+        const int b = (int)(r / p.ntz);
+        const int x0 = tx * p.tx - p.pad, y0 = ty * p.ty - p.pad, z0 = tz * p.tz - p.pad;
+        const uint8_t* bsrc = p.b_img + (size_t)nt * p.k_iters * p.b_bytes;
+        for (int kit = 0; kit < p.k_iters; ++kit) {
+          const int q = kit / p.n_gs, g0 = (kit - q * p.n_gs) * p.gs;
+          int qx, qy, qz;
+          if (p.k == 3) { qz = q / (df * df); qy = (q / df) % df; qx = q % df; }
+          else { qz = 0; qy = q / df; qx = q % df; }
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
+          uint8_t* sB = sA + a_total;
+          mbar_arrive_expect_tx(&full[stage], p.a_bytes + p.b_bytes);
+          if (p.merged_bc)
+            tma_load_5d(sA, &tmap, &full[stage], 0, x0 + qx, y0 + qy, z0 + qz, b * p.G + g0);
+          else
+            tma_load_5d(sA, &tmap, &full[stage], 0, x0 + qx, y0 + qy, g0, b);
+          bulk_load(sB, bsrc + (size_t)kit * p.b_bytes, p.b_bytes, &full[stage]);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      const uint32_t idesc = instr_desc(PREC == kPrecBf16 ? 1u : 2u, 128u, (uint32_t)p.n_tile);
+      const uint32_t b_lbo = (uint32_t)p.n_tile * 16u, b_kstep = (uint32_t)p.n_tile * 32u;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.n_tile);
+        for (int kit = 0; kit < p.k_iters; ++kit) {
+          if (kSplit) mbar_wait(&lo_ready[stage], phase);
+          else mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
+          const uint32_t sB = sA + a_total;
+          for (int s = 0; s < p.ks; ++s) {
+            const uint32_t a_addr = sA + (uint32_t)s * 4096u;
+            const uint64_t adesc = (RB == 32) ? smem_desc(a_addr, 16, 256, kLayoutA)
+                                              : smem_desc(a_addr, 2048, 128, kLayoutA);
+            const uint32_t b_addr = sB + (uint32_t)s * b_kstep;
+            const uint64_t bdesc = smem_desc(b_addr, b_lbo, 128, kSwizzleNone);
+            const uint32_t accum = (kit > 0 || s > 0) ? 1u : 0u;
+            if constexpr (kSplit) {
+              const uint64_t adesc_lo = (RB == 32) ? smem_desc(a_addr + p.a_bytes, 16, 256, kLayoutA)
+                                                   : smem_desc(a_addr + p.a_bytes, 2048, 128, kLayoutA);
+              const uint64_t bdesc_lo = smem_desc(b_addr + p.b_img_bytes, b_lbo, 128, kSwizzleNone);
+              mma_tf32(d_tmem, adesc_lo, bdesc, idesc, accum);
+              mma_tf32(d_tmem, adesc, bdesc_lo, idesc, 1u);
+              mma_tf32(d_tmem, adesc, bdesc, idesc, 1u);
+            } else if constexpr (PREC == kPrecTf32) {
+              mma_tf32(d_tmem, adesc, bdesc, idesc, accum);
+            } else {
+              mma_bf16(d_tmem, adesc, bdesc, idesc, accum);
+            }
+          }
+          mma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ===================== epilogue =====================
+    const int ew = warp - 4;
+    const int row = ew * 32 + lane;
+    const int lx = row % p.tx, ly = (row / p.tx) % p.ty, lz = row / (p.tx * p.ty);
+    const int d_out = p.d_out;
+    const long long P_out = (p.k == 3) ? (long long)d_out * d_out * d_out : (long long)d_out * d_out;
+    const long long P_res = (p.k == 3) ? (long long)p.res_side * p.res_side * p.res_side
+                                       : (long long)p.res_side * p.res_side;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      long long r = t;
+      const int nt = (int)(r % p.n_ntiles); r /= p.n_ntiles;
+      const int tx = (int)(r % p.ntx); r /= p.ntx;
+      const int ty = (int)(r % p.nty); r /= p.nty;
+      const int tz = (int)(r % p.ntz);
+      const int b = (int)(r / p.ntz);
+      const int ox = tx * p.tx + lx, oy = ty * p.ty + ly, oz = tz * p.tz + lz;
+      const bool valid = ox < d_out && oy < d_out && oz < ((p.k == 3) ? d_out : 1);
+      const long long pix = (p.k == 3) ? ((long long)oz * d_out + oy) * d_out + ox : (long long)oy * d_out + ox;
+      long long pres = 0;
+      if (p.resid) {
+        const int rs = p.res_side, cr = p.res_crop;
+        pres = (p.k == 3) ? ((long long)(oz + cr) * rs + (oy + cr)) * rs + (ox + cr)
+                          : (long long)(oy + cr) * rs + (ox + cr);
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * p.n_tile);
+      for (int c0 = 0; c0 < p.n_tile; c0 += 32) {
+        const int n0 = nt * p.n_tile + c0;
+        if (n0 >= p.N) break;
+        uint32_t rr[32];
+        tmem_ld32(taddr + (uint32_t)c0, rr);
+        tmem_ld_wait();
+        if (valid) {
+#pragma unroll
+          for (int cc = 0; cc < 32 / NB; ++cc) {
+            const int co = n0 / NB + cc;
+            if (co < p.C_out) {
+              float v[NB];
+#pragma unroll
+              for (int j = 0; j < NB; ++j) v[j] = __uint_as_float(rr[cc * NB + j]) + __ldg(p.bias + j * p.C_out + co);
+              if (p.act_mode >= 0) {
+                const float gte = act_gate<NB>(v, p.act_mode, p.act_w + co * NB,
+                                               p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K);
+#pragma unroll
+                for (int j = 0; j < NB; ++j) v[j] *= gte;
+              }
+              if (p.resid) {
+                const float4* rp = reinterpret_cast<const float4*>(p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB);
+#pragma unroll
+                for (int j = 0; j < NB / 4; ++j) {
+                  const float4 q4 = __ldg(rp + j);
+                  v[4 * j] += q4.x; v[4 * j + 1] += q4.y; v[4 * j + 2] += q4.z; v[4 * j + 3] += q4.w;
+                }
+              }
+              if (p.y) {
+                float4* yp = reinterpret_cast<float4*>(p.y + (((long long)b * p.C_out + co) * P_out + pix) * NB);
+#pragma unroll
+                for (int j = 0; j < NB / 4; ++j) yp[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              }
+              if (p.y_bf16) {
+                if (p.ybf_pairs) {  // 2-D: (B, Gy, P, [2 ch x 4 blades])
+                  __nv_bfloat16* yp = p.y_bf16 + (((long long)b * p.ybf_groups + (co >> 1)) * P_out + pix) * 8 + (co & 1) * 4;
+                  __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]);
+                  __nv_bfloat162 h1 = __floats2bfloat162_rn(v[2], v[3]);
+                  uint2 u;
+                  u.x = *reinterpret_cast<uint32_t*>(&h0);
+                  u.y = *reinterpret_cast<uint32_t*>(&h1);
+                  *reinterpret_cast<uint2*>(yp) = u;
+                } else {  // 3-D: (B, Gy, P, 8 blades)
+                  __nv_bfloat16* yp = p.y_bf16 + (((long long)b * p.ybf_groups + co) * P_out + pix) * 8;
+                  uint4 u;
+                  __nv_bfloat162 h;
+                  h = __floats2bfloat162_rn(v[0], v[1]); u.x = *reinterpret_cast<uint32_t*>(&h);
+                  h = __floats2bfloat162_rn(v[2], v[3]); u.y = *reinterpret_cast<uint32_t*>(&h);
+                  h = __floats2bfloat162_rn(v[4 % NB], v[5 % NB]); u.z = *reinterpret_cast<uint32_t*>(&h);
+                  h = __floats2bfloat162_rn(v[6 % NB], v[7 % NB]); u.w = *reinterpret_cast<uint32_t*>(&h);
+                  *reinterpret_cast<uint4*>(yp) = u;
+                }
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp >= 8) {
+    // ===================== 3xTF32 splitter =====================
+    if constexpr (kSplit) {
+      const int tid = threadIdx.x - 256;
+      int stage = 0;
+      uint32_t phase = 0;
+      const int n4 = (int)(p.a_bytes / 16);
+      for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        for (int kit = 0; kit < p.k_iters; ++kit) {
+          mbar_wait(&full[stage], phase);
+          uint4* a = reinterpret_cast<uint4*>(smem + (size_t)stage * p.stage_bytes);
+          float4* lo = reinterpret_cast<float4*>(smem + (size_t)stage * p.stage_bytes + p.a_bytes);
+          for (int i = tid; i < n4; i += 128) {
+            uint4 v = a[i];
+            uint4 h;
+            h.x = v.x & 0xFFFFE000u; h.y = v.y & 0xFFFFE000u; h.z = v.z & 0xFFFFE000u; h.w = v.w & 0xFFFFE000u;
+            float4 l;
+            l.x = __uint_as_float(v.x) - __uint_as_float(h.x);
+            l.y = __uint_as_float(v.y) - __uint_as_float(h.y);
+            l.z = __uint_as_float(v.z) - __uint_as_float(h.z);
+            l.w = __uint_as_float(v.w) - __uint_as_float(h.w);
+            a[i] = h;
+            lo[i] = l;
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(&lo_ready[stage]);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+template <int NB, int PREC>
+static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const ConvKParams& p,
+                            int grid, cudaStream_t s) {
+  auto kfn = conv_tc_kernel<NB, PREC>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)plan.smem_bytes);
+  if (e != cudaSuccess) return e;
+  kfn<<<grid, kConvThreads, plan.smem_bytes, s>>>(tmap, p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const ConvKParams& p,
+                        int grid, cudaStream_t s) {
+  if (plan.nb == 4) {
+    if (plan.prec == kPrecFp32x3) return launch_t<4, kPrecFp32x3>(plan, tmap, p, grid, s);
+    if (plan.prec == kPrecTf32) return launch_t<4, kPrecTf32>(plan, tmap, p, grid, s);
+    return launch_t<4, kPrecBf16>(plan, tmap, p, grid, s);
+  }
+  if (plan.prec == kPrecFp32x3) return launch_t<8, kPrecFp32x3>(plan, tmap, p, grid, s);
+  if (plan.prec == kPrecTf32) return launch_t<8, kPrecTf32>(plan, tmap, p, grid, s);
+  return launch_t<8, kPrecBf16>(plan, tmap, p, grid, s);
+}
+
+// fp32 protocol (B, C, P, NB) -> bf16 A-ready layout (B, G, P, 8):
+//   NB == 8: group = channel (G >= C, padding channels zero);
+//   NB == 4: group = channel pair, element (g, p, h*4 + t) = x[2g+h, p, t].
+__global__ void pack_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int nb,
+                                 long long B, int C, long long P, int G, int pairs) {
+  const long long total = B * G * P;  // one 16-byte output row per thread
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long pp = i % P;
+    const long long bg = i / P;
+    const int g = (int)(bg % G);
+    const long long b = bg / G;
+    float v[8];
+    if (pairs) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 2 * g + h;
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c < C) q = __ldg(reinterpret_cast<const float4*>(x + ((b * C + c) * P + pp) * 4));
+        v[4 * h] = q.x; v[4 * h + 1] = q.y; v[4 * h + 2] = q.z; v[4 * h + 3] = q.w;
+      }
+    } else {
+      if (g < C) {
+        const float4* src = reinterpret_cast<const float4*>(x + ((b * C + g) * P + pp) * 8);
+        const float4 q0 = __ldg(src), q1 = __ldg(src + 1);
+        v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w;
+        v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 0.f;
+      }
+    }
+    uint4 u;
+    __nv_bfloat162 h;
+    h = __floats2bfloat162_rn(v[0], v[1]); u.x = *reinterpret_cast<uint32_t*>(&h);
+    h = __floats2bfloat162_rn(v[2], v[3]); u.y = *reinterpret_cast<uint32_t*>(&h);
+    h = __floats2bfloat162_rn(v[4], v[5]); u.z = *reinterpret_cast<uint32_t*>(&h);
+    h = __floats2bfloat162_rn(v[6], v[7]); u.w = *reinterpret_cast<uint32_t*>(&h);
+    reinterpret_cast<uint4*>(out)[i] = u;
+  }
+}
+
+cudaError_t launch_pack_bf16(const float* x, __nv_bfloat16* out, int nb, long long B, int C,
+                             long long P, int G, int pairs, cudaStream_t s) {
+  const long long total = B * G * P;
+  long long blocks = (total + 255) / 256;
+  const long long cap = (long long)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  pack_bf16_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, out, nb, B, C, P, G, pairs);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace cl

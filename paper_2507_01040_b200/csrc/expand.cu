@@ -1,0 +1,123 @@
+// expand.cu -- (1) on-device Clifford kernel construction.
+//
+// The real (C_out*N_B) x (C_in*N_B) x Q filter of conv.py:188-202 has entry
+//   W[(co,t), (ci,j), q] = coeff(t^j, j) * f[t^j, ci, co, q],
+// coeff from the blade-product table of the signature (algebra.py:87-99),
+// including zero (degenerate) and negative metric values. Every entry is a
+// single signed filter value, so construction is exact.
+//
+// Two outputs:
+//  * the reference layout (for parity tests / export), and
+//  * the tensor-core operand images used by conv_tc.cu, built ONCE per layer
+//    at create time: per (N-tile, K-iteration) a contiguous block of K-major
+//    SWIZZLE_NONE UMMA core matrices [image][k-step][2 x 16 B chunks][n_tile
+//    rows][16 B], images = {hi, lo} for 3xTF32, {tf32} or {bf16}.
+#include "common.cuh"
+#include "internal.h"
+
+namespace cl {
+
+struct Sig {
+  int g[3];
+  int k;
+};
+
+__device__ __forceinline__ float expanded_entry(const Sig& sg, const float* __restrict__ f, int nb,
+                                                int C_in, int C_out, int Q, int co, int t, int ci,
+                                                int j, int q) {
+  const int i = t ^ j;
+  const int c = blade_coeff(i, j, sg.g, sg.k);
+  if (c == 0) return 0.f;
+  const float v = __ldg(f + (((long long)i * C_in + ci) * C_out + co) * Q + q);
+  return c > 0 ? v : -v;
+}
+
+__global__ void expand_ref_kernel(Sig sg, const float* __restrict__ f, int C_in, int C_out, int Q,
+                                  float* __restrict__ out) {
+  const int nb = 1 << sg.k;
+  const long long total = (long long)C_out * nb * C_in * nb * Q;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(idx % Q);
+    long long r = idx / Q;
+    const int j = (int)(r % nb); r /= nb;
+    const int ci = (int)(r % C_in); r /= C_in;
+    const int t = (int)(r % nb);
+    const int co = (int)(r / nb);
+    out[idx] = expanded_entry(sg, f, nb, C_in, C_out, Q, co, t, ci, j, q);
+  }
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// One thread per (n_tile, k_iter, k_local, row); writes every image.
+__global__ void expand_img_kernel(Sig sg, const float* __restrict__ f, int C_in, int C_out,
+                                  ConvPlan pl, uint8_t* __restrict__ img) {
+  const int nb = pl.nb;
+  const int k_stage = pl.ks * 32 / pl.esize;  // K elements per stage
+  const long long total = (long long)pl.n_ntiles * pl.k_iters * k_stage * pl.n_tile;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(idx % pl.n_tile);
+    long long r = idx / pl.n_tile;
+    const int kl = (int)(r % k_stage); r /= k_stage;
+    const int kit = (int)(r % pl.k_iters);
+    const int nt = (int)(r / pl.k_iters);
+    const int q = kit / pl.n_gs, gsi = kit % pl.n_gs;
+    const int n = nt * pl.n_tile + row;
+    const int co = n / nb, t = n % nb;
+    const int ci = gsi * pl.cps + kl / nb, j = kl % nb;
+    float w = 0.f;
+    if (co < C_out && ci < C_in) w = expanded_entry(sg, f, nb, C_in, C_out, pl.Q, co, t, ci, j, q);
+    // position inside the stage image
+    const int byte_k = kl * pl.esize;
+    const int s = byte_k >> 5, h = (byte_k >> 4) & 1, e = (byte_k & 15) / pl.esize;
+    uint8_t* base = img + ((size_t)nt * pl.k_iters + kit) * pl.b_bytes;
+    const size_t off = (size_t)s * pl.n_tile * 32 + (size_t)h * pl.n_tile * 16 + (size_t)row * 16 +
+                       (size_t)e * pl.esize;
+    if (pl.prec == kPrecFp32x3) {
+      const float hi = __uint_as_float(__float_as_uint(w) & 0xFFFFE000u);
+      *reinterpret_cast<float*>(base + off) = hi;
+      *reinterpret_cast<float*>(base + pl.b_img_bytes + off) = w - hi;
+    } else if (pl.prec == kPrecTf32) {
+      *reinterpret_cast<float*>(base + off) = tf32_rna(w);
+    } else {
+      *reinterpret_cast<__nv_bfloat16*>(base + off) = __float2bfloat16_rn(w);
+    }
+  }
+}
+
+static unsigned grid_for(long long total) {
+  long long blocks = (total + 255) / 256;
+  const long long cap = (long long)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  return (unsigned)(blocks < 1 ? 1 : blocks);
+}
+
+cudaError_t launch_expand_ref(const int* g, int k, const float* f, int C_in, int C_out, int Q,
+                              float* out, cudaStream_t s) {
+  Sig sg{{0, 0, 0}, k};
+  for (int i = 0; i < k; ++i) sg.g[i] = g[i];
+  const int nb = 1 << k;
+  const long long total = (long long)C_out * nb * C_in * nb * Q;
+  expand_ref_kernel<<<grid_for(total), 256, 0, s>>>(sg, f, C_in, C_out, Q, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand_images(const int* g, const ConvPlan& pl, const float* f, int C_in,
+                                 int C_out, uint8_t* img, cudaStream_t s) {
+  Sig sg{{0, 0, 0}, pl.k};
+  for (int i = 0; i < pl.k; ++i) sg.g[i] = g[i];
+  const long long total =
+      (long long)pl.n_ntiles * pl.k_iters * (pl.ks * 32 / pl.esize) * pl.n_tile;
+  expand_img_kernel<<<grid_for(total), 256, 0, s>>>(sg, f, C_in, C_out, pl, img);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace cl

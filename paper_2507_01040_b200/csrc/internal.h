@@ -1,0 +1,92 @@
+// internal.h -- host-side plan / parameter structs shared by the CUDA
+// translation units of libclifford_b200.so (not part of the C-ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace cl {
+
+enum Prec : int { kPrecFp32x3 = 0, kPrecTf32 = 1, kPrecBf16 = 2 };
+
+constexpr int kTileM = 128;          // output pixels per tile (= TMEM lanes)
+constexpr int kConvThreads = 384;    // 12 warps, see conv_tc.cu
+constexpr int kMaxSmem = 232448;     // 227 KB opt-in dynamic shared memory per CTA
+
+// Tiling plan of one conv layer, fixed at create time (conv.py:101-140 fixes
+// its CPU kernel parameters at the same point).
+struct ConvPlan {
+  int k, nb;            // spatial rank, blades
+  int prec;             // Prec
+  int esize;            // operand element bytes (4 fp32/tf32, 2 bf16)
+  int rb;               // bytes of one A row-group (16 or 32)
+  int epg;              // operand elements per row-group (rb / esize)
+  int merged_bc;        // tensor-map dim 4 = b*G + g (3-D) instead of separate (g, b) dims
+  int G;                // row-groups per sample in the A tensor (padded)
+  int gs;               // row-groups per pipeline stage
+  int ks;               // MMA K-steps (32 B of K per row) per stage
+  int n_gs;             // stages per filter tap
+  int Q, d_filter;      // taps
+  int k_iters;          // Q * n_gs
+  int cps;              // channels per stage = gs * epg / nb
+  int N, n_tile, n_ntiles;
+  int tx, ty, tz;       // output tile extents (tx*ty*tz == 128)
+  uint32_t a_bytes, b_img_bytes, b_bytes, stage_bytes;
+  int n_img;            // B images per stage (2 for 3xTF32 hi/lo)
+  int stages;
+  uint32_t tmem_cols;
+  size_t smem_bytes;
+};
+
+struct ConvKParams {
+  int B, k, nb;
+  int d_in, d_out, pad;
+  int tx, ty, tz, ntx, nty, ntz;
+  int n_ntiles, n_tile, N, C_out;
+  long long num_tiles;
+  int d_filter, n_gs, gs, G, merged_bc, k_iters, ks;
+  uint32_t a_bytes, b_bytes, b_img_bytes, stage_bytes, tmem_cols;
+  int stages;
+  const uint8_t* b_img;
+  const float* bias;          // (NB, C_out)
+  float* y;                   // fp32 protocol output (or null)
+  __nv_bfloat16* y_bf16;      // bf16 A-ready output (or null)
+  int ybf_pairs;              // 1: 2-D channel-pair interleave (B, Gy, P, 8)
+  int ybf_groups;             // groups per sample of the bf16 output tensor
+  const float* resid;         // residual source (protocol layout) or null
+  int res_side, res_crop;     // residual spatial side and centre-crop offset
+  int act_mode;               // -1 none, 0 Linear, 1 Sum, 2 Mean
+  const float* act_w;         // (C_out, NB) blade-keyed weights / 0-1 mask
+  const float* act_b;         // (C_out) Linear bias
+  float act_K;                // K as float (Mean divisor)
+};
+
+struct ActParams {
+  const float* x;
+  float* y;
+  long long n_mv;     // B * C * P multivectors
+  long long P;
+  int C;
+  int mode;
+  const float* w;     // (C, NB)
+  const float* b;     // (C)
+  float Kf;
+};
+
+// launchers (conv_tc.cu / expand.cu / activation.cu)
+cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const ConvKParams& p,
+                        int grid, cudaStream_t s);
+cudaError_t launch_expand_ref(const int* g, int k, const float* f, int C_in, int C_out, int Q,
+                              float* out, cudaStream_t s);
+cudaError_t launch_expand_images(const int* g, const ConvPlan& plan, const float* f, int C_in,
+                                 int C_out, uint8_t* img, cudaStream_t s);
+cudaError_t launch_pack_bf16(const float* x, __nv_bfloat16* out, int nb, long long B, int C,
+                             long long P, int G, int pairs, cudaStream_t s);
+cudaError_t launch_act(int nb, const ActParams& p, cudaStream_t s);
+
+int num_sms();
+void count_launch(int n = 1);
+
+}  // namespace cl

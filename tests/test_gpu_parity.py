@@ -1,0 +1,315 @@
+"""GPU parity: the B200 path (through the C-ABI) against the CPU oracle.
+
+Tolerances (D3, the reference's own metric bench.py:74-88):
+  * expanded kernel: bit-exact (+-0 equal)
+  * conv/block fp32 (int8-slice exact accumulation): max_rel_error(floor=1e-2) <= 1e-4
+  * conv 3xTF32: max_rel_error(floor=max|ref|) <= 1e-5 (normwise)
+  * conv TF32 / BF16: max_rel_error(floor=max|ref|) <= 2e-2 (stated bound)
+  * activation: max_abs_error <= 1e-5 (activation.py:7, tests/test_activation.py:160-173)
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2507_01040_b200 as M  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def make_conv(rng, g, B, ci, co, d, df, prec="fp32", padding="valid", fscale=None):
+    k = len(g)
+    nb = 1 << k
+    x = rng.standard_normal((B, ci, d ** k, nb)).astype(np.float32)
+    fan = ci * nb * df ** k
+    bound = fscale if fscale is not None else 1.0 / np.sqrt(fan)
+    f = rng.uniform(-bound, bound, (nb, ci, co, df ** k)).astype(np.float32)
+    b = (rng.standard_normal((nb, co)) * 0.01).astype(np.float32)
+    layer = M.make_conv_layer(M.Dims(B, ci, co, d, df, k), M.Signature(tuple(g)), f, b,
+                              precision=prec, padding=padding)
+    pad = (df - 1) // 2 if padding == "same" else 0
+    return x, f, b, layer, pad
+
+
+def run_dev(fn, x, *a):
+    return fn(torch.from_numpy(x).cuda(), *a).cpu().numpy()
+
+
+def assert_conv_close(y, ref, prec):
+    if prec == "fp32":
+        assert O.max_rel_error(y, ref) <= 1e-4, O.max_rel_error(y, ref)
+    elif prec == "3xtf32":
+        e = O.max_rel_error(y, ref, floor=float(np.abs(ref).max()) + 1e-30)
+        assert e <= 1e-5, e
+    else:
+        e = O.max_rel_error(y, ref, floor=float(np.abs(ref).max()) + 1e-30)
+        assert e <= 2e-2, e
+
+
+# ---- (1) kernel construction: bit-exact for all 36 signatures ----------------
+
+@pytest.mark.parametrize("g", O.all_signatures(3))
+def test_expanded_kernel_bit_exact_all_signatures(g):
+    rng = np.random.default_rng(abs(hash(g)) % 2 ** 32)
+    k = len(g)
+    nb = 1 << k
+    f = rng.standard_normal((nb, 3, 2, 2 ** k)).astype(np.float32)
+    layer = M.make_conv_layer(M.Dims(1, 3, 2, 3, 2, k), M.Signature(g), f, np.zeros((nb, 2), np.float32))
+    W = M.build_expanded_kernel(layer).cpu().numpy()
+    assert np.array_equal(W, O.expanded_kernel(f, g))
+
+
+def test_expanded_kernel_golden(golden):
+    for n in range(10):
+        g = tuple(int(v) for v in golden[f"conv{n}_g"])
+        B, ci, co, di, df, k = (int(v) for v in golden[f"conv{n}_dims"])
+        layer = M.make_conv_layer(M.Dims(B, ci, co, di, df, k), M.Signature(g),
+                                  golden[f"conv{n}_f"], golden[f"conv{n}_b"])
+        W = M.build_expanded_kernel(layer).cpu().numpy()
+        assert np.array_equal(W, golden[f"conv{n}_W"]), n
+
+
+# ---- (2) convolution -------------------------------------------------------------
+
+@pytest.mark.parametrize("prec", ["fp32", "3xtf32", "tf32", "bf16"])
+def test_conv_golden_cases(golden, prec):
+    for n in range(10):
+        g = tuple(int(v) for v in golden[f"conv{n}_g"])
+        B, ci, co, di, df, k = (int(v) for v in golden[f"conv{n}_dims"])
+        if k == 1:
+            continue
+        layer = M.make_conv_layer(M.Dims(B, ci, co, di, df, k), M.Signature(g),
+                                  golden[f"conv{n}_f"], golden[f"conv{n}_b"], precision=prec)
+        y = run_dev(M.conv_forward, golden[f"conv{n}_x"], layer)
+        assert_conv_close(y, golden[f"conv{n}_y"], prec)
+
+
+SIGS = [(1, 1), (-1, 1), (0, 1), (1, 1, 1), (1, -1, 0), (-1, 0, 1), (0, 0, 1)]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "3xtf32", "tf32", "bf16"])
+@pytest.mark.parametrize("g", SIGS)
+@pytest.mark.parametrize("padding", ["valid", "same"])
+def test_conv_signatures(prec, g, padding):
+    rng = np.random.default_rng(7)
+    k = len(g)
+    d = 9 if k == 2 else 6
+    x, f, b, layer, pad = make_conv(rng, g, 2, 5, 6, d, 3, prec, padding)
+    y = run_dev(M.conv_forward, x, layer)
+    assert_conv_close(y, O.conv_ref(x, f, b, g, d, 3, pad), prec)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+@pytest.mark.parametrize("shape", [
+    ((1, 1), 1, 1, 1, 4, 1),      # 1x1 conv, single channel
+    ((1, 1), 3, 7, 3, 5, 5),      # d_out = 1
+    ((1, 1), 2, 3, 9, 40, 3),     # odd channels, several x tiles
+    ((1, 1), 1, 64, 64, 16, 3),
+    ((1, 1, 1), 1, 3, 5, 7, 1),
+    ((1, 1, 1), 2, 16, 16, 9, 3),
+    ((1, 1, 1), 1, 5, 3, 4, 4),   # even filter, valid
+    ((1, -1), 3, 33, 17, 11, 3),  # N not a multiple of 32
+])
+def test_conv_edge_shapes(prec, shape):
+    g, B, ci, co, d, df = shape
+    rng = np.random.default_rng(11)
+    x, f, b, layer, pad = make_conv(rng, g, B, ci, co, d, df, prec)
+    y = run_dev(M.conv_forward, x, layer)
+    assert_conv_close(y, O.conv_ref(x, f, b, g, d, df, pad), prec)
+
+
+def test_conv_identity_filter():
+    # tests/test_conv.py:31-35: scalar-1 filter, zero bias -> identity
+    dims = M.Dims(B=2, C_in=3, C_out=3, d_image=4, d_filter=1, k=2)
+    f = np.zeros(dims.filters_shape(), np.float32)
+    f[0] = np.eye(3, dtype=np.float32)[:, :, None]
+    layer = M.make_conv_layer(dims, M.Signature((1, 1)), f, np.zeros(dims.bias_shape(), np.float32))
+    x = np.random.default_rng(0).standard_normal(dims.input_shape()).astype(np.float32)
+    np.testing.assert_allclose(run_dev(M.conv_forward, x, layer), x, rtol=1e-6, atol=1e-7)
+
+
+def test_conv_bias_broadcast():
+    # tests/test_conv.py:37-45 (k=2 here): zero input -> bias everywhere
+    dims = M.Dims(B=2, C_in=2, C_out=3, d_image=4, d_filter=3, k=2)
+    rng = np.random.default_rng(1)
+    f = rng.standard_normal(dims.filters_shape()).astype(np.float32)
+    bias = rng.standard_normal(dims.bias_shape()).astype(np.float32)
+    layer = M.make_conv_layer(dims, M.Signature((-1, 1)), f, bias)
+    out = run_dev(M.conv_forward, np.zeros(dims.input_shape(), np.float32), layer)
+    np.testing.assert_allclose(out, np.broadcast_to(bias.T[None, :, None, :], out.shape), atol=1e-7)
+
+
+def test_conv_empty_batch():
+    rng = np.random.default_rng(0)
+    _, f, b, _, _ = make_conv(rng, (1, 1), 1, 2, 2, 5, 3)
+    layer = M.make_conv_layer(M.Dims(1, 2, 2, 5, 3, 2), M.Signature((1, 1)), f, b)
+    h = layer.handle()
+    from paper_2507_01040_b200 import _lib
+    import ctypes
+    assert _lib.load().cl_conv_forward(ctypes.c_void_p(h), None, None, 0, None) == 0
+
+
+def test_conv_host_path_numpy():
+    rng = np.random.default_rng(5)
+    x, f, b, layer, pad = make_conv(rng, (1, 1, 1), 3, 4, 4, 8, 3, "fp32", "same")
+    y = M.conv_forward(x, layer)  # numpy in -> host path of the C-ABI
+    assert isinstance(y, np.ndarray)
+    assert_conv_close(y, O.conv_ref(x, f, b, (1, 1, 1), 8, 3, pad), "fp32")
+
+
+def test_conv_batch_independence():
+    rng = np.random.default_rng(9)
+    x, f, b, layer, _ = make_conv(rng, (1, 1), 5, 4, 4, 12, 3)
+    y = run_dev(M.conv_forward, x, layer)
+    one = M.make_conv_layer(M.Dims(1, 4, 4, 12, 3, 2), M.Signature((1, 1)), f, b)
+    for i in (0, 4):
+        np.testing.assert_array_equal(run_dev(M.conv_forward, x[i:i + 1], one)[0], y[i])
+
+
+def test_conv_linearity():
+    # tests/test_conv.py:143-152: conv(a x1 + x2) - bias = a (conv(x1)-bias) + (conv(x2)-bias)
+    rng = np.random.default_rng(3)
+    x1, f, _, _, _ = make_conv(rng, (1, 1, 1), 2, 4, 4, 6, 3)
+    x2 = rng.standard_normal(x1.shape).astype(np.float32)
+    layer = M.make_conv_layer(M.Dims(2, 4, 4, 6, 3, 3), M.Signature((1, 1, 1)), f, np.zeros((8, 4), np.float32))
+    a = np.float32(0.75)
+    lhs = run_dev(M.conv_forward, (a * x1 + x2).astype(np.float32), layer)
+    rhs = a * run_dev(M.conv_forward, x1, layer) + run_dev(M.conv_forward, x2, layer)
+    assert O.max_rel_error(lhs, rhs) <= 1e-4
+
+
+def test_conv_shape_errors():
+    rng = np.random.default_rng(0)
+    x, f, b, layer, _ = make_conv(rng, (1, 1), 2, 3, 3, 6, 3)
+    with pytest.raises(M.errors.ShapeMismatch):
+        M.conv_forward(torch.zeros((2, 3, 35, 4), device="cuda"), layer)
+    with pytest.raises(ValueError):
+        M.conv_forward(torch.from_numpy(x).cuda(), layer, "nonsense")
+
+
+# ---- (3) activation -----------------------------------------------------------------
+
+def test_activation_golden(golden):
+    for n in range(int(golden["act_count"])):
+        k, mode, K = (int(v) for v in golden[f"act{n}_meta"])
+        if k == 1:
+            continue
+        ki = tuple(int(v) for v in golden[f"act{n}_ki"])
+        w = golden[f"act{n}_w"] if mode == 0 else None
+        b = golden[f"act{n}_bias"] if mode == 0 else None
+        cfg = M.make_activation_config(M.Signature((1,) * k), mode, ki, w, b)
+        y = run_dev(M.activation_forward, golden[f"act{n}_x"], cfg)
+        assert O.max_abs_error(y, golden[f"act{n}_y"]) <= 1e-5, n
+
+
+def test_activation_spatial_golden(golden):
+    for mode in (0, 1, 2):
+        w = golden[f"sact{mode}_w"] if mode == 0 else None
+        b = golden[f"sact{mode}_bias"] if mode == 0 else None
+        cfg = M.make_activation_config(M.Signature((1, 1, 1)), mode, tuple(range(8)), w, b)
+        y = run_dev(M.activation_forward, golden[f"sact{mode}_x"], cfg)
+        assert O.max_abs_error(y, golden[f"sact{mode}_y"]) <= 1e-5
+
+
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("C,P,B", [(1, 1, 1), (13, 7, 3), (64, 1000, 2), (3, 4097, 1)])
+def test_activation_shapes(k, mode, C, P, B):
+    nb = 1 << k
+    rng = np.random.default_rng(k * 100 + mode)
+    ki = tuple(int(i) for i in rng.permutation(nb)[: max(1, nb - mode)])
+    w = rng.uniform(-0.5, 0.5, (C, len(ki))).astype(np.float32) if mode == 0 else None
+    b = (rng.standard_normal(C) * 0.1).astype(np.float32) if mode == 0 else None
+    cfg = M.make_activation_config(M.Signature((1,) * k), mode, ki, w, b)
+    x = (rng.standard_normal((B, C, P, nb)) * 3).astype(np.float32)
+    y = run_dev(M.activation_forward, x, cfg)
+    assert O.max_abs_error(y, O.activation_ref(x, mode, ki, w, b)) <= 1e-5
+    # flat (B, C, N_B) form
+    y3 = run_dev(M.activation_forward, x[:, :, 0, :].copy(), cfg)
+    assert O.max_abs_error(y3, O.activation_ref(x[:, :, 0, :], mode, ki, w, b)) <= 1e-5
+
+
+def test_activation_sigmoid_accuracy():
+    # tests/test_activation.py:48-59: gate within 1e-6 of the fp64 sigmoid on [-30, 30]
+    s_vals = np.linspace(-30, 30, 4001).astype(np.float32)
+    x = np.ones((1, s_vals.size, 4), np.float32)
+    x[0, :, 0] = s_vals
+    cfg = M.make_activation_config(M.Signature((1, 1)), 1, (0,))
+    gate = run_dev(M.activation_forward, x, cfg)[0, :, 1]
+    want = 1.0 / (1.0 + np.exp(-s_vals.astype(np.float64)))
+    assert np.max(np.abs(gate - want)) < 1e-6
+
+
+def test_activation_host_path():
+    rng = np.random.default_rng(2)
+    cfg = M.make_activation_config(M.Signature((1, 1)), 2, (0, 1, 2, 3))
+    x = rng.standard_normal((4, 6, 33, 4)).astype(np.float32)
+    y = M.activation_forward(x, cfg)
+    assert O.max_abs_error(y, O.activation_ref(x, 2, (0, 1, 2, 3))) <= 1e-5
+
+
+# ---- (4) block ------------------------------------------------------------------------
+
+def _block_from_golden(golden, name, prec="fp32"):
+    meta = golden[f"{name}_meta"]
+    k = int(meta[3])
+    g = tuple(int(v) for v in meta[:k])
+    pad, residual, mode, B, C, d = (int(v) for v in meta[4:10])
+    aw = golden[f"{name}_aw"] if mode == 0 else None
+    ab = golden[f"{name}_ab"] if mode == 0 else None
+    blk = M.make_basic_block(M.Signature(g), B, C, C, C, d, golden[f"{name}_f1"], golden[f"{name}_b1"], mode,
+                             golden[f"{name}_f2"], golden[f"{name}_b2"], act_weight=aw, act_bias=ab,
+                             padding="same" if pad else "valid", residual=bool(residual), precision=prec)
+    return blk
+
+
+@pytest.mark.parametrize("name", ["blk2v", "blk2s", "blk3s", "blk3v"])
+@pytest.mark.parametrize("prec", ["fp32", "3xtf32", "bf16"])
+def test_block_golden(golden, name, prec):
+    blk = _block_from_golden(golden, name, prec)
+    y = run_dev(M.block_forward, golden[f"{name}_x"], blk)
+    ref = golden[f"{name}_y"]
+    assert_conv_close(y, ref, prec)
+
+
+@pytest.mark.parametrize("g,mode,padding,residual", [
+    ((1, 1), 0, "same", True), ((1, 1, 1), 2, "same", True), ((1, 1), 1, "valid", False),
+    ((1, -1, 0), 0, "valid", True)])
+def test_block_random(g, mode, padding, residual):
+    rng = np.random.default_rng(4)
+    k = len(g)
+    nb = 1 << k
+    B, C, d = 2, 6, 10 if k == 2 else 8
+    fan = C * nb * 3 ** k
+    f1 = rng.uniform(-1, 1, (nb, C, C, 3 ** k)).astype(np.float32) / np.float32(np.sqrt(fan))
+    f2 = rng.uniform(-1, 1, (nb, C, C, 3 ** k)).astype(np.float32) / np.float32(np.sqrt(fan))
+    b1 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
+    b2 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
+    aw = rng.uniform(-0.5, 0.5, (C, nb)).astype(np.float32) if mode == 0 else None
+    ab = (rng.standard_normal(C) * 0.1).astype(np.float32) if mode == 0 else None
+    x = rng.standard_normal((B, C, d ** k, nb)).astype(np.float32)
+    blk = M.make_basic_block(M.Signature(g), B, C, C, C, d, f1, b1, mode, f2, b2, act_weight=aw, act_bias=ab,
+                             padding=padding, residual=residual)
+    y = run_dev(M.block_forward, x, blk)
+    ref = O.block_ref(x, g, d, f1, b1, mode, tuple(range(nb)), aw, ab, f2, b2, padding=padding, residual=residual)
+    assert_conv_close(y, ref, "fp32")
+    yh = M.block_forward(x, blk)  # host path, chunked
+    assert np.array_equal(yh, y)
+
+
+def test_launch_counter_moves():
+    from paper_2507_01040_b200 import _lib
+    n0 = _lib.launch_count()
+    cfg = M.make_activation_config(M.Signature((1, 1)), 1, (0, 1, 2, 3))
+    M.activation_forward(torch.zeros((1, 1, 4), device="cuda"), cfg)
+    torch.cuda.synchronize()
+    assert _lib.launch_count() > n0

@@ -1,0 +1,149 @@
+"""CPU-only checks: the C-ABI library loads and exports every symbol the
+header declares; host-side algebra (the same C code that builds the device
+kernels) matches the reference golden tables; host validation mirrors the
+reference's exceptions; MVTF wire format; FLOP models. No GPU compute."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2507_01040_b200 as M
+from paper_2507_01040_b200 import _lib, errors as E
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "clifford_b200.h")).read()
+    return sorted(set(re.findall(r"\b(cl_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 19
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.EXPORTS)
+    assert lib.cl_version().startswith(b"clifford_b200")
+
+
+def test_library_is_sm100a_native():
+    # the fatbin carries sm_100a SASS with tcgen05 / TMA instructions
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "UTCHMMA" in out or "UTCQMMA" in out or "UTCIMMA" in out
+    assert "UTMALDG" in out
+
+
+def test_product_tables_via_c_abi(golden):
+    for s in golden["sig_list"]:
+        g = tuple(int(v) for v in str(s).split("_"))
+        tgt, cof = M.product_table(M.Signature(g))
+        np.testing.assert_array_equal(tgt, golden[f"table_target_{s}"])
+        np.testing.assert_array_equal(cof, golden[f"table_coeff_{s}"])
+        assert M.schedule_terms(M.Signature(g)) == len(golden[f"sched_{s}"])
+
+
+def test_blade_product_known_answers():
+    assert M.blade_product(1, 1, M.Signature((1, 1))) == (0, 1)
+    assert M.blade_product(1, 1, M.Signature((-1, 1))) == (0, -1)
+    assert M.blade_product(1, 1, M.Signature((0, 1))) == (0, 0)
+    assert M.blade_product(2, 1, M.Signature((1, 1))) == (3, -1)
+    assert M.blade_product(3, 3, M.Signature((1, 1))) == (0, -1)
+
+
+def test_signature_validation():
+    with pytest.raises(E.InvalidSignature):
+        M.validate_signature((0, 0))
+    with pytest.raises(E.InvalidMetricValue):
+        M.validate_signature((1, 2))
+    with pytest.raises(E.InvalidSignature):
+        M.validate_signature(())
+    assert M.validate_signature((1.0, -1.0, 0.0)).g == (1, -1, 0)
+    g = (_lib.C.c_int32 * 2)(0, 0)
+    assert _lib.load().cl_validate_signature(g, 2) == 1
+    g = (_lib.C.c_int32 * 2)(1, 2)
+    assert _lib.load().cl_validate_signature(g, 2) == 2
+    with pytest.raises(E.InvalidMetricValue):
+        _lib.check(2)
+
+
+def test_dims_and_layer_validation():
+    with pytest.raises(E.ShapeMismatch):
+        M.Dims(1, 1, 1, 3, 4, 2)
+    with pytest.raises(E.ShapeMismatch):
+        M.Dims(0, 1, 1, 3, 1, 2)
+    d = M.Dims(2, 3, 4, 6, 3, 2)
+    assert d.input_shape() == (2, 3, 36, 4) and d.output_shape() == (2, 4, 16, 4)
+    sig = M.Signature((1, 1))
+    f = np.zeros(d.filters_shape(), np.float32)
+    b = np.zeros(d.bias_shape(), np.float32)
+    with pytest.raises(E.ShapeMismatch):
+        M.make_conv_layer(d, M.Signature((1, 1, 1)), f, b)
+    with pytest.raises(E.ShapeMismatch):
+        M.make_conv_layer(d, sig, f[:, :2], b)
+    with pytest.raises(E.ShapeMismatch):
+        M.make_conv_layer(d, sig, f, b[:, :1])
+    with pytest.raises(E.ShapeMismatch):
+        M.make_conv_layer(d, sig, f, b, W=0)
+    layer = M.make_conv_layer(d, sig, f, b, padding="same")
+    assert layer.d_out == 6 and layer.output_shape() == (2, 4, 36, 4)
+    assert not layer.filters.flags.writeable
+
+
+def test_activation_config_validation():
+    s2 = M.Signature((1, 1))
+    with pytest.raises(E.ModeConfigMismatch):
+        M.make_activation_config(s2, M.AggMode.LINEAR, (0, 1))
+    with pytest.raises(E.ModeConfigMismatch):
+        M.make_activation_config(s2, M.AggMode.SUM, (0, 1), weight=np.ones((3, 2)), bias=np.ones(3))
+    with pytest.raises(E.IndexOutOfRange):
+        M.make_activation_config(s2, M.AggMode.SUM, (1, 1))
+    with pytest.raises(E.IndexOutOfRange):
+        M.make_activation_config(s2, M.AggMode.MEAN, (0, 4))
+    with pytest.raises(E.ShapeMismatch):
+        M.make_activation_config(s2, M.AggMode.LINEAR, (0, 1), weight=np.ones((3, 3)), bias=np.ones(3))
+    cfg = M.make_activation_config(M.Signature((1,)), 1, (0,))
+    assert cfg.agg_mode is M.AggMode.SUM and cfg.K == 1
+
+
+def test_flop_models(golden):
+    for n in range(10):
+        g = tuple(int(v) for v in golden[f"conv{n}_g"])
+        B, ci, co, di, df, k = (int(v) for v in golden[f"conv{n}_dims"])
+        assert M.conv_flops(M.Dims(B, ci, co, di, df, k), M.Signature(g)) == int(golden[f"conv{n}_flops"])
+    got = [M.activation_flops(5, 7, nb, K, m) for nb, K in ((4, 4), (8, 8), (8, 3)) for m in (0, 1, 2)]
+    np.testing.assert_array_equal(got, golden["act_flops"])
+    # BASELINE config FLOP counts
+    assert M.conv_flops(M.Dims(8, 16, 16, 32, 3, 2), M.Signature((1, 1))) == 531_302_400
+    assert M.conv_flops(M.Dims(16, 32, 32, 32, 3, 3), M.Signature((1, 1, 1))) == 1_528_934_400_000
+    assert M.conv_flops(M.Dims(16, 32, 32, 32, 3, 3), M.Signature((1, -1, 0))) == 1_146_728_448_000
+    assert M.conv_flops(M.Dims(256, 64, 64, 32, 3, 3), M.Signature((1, 1, 1)), padding="same") == 118_751_550_767_104
+
+
+def test_mvtf_roundtrip(tmp_path, golden):
+    p = tmp_path / "t.mvtf"
+    M.write_tensor(p, golden["mvtf_arr"], M.LayoutTag.CONV_INPUT, 2)
+    assert p.read_bytes() == golden["mvtf_bytes"].tobytes()
+    tf = M.read_tensor(p)
+    np.testing.assert_array_equal(tf.data, golden["mvtf_arr"])
+    assert tf.tag == M.LayoutTag.CONV_INPUT and tf.k == 2
+    p.write_bytes(b"XXXX" + p.read_bytes()[4:])
+    with pytest.raises(E.ShapeMismatch):
+        M.read_tensor(p)
+
+
+def test_no_oracle_in_product():
+    # the product package must never import the oracle (no CPU fallback)
+    pkg = os.path.join(ROOT, "paper_2507_01040_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith(".py"):
+                src = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
