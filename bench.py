@@ -49,9 +49,9 @@ def load_peaks():
 def mode_peak(precision, peaks, sustained=True):
     """Effective dense tensor peak (TFLOP/s of algorithmic work) of a mode,
     derived from the measured bf16 GEMM peak: tf32 = bf16/2; 3xTF32 = tf32/3;
-    fp32 (int8 slices, 6 MMAs per product) = (2*bf16)/6."""
+    fp32 (int8 digit slices: 10 int8 MMAs per K-step, int8 = 2 x bf16) = 2*bf16/10."""
     bf16 = peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"]
-    return {"bf16": bf16, "tf32": bf16 / 2, "3xtf32": bf16 / 6, "fp32": 2 * bf16 / 6}[precision]
+    return {"bf16": bf16, "tf32": bf16 / 2, "3xtf32": bf16 / 6, "fp32": 2 * bf16 / 10}[precision]
 
 
 class ClockSampler:
@@ -353,7 +353,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
-    ap.add_argument("--precision", default="3xtf32", choices=["fp32", "3xtf32", "tf32", "bf16"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "3xtf32", "tf32", "bf16"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -59,9 +59,11 @@ typedef enum {
 
 /* Arithmetic mode of the tensor-core convolution. */
 typedef enum {
-  CL_PREC_FP32 = 0, /* 3xTF32 split: fp32-accurate (max_rel_error <= 1e-4) */
-  CL_PREC_TF32 = 1, /* single TF32 pass */
-  CL_PREC_BF16 = 2  /* BF16 operands, fp32 accumulate */
+  CL_PREC_FP32 = 0,   /* fp32-accurate: int8 digit slices, exact s32 accumulation
+                         (max_rel_error <= 1e-4 vs the fp64 oracle) */
+  CL_PREC_TF32 = 1,   /* single TF32 pass */
+  CL_PREC_BF16 = 2,   /* BF16 operands, fp32 accumulate */
+  CL_PREC_3XTF32 = 3  /* 3xTF32 split (hi/lo), fp32 tensor-core accumulation */
 } cl_precision;
 
 typedef enum { CL_PAD_VALID = 0, CL_PAD_SAME = 1 } cl_padding;

@@ -4,8 +4,8 @@ Drop-in for the reference layer API (conv.py:77-140, :371-387): the same
 `make_conv_layer(dims, sig, filters, bias, W=None, U=1)` constructor, the same
 protocol layouts, `conv_forward(x, layer, variant)` and `conv_flops`. The
 forward runs libclifford_b200.so's implicit-GEMM tcgen05 kernel; there is no
-CPU path. Extensions (keyword-only): `precision` in {"fp32" (3xTF32),
-"tf32", "bf16"} and `padding` in {"valid", "same"}.
+CPU path. Extensions (keyword-only): `precision` in {"fp32" (int8 digit slices,
+exact accumulation), "3xtf32", "tf32", "bf16"} and `padding` in {"valid", "same"}.
 
 Inputs: a CUDA torch tensor runs the device path and returns a CUDA tensor;
 a numpy array (or CPU tensor) runs the host path of the C-ABI, which copies
@@ -24,7 +24,7 @@ from .algebra import Signature, schedule_flop_count
 from .errors import ShapeMismatch
 from .layout import Dims
 
-PRECISIONS = {"fp32": 0, "3xtf32": 0, "tf32": 1, "bf16": 2}
+PRECISIONS = {"fp32": 0, "tf32": 1, "bf16": 2, "3xtf32": 3}
 PADDINGS = {"valid": 0, "same": 1}
 # The reference variant names are accepted so existing callers keep working;
 # all of them run the B200 kernel (there is no CPU implementation here).

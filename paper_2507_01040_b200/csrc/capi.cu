@@ -104,14 +104,19 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
   pl.k = k;
   pl.nb = nb;
   pl.prec = prec;
-  pl.esize = prec == kPrecBf16 ? 2 : 4;
-  pl.rb = prec == kPrecBf16 ? 16 : nb * 4;
+  const bool i8 = prec == kPrecFp32;
+  pl.esize = i8 ? 1 : (prec == kPrecBf16 ? 2 : 4);
+  pl.rb = (prec == kPrecBf16 || i8) ? 16 : nb * 4;
   pl.epg = pl.rb / pl.esize;
   pl.merged_bc = (k == 3);
   pl.d_filter = d_filter;
   pl.Q = ipow(d_filter, k);
-  const bool pairs = (prec == kPrecBf16 && nb == 4);
-  const int G_real = pairs ? (C_in + 1) / 2 : C_in;
+  // row-groups per sample: int8 groups hold 16/nb channels, bf16 2-D groups
+  // a channel pair, otherwise one channel
+  int G_real;
+  if (i8) G_real = (C_in * nb + 15) / 16;
+  else if (prec == kPrecBf16 && nb == 4) G_real = (C_in + 1) / 2;
+  else G_real = C_in;
   const int gpk = 32 / pl.rb;  // row-groups per 32-byte K step
 
   // spatial tile (tx * ty * tz == 128)
@@ -128,11 +133,16 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
   pl.ty = ty;
   pl.tz = tz;
 
+  pl.n_img = i8 ? kDigits : (prec == kPrec3xTf32 ? 2 : 1);
+  pl.n_a = pl.n_img;
+  pl.n_tma_a = i8 ? kDigits : 1;
+  pl.levels = i8 ? kDigits : 1;
+  pl.acc_slots = i8 ? 1 : 2;
+  const int max_tile = i8 ? 128 : 256;  // levels x n_tile x slots <= 512 TMEM columns
   pl.N = C_out * nb;
-  pl.n_ntiles = (pl.N + 255) / 256;
+  pl.n_ntiles = (pl.N + max_tile - 1) / max_tile;
   const int per = (pl.N + pl.n_ntiles - 1) / pl.n_ntiles;
   pl.n_tile = ((per + 31) / 32) * 32;
-  pl.n_img = prec == kPrecFp32x3 ? 2 : 1;
 
   const int G_pad_min = ((G_real + gpk - 1) / gpk) * gpk;
   int best = -1;
@@ -142,8 +152,8 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
     if (gs > G_pad_min) continue;
     int G, n_gs;
     if (pl.merged_bc) {
-      if (prec == kPrecBf16) {
-        G = ((G_real + gs - 1) / gs) * gs;  // pack pass zero-pads channels
+      if (prec == kPrecBf16 || i8) {
+        G = ((G_real + gs - 1) / gs) * gs;  // the pack / slice pass zero-pads groups
       } else {
         if (G_real % gs) continue;
         G = G_real;
@@ -151,7 +161,7 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
       n_gs = G / gs;
     } else {
       G = G_real;
-      n_gs = (G_real + gs - 1) / gs;  // TMA OOB zero-fills missing channels
+      n_gs = (G_real + gs - 1) / gs;  // TMA OOB zero-fills missing groups
     }
     ConvPlan c = pl;
     c.ks = ks;
@@ -163,16 +173,16 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
     c.a_bytes = (uint32_t)(kTileM * gs * pl.rb);
     c.b_img_bytes = (uint32_t)(ks * pl.n_tile * 32);
     c.b_bytes = c.b_img_bytes * pl.n_img;
-    c.stage_bytes = c.a_bytes * (prec == kPrecFp32x3 ? 2 : 1) + c.b_bytes;
+    c.stage_bytes = c.a_bytes * pl.n_a + c.b_bytes;
     c.stages = std::min(8, (int)((kMaxSmem - 2048) / c.stage_bytes));
-    if (c.stages >= 4) { bestp = c; best = 4; break; }
+    if (c.stages >= 4 || (i8 && c.stages >= 3)) { bestp = c; best = 4; break; }
     if (c.stages >= 2 && best < c.stages) { bestp = c; best = c.stages; }
   }
   if (best < 0) return false;
   pl = bestp;
-  pl.tmem_cols = (uint32_t)std::max(32, pow2_at_least(2 * pl.n_tile));
+  pl.tmem_cols = (uint32_t)std::max(32, pow2_at_least(pl.levels * pl.n_tile * pl.acc_slots));
   pl.smem_bytes = (size_t)pl.stages * pl.stage_bytes + 1024 + 256;
-  return true;
+  return pl.tmem_cols <= 512;
 }
 
 }  // namespace cl
@@ -188,6 +198,7 @@ struct cl_conv {
   float* filters = nullptr;  // (NB, C_in, C_out, Q) device copy
   float* bias = nullptr;     // (NB, C_out)
   uint8_t* img = nullptr;    // tensor-core operand images
+  float* w_scale = nullptr;  // kPrecFp32: per-column digit scales
   ConvPlan plan;
 };
 
@@ -260,8 +271,9 @@ int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, in
     return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "C_in, C_out, d_image, d_filter must be >= 1");
   if (padding != CL_PAD_VALID && padding != CL_PAD_SAME)
     return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "padding must be 0 (valid) or 1 (same)");
-  if (precision < 0 || precision > 2)
-    return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "precision must be 0 (fp32), 1 (tf32) or 2 (bf16)");
+  if (precision < 0 || precision > 3)
+    return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid",
+                "precision must be 0 (fp32), 1 (tf32), 2 (bf16) or 3 (3xtf32)");
   const int pad = padding == CL_PAD_SAME ? (d_filter - 1) / 2 : 0;
   if (padding == CL_PAD_SAME && (d_filter % 2) == 0)
     return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "same padding needs an odd d_filter");
@@ -293,14 +305,17 @@ int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, in
   const size_t nbias = (size_t)h->nb * C_out;
   const size_t nimg = (size_t)h->plan.n_ntiles * h->plan.k_iters * h->plan.b_bytes;
   cudaError_t e;
+  const size_t nscale = (size_t)h->plan.n_ntiles * h->plan.n_tile;
   if ((e = cudaMalloc(&h->filters, nf * 4)) != cudaSuccess || (e = cudaMalloc(&h->bias, nbias * 4)) != cudaSuccess ||
-      (e = cudaMalloc(&h->img, nimg)) != cudaSuccess) {
+      (e = cudaMalloc(&h->img, nimg)) != cudaSuccess || (e = cudaMalloc(&h->w_scale, nscale * 4)) != cudaSuccess) {
     cl_conv_destroy(h);
     return cuda_fail(e, "cl_conv_create alloc");
   }
   if ((e = cudaMemcpyAsync(h->filters, filters, nf * 4, cudaMemcpyDefault, s)) != cudaSuccess ||
       (e = cudaMemcpyAsync(h->bias, bias, nbias * 4, cudaMemcpyDefault, s)) != cudaSuccess ||
-      (e = launch_expand_images(h->g, h->plan, h->filters, C_in, C_out, h->img, s)) != cudaSuccess ||
+      (precision == kPrecFp32 &&
+       (e = launch_weight_colscale(h->g, h->plan, h->filters, C_in, C_out, h->w_scale, s)) != cudaSuccess) ||
+      (e = launch_expand_images(h->g, h->plan, h->filters, C_in, C_out, h->w_scale, h->img, s)) != cudaSuccess ||
       (e = cudaStreamSynchronize(s)) != cudaSuccess) {
     cl_conv_destroy(h);
     return cuda_fail(e, "cl_conv_create");
@@ -320,6 +335,7 @@ void cl_conv_destroy(cl_conv* h) {
   cudaFree(h->filters);
   cudaFree(h->bias);
   cudaFree(h->img);
+  cudaFree(h->w_scale);
   delete h;
 }
 
@@ -349,6 +365,8 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   const cuuint64_t rowb = (cuuint64_t)pl.rb;
   const bool bf = pl.prec == kPrecBf16;
+  const bool i8 = pl.prec == kPrecFp32;
+  const cuuint64_t planes = (cuuint64_t)pl.n_tma_a;  // int8 digit planes stacked over the batch
   dims[0] = (cuuint64_t)pl.epg;
   dims[1] = D;
   dims[2] = D;
@@ -359,21 +377,22 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
   strides[1] = rowb * D;
   if (pl.merged_bc) {
     dims[3] = D;
-    dims[4] = (cuuint64_t)B * (cuuint64_t)pl.G;
+    dims[4] = planes * (cuuint64_t)B * (cuuint64_t)pl.G;
     strides[2] = rowb * D * D;
     strides[3] = rowb * D * D * D;
     box[3] = (cuuint32_t)pl.tz;
     box[4] = (cuuint32_t)pl.gs;
   } else {
-    const cuuint64_t Gt = bf ? (cuuint64_t)pl.G : (cuuint64_t)h->C_in;
+    const cuuint64_t Gt = (bf || i8) ? (cuuint64_t)pl.G : (cuuint64_t)h->C_in;
     dims[3] = Gt;
-    dims[4] = (cuuint64_t)B;
+    dims[4] = planes * (cuuint64_t)B;
     strides[2] = rowb * D * D;
     strides[3] = rowb * D * D * Gt;
     box[3] = (cuuint32_t)pl.gs;
     box[4] = 1;
   }
-  CUresult r = enc(map, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
+  CUresult r = enc(map, i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                           : (bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32), 5,
                    const_cast<void*>(xsrc), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    pl.rb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -389,8 +408,19 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   if (B == 0) return CL_OK;
   const long long P_in = (long long)ipow(h->d_image, h->k);
   __nv_bfloat16* packed = nullptr;
+  int8_t* digits = nullptr;
+  float* a_scale = nullptr;
   const void* src = x;
-  if (pl.prec == kPrecBf16) {
+  if (pl.prec == kPrecFp32) {
+    const size_t bytes = (size_t)kDigits * B * pl.G * P_in * 16;
+    CL_CUDA(cudaMallocAsync((void**)&digits, bytes + (size_t)B * 8 + 64, s), "conv digit alloc");
+    unsigned* amax = reinterpret_cast<unsigned*>(digits + bytes);
+    a_scale = reinterpret_cast<float*>(digits + bytes + (size_t)B * 4);
+    const long long per_sample = (long long)h->C_in * P_in * h->nb;
+    CL_CUDA(launch_sample_absmax(x, B, per_sample, amax, s), "absmax");
+    CL_CUDA(launch_slice_input(x, amax, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G, s), "slice_input");
+    src = digits;
+  } else if (pl.prec == kPrecBf16) {
     if (xbf) {
       src = xbf;
     } else {
@@ -403,6 +433,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   CUtensorMap map;
   if (int st = encode_input_map(h, src, B, &map)) {
     if (packed) cudaFreeAsync(packed, s);
+    if (digits) cudaFreeAsync(digits, s);
     return st;
   }
   ConvKParams p{};
@@ -436,6 +467,12 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.stage_bytes = pl.stage_bytes;
   p.tmem_cols = pl.tmem_cols;
   p.stages = pl.stages;
+  p.n_a = pl.n_a;
+  p.n_tma_a = pl.n_tma_a;
+  p.levels = pl.levels;
+  p.acc_slots = pl.acc_slots;
+  p.a_scale = a_scale;
+  p.w_scale = h->w_scale;
   p.b_img = h->img;
   p.bias = h->bias;
   p.y = y;
@@ -452,6 +489,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   const int grid = (int)std::min<long long>(p.num_tiles, (long long)num_sms());
   cudaError_t e = launch_conv(pl, map, p, grid, s);
   if (packed) cudaFreeAsync(packed, s);
+  if (digits) cudaFreeAsync(digits, s);
   if (e != cudaSuccess) return cuda_fail(e, "conv_tc launch");
   return CL_OK;
 }

@@ -136,6 +136,15 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// kind::i8 (s8 x s8 -> s32 accumulator: exact integer accumulation)
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // Arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
@@ -156,11 +165,42 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+// 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 #endif  // __CUDACC__
+
+// ---- int8 digit slicing (kPrecFp32, see slice.cu) --------------------------
+#if defined(__CUDACC__)
+// power-of-two s with amax * 128/127 <= s (so the leading digit fits in [-127, 127])
+__device__ __forceinline__ float pow2_scale_for(float amax) {
+  if (!(amax > 0.f)) return 1.f;
+  int e;
+  frexpf(amax * 1.0079f, &e);
+  return ldexpf(1.f, e);
+}
+// u (|u| <= 127/128) -> 4 signed digits, u = sum_i d_i 2^(-7 i) + O(2^-29)
+__device__ __forceinline__ void digits4(float u, int8_t (&d)[4]) {
+  float t = u * 128.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float di = rintf(t);
+    d[i] = (int8_t)(int)di;
+    t = (t - di) * 128.f;  // exact: |t - di| <= 1/2
+  }
+}
+#endif
 
 // ---- UMMA descriptors (layouts: cute/arch/mma_sm100_desc.hpp conventions) ---
 enum : uint32_t { kSwizzleNone = 0, kSwizzle32B = 6 };
@@ -179,6 +219,10 @@ CL_HD uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t la
 // fmt: 1 = BF16, 2 = TF32 (kind::f16 / kind::tf32 operand format codes).
 CL_HD uint32_t instr_desc(uint32_t fmt, uint32_t M, uint32_t N) {
   return (1u << 4) | (fmt << 7) | (fmt << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+// kind::i8: signed A and B (format 1), s32 accumulator (c_format 2).
+CL_HD uint32_t instr_desc_i8(uint32_t M, uint32_t N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
 }  // namespace cl

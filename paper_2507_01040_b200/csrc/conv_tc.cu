@@ -42,8 +42,9 @@ __device__ __forceinline__ float act_gate(const float (&v)[NB], int mode, const 
 template <int NB, int PREC>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ConvKParams p) {
-  constexpr bool kSplit = (PREC == kPrecFp32x3);
-  constexpr int RB = (PREC == kPrecBf16) ? 16 : NB * 4;
+  constexpr bool kSplit = (PREC == kPrec3xTf32);
+  constexpr bool kInt8 = (PREC == kPrecFp32);
+  constexpr int RB = (PREC == kPrecBf16 || kInt8) ? 16 : NB * 4;
   constexpr uint32_t kLayoutA = (RB == 32) ? kSwizzle32B : kSwizzleNone;
 
   extern __shared__ uint8_t smem_raw[];
@@ -79,7 +80,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const long long num_tiles = p.num_tiles;
-  const uint32_t a_total = kSplit ? 2 * p.a_bytes : p.a_bytes;
+  const uint32_t a_total = p.a_bytes * (uint32_t)p.n_a;
+  const int slots = p.acc_slots;
+  const uint32_t slot_cols = (uint32_t)(p.levels * p.n_tile);
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -87,6 +90,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       const int df = p.d_filter;
+      const uint32_t tx_bytes = p.a_bytes * (uint32_t)p.n_tma_a + p.b_bytes;
       for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         long long r = t;
         const int nt = (int)(r % p.n_ntiles); r /= p.n_ntiles;
@@ -104,11 +108,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
           uint8_t* sB = sA + a_total;
-          mbar_arrive_expect_tx(&full[stage], p.a_bytes + p.b_bytes);
-          if (p.merged_bc)
-            tma_load_5d(sA, &tmap, &full[stage], 0, x0 + qx, y0 + qy, z0 + qz, b * p.G + g0);
-          else
-            tma_load_5d(sA, &tmap, &full[stage], 0, x0 + qx, y0 + qy, g0, b);
+          mbar_arrive_expect_tx(&full[stage], tx_bytes);
+          for (int d = 0; d < p.n_tma_a; ++d) {
+            const int bb = d * p.B + b;  // digit planes are stacked over the batch
+            if (p.merged_bc)
+              tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, y0 + qy, z0 + qz, bb * p.G + g0);
+            else
+              tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, y0 + qy, g0, bb);
+          }
           bulk_load(sB, bsrc + (size_t)kit * p.b_bytes, p.b_bytes, &full[stage]);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
@@ -117,7 +124,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
-      const uint32_t idesc = instr_desc(PREC == kPrecBf16 ? 1u : 2u, 128u, (uint32_t)p.n_tile);
+      const uint32_t idesc = kInt8 ? instr_desc_i8(128u, (uint32_t)p.n_tile)
+                                   : instr_desc(PREC == kPrecBf16 ? 1u : 2u, 128u, (uint32_t)p.n_tile);
       const uint32_t b_lbo = (uint32_t)p.n_tile * 16u, b_kstep = (uint32_t)p.n_tile * 32u;
       int stage = 0;
       uint32_t phase = 0;
@@ -126,7 +134,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.n_tile);
+        const uint32_t d_tmem = tmem_base + (uint32_t)acc * slot_cols;
         for (int kit = 0; kit < p.k_iters; ++kit) {
           if (kSplit) mbar_wait(&lo_ready[stage], phase);
           else mbar_wait(&full[stage], phase);
@@ -135,29 +143,44 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const uint32_t sB = sA + a_total;
           for (int s = 0; s < p.ks; ++s) {
             const uint32_t a_addr = sA + (uint32_t)s * 4096u;
-            const uint64_t adesc = (RB == 32) ? smem_desc(a_addr, 16, 256, kLayoutA)
-                                              : smem_desc(a_addr, 2048, 128, kLayoutA);
             const uint32_t b_addr = sB + (uint32_t)s * b_kstep;
-            const uint64_t bdesc = smem_desc(b_addr, b_lbo, 128, kSwizzleNone);
-            const uint32_t accum = (kit > 0 || s > 0) ? 1u : 0u;
-            if constexpr (kSplit) {
-              const uint64_t adesc_lo = (RB == 32) ? smem_desc(a_addr + p.a_bytes, 16, 256, kLayoutA)
-                                                   : smem_desc(a_addr + p.a_bytes, 2048, 128, kLayoutA);
-              const uint64_t bdesc_lo = smem_desc(b_addr + p.b_img_bytes, b_lbo, 128, kSwizzleNone);
-              mma_tf32(d_tmem, adesc_lo, bdesc, idesc, accum);
-              mma_tf32(d_tmem, adesc, bdesc_lo, idesc, 1u);
-              mma_tf32(d_tmem, adesc, bdesc, idesc, 1u);
-            } else if constexpr (PREC == kPrecTf32) {
-              mma_tf32(d_tmem, adesc, bdesc, idesc, accum);
+            const uint32_t first = (kit == 0 && s == 0) ? 1u : 0u;
+            if constexpr (kInt8) {
+              // D_L += A_i * B_j over digit pairs with i + j = L <= 3 (Ozaki levels)
+#pragma unroll
+              for (int L = 0; L < kDigits; ++L) {
+#pragma unroll
+                for (int i = 0; i <= L; ++i) {
+                  const int j = L - i;
+                  const uint64_t adesc = smem_desc(a_addr + (uint32_t)i * p.a_bytes, 2048, 128, kSwizzleNone);
+                  const uint64_t bdesc = smem_desc(b_addr + (uint32_t)j * p.b_img_bytes, b_lbo, 128, kSwizzleNone);
+                  mma_i8(d_tmem + (uint32_t)(L * p.n_tile), adesc, bdesc, idesc, (first && i == 0) ? 0u : 1u);
+                }
+              }
             } else {
-              mma_bf16(d_tmem, adesc, bdesc, idesc, accum);
+              const uint64_t adesc = (RB == 32) ? smem_desc(a_addr, 16, 256, kLayoutA)
+                                                : smem_desc(a_addr, 2048, 128, kLayoutA);
+              const uint64_t bdesc = smem_desc(b_addr, b_lbo, 128, kSwizzleNone);
+              const uint32_t accum = first ? 0u : 1u;
+              if constexpr (kSplit) {
+                const uint64_t adesc_lo = (RB == 32) ? smem_desc(a_addr + p.a_bytes, 16, 256, kLayoutA)
+                                                     : smem_desc(a_addr + p.a_bytes, 2048, 128, kLayoutA);
+                const uint64_t bdesc_lo = smem_desc(b_addr + p.b_img_bytes, b_lbo, 128, kSwizzleNone);
+                mma_tf32(d_tmem, adesc_lo, bdesc, idesc, accum);
+                mma_tf32(d_tmem, adesc, bdesc_lo, idesc, 1u);
+                mma_tf32(d_tmem, adesc, bdesc, idesc, 1u);
+              } else if constexpr (PREC == kPrecTf32) {
+                mma_tf32(d_tmem, adesc, bdesc, idesc, accum);
+              } else {
+                mma_bf16(d_tmem, adesc, bdesc, idesc, accum);
+              }
             }
           }
           mma_commit(&empty[stage]);  // smem slot free once these MMAs retire
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
         mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (++acc == slots) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -187,23 +210,50 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         pres = (p.k == 3) ? ((long long)(oz + cr) * rs + (oy + cr)) * rs + (ox + cr)
                           : (long long)(oy + cr) * rs + (ox + cr);
       }
+      double a_sc = 0.0;
+      if constexpr (kInt8) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * p.n_tile);
-      for (int c0 = 0; c0 < p.n_tile; c0 += 32) {
+      const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)acc * slot_cols;
+      for (int c0 = 0; c0 < p.n_tile; c0 += 16) {
         const int n0 = nt * p.n_tile + c0;
         if (n0 >= p.N) break;
-        uint32_t rr[32];
-        tmem_ld32(taddr + (uint32_t)c0, rr);
-        tmem_ld_wait();
+        float vv[16];
+        if constexpr (kInt8) {
+          uint32_t l0[16], l1[16], l2[16], l3[16];
+          tmem_ld16(taddr + (uint32_t)c0, l0);
+          tmem_ld16(taddr + (uint32_t)(p.n_tile + c0), l1);
+          tmem_ld16(taddr + (uint32_t)(2 * p.n_tile + c0), l2);
+          tmem_ld16(taddr + (uint32_t)(3 * p.n_tile + c0), l3);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            // exact integer levels combined in fp64: L0 + L1 2^-7 + L2 2^-14 + L3 2^-21
+            const double s = (double)(int)l0[c] + (double)(int)l1[c] * (1.0 / 128.0) +
+                             (double)(int)l2[c] * (1.0 / 16384.0) + (double)(int)l3[c] * (1.0 / 2097152.0);
+            const int n = min(n0 + c, p.N - 1);
+            const int co = n / NB, tb = n % NB;
+            const double v = s * a_sc * (double)__ldg(p.w_scale + n) + (double)__ldg(p.bias + tb * p.C_out + co);
+            vv[c] = (float)v;
+          }
+        } else {
+          uint32_t rr[16];
+          tmem_ld16(taddr + (uint32_t)c0, rr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const int n = min(n0 + c, p.N - 1);
+            vv[c] = __uint_as_float(rr[c]) + __ldg(p.bias + (n % NB) * p.C_out + n / NB);
+          }
+        }
         if (valid) {
 #pragma unroll
-          for (int cc = 0; cc < 32 / NB; ++cc) {
+          for (int cc = 0; cc < 16 / NB; ++cc) {
             const int co = n0 / NB + cc;
             if (co < p.C_out) {
               float v[NB];
 #pragma unroll
-              for (int j = 0; j < NB; ++j) v[j] = __uint_as_float(rr[cc * NB + j]) + __ldg(p.bias + j * p.C_out + co);
+              for (int j = 0; j < NB; ++j) v[j] = vv[cc * NB + j];
               if (p.act_mode >= 0) {
                 const float gte = act_gate<NB>(v, p.act_mode, p.act_w + co * NB,
                                                p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K);
@@ -249,7 +299,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == slots) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 8) {
     // ===================== 3xTF32 splitter =====================
@@ -306,13 +356,19 @@ static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const
 cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const ConvKParams& p,
                         int grid, cudaStream_t s) {
   if (plan.nb == 4) {
-    if (plan.prec == kPrecFp32x3) return launch_t<4, kPrecFp32x3>(plan, tmap, p, grid, s);
-    if (plan.prec == kPrecTf32) return launch_t<4, kPrecTf32>(plan, tmap, p, grid, s);
-    return launch_t<4, kPrecBf16>(plan, tmap, p, grid, s);
+    switch (plan.prec) {
+      case kPrecFp32: return launch_t<4, kPrecFp32>(plan, tmap, p, grid, s);
+      case kPrec3xTf32: return launch_t<4, kPrec3xTf32>(plan, tmap, p, grid, s);
+      case kPrecTf32: return launch_t<4, kPrecTf32>(plan, tmap, p, grid, s);
+      default: return launch_t<4, kPrecBf16>(plan, tmap, p, grid, s);
+    }
   }
-  if (plan.prec == kPrecFp32x3) return launch_t<8, kPrecFp32x3>(plan, tmap, p, grid, s);
-  if (plan.prec == kPrecTf32) return launch_t<8, kPrecTf32>(plan, tmap, p, grid, s);
-  return launch_t<8, kPrecBf16>(plan, tmap, p, grid, s);
+  switch (plan.prec) {
+    case kPrecFp32: return launch_t<8, kPrecFp32>(plan, tmap, p, grid, s);
+    case kPrec3xTf32: return launch_t<8, kPrec3xTf32>(plan, tmap, p, grid, s);
+    case kPrecTf32: return launch_t<8, kPrecTf32>(plan, tmap, p, grid, s);
+    default: return launch_t<8, kPrecBf16>(plan, tmap, p, grid, s);
+  }
 }
 
 // fp32 protocol (B, C, P, NB) -> bf16 A-ready layout (B, G, P, 8):

@@ -11,7 +11,8 @@
 //  * the tensor-core operand images used by conv_tc.cu, built ONCE per layer
 //    at create time: per (N-tile, K-iteration) a contiguous block of K-major
 //    SWIZZLE_NONE UMMA core matrices [image][k-step][2 x 16 B chunks][n_tile
-//    rows][16 B], images = {hi, lo} for 3xTF32, {tf32} or {bf16}.
+//    rows][16 B], images = {hi, lo} for 3xTF32, {tf32}, {bf16} or the four
+//    int8 digits of the fp32-accurate mode (per-column power-of-two scale).
 #include "common.cuh"
 #include "internal.h"
 
@@ -56,7 +57,7 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 // One thread per (n_tile, k_iter, k_local, row); writes every image.
 __global__ void expand_img_kernel(Sig sg, const float* __restrict__ f, int C_in, int C_out,
-                                  ConvPlan pl, uint8_t* __restrict__ img) {
+                                  ConvPlan pl, const float* __restrict__ w_scale, uint8_t* __restrict__ img) {
   const int nb = pl.nb;
   const int k_stage = pl.ks * 32 / pl.esize;  // K elements per stage
   const long long total = (long long)pl.n_ntiles * pl.k_iters * k_stage * pl.n_tile;
@@ -79,7 +80,12 @@ __global__ void expand_img_kernel(Sig sg, const float* __restrict__ f, int C_in,
     uint8_t* base = img + ((size_t)nt * pl.k_iters + kit) * pl.b_bytes;
     const size_t off = (size_t)s * pl.n_tile * 32 + (size_t)h * pl.n_tile * 16 + (size_t)row * 16 +
                        (size_t)e * pl.esize;
-    if (pl.prec == kPrecFp32x3) {
+    if (pl.prec == kPrecFp32) {
+      int8_t d[4];
+      digits4(w / __ldg(w_scale + n), d);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) *reinterpret_cast<int8_t*>(base + (size_t)k * pl.b_img_bytes + off) = d[k];
+    } else if (pl.prec == kPrec3xTf32) {
       const float hi = __uint_as_float(__float_as_uint(w) & 0xFFFFE000u);
       *reinterpret_cast<float*>(base + off) = hi;
       *reinterpret_cast<float*>(base + pl.b_img_bytes + off) = w - hi;
@@ -110,12 +116,12 @@ cudaError_t launch_expand_ref(const int* g, int k, const float* f, int C_in, int
 }
 
 cudaError_t launch_expand_images(const int* g, const ConvPlan& pl, const float* f, int C_in,
-                                 int C_out, uint8_t* img, cudaStream_t s) {
+                                 int C_out, const float* w_scale, uint8_t* img, cudaStream_t s) {
   Sig sg{{0, 0, 0}, pl.k};
   for (int i = 0; i < pl.k; ++i) sg.g[i] = g[i];
   const long long total =
       (long long)pl.n_ntiles * pl.k_iters * (pl.ks * 32 / pl.esize) * pl.n_tile;
-  expand_img_kernel<<<grid_for(total), 256, 0, s>>>(sg, f, C_in, C_out, pl, img);
+  expand_img_kernel<<<grid_for(total), 256, 0, s>>>(sg, f, C_in, C_out, pl, w_scale, img);
   count_launch();
   return cudaGetLastError();
 }

@@ -9,7 +9,13 @@
 
 namespace cl {
 
-enum Prec : int { kPrecFp32x3 = 0, kPrecTf32 = 1, kPrecBf16 = 2 };
+// Arithmetic modes (values = the C-ABI cl_precision codes):
+//   kPrecFp32    int8 digit slices (Ozaki scheme), exact s32 TMEM accumulation
+//   kPrecTf32    one TF32 pass
+//   kPrecBf16    BF16 operands
+//   kPrec3xTf32  3xTF32 split (hi/lo), fp32 TMEM accumulation
+enum Prec : int { kPrecFp32 = 0, kPrecTf32 = 1, kPrecBf16 = 2, kPrec3xTf32 = 3 };
+constexpr int kDigits = 4;  // int8 digits per operand in kPrecFp32
 
 constexpr int kTileM = 128;          // output pixels per tile (= TMEM lanes)
 constexpr int kConvThreads = 384;    // 12 warps, see conv_tc.cu
@@ -34,7 +40,11 @@ struct ConvPlan {
   int N, n_tile, n_ntiles;
   int tx, ty, tz;       // output tile extents (tx*ty*tz == 128)
   uint32_t a_bytes, b_img_bytes, b_bytes, stage_bytes;
-  int n_img;            // B images per stage (2 for 3xTF32 hi/lo)
+  int n_img;            // B images per stage (2 for 3xTF32 hi/lo, 4 int8 digits)
+  int n_a;              // A tiles per stage (2 for 3xTF32 hi/lo, 4 int8 digits)
+  int n_tma_a;          // A tensor loads per stage (4 for int8 digits, else 1)
+  int levels;           // TMEM accumulators per tile (4 digit levels for kPrecFp32)
+  int acc_slots;        // accumulator buffers (2 = epilogue overlaps next tile's MMA)
   int stages;
   uint32_t tmem_cols;
   size_t smem_bytes;
@@ -48,8 +58,10 @@ struct ConvKParams {
   long long num_tiles;
   int d_filter, n_gs, gs, G, merged_bc, k_iters, ks;
   uint32_t a_bytes, b_bytes, b_img_bytes, stage_bytes, tmem_cols;
-  int stages;
+  int stages, n_a, n_tma_a, levels, acc_slots;
   const uint8_t* b_img;
+  const float* a_scale;       // kPrecFp32: per-sample power-of-two scale of the A digits
+  const float* w_scale;       // kPrecFp32: per-column power-of-two scale of the B digits
   const float* bias;          // (NB, C_out)
   float* y;                   // fp32 protocol output (or null)
   __nv_bfloat16* y_bf16;      // bf16 A-ready output (or null)
@@ -81,10 +93,17 @@ cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const Con
 cudaError_t launch_expand_ref(const int* g, int k, const float* f, int C_in, int C_out, int Q,
                               float* out, cudaStream_t s);
 cudaError_t launch_expand_images(const int* g, const ConvPlan& plan, const float* f, int C_in,
-                                 int C_out, uint8_t* img, cudaStream_t s);
+                                 int C_out, const float* w_scale, uint8_t* img, cudaStream_t s);
 cudaError_t launch_pack_bf16(const float* x, __nv_bfloat16* out, int nb, long long B, int C,
                              long long P, int G, int pairs, cudaStream_t s);
 cudaError_t launch_act(int nb, const ActParams& p, cudaStream_t s);
+// kPrecFp32 operand preparation (slice.cu)
+cudaError_t launch_sample_absmax(const float* x, long long B, long long per_sample, unsigned* amax,
+                                 cudaStream_t s);
+cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* digits, float* scale,
+                               int nb, long long B, int C, long long P, int G, cudaStream_t s);
+cudaError_t launch_weight_colscale(const int* g, const ConvPlan& pl, const float* f, int C_in, int C_out,
+                                   float* w_scale, cudaStream_t s);
 
 int num_sms();
 void count_launch(int n = 1);

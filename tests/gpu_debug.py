@@ -45,6 +45,8 @@ def main():
         ok = np.array_equal(W, O.expanded_kernel(f, g))
         print("expand", g, "bit-exact" if ok else "MISMATCH")
     cases = [
+        ((1, 1), 2, 4, 4, 8, 3, "3xtf32"),
+        ((1, 1, 1), 2, 32, 32, 16, 3, "3xtf32"),
         ((1, 1), 2, 4, 4, 8, 3, "fp32"),
         ((1, 1), 2, 4, 4, 8, 3, "tf32"),
         ((1, 1), 2, 4, 4, 8, 3, "bf16"),
