@@ -233,7 +233,7 @@ def run_ours(args):
                                  act_weight=aw, act_bias=ab, padding=spec.padding, residual=True,
                                  precision=prec)
         blk.handle()
-        run = lambda xx: M.block_forward(xx, blk)  # noqa: E731
+        run = lambda xx, out=None: M.block_forward(xx, blk, out=out)  # noqa: E731
         flops_per_sample = blk.flops() / nloc
         conv_layer = blk.conv2
     elif spec.kind == "conv":
@@ -242,17 +242,18 @@ def run_ours(args):
         layer = M.make_conv_layer(M.Dims(nloc, spec.C, spec.C, spec.d, spec.d_filter, spec.k), sig, f, b,
                                   precision=prec, padding=spec.padding)
         layer.handle()
-        run = lambda xx: M.conv_forward(xx, layer)  # noqa: E731
+        run = lambda xx, out=None: M.conv_forward(xx, layer, out=out)  # noqa: E731
         flops_per_sample = M.conv_flops(layer.dims, layer) / nloc
         conv_layer = layer
     else:
         raise SystemExit("activation config: use --config 1..5 with kind conv/block")
 
     x = W.make_input(spec, lo, nloc, device=dev)
+    y = run(x)
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        y = run(x)
+        y = run(x, out=y)
     torch.cuda.synchronize()
     barrier(world)
 
@@ -264,7 +265,7 @@ def run_ours(args):
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
         for _ in range(args.steps):
-            y = run(x)
+            y = run(x, out=y)
         ev1.record()
         torch.cuda.synchronize()
         barrier(world)
@@ -297,12 +298,13 @@ def run_ours(args):
     if not args.no_e2e:
         xh = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
         xh.copy_(x)
-        run(xh)  # warm (allocates the pinned output of the host path)
+        yh = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
+        run(xh, out=yh)  # warm: host-pipeline streams / staging buffers
         barrier(world)
         t0 = time.perf_counter()
         ne = max(1, args.e2e_steps)
         for _ in range(ne):
-            yh = run(xh)
+            run(xh, out=yh)
             s = float(yh.view(-1)[0])  # host read of the result
         t_e2e = (time.perf_counter() - t0) / ne
         t_e2e = max_over_ranks(t_e2e, world)
@@ -310,7 +312,7 @@ def run_ours(args):
                "h2d_bytes_per_step": int(x.numel() * 4) * world,
                "d2h_bytes_per_step": int(y.numel() * 4) * world,
                "path": "block_forward(pinned host tensor) -> cl_block_forward_host (chunked H2D/compute/D2H over 2 streams)"}
-        del xh
+        del xh, yh
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -95,6 +95,12 @@ int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, in
 int cl_conv_out_side(const cl_conv* h, int* d_out);
 /* x_dev (B, C_in, d_image^k, N_B) -> y_dev (B, C_out, d_out^k, N_B) */
 int cl_conv_forward(const cl_conv* h, const float* x_dev, float* y_dev, int64_t B, void* stream);
+/* explicit-workspace variant: ws (device) of >= cl_conv_workspace_bytes(h, B) bytes
+ * (int8 digit planes of the input in fp32 mode, packed bf16 input in bf16 mode).
+ * cl_conv_forward uses a per-(handle, stream) cached workspace instead. */
+size_t cl_conv_workspace_bytes(const cl_conv* h, int64_t B);
+int cl_conv_forward_ws(const cl_conv* h, const float* x_dev, float* y_dev, int64_t B, void* ws,
+                       size_t ws_bytes, void* stream);
 /* host (pinned or pageable) buffers; copies in/out inside the call, chunked over the batch */
 int cl_conv_forward_host(const cl_conv* h, const float* x_host, float* y_host, int64_t B,
                          void* stream);
@@ -116,6 +122,9 @@ void cl_act_destroy(cl_act* h);
 int cl_block_create(const cl_conv* conv1, const cl_act* act, const cl_conv* conv2, int residual,
                     cl_block** out);
 int cl_block_forward(const cl_block* h, const float* x_dev, float* y_dev, int64_t B, void* stream);
+size_t cl_block_workspace_bytes(const cl_block* h, int64_t B);
+int cl_block_forward_ws(const cl_block* h, const float* x_dev, float* y_dev, int64_t B, void* ws,
+                        size_t ws_bytes, void* stream);
 /* host buffers, streamed through the GPU in chunks of `chunk` samples
  * (0 = automatic) with copy/compute overlap */
 int cl_block_forward_host(const cl_block* h, const float* x_host, float* y_host, int64_t B,

@@ -19,6 +19,7 @@ import numpy as np
 
 from . import _device, _lib
 from .algebra import Signature
+from .conv import _out
 from .errors import IndexOutOfRange, ModeConfigMismatch, ShapeMismatch
 
 VARIANTS = ("b200", "reference", "hoisted", "packed", "specialized")
@@ -107,7 +108,7 @@ def _dims(x, cfg: ActivationConfig):
     return B, C_, P
 
 
-def activation_forward(x, cfg: ActivationConfig, variant: str = "b200"):
+def activation_forward(x, cfg: ActivationConfig, variant: str = "b200", out=None):
     """Gated scaling of every multivector (activation.py:400-416 semantics)."""
     if variant not in VARIANTS:
         raise ValueError(f"unknown activation variant {variant!r}")
@@ -117,19 +118,19 @@ def activation_forward(x, cfg: ActivationConfig, variant: str = "b200"):
         torch = _device.torch_mod()
         with torch.cuda.device(x.device):
             xc = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
-            y = torch.empty_like(xc)
+            y = _out(out, tuple(xc.shape), x.device)
             _lib.check(lib.cl_act_forward(C.c_void_p(cfg.handle(C_)), C.c_void_p(xc.data_ptr()),
                                           C.c_void_p(y.data_ptr()), B, P, C.c_void_p(_device.stream_ptr())))
         return y
     if _device.is_cpu_tensor(x):
         torch = _device.torch_mod()
         xc = x.float().contiguous()
-        y = torch.empty(xc.shape, dtype=torch.float32, pin_memory=xc.is_pinned())
+        y = _out(out, tuple(xc.shape), None, pinned=xc.is_pinned())
         _lib.check(lib.cl_act_forward_host(C.c_void_p(cfg.handle(C_)), C.c_void_p(xc.data_ptr()),
                                            C.c_void_p(y.data_ptr()), B, P, C.c_void_p(_device.stream_ptr())))
         return y
     xa = np.ascontiguousarray(x, dtype=np.float32)
-    y = np.empty_like(xa)
+    y = out if out is not None else np.empty_like(xa)
     _lib.check(lib.cl_act_forward_host(C.c_void_p(cfg.handle(C_)), C.c_void_p(xa.ctypes.data),
                                        C.c_void_p(y.ctypes.data), B, P, C.c_void_p(_device.stream_ptr())))
     return y

@@ -17,7 +17,7 @@ import numpy as np
 from . import _device, _lib
 from .activation import ActivationConfig, AggMode, make_activation_config
 from .algebra import Signature
-from .conv import ConvLayer, conv_flops, make_conv_layer
+from .conv import ConvLayer, _out, conv_flops, make_conv_layer
 from .errors import ShapeMismatch
 from .layout import Dims
 
@@ -82,7 +82,7 @@ def make_basic_block(sig: Signature, B: int, C_in: int, C_mid: int, C_out: int, 
     return BasicBlock(conv1, act, conv2, residual)
 
 
-def block_forward(x, blk: BasicBlock, chunk: int = 0):
+def block_forward(x, blk: BasicBlock, chunk: int = 0, out=None):
     """y = conv2(act(conv1(x))) [+ x] (block.ts:134-148 + residual)."""
     if tuple(x.shape) != blk.input_shape():
         raise ShapeMismatch(f"input shape {tuple(x.shape)}, expected {blk.input_shape()}")
@@ -92,19 +92,19 @@ def block_forward(x, blk: BasicBlock, chunk: int = 0):
         torch = _device.torch_mod()
         with torch.cuda.device(x.device):
             xc = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
-            y = torch.empty(blk.output_shape(), device=x.device, dtype=torch.float32)
+            y = _out(out, blk.output_shape(), x.device)
             _lib.check(lib.cl_block_forward(C.c_void_p(blk.handle()), C.c_void_p(xc.data_ptr()),
                                             C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
         return y
     if _device.is_cpu_tensor(x):
         torch = _device.torch_mod()
         xc = x.float().contiguous()
-        y = torch.empty(blk.output_shape(), dtype=torch.float32, pin_memory=xc.is_pinned())
+        y = _out(out, blk.output_shape(), None, pinned=xc.is_pinned())
         _lib.check(lib.cl_block_forward_host(C.c_void_p(blk.handle()), C.c_void_p(xc.data_ptr()),
                                              C.c_void_p(y.data_ptr()), B, chunk, C.c_void_p(_device.stream_ptr())))
         return y
     xa = np.ascontiguousarray(x, dtype=np.float32)
-    y = np.empty(blk.output_shape(), dtype=np.float32)
+    y = out if out is not None else np.empty(blk.output_shape(), dtype=np.float32)
     _lib.check(lib.cl_block_forward_host(C.c_void_p(blk.handle()), C.c_void_p(xa.ctypes.data),
                                          C.c_void_p(y.ctypes.data), B, chunk, C.c_void_p(_device.stream_ptr())))
     return y

@@ -99,14 +99,31 @@ def make_conv_layer(dims: Dims, sig: Signature, filters, bias, W: int | None = N
     return ConvLayer(dims, sig, _device.frozen_f32(f), _device.frozen_f32(b), precision, padding, W, U)
 
 
+def _out(out, shape, device, pinned=False):
+    """Validate a caller-provided output tensor or allocate one."""
+    torch = _device.torch_mod()
+    if out is None:
+        if device is None:
+            return torch.empty(shape, dtype=torch.float32, pin_memory=pinned)
+        return torch.empty(shape, device=device, dtype=torch.float32)
+    if tuple(out.shape) != tuple(shape) or out.dtype != torch.float32 or not out.is_contiguous():
+        raise ShapeMismatch(f"out has shape {tuple(out.shape)}, expected contiguous float32 {tuple(shape)}")
+    if (device is None) == out.is_cuda:
+        raise ShapeMismatch("out must live on the same side (host/device) as the input")
+    return out
+
+
 def _check_input(x, layer: ConvLayer):
     shape = tuple(x.shape)
     if shape != layer.dims.input_shape():
         raise ShapeMismatch(f"input shape {shape}, expected {layer.dims.input_shape()}")
 
 
-def conv_forward(x, layer: ConvLayer, variant: str = "b200"):
-    """Protocol-to-protocol forward pass (conv.py:371-381) on the B200."""
+def conv_forward(x, layer: ConvLayer, variant: str = "b200", out=None):
+    """Protocol-to-protocol forward pass (conv.py:371-381) on the B200.
+
+    `out` (optional) receives the result (a CUDA tensor for CUDA input, a
+    CPU tensor / numpy array for host input)."""
     if variant not in VARIANTS:
         raise ValueError(f"unknown conv variant {variant!r}")
     _check_input(x, layer)
@@ -116,19 +133,19 @@ def conv_forward(x, layer: ConvLayer, variant: str = "b200"):
         torch = _device.torch_mod()
         with torch.cuda.device(x.device):
             xc = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
-            y = torch.empty(layer.output_shape(B), device=x.device, dtype=torch.float32)
+            y = _out(out, layer.output_shape(B), x.device)
             _lib.check(lib.cl_conv_forward(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
                                            C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
         return y
     if _device.is_cpu_tensor(x):
         torch = _device.torch_mod()
         xc = x.float().contiguous()
-        y = torch.empty(layer.output_shape(B), dtype=torch.float32, pin_memory=xc.is_pinned())
+        y = _out(out, layer.output_shape(B), None, pinned=xc.is_pinned())
         _lib.check(lib.cl_conv_forward_host(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
                                             C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
         return y
     xa = np.ascontiguousarray(x, dtype=np.float32)
-    y = np.empty(layer.output_shape(B), dtype=np.float32)
+    y = out if out is not None else np.empty(layer.output_shape(B), dtype=np.float32)
     _lib.check(lib.cl_conv_forward_host(C.c_void_p(layer.handle()), C.c_void_p(xa.ctypes.data),
                                         C.c_void_p(y.ctypes.data), B, C.c_void_p(_device.stream_ptr())))
     return y

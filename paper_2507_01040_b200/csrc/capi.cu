@@ -190,6 +190,67 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
 using namespace cl;
 
 // ---------------------------------------------------------------------------
+// workspaces: per-(handle, stream) device buffers, grown on demand and reused
+// across calls (stream order makes reuse on one stream safe; different
+// streams get different buffers, so concurrent forwards stay independent).
+// ---------------------------------------------------------------------------
+namespace cl {
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct WsCache {
+  std::mutex m;
+  struct Ent {
+    cudaStream_t s;
+    void* p;
+    size_t n;
+  };
+  std::vector<Ent> v;
+  int get(cudaStream_t s, size_t n, void** out) {
+    std::lock_guard<std::mutex> lk(m);
+    *out = nullptr;
+    if (n == 0) return CL_OK;
+    for (auto& e : v) {
+      if (e.s != s) continue;
+      if (e.n >= n) { *out = e.p; return CL_OK; }
+      cudaError_t er = cudaStreamSynchronize(s);  // old buffer may still be in use on s
+      if (er != cudaSuccess) return cuda_fail(er, "workspace grow");
+      cudaFree(e.p);
+      e.p = nullptr;
+      e.n = 0;
+      er = cudaMalloc(&e.p, n);
+      if (er != cudaSuccess) return cuda_fail(er, "workspace alloc");
+      e.n = n;
+      *out = e.p;
+      return CL_OK;
+    }
+    void* p = nullptr;
+    cudaError_t er = cudaMalloc(&p, n);
+    if (er != cudaSuccess) return cuda_fail(er, "workspace alloc");
+    v.push_back({s, p, n});
+    *out = p;
+    return CL_OK;
+  }
+  ~WsCache() {
+    for (auto& e : v) cudaFree(e.p);
+  }
+};
+
+// Host-buffer pipeline state of one handle: two streams and their staging
+// buffers + workspaces, reused across calls (host calls on one handle are
+// serialised by the mutex; they are synchronous anyway).
+struct HostPipe {
+  std::mutex m;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  WsCache stage[2];
+  WsCache ws[2];
+  ~HostPipe() {
+    for (auto& x : st)
+      if (x) cudaStreamDestroy(x);
+  }
+};
+}  // namespace cl
+
+// ---------------------------------------------------------------------------
 // handles
 // ---------------------------------------------------------------------------
 struct cl_conv {
@@ -200,6 +261,8 @@ struct cl_conv {
   uint8_t* img = nullptr;    // tensor-core operand images
   float* w_scale = nullptr;  // kPrecFp32: per-column digit scales
   ConvPlan plan;
+  mutable WsCache ws;
+  mutable HostPipe host;
 };
 
 struct cl_act {
@@ -207,6 +270,7 @@ struct cl_act {
   int ki[8];
   float* w = nullptr;  // (C, NB) blade-keyed weights (Linear) or 0/1 mask
   float* b = nullptr;  // (C) bias (zeros unless Linear)
+  mutable HostPipe host;
 };
 
 struct cl_block {
@@ -215,6 +279,8 @@ struct cl_block {
   const cl_conv* c2;
   int residual;
   int res_crop;
+  mutable WsCache ws;
+  mutable HostPipe host;
 };
 
 extern "C" {
@@ -400,20 +466,29 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
   return CL_OK;
 }
 
+// Workspace bytes of one conv launch: int8 digit planes + per-sample
+// amax/scale (fp32 mode) or the packed bf16 input (bf16 mode).
+static size_t conv_ws_bytes(const cl_conv* h, long long B, bool prepacked) {
+  const ConvPlan& pl = h->plan;
+  const size_t P_in = (size_t)ipow(h->d_image, h->k);
+  if (pl.prec == kPrecFp32) return align_up((size_t)kDigits * B * pl.G * P_in * 16, 256) + align_up((size_t)B * 8, 256);
+  if (pl.prec == kPrecBf16 && !prepacked) return align_up((size_t)B * pl.G * P_in * 16, 256);
+  return 0;
+}
+
 // Run one conv on device buffers. `xbf` (optional) is an already packed bf16
-// A-ready input (bf16 layers); otherwise x is packed here when needed.
+// A-ready input (bf16 layers); otherwise x is sliced / packed here into `ws`
+// (conv_ws_bytes(h, B, xbf != nullptr) bytes).
 static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, float* y, long long B,
-                    const Epi& epi, cudaStream_t s) {
+                    const Epi& epi, void* ws, cudaStream_t s) {
   const ConvPlan& pl = h->plan;
   if (B == 0) return CL_OK;
   const long long P_in = (long long)ipow(h->d_image, h->k);
-  __nv_bfloat16* packed = nullptr;
-  int8_t* digits = nullptr;
   float* a_scale = nullptr;
   const void* src = x;
   if (pl.prec == kPrecFp32) {
-    const size_t bytes = (size_t)kDigits * B * pl.G * P_in * 16;
-    CL_CUDA(cudaMallocAsync((void**)&digits, bytes + (size_t)B * 8 + 64, s), "conv digit alloc");
+    const size_t bytes = align_up((size_t)kDigits * B * pl.G * P_in * 16, 256);
+    int8_t* digits = reinterpret_cast<int8_t*>(ws);
     unsigned* amax = reinterpret_cast<unsigned*>(digits + bytes);
     a_scale = reinterpret_cast<float*>(digits + bytes + (size_t)B * 4);
     const long long per_sample = (long long)h->C_in * P_in * h->nb;
@@ -424,18 +499,13 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
     if (xbf) {
       src = xbf;
     } else {
-      const size_t bytes = (size_t)B * pl.G * P_in * 16;
-      CL_CUDA(cudaMallocAsync((void**)&packed, bytes, s), "conv bf16 pack alloc");
+      __nv_bfloat16* packed = reinterpret_cast<__nv_bfloat16*>(ws);
       CL_CUDA(launch_pack_bf16(x, packed, h->nb, B, h->C_in, P_in, pl.G, h->nb == 4, s), "pack_bf16");
       src = packed;
     }
   }
   CUtensorMap map;
-  if (int st = encode_input_map(h, src, B, &map)) {
-    if (packed) cudaFreeAsync(packed, s);
-    if (digits) cudaFreeAsync(digits, s);
-    return st;
-  }
+  if (int st = encode_input_map(h, src, B, &map)) return st;
   ConvKParams p{};
   p.B = (int)B;
   p.k = h->k;
@@ -488,61 +558,55 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.act_K = epi.act ? (float)epi.act->K : 1.f;
   const int grid = (int)std::min<long long>(p.num_tiles, (long long)num_sms());
   cudaError_t e = launch_conv(pl, map, p, grid, s);
-  if (packed) cudaFreeAsync(packed, s);
-  if (digits) cudaFreeAsync(digits, s);
   if (e != cudaSuccess) return cuda_fail(e, "conv_tc launch");
   return CL_OK;
 }
 
 // Generic host-buffer runner: the batch is streamed through the device in
 // chunks on two streams, so chunk i+1's H2D copy overlaps chunk i's compute
-// and chunk i-1's D2H copy (copy engines and SMs work concurrently).
-template <class F>
-static int host_chunked(long long B, size_t in_per, size_t out_per, long long chunk, const float* xh,
-                        float* yh, cudaStream_t user, F&& fwd) {
+// and chunk i-1's D2H copy (copy engines and SMs work concurrently). Streams,
+// staging buffers and workspaces persist in the handle's HostPipe.
+template <class WsFn, class F>
+static int host_chunked(HostPipe& hp, long long B, size_t in_per, size_t out_per, long long chunk,
+                        const float* xh, float* yh, cudaStream_t user, WsFn&& ws_bytes, F&& fwd) {
   if (B == 0) return CL_OK;
+  std::lock_guard<std::mutex> lk(hp.m);
   if (chunk <= 0) {
-    const size_t target = (size_t)256 << 20;  // ~256 MB of input per chunk
+    const size_t target = (size_t)512 << 20;  // ~512 MB of input per chunk
     chunk = std::max<long long>(1, (long long)(target / std::max<size_t>(in_per, 1)));
     chunk = std::min<long long>(chunk, std::max<long long>(1, (B + 1) / 2));
   }
   chunk = std::min(chunk, B);
-  cudaStream_t st[2];
-  CL_CUDA(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking), "stream create");
-  CL_CUDA(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking), "stream create");
+  for (int i = 0; i < 2; ++i)
+    if (!hp.st[i]) CL_CUDA(cudaStreamCreateWithFlags(&hp.st[i], cudaStreamNonBlocking), "stream create");
   cudaEvent_t start;
   CL_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming), "event");
   CL_CUDA(cudaEventRecord(start, user), "event record");
-  float* dx[2] = {nullptr, nullptr};
-  float* dy[2] = {nullptr, nullptr};
+  void* stg[2];
+  void* wsp[2];
   int rc = CL_OK;
   for (int i = 0; i < 2 && rc == CL_OK; ++i) {
-    cudaStreamWaitEvent(st[i], start, 0);
-    if (cudaMallocAsync((void**)&dx[i], in_per * chunk, st[i]) != cudaSuccess ||
-        cudaMallocAsync((void**)&dy[i], out_per * chunk, st[i]) != cudaSuccess)
-      rc = fail(CL_ERR_CUDA, "CudaError", "host path staging alloc failed");
+    cudaStreamWaitEvent(hp.st[i], start, 0);
+    rc = hp.stage[i].get(hp.st[i], align_up(in_per * chunk, 256) + out_per * chunk, &stg[i]);
+    if (rc == CL_OK) rc = hp.ws[i].get(hp.st[i], ws_bytes(chunk), &wsp[i]);
   }
   int it = 0;
   for (long long b0 = 0; b0 < B && rc == CL_OK; b0 += chunk, ++it) {
     const long long nb = std::min(chunk, B - b0);
     const int i = it & 1;
-    cudaError_t e = cudaMemcpyAsync(dx[i], reinterpret_cast<const char*>(xh) + (size_t)b0 * in_per,
-                                    (size_t)nb * in_per, cudaMemcpyHostToDevice, st[i]);
+    float* dx = reinterpret_cast<float*>(stg[i]);
+    float* dy = reinterpret_cast<float*>(reinterpret_cast<char*>(stg[i]) + align_up(in_per * chunk, 256));
+    cudaError_t e = cudaMemcpyAsync(dx, reinterpret_cast<const char*>(xh) + (size_t)b0 * in_per,
+                                    (size_t)nb * in_per, cudaMemcpyHostToDevice, hp.st[i]);
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D"); break; }
-    rc = fwd(dx[i], dy[i], nb, st[i]);
+    rc = fwd(dx, dy, nb, wsp[i], hp.st[i]);
     if (rc != CL_OK) break;
-    e = cudaMemcpyAsync(reinterpret_cast<char*>(yh) + (size_t)b0 * out_per, dy[i], (size_t)nb * out_per,
-                        cudaMemcpyDeviceToHost, st[i]);
+    e = cudaMemcpyAsync(reinterpret_cast<char*>(yh) + (size_t)b0 * out_per, dy, (size_t)nb * out_per,
+                        cudaMemcpyDeviceToHost, hp.st[i]);
     if (e != cudaSuccess) { rc = cuda_fail(e, "D2H"); break; }
   }
-  for (int i = 0; i < 2; ++i) {
-    if (dx[i]) cudaFreeAsync(dx[i], st[i]);
-    if (dy[i]) cudaFreeAsync(dy[i], st[i]);
-  }
-  cudaError_t e0 = cudaStreamSynchronize(st[0]);
-  cudaError_t e1 = cudaStreamSynchronize(st[1]);
-  cudaStreamDestroy(st[0]);
-  cudaStreamDestroy(st[1]);
+  cudaError_t e0 = cudaStreamSynchronize(hp.st[0]);
+  cudaError_t e1 = cudaStreamSynchronize(hp.st[1]);
   cudaEventDestroy(start);
   if (rc == CL_OK && e0 != cudaSuccess) rc = cuda_fail(e0, "host path");
   if (rc == CL_OK && e1 != cudaSuccess) rc = cuda_fail(e1, "host path");
@@ -553,20 +617,35 @@ static int host_chunked(long long B, size_t in_per, size_t out_per, long long ch
 
 extern "C" {
 
+size_t cl_conv_workspace_bytes(const cl_conv* h, int64_t B) { return h ? conv_ws_bytes(h, B, false) : 0; }
+
+int cl_conv_forward_ws(const cl_conv* h, const float* x, float* y, int64_t B, void* ws, size_t ws_bytes,
+                       void* stream) {
+  if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null conv handle");
+  if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
+  if (ws_bytes < conv_ws_bytes(h, B, false))
+    return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "workspace too small");
+  return conv_run(h, x, nullptr, y, B, Epi{}, ws, (cudaStream_t)stream);
+}
+
 int cl_conv_forward(const cl_conv* h, const float* x, float* y, int64_t B, void* stream) {
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null conv handle");
   if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
-  return conv_run(h, x, nullptr, y, B, Epi{}, (cudaStream_t)stream);
+  void* ws = nullptr;
+  if (int rc = h->ws.get((cudaStream_t)stream, conv_ws_bytes(h, B, false), &ws)) return rc;
+  return conv_run(h, x, nullptr, y, B, Epi{}, ws, (cudaStream_t)stream);
 }
 
 int cl_conv_forward_host(const cl_conv* h, const float* xh, float* yh, int64_t B, void* stream) {
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null conv handle");
   const size_t in_per = (size_t)h->C_in * ipow(h->d_image, h->k) * h->nb * 4;
   const size_t out_per = (size_t)h->C_out * ipow(h->d_out, h->k) * h->nb * 4;
-  return host_chunked(B, in_per, out_per, 0, xh, yh, (cudaStream_t)stream,
-                      [&](const float* dx, float* dy, long long nb, cudaStream_t s) {
-                        return conv_run(h, dx, nullptr, dy, nb, Epi{}, s);
-                      });
+  return host_chunked(
+      h->host, B, in_per, out_per, 0, xh, yh, (cudaStream_t)stream,
+      [&](long long nb) { return conv_ws_bytes(h, nb, false); },
+      [&](const float* dx, float* dy, long long nb, void* ws, cudaStream_t s) {
+        return conv_run(h, dx, nullptr, dy, nb, Epi{}, ws, s);
+      });
 }
 
 // ---- activation -------------------------------------------------------------
@@ -646,10 +725,11 @@ int cl_act_forward(const cl_act* h, const float* x, float* y, int64_t B, int64_t
 int cl_act_forward_host(const cl_act* h, const float* xh, float* yh, int64_t B, int64_t P, void* stream) {
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null activation handle");
   const size_t per = (size_t)h->C * P * h->nb * 4;
-  return host_chunked(B, per, per, 0, xh, yh, (cudaStream_t)stream,
-                      [&](const float* dx, float* dy, long long nb, cudaStream_t s) {
-                        return cl_act_forward(h, dx, dy, nb, P, s);
-                      });
+  return host_chunked(
+      h->host, B, per, per, 0, xh, yh, (cudaStream_t)stream, [](long long) { return (size_t)0; },
+      [&](const float* dx, float* dy, long long nb, void*, cudaStream_t s) {
+        return cl_act_forward(h, dx, dy, nb, P, s);
+      });
 }
 
 void cl_act_destroy(cl_act* h) {
@@ -691,64 +771,81 @@ int cl_block_create(const cl_conv* c1, const cl_act* act, const cl_conv* c2, int
 }  // extern "C"
 
 namespace cl {
-static int block_run(const cl_block* h, const float* x, float* y, long long B, cudaStream_t s) {
+// block workspace: [mid activation | conv workspace (max of both convs)]
+static size_t block_mid_bytes(const cl_block* h, long long B) {
+  const cl_conv* c1 = h->c1;
+  const cl_conv* c2 = h->c2;
+  const size_t P1 = (size_t)ipow(c1->d_out, c1->k);
+  if (c1->prec == kPrecBf16) return align_up((size_t)B * c2->plan.G * P1 * 16, 256);
+  return align_up((size_t)B * c1->C_out * P1 * c1->nb * 4, 256);
+}
+static size_t block_ws_bytes(const cl_block* h, long long B) {
+  const bool bf = h->c1->prec == kPrecBf16;
+  return block_mid_bytes(h, B) + std::max(conv_ws_bytes(h->c1, B, false), conv_ws_bytes(h->c2, B, bf));
+}
+
+static int block_run(const cl_block* h, const float* x, float* y, long long B, void* ws, cudaStream_t s) {
   const cl_conv* c1 = h->c1;
   const cl_conv* c2 = h->c2;
   if (B == 0) return CL_OK;
-  const long long P1 = (long long)ipow(c1->d_out, c1->k);
+  const size_t mid_bytes = block_mid_bytes(h, B);
+  void* mid = ws;
+  void* cws = reinterpret_cast<char*>(ws) + mid_bytes;
   Epi e1;
   e1.act = h->act;
-  void* mid = nullptr;
-  int rc = CL_OK;
+  Epi e2;
+  if (h->residual) {
+    e2.resid = x;
+    e2.res_side = c1->d_image;
+    e2.res_crop = h->res_crop;
+  }
   if (c1->prec == kPrecBf16) {
     // conv1's epilogue writes conv2's packed bf16 operand directly
-    const int G2 = c2->plan.G;
-    const size_t bytes = (size_t)B * G2 * P1 * 16;
-    CL_CUDA(cudaMallocAsync(&mid, bytes, s), "block mid alloc");
     const bool pairs = c2->nb == 4;
     const int real_groups = pairs ? (c2->C_in + 1) / 2 : c2->C_in;
-    if (G2 != real_groups || (pairs && (c2->C_in & 1)))
-      CL_CUDA(cudaMemsetAsync(mid, 0, bytes, s), "block mid memset");
+    if (c2->plan.G != real_groups || (pairs && (c2->C_in & 1)))
+      CL_CUDA(cudaMemsetAsync(mid, 0, mid_bytes, s), "block mid memset");
     e1.y_bf16 = (__nv_bfloat16*)mid;
-    e1.ybf_groups = G2;
+    e1.ybf_groups = c2->plan.G;
     e1.ybf_pairs = pairs ? 1 : 0;
-    rc = conv_run(c1, x, nullptr, nullptr, B, e1, s);
-    if (rc == CL_OK) {
-      Epi e2;
-      if (h->residual) { e2.resid = x; e2.res_side = c1->d_image; e2.res_crop = h->res_crop; }
-      rc = conv_run(c2, nullptr, (const __nv_bfloat16*)mid, y, B, e2, s);
-    }
-  } else {
-    const size_t bytes = (size_t)B * c1->C_out * P1 * c1->nb * 4;
-    CL_CUDA(cudaMallocAsync(&mid, bytes, s), "block mid alloc");
-    rc = conv_run(c1, x, nullptr, (float*)mid, B, e1, s);
-    if (rc == CL_OK) {
-      Epi e2;
-      if (h->residual) { e2.resid = x; e2.res_side = c1->d_image; e2.res_crop = h->res_crop; }
-      rc = conv_run(c2, (const float*)mid, nullptr, y, B, e2, s);
-    }
+    if (int rc = conv_run(c1, x, nullptr, nullptr, B, e1, cws, s)) return rc;
+    return conv_run(c2, nullptr, (const __nv_bfloat16*)mid, y, B, e2, cws, s);
   }
-  cudaFreeAsync(mid, s);
-  return rc;
+  if (int rc = conv_run(c1, x, nullptr, (float*)mid, B, e1, cws, s)) return rc;
+  return conv_run(c2, (const float*)mid, nullptr, y, B, e2, cws, s);
 }
 }  // namespace cl
 
 extern "C" {
 
+size_t cl_block_workspace_bytes(const cl_block* h, int64_t B) { return h ? block_ws_bytes(h, B) : 0; }
+
+int cl_block_forward_ws(const cl_block* h, const float* x, float* y, int64_t B, void* ws, size_t ws_bytes,
+                        void* stream) {
+  if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null block handle");
+  if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
+  if (ws_bytes < block_ws_bytes(h, B)) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "workspace too small");
+  return block_run(h, x, y, B, ws, (cudaStream_t)stream);
+}
+
 int cl_block_forward(const cl_block* h, const float* x, float* y, int64_t B, void* stream) {
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null block handle");
   if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
-  return block_run(h, x, y, B, (cudaStream_t)stream);
+  void* ws = nullptr;
+  if (int rc = h->ws.get((cudaStream_t)stream, block_ws_bytes(h, B), &ws)) return rc;
+  return block_run(h, x, y, B, ws, (cudaStream_t)stream);
 }
 
 int cl_block_forward_host(const cl_block* h, const float* xh, float* yh, int64_t B, int64_t chunk, void* stream) {
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null block handle");
   const size_t in_per = (size_t)h->c1->C_in * ipow(h->c1->d_image, h->c1->k) * h->c1->nb * 4;
   const size_t out_per = (size_t)h->c2->C_out * ipow(h->c2->d_out, h->c2->k) * h->c2->nb * 4;
-  return host_chunked(B, in_per, out_per, chunk, xh, yh, (cudaStream_t)stream,
-                      [&](const float* dx, float* dy, long long nb, cudaStream_t s) {
-                        return block_run(h, dx, dy, nb, s);
-                      });
+  return host_chunked(
+      h->host, B, in_per, out_per, chunk, xh, yh, (cudaStream_t)stream,
+      [&](long long nb) { return block_ws_bytes(h, nb); },
+      [&](const float* dx, float* dy, long long nb, void* ws, cudaStream_t s) {
+        return block_run(h, dx, dy, nb, ws, s);
+      });
 }
 
 void cl_block_destroy(cl_block* h) { delete h; }
