@@ -274,20 +274,16 @@ def run_ours(args):
     t_step = max_over_ranks(t_step, world)
     value = spec.B / t_step  # whole-job samples/s
 
-    # ---- dominant kernel: the conv launch, timed alone with CUDA events ----
+    # ---- dominant kernel: the tensor-core conv launch alone, CUDA events on its stream ----
+    import ctypes
     xc = x if spec.kind == "conv" else torch.empty(conv_layer.dims.input_shape(), device=dev).normal_()
-    for _ in range(2):
-        M.conv_forward(xc, conv_layer)
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    nrep = max(2, args.steps)
-    e0.record()
-    for _ in range(nrep):
-        M.conv_forward(xc, conv_layer)
-    e1.record()
-    torch.cuda.synchronize()
-    t_conv = e0.elapsed_time(e1) / 1e3 / nrep
+    yc = torch.empty(conv_layer.output_shape(), device=dev)
+    ms = ctypes.c_float()
+    _lib.check(lib.cl_conv_time_kernel(ctypes.c_void_p(conv_layer.handle()), ctypes.c_void_p(xc.data_ptr()),
+                                       ctypes.c_void_p(yc.data_ptr()), conv_layer.dims.B, max(2, args.steps),
+                                       ctypes.c_void_p(torch.cuda.current_stream().cuda_stream), ctypes.byref(ms)))
+    t_conv = ms.value / 1e3
+    del yc
     conv_flops = M.conv_flops(conv_layer.dims, conv_layer)
     achieved = conv_flops / t_conv / 1e12
     peak = mode_peak(prec, peaks, sustained=True)

@@ -101,6 +101,10 @@ int cl_conv_forward(const cl_conv* h, const float* x_dev, float* y_dev, int64_t 
 size_t cl_conv_workspace_bytes(const cl_conv* h, int64_t B);
 int cl_conv_forward_ws(const cl_conv* h, const float* x_dev, float* y_dev, int64_t B, void* ws,
                        size_t ws_bytes, void* stream);
+/* diagnostics: prepares the operand once, then times `reps` launches of the
+ * tensor-core conv kernel alone with CUDA events on `stream` */
+int cl_conv_time_kernel(const cl_conv* h, const float* x_dev, float* y_dev, int64_t B, int reps,
+                        void* stream, float* avg_ms);
 /* host (pinned or pageable) buffers; copies in/out inside the call, chunked over the batch */
 int cl_conv_forward_host(const cl_conv* h, const float* x_host, float* y_host, int64_t B,
                          void* stream);

@@ -19,6 +19,7 @@
 namespace cl {
 
 static thread_local std::string g_last_error;
+static thread_local bool g_time_kernel_only = false;  // cl_conv_time_kernel: skip operand preparation
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -486,21 +487,24 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   const long long P_in = (long long)ipow(h->d_image, h->k);
   float* a_scale = nullptr;
   const void* src = x;
+  const bool prep = !g_time_kernel_only;
   if (pl.prec == kPrecFp32) {
     const size_t bytes = align_up((size_t)kDigits * B * pl.G * P_in * 16, 256);
     int8_t* digits = reinterpret_cast<int8_t*>(ws);
     unsigned* amax = reinterpret_cast<unsigned*>(digits + bytes);
     a_scale = reinterpret_cast<float*>(digits + bytes + (size_t)B * 4);
     const long long per_sample = (long long)h->C_in * P_in * h->nb;
-    CL_CUDA(launch_sample_absmax(x, B, per_sample, amax, s), "absmax");
-    CL_CUDA(launch_slice_input(x, amax, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G, s), "slice_input");
+    if (prep) {
+      CL_CUDA(launch_sample_absmax(x, B, per_sample, amax, s), "absmax");
+      CL_CUDA(launch_slice_input(x, amax, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G, s), "slice_input");
+    }
     src = digits;
   } else if (pl.prec == kPrecBf16) {
     if (xbf) {
       src = xbf;
     } else {
       __nv_bfloat16* packed = reinterpret_cast<__nv_bfloat16*>(ws);
-      CL_CUDA(launch_pack_bf16(x, packed, h->nb, B, h->C_in, P_in, pl.G, h->nb == 4, s), "pack_bf16");
+      if (prep) CL_CUDA(launch_pack_bf16(x, packed, h->nb, B, h->C_in, P_in, pl.G, h->nb == 4, s), "pack_bf16");
       src = packed;
     }
   }
@@ -634,6 +638,35 @@ int cl_conv_forward(const cl_conv* h, const float* x, float* y, int64_t B, void*
   void* ws = nullptr;
   if (int rc = h->ws.get((cudaStream_t)stream, conv_ws_bytes(h, B, false), &ws)) return rc;
   return conv_run(h, x, nullptr, y, B, Epi{}, ws, (cudaStream_t)stream);
+}
+
+int cl_conv_time_kernel(const cl_conv* h, const float* x, float* y, int64_t B, int reps, void* stream,
+                        float* avg_ms) {
+  if (!h || !avg_ms || reps < 1) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  void* ws = nullptr;
+  if (int rc = h->ws.get(s, conv_ws_bytes(h, B, false), &ws)) return rc;
+  // first call prepares the operand (slice / pack) in ws; the timed calls
+  // re-launch only the tensor-core kernel on the prepared operand
+  if (int rc = conv_run(h, x, nullptr, y, B, Epi{}, ws, s)) return rc;
+  g_time_kernel_only = true;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  int rc = CL_OK;
+  for (int i = 0; i < reps && rc == CL_OK; ++i) rc = conv_run(h, x, nullptr, y, B, Epi{}, ws, s);
+  cudaEventRecord(e1, s);
+  g_time_kernel_only = false;
+  cudaError_t e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc != CL_OK) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "time_kernel");
+  *avg_ms = ms / reps;
+  return CL_OK;
 }
 
 int cl_conv_forward_host(const cl_conv* h, const float* xh, float* yh, int64_t B, void* stream) {
