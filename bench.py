@@ -203,6 +203,76 @@ def run_reference(args):
     return 0
 
 
+def run_activation(args, spec, world, rank, local, dev, peaks, peak_kind, lib):
+    """cfg2: standalone multivector activation, HBM-bound; value = GB/s of
+    algorithmic traffic (read + write of the (B, C, P, N_B) tensor)."""
+    import torch
+    import paper_2507_01040_b200 as M
+    from paper_2507_01040_b200 import workloads as W
+    lo, hi = W.shard(spec.B, rank, world)
+    nloc = hi - lo
+    wgt, bias = W.act_params(spec)
+    modes = [spec.mode] if not args.all_modes else [0, 1, 2]
+    x = W.make_input(spec, lo, nloc, device=dev)
+    y = torch.empty_like(x)
+    nbytes = 2 * x.numel() * 4
+    res = {}
+    for mode in modes:
+        cfg = M.make_activation_config(M.Signature(spec.g), mode, tuple(range(spec.nb)),
+                                       wgt if mode == 0 else None, bias if mode == 0 else None)
+        for _ in range(args.warmup):
+            M.activation_forward(x, cfg, out=y)
+        torch.cuda.synchronize()
+        barrier(world)
+        launches0 = lib.cl_launch_count()
+        reps = max(args.steps, 20)  # a step is ~0.1 ms: time enough launches
+        with ClockSampler(local) as clk:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                M.activation_forward(x, cfg, out=y)
+            e1.record()
+            torch.cuda.synchronize()
+        t = max_over_ranks(e0.elapsed_time(e1) / 1e3 / reps, world)
+        res[mode] = (t, lib.cl_launch_count() - launches0, clk.summary())
+    mode = spec.mode
+    t, launches, clocks = res[mode]
+    gbs = nbytes * world / t / 1e9
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        yh = torch.empty_like(xh).pin_memory()
+        cfg = M.make_activation_config(M.Signature(spec.g), mode, tuple(range(spec.nb)),
+                                       wgt if mode == 0 else None, bias if mode == 0 else None)
+        M.activation_forward(xh, cfg, out=yh)
+        t0 = time.perf_counter()
+        for _ in range(max(1, args.e2e_steps)):
+            M.activation_forward(xh, cfg, out=yh)
+            float(yh.view(-1)[0])
+        te = max_over_ranks((time.perf_counter() - t0) / max(1, args.e2e_steps), world)
+        e2e = {"value": nbytes * world / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": x.numel() * 4 * world,
+               "d2h_bytes_per_step": x.numel() * 4 * world}
+    if rank == 0:
+        peak = peaks["hbm_gbs"]
+        line = {
+            "metric": "multivector activation HBM GB/s (cfg2)", "value": gbs, "unit": "GB/s", "n_gpus": world,
+            "steps": reps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded, BASELINE.json distributions)",
+            "config": {"workload": spec.name, "global_batch": spec.B, "mode": mode,
+                       "l2": "inputs larger than L2 (%.2f GB)" % (x.numel() * 4 / 1e9)},
+            "roofline": {"bound": "hbm", "achieved": gbs / world, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / world / peak, "frac_of_8TBs": gbs / world / 8000.0, "traffic": None,
+                         "kernel": "act_kernel", "peak_basis": f"{peak_kind} hbm_gbs copy bandwidth"},
+            "modes": {str(m): {"ms": v[0] * 1e3, "GB/s": nbytes * world / v[0] / 1e9} for m, v in res.items()},
+            "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": None, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_ours(args):
     import torch
     import paper_2507_01040_b200 as M
@@ -246,7 +316,7 @@ def run_ours(args):
         flops_per_sample = M.conv_flops(layer.dims, layer) / nloc
         conv_layer = layer
     else:
-        raise SystemExit("activation config: use --config 1..5 with kind conv/block")
+        return run_activation(args, spec, world, rank, local, dev, peaks, peak_kind, lib)
 
     x = W.make_input(spec, lo, nloc, device=dev)
     y = run(x)
@@ -356,6 +426,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--warmup-cpu", action="store_true")
+    ap.add_argument("--all-modes", action="store_true", help="activation: time Linear, Sum and Mean")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

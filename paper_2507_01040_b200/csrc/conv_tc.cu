@@ -123,27 +123,35 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
-      const uint32_t idesc = kInt8 ? instr_desc_i8(128u, (uint32_t)p.n_tile)
-                                   : instr_desc(PREC == kPrecBf16 ? 1u : 2u, 128u, (uint32_t)p.n_tile);
-      const uint32_t b_lbo = (uint32_t)p.n_tile * 16u, b_kstep = (uint32_t)p.n_tile * 32u;
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+    // The warp runs the loop converged (all lanes wait on the barriers, all
+    // values warp-uniform); one elected lane issues tcgen05.mma + commit.
+    // Descriptors are template + (address >> 4): start address is the low
+    // 14-bit field, and shared addresses < 2^18 never carry out of it.
+    const uint32_t idesc = kInt8 ? instr_desc_i8(128u, (uint32_t)p.n_tile)
+                                 : instr_desc(PREC == kPrecBf16 ? 1u : 2u, 128u, (uint32_t)p.n_tile);
+    const uint64_t a_tmpl = (RB == 32) ? smem_desc(0, 16, 256, kLayoutA) : smem_desc(0, 2048, 128, kLayoutA);
+    const uint64_t b_tmpl = smem_desc(0, (uint32_t)p.n_tile * 16u, 128, kSwizzleNone);
+    const uint32_t a_img4 = p.a_bytes >> 4, b_img4 = p.b_img_bytes >> 4;
+    const uint32_t b_ks4 = ((uint32_t)p.n_tile * 32u) >> 4;
+    const uint32_t a_tot4 = a_total >> 4;
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)acc * slot_cols;
+      for (int kit = 0; kit < p.k_iters; ++kit) {
+        if (kSplit) mbar_wait(&lo_ready[stage], phase);
+        else mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)acc * slot_cols;
-        for (int kit = 0; kit < p.k_iters; ++kit) {
-          if (kSplit) mbar_wait(&lo_ready[stage], phase);
-          else mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t sA = smem_u32(smem + (size_t)stage * p.stage_bytes);
-          const uint32_t sB = sA + a_total;
+        const uint32_t sA4 = smem_u32(smem + (size_t)stage * p.stage_bytes) >> 4;
+        const uint32_t sB4 = sA4 + a_tot4;
+        if (elect_one()) {
           for (int s = 0; s < p.ks; ++s) {
-            const uint32_t a_addr = sA + (uint32_t)s * 4096u;
-            const uint32_t b_addr = sB + (uint32_t)s * b_kstep;
+            const uint64_t a0 = a_tmpl + (uint64_t)(sA4 + (uint32_t)s * 256u);
+            const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)s * b_ks4);
             const uint32_t first = (kit == 0 && s == 0) ? 1u : 0u;
             if constexpr (kInt8) {
               // D_L += A_i * B_j over digit pairs with i + j = L <= 3 (Ozaki levels)
@@ -152,36 +160,27 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
                 for (int i = 0; i <= L; ++i) {
                   const int j = L - i;
-                  const uint64_t adesc = smem_desc(a_addr + (uint32_t)i * p.a_bytes, 2048, 128, kSwizzleNone);
-                  const uint64_t bdesc = smem_desc(b_addr + (uint32_t)j * p.b_img_bytes, b_lbo, 128, kSwizzleNone);
-                  mma_i8(d_tmem + (uint32_t)(L * p.n_tile), adesc, bdesc, idesc, (first && i == 0) ? 0u : 1u);
+                  mma_i8(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * a_img4),
+                         b0 + (uint64_t)(j * b_img4), idesc, (first && i == 0) ? 0u : 1u);
                 }
               }
+            } else if constexpr (kSplit) {
+              mma_tf32(d_tmem, a0 + a_img4, b0, idesc, first ? 0u : 1u);  // A_lo * B_hi
+              mma_tf32(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
+              mma_tf32(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
+            } else if constexpr (PREC == kPrecTf32) {
+              mma_tf32(d_tmem, a0, b0, idesc, first ? 0u : 1u);
             } else {
-              const uint64_t adesc = (RB == 32) ? smem_desc(a_addr, 16, 256, kLayoutA)
-                                                : smem_desc(a_addr, 2048, 128, kLayoutA);
-              const uint64_t bdesc = smem_desc(b_addr, b_lbo, 128, kSwizzleNone);
-              const uint32_t accum = first ? 0u : 1u;
-              if constexpr (kSplit) {
-                const uint64_t adesc_lo = (RB == 32) ? smem_desc(a_addr + p.a_bytes, 16, 256, kLayoutA)
-                                                     : smem_desc(a_addr + p.a_bytes, 2048, 128, kLayoutA);
-                const uint64_t bdesc_lo = smem_desc(b_addr + p.b_img_bytes, b_lbo, 128, kSwizzleNone);
-                mma_tf32(d_tmem, adesc_lo, bdesc, idesc, accum);
-                mma_tf32(d_tmem, adesc, bdesc_lo, idesc, 1u);
-                mma_tf32(d_tmem, adesc, bdesc, idesc, 1u);
-              } else if constexpr (PREC == kPrecTf32) {
-                mma_tf32(d_tmem, adesc, bdesc, idesc, accum);
-              } else {
-                mma_bf16(d_tmem, adesc, bdesc, idesc, accum);
-              }
+              mma_bf16(d_tmem, a0, b0, idesc, first ? 0u : 1u);
             }
           }
           mma_commit(&empty[stage]);  // smem slot free once these MMAs retire
-          if (++stage == S) { stage = 0; phase ^= 1; }
+          if (kit == p.k_iters - 1) mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
         }
-        mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
-        if (++acc == slots) { acc = 0; acc_phase ^= 1; }
+        __syncwarp();
+        if (++stage == S) { stage = 0; phase ^= 1; }
       }
+      if (++acc == slots) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4 && warp < 8) {
     // ===================== epilogue =====================
