@@ -46,12 +46,32 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def load_mode_peaks():
+    """Per-MMA-kind cuBLAS peaks measured on this pool's B200s by
+    tools/measure_peaks.py (same method as MEASURED_PEAKS.json), committed
+    under profiles/."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_mode_peaks.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def mode_peak(precision, peaks, sustained=True):
-    """Effective dense tensor peak (TFLOP/s of algorithmic work) of a mode,
-    derived from the measured bf16 GEMM peak: tf32 = bf16/2; 3xTF32 = tf32/3;
-    fp32 (int8 digit slices: 10 int8 MMAs per K-step, int8 = 2 x bf16) = 2*bf16/10."""
-    bf16 = peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"]
-    return {"bf16": bf16, "tf32": bf16 / 2, "3xtf32": bf16 / 6, "fp32": 2 * bf16 / 10}[precision]
+    """Effective dense tensor peak (TFLOP/s of ALGORITHMIC work) of a conv mode:
+    bf16 = cuBLAS bf16; tf32 = cuBLAS tf32; 3xtf32 = tf32 / 3 (three MMAs per
+    product); fp32 = cuBLAS int8 / 10 (ten int8 digit-pair MMAs per product).
+    bf16 comes from MEASURED_PEAKS.json, tf32/int8 from profiles/r01_mode_peaks.json
+    (falling back to bf16/2 and 2*bf16 when absent). Returns (peak, basis)."""
+    sfx = "_sustained" if sustained else ""
+    bf16 = peaks["bf16_tflops" + sfx]
+    mp = load_mode_peaks()
+    if mp:
+        tf32, i8, basis = mp["tf32_tflops" + sfx], mp["int8_tops" + sfx], "measured cuBLAS (profiles/r01_mode_peaks.json)"
+    else:
+        tf32, i8, basis = bf16 / 2, 2 * bf16, "derived from MEASURED_PEAKS bf16"
+    val = {"bf16": bf16, "tf32": tf32, "3xtf32": tf32 / 3, "fp32": i8 / 10}[precision]
+    return val, basis + (" sustained" if sustained else " burst")
 
 
 class ClockSampler:
@@ -356,7 +376,8 @@ def run_ours(args):
     del yc
     conv_flops = M.conv_flops(conv_layer.dims, conv_layer)
     achieved = conv_flops / t_conv / 1e12
-    peak = mode_peak(prec, peaks, sustained=True)
+    peak, peak_basis = mode_peak(prec, peaks, sustained=True)
+    peak_burst, _ = mode_peak(prec, peaks, sustained=False)
     conv_share = (t_conv * (2 if spec.kind == "block" else 1)) / (t_step)
 
     # ---- end to end through the public API with pinned HOST buffers ----
@@ -402,7 +423,7 @@ def run_ours(args):
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "kernel": "conv_tc_kernel (conv2 of the block)",
-                         "peak_basis": f"{prec} effective peak derived from {peak_kind} bf16_tflops_sustained",
+                         "peak_basis": f"{prec}: {peak_basis}", "frac_of_burst": achieved / peak_burst,
                          "kernel_share_of_step": conv_share},
             "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": cpu,
             "clocks": clk.summary(),

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -20,6 +21,7 @@ namespace cl {
 
 static thread_local std::string g_last_error;
 static thread_local bool g_time_kernel_only = false;  // cl_conv_time_kernel: skip operand preparation
+static bool g_no_cluster = getenv("CL_NO_CLUSTER") != nullptr;  // debug: disable B multicast
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -527,7 +529,10 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.n_tile = pl.n_tile;
   p.N = pl.N;
   p.C_out = h->C_out;
-  p.num_tiles = (long long)B * p.ntz * p.nty * p.ntx * p.n_ntiles;
+  p.num_m_tiles = (long long)B * p.ntz * p.nty * p.ntx;
+  p.cs = (p.num_m_tiles >= 2 && !g_no_cluster) ? 2 : 1;  // pairs share B stages by TMA multicast
+  p.num_tiles = ((p.num_m_tiles + p.cs - 1) / p.cs) * p.cs * p.n_ntiles;
+  p.dbg_nomc = getenv("CL_DBG_NOMC") != nullptr;
   p.d_filter = h->d_filter;
   p.n_gs = pl.n_gs;
   p.gs = pl.gs;
@@ -560,7 +565,8 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.act_w = epi.act ? epi.act->w : nullptr;
   p.act_b = epi.act ? epi.act->b : nullptr;
   p.act_K = epi.act ? (float)epi.act->K : 1.f;
-  const int grid = (int)std::min<long long>(p.num_tiles, (long long)num_sms());
+  int grid = (int)std::min<long long>(p.num_tiles, (long long)num_sms());
+  grid -= grid % p.cs;
   cudaError_t e = launch_conv(pl, map, p, grid, s);
   if (e != cudaSuccess) return cuda_fail(e, "conv_tc launch");
   return CL_OK;

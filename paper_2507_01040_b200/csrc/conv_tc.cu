@@ -39,6 +39,24 @@ __device__ __forceinline__ float act_gate(const float (&v)[NB], int mode, const 
   return 1.f / (1.f + expf(-s));
 }
 
+// Persistent tile order: CTAs of one cluster (consecutive blockIdx, rank r)
+// take consecutive pixel tiles of the SAME N tile so they can share each B
+// stage by multicast; N tiles of one pixel-tile group run back to back (A
+// reuse in L2). Returns false for cluster padding tiles (no output).
+__device__ __forceinline__ bool decode_tile(const ConvKParams& p, long long t, int crank, int& nt, int& tx,
+                                            int& ty, int& tz, int& b) {
+  const long long c = t / p.cs;
+  nt = (int)(c % p.n_ntiles);
+  long long m = (c / p.n_ntiles) * p.cs + crank;
+  const bool real = m < p.num_m_tiles;
+  if (!real) m = p.num_m_tiles - 1;
+  tx = (int)(m % p.ntx); m /= p.ntx;
+  ty = (int)(m % p.nty); m /= p.nty;
+  tz = (int)(m % p.ntz);
+  b = (int)(m / p.ntz);
+  return real;
+}
+
 template <int NB, int PREC>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ConvKParams p) {
@@ -60,10 +78,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
+  const int cs = p.cs;
+  const uint16_t cmask = (uint16_t)((1u << cs) - 1u);
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], p.dbg_nomc ? 1u : (uint32_t)cs);  // one MMA commit from every CTA of the cluster
       mbar_init(&lo_ready[s], 128);
     }
     for (int a = 0; a < 2; ++a) {
@@ -76,8 +96,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
   tc_fence_before();
   __syncthreads();
+  if (cs > 1) cluster_sync();  // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const int crank = cs > 1 ? (int)cluster_ctarank() : 0;
 
   const long long num_tiles = p.num_tiles;
   const uint32_t a_total = p.a_bytes * (uint32_t)p.n_a;
@@ -92,12 +114,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int df = p.d_filter;
       const uint32_t tx_bytes = p.a_bytes * (uint32_t)p.n_tma_a + p.b_bytes;
       for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        long long r = t;
-        const int nt = (int)(r % p.n_ntiles); r /= p.n_ntiles;
-        const int tx = (int)(r % p.ntx); r /= p.ntx;
-        const int ty = (int)(r % p.nty); r /= p.nty;
-        const int tz = (int)(r % p.ntz);
-        const int b = (int)(r / p.ntz);
+        int nt, tx, ty, tz, b;
+        decode_tile(p, t, crank, nt, tx, ty, tz, b);
         const int x0 = tx * p.tx - p.pad, y0 = ty * p.ty - p.pad, z0 = tz * p.tz - p.pad;
         const uint8_t* bsrc = p.b_img + (size_t)nt * p.k_iters * p.b_bytes;
         for (int kit = 0; kit < p.k_iters; ++kit) {
@@ -116,7 +134,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             else
               tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, y0 + qy, g0, bb);
           }
-          bulk_load(sB, bsrc + (size_t)kit * p.b_bytes, p.b_bytes, &full[stage]);
+          if (cs == 1 || p.dbg_nomc) {
+            bulk_load(sB, bsrc + (size_t)kit * p.b_bytes, p.b_bytes, &full[stage]);
+          } else {  // this CTA's slice of the stage, multicast to the whole cluster
+            const uint32_t sl = p.b_bytes / (uint32_t)cs;
+            bulk_load_multicast(sB + crank * sl, bsrc + (size_t)kit * p.b_bytes + crank * sl, sl, &full[stage], cmask);
+          }
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
@@ -174,7 +197,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               mma_bf16(d_tmem, a0, b0, idesc, first ? 0u : 1u);
             }
           }
-          mma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+          // smem slot free (in every CTA of the cluster) once these MMAs retire
+          if (cs == 1 || p.dbg_nomc) mma_commit(&empty[stage]);
+          else mma_commit_multicast(&empty[stage], cmask);
           if (kit == p.k_iters - 1) mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
         }
         __syncwarp();
@@ -194,14 +219,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      long long r = t;
-      const int nt = (int)(r % p.n_ntiles); r /= p.n_ntiles;
-      const int tx = (int)(r % p.ntx); r /= p.ntx;
-      const int ty = (int)(r % p.nty); r /= p.nty;
-      const int tz = (int)(r % p.ntz);
-      const int b = (int)(r / p.ntz);
+      int nt, tx, ty, tz, b;
+      const bool real = decode_tile(p, t, crank, nt, tx, ty, tz, b);
       const int ox = tx * p.tx + lx, oy = ty * p.ty + ly, oz = tz * p.tz + lz;
-      const bool valid = ox < d_out && oy < d_out && oz < ((p.k == 3) ? d_out : 1);
+      const bool valid = real && ox < d_out && oy < d_out && oz < ((p.k == 3) ? d_out : 1);
       const long long pix = (p.k == 3) ? ((long long)oz * d_out + oy) * d_out + ox : (long long)oy * d_out + ox;
       long long pres = 0;
       if (p.resid) {
@@ -210,7 +231,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                           : (long long)(oy + cr) * rs + (ox + cr);
       }
       double a_sc = 0.0;
-      if constexpr (kInt8) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
+      if constexpr (kInt8) if (real) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)acc * slot_cols;
@@ -334,6 +355,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (cs > 1) cluster_sync();  // no CTA leaves while a peer may still multicast into it
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
@@ -347,8 +369,21 @@ static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)plan.smem_bytes);
   if (e != cudaSuccess) return e;
-  kfn<<<grid, kConvThreads, plan.smem_bytes, s>>>(tmap, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kConvThreads);
+  cfg.dynamicSmemBytes = plan.smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)p.cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kfn, tmap, p);
   count_launch();
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

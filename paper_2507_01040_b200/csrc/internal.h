@@ -59,6 +59,9 @@ struct ConvKParams {
   int d_filter, n_gs, gs, G, merged_bc, k_iters, ks;
   uint32_t a_bytes, b_bytes, b_img_bytes, stage_bytes, tmem_cols;
   int stages, n_a, n_tma_a, levels, acc_slots;
+  int cs;                     // cluster size: CTAs sharing each B stage by multicast (1 or 2)
+  long long num_m_tiles;      // real pixel tiles (tiles beyond are cluster padding)
+  int dbg_nomc;               // debug: cluster launch without B multicast
   const uint8_t* b_img;
   const float* a_scale;       // kPrecFp32: per-sample power-of-two scale of the A digits
   const float* w_scale;       // kPrecFp32: per-column power-of-two scale of the B digits
