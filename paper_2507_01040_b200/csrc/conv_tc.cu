@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // The warp runs the loop converged (all lanes wait on the barriers, all
     // values warp-uniform); one elected lane issues tcgen05.mma + commit.
     // Descriptors are template + (address >> 4): start address is the low
-    // 14-bit field, and shared addresses < 2^18 never carry out of it.
+    // 14-bit field, and CTA-local shared addresses < 2^18 never carry out of it.
     const uint32_t idesc = kInt8 ? instr_desc_i8(128u, (uint32_t)p.n_tile)
                                  : instr_desc(PREC == kPrecBf16 ? 1u : 2u, 128u, (uint32_t)p.n_tile);
     const uint64_t a_tmpl = (RB == 32) ? smem_desc(0, 16, 256, kLayoutA) : smem_desc(0, 2048, 128, kLayoutA);
@@ -169,7 +169,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (kSplit) mbar_wait(&lo_ready[stage], phase);
         else mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t sA4 = smem_u32(smem + (size_t)stage * p.stage_bytes) >> 4;
+        // (cluster launches return cluster-window shared addresses: keep the
+        // CTA-local 18 bits so nothing carries past the 14-bit start field)
+        const uint32_t sA4 = (smem_u32(smem + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
         const uint32_t sB4 = sA4 + a_tot4;
         if (elect_one()) {
           for (int s = 0; s < p.ks; ++s) {
