@@ -218,23 +218,28 @@ __device__ __forceinline__ void tmem_ld_wait() {
 #endif  // __CUDACC__
 
 // ---- int8 digit slicing (kPrecFp32, see slice.cu) --------------------------
+// v = s * sum_i d_i 2^(-7-8(i-1)) with balanced base-256 digits d_i in [-128, 127]
+// (two's-complement bytes of the rounded fixed-point value).
 #if defined(__CUDACC__)
-// power-of-two s with amax * 128/127 <= s (so the leading digit fits in [-127, 127])
+// power-of-two s with amax * 128/126 <= s: the leading digit stays in [-127, 127]
 __device__ __forceinline__ float pow2_scale_for(float amax) {
   if (!(amax > 0.f)) return 1.f;
   int e;
-  frexpf(amax * 1.0079f, &e);
+  frexpf(amax * 1.016f, &e);
   return ldexpf(1.f, e);
 }
-// u (|u| <= 127/128) -> 4 signed digits, u = sum_i d_i 2^(-7 i) + O(2^-29)
-__device__ __forceinline__ void digits4(float u, int8_t (&d)[4]) {
-  float t = u * 128.f;
+// u (|u| <= 126/128) -> ND balanced base-256 digits, most significant first;
+// |u - sum_i d_i 2^(-7-8(i-1))| <= 2^(-8 ND)
+template <int ND>
+__device__ __forceinline__ void digits_b256(float u, int8_t (&d)[ND]) {
+  int X = __float2int_rn(ldexpf(u, 8 * ND - 1));  // exact scaling, one rounding
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float di = rintf(t);
-    d[i] = (int8_t)(int)di;
-    t = (t - di) * 128.f;  // exact: |t - di| <= 1/2
+  for (int i = ND - 1; i > 0; --i) {
+    const int lo = (int)(int8_t)(X & 0xFF);
+    d[i] = (int8_t)lo;
+    X = (X - lo) >> 8;
   }
+  d[0] = (int8_t)X;
 }
 #endif
 

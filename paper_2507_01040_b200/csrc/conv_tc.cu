@@ -179,11 +179,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)s * b_ks4);
             const uint32_t first = (kit == 0 && s == 0) ? 1u : 0u;
             if constexpr (kInt8) {
-              // D_L += A_i * B_j over digit pairs with i + j = L <= 3 (Ozaki levels)
+              // D_L += A_i * B_j over digit pairs with i + j = L <= 3 (Ozaki levels;
+              // A has 4 digits, B 3): 9 MMAs per K step
 #pragma unroll
-              for (int L = 0; L < kDigits; ++L) {
+              for (int L = 0; L < kLevels; ++L) {
 #pragma unroll
-                for (int i = 0; i <= L; ++i) {
+                for (int i = (L > kDigitsW - 1 ? L - (kDigitsW - 1) : 0); i <= L && i < kDigitsA; ++i) {
                   const int j = L - i;
                   mma_i8(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * a_img4),
                          b0 + (uint64_t)(j * b_img4), idesc, (first && i == 0) ? 0u : 1u);
@@ -250,9 +251,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
-            // exact integer levels combined in fp64: L0 + L1 2^-7 + L2 2^-14 + L3 2^-21
-            const double s = (double)(int)l0[c] + (double)(int)l1[c] * (1.0 / 128.0) +
-                             (double)(int)l2[c] * (1.0 / 16384.0) + (double)(int)l3[c] * (1.0 / 2097152.0);
+            // exact integer levels combined in fp64: L0 + L1 2^-8 + L2 2^-16 + L3 2^-24
+            const double s = (double)(int)l0[c] + (double)(int)l1[c] * (1.0 / 256.0) +
+                             (double)(int)l2[c] * (1.0 / 65536.0) + (double)(int)l3[c] * (1.0 / 16777216.0);
             const int n = min(n0 + c, p.N - 1);
             const int co = n / NB, tb = n % NB;
             const double v = s * a_sc * (double)__ldg(p.w_scale + n) + (double)__ldg(p.bias + tb * p.C_out + co);

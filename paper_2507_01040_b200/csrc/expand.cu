@@ -12,7 +12,7 @@
 //    at create time: per (N-tile, K-iteration) a contiguous block of K-major
 //    SWIZZLE_NONE UMMA core matrices [image][k-step][2 x 16 B chunks][n_tile
 //    rows][16 B], images = {hi, lo} for 3xTF32, {tf32}, {bf16} or the four
-//    int8 digits of the fp32-accurate mode (per-column power-of-two scale).
+//    three int8 digits of the fp32-accurate mode (per-column power-of-two scale).
 #include "common.cuh"
 #include "internal.h"
 
@@ -81,10 +81,10 @@ __global__ void expand_img_kernel(Sig sg, const float* __restrict__ f, int C_in,
     const size_t off = (size_t)s * pl.n_tile * 32 + (size_t)h * pl.n_tile * 16 + (size_t)row * 16 +
                        (size_t)e * pl.esize;
     if (pl.prec == kPrecFp32) {
-      int8_t d[4];
-      digits4(w / __ldg(w_scale + n), d);
+      int8_t d[kDigitsW];
+      digits_b256<kDigitsW>(w / __ldg(w_scale + n), d);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) *reinterpret_cast<int8_t*>(base + (size_t)k * pl.b_img_bytes + off) = d[k];
+      for (int k = 0; k < kDigitsW; ++k) *reinterpret_cast<int8_t*>(base + (size_t)k * pl.b_img_bytes + off) = d[k];
     } else if (pl.prec == kPrec3xTf32) {
       const float hi = __uint_as_float(__float_as_uint(w) & 0xFFFFE000u);
       *reinterpret_cast<float*>(base + off) = hi;

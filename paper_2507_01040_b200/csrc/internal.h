@@ -15,7 +15,9 @@ namespace cl {
 //   kPrecBf16    BF16 operands
 //   kPrec3xTf32  3xTF32 split (hi/lo), fp32 TMEM accumulation
 enum Prec : int { kPrecFp32 = 0, kPrecTf32 = 1, kPrecBf16 = 2, kPrec3xTf32 = 3 };
-constexpr int kDigits = 4;  // int8 digits per operand in kPrecFp32
+constexpr int kDigitsA = 4;  // int8 digits per activation value in kPrecFp32 (31 bits)
+constexpr int kDigitsW = 3;  // int8 digits per filter value (23 bits, per-column scale)
+constexpr int kLevels = 4;   // digit-pair levels kept: i + j <= 3 (0-based)
 
 constexpr int kTileM = 128;          // output pixels per tile (= TMEM lanes)
 constexpr int kConvThreads = 384;    // 12 warps, see conv_tc.cu

@@ -1,11 +1,11 @@
 // slice.cu -- operand preparation for the fp32-accurate mode (kPrecFp32).
 //
-// Each fp32 value v is written as  v = s * sum_{i=1..4} d_i 2^(-7 i)  with a
+// Each fp32 value v is written as  v = s * sum_i d_i 2^(-7-8(i-1))  with a
 // power-of-two scale s (per sample for activations, per output column for
-// the expanded filter) and signed digits d_1 in [-127, 127],
-// d_2..d_4 in [-64, 64] (round-to-nearest remainders), so |error| <= s 2^-29.
-// Digit products d_i w_j are then summed EXACTLY by tcgen05 kind::i8 into
-// s32 TMEM accumulators, one per level L = i + j - 2 <= 3 (see conv_tc.cu);
+// the expanded filter) and balanced base-256 int8 digits: 4 for activations
+// (|error| <= s 2^-32), 3 for filters (|error| <= s 2^-24). Digit products
+// d_i w_j are then summed EXACTLY by tcgen05 kind::i8 into s32 TMEM
+// accumulators, one per level L = i + j <= 3 (0-based; see conv_tc.cu);
 // the truncating fp32 accumulation of the tf32/bf16 tensor-core paths never
 // touches the result.
 #include <algorithm>
@@ -82,7 +82,7 @@ __global__ void slice_input_kernel(const float* __restrict__ x, const unsigned* 
       }
       for (int j = 0; j < nb; ++j) {
         int8_t d[4];
-        digits4(v[j] * inv, d);
+        digits_b256<4>(v[j] * inv, d);
 #pragma unroll
         for (int k = 0; k < 4; ++k) dg[k][cl * nb + j] = d[k];
       }
