@@ -183,11 +183,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               // A has 4 digits, B 3): 9 MMAs per K step
 #pragma unroll
               for (int L = 0; L < kLevels; ++L) {
+                const int i0 = L > kDigitsW - 1 ? L - (kDigitsW - 1) : 0;
 #pragma unroll
-                for (int i = (L > kDigitsW - 1 ? L - (kDigitsW - 1) : 0); i <= L && i < kDigitsA; ++i) {
+                for (int i = i0; i <= L && i < kDigitsA; ++i) {
                   const int j = L - i;
                   mma_i8(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * a_img4),
-                         b0 + (uint64_t)(j * b_img4), idesc, (first && i == 0) ? 0u : 1u);
+                         b0 + (uint64_t)(j * b_img4), idesc, (first && i == i0) ? 0u : 1u);
                 }
               }
             } else if constexpr (kSplit) {
