@@ -60,7 +60,7 @@ def load_mode_peaks():
 def mode_peak(precision, peaks, sustained=True):
     """Effective dense tensor peak (TFLOP/s of ALGORITHMIC work) of a conv mode:
     bf16 = cuBLAS bf16; tf32 = cuBLAS tf32; 3xtf32 = tf32 / 3 (three MMAs per
-    product); fp32 = cuBLAS int8 / 9 (nine int8 digit-pair MMAs per product).
+    product); fp32 = cuBLAS int8 / 10 (ten int8 digit-pair MMAs per product).
     bf16 comes from MEASURED_PEAKS.json, tf32/int8 from profiles/r01_mode_peaks.json
     (falling back to bf16/2 and 2*bf16 when absent). Returns (peak, basis)."""
     sfx = "_sustained" if sustained else ""
@@ -70,7 +70,7 @@ def mode_peak(precision, peaks, sustained=True):
         tf32, i8, basis = mp["tf32_tflops" + sfx], mp["int8_tops" + sfx], "measured cuBLAS (profiles/r01_mode_peaks.json)"
     else:
         tf32, i8, basis = bf16 / 2, 2 * bf16, "derived from MEASURED_PEAKS bf16"
-    val = {"bf16": bf16, "tf32": tf32, "3xtf32": tf32 / 3, "fp32": i8 / 9}[precision]
+    val = {"bf16": bf16, "tf32": tf32, "3xtf32": tf32 / 3, "fp32": i8 / 10}[precision]
     return val, basis + (" sustained" if sustained else " burst")
 
 

@@ -366,9 +366,9 @@ int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, in
   h->pad = pad;
   h->d_out = d_out;
   h->prec = precision;
-  if (precision == CL_PREC_FP32 && (long long)ipow(d_filter, k) * C_in * (1 << k) > 43000) {
-    delete h;  // s32 level accumulators: 3 x 128 x 128 x K must stay below 2^31
-    return fail(CL_ERR_UNSUPPORTED, "Unsupported", "fp32 mode supports K = d_filter^k * C_in * N_B <= 43000");
+  if (precision == CL_PREC_FP32 && (long long)ipow(d_filter, k) * C_in * (1 << k) > 32000) {
+    delete h;  // s32 level accumulators: 4 pairs x 128 x 128 x K must stay below 2^31
+    return fail(CL_ERR_UNSUPPORTED, "Unsupported", "fp32 mode supports K = d_filter^k * C_in * N_B <= 32000");
   }
   if (!plan_conv(k, h->nb, precision, C_in, C_out, d_out, d_filter, h->plan)) {
     delete h;

@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)s * b_ks4);
             const uint32_t first = (kit == 0 && s == 0) ? 1u : 0u;
             if constexpr (kInt8) {
-              // D_L += A_i * B_j over digit pairs with i + j = L <= 3 (Ozaki levels;
-              // A has 4 digits, B 3): 9 MMAs per K step
+              // D_L += A_i * B_j over digit pairs with i + j = L <= 3 (Ozaki levels,
+              // 4 digits each): 10 MMAs per K step
 #pragma unroll
               for (int L = 0; L < kLevels; ++L) {
                 const int i0 = L > kDigitsW - 1 ? L - (kDigitsW - 1) : 0;

@@ -12,7 +12,7 @@
 //    at create time: per (N-tile, K-iteration) a contiguous block of K-major
 //    SWIZZLE_NONE UMMA core matrices [image][k-step][2 x 16 B chunks][n_tile
 //    rows][16 B], images = {hi, lo} for 3xTF32, {tf32}, {bf16} or the four
-//    three int8 digits of the fp32-accurate mode (per-column power-of-two scale).
+//    four int8 digits of the fp32-accurate mode (per-column power-of-two scale).
 #include "common.cuh"
 #include "internal.h"
 

@@ -16,7 +16,7 @@ namespace cl {
 //   kPrec3xTf32  3xTF32 split (hi/lo), fp32 TMEM accumulation
 enum Prec : int { kPrecFp32 = 0, kPrecTf32 = 1, kPrecBf16 = 2, kPrec3xTf32 = 3 };
 constexpr int kDigitsA = 4;  // int8 digits per activation value in kPrecFp32 (31 bits)
-constexpr int kDigitsW = 3;  // int8 digits per filter value (23 bits, per-column scale)
+constexpr int kDigitsW = 4;  // int8 digits per filter value (31 bits, per-column scale)
 constexpr int kLevels = 4;   // digit-pair levels kept: i + j <= 3 (0-based)
 
 constexpr int kTileM = 128;          // output pixels per tile (= TMEM lanes)

@@ -2,8 +2,8 @@
 //
 // Each fp32 value v is written as  v = s * sum_i d_i 2^(-7-8(i-1))  with a
 // power-of-two scale s (per sample for activations, per output column for
-// the expanded filter) and balanced base-256 int8 digits: 4 for activations
-// (|error| <= s 2^-32), 3 for filters (|error| <= s 2^-24). Digit products
+// the expanded filter) and 4 balanced base-256 int8 digits (|error| <= s 2^-32,
+// finer than the fp32 operands themselves near the scale). Digit products
 // d_i w_j are then summed EXACTLY by tcgen05 kind::i8 into s32 TMEM
 // accumulators, one per level L = i + j <= 3 (0-based; see conv_tc.cu);
 // the truncating fp32 accumulation of the tf32/bf16 tensor-core paths never
