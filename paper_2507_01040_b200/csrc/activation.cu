@@ -79,19 +79,31 @@ __global__ void __launch_bounds__(256) act_kernel(ActParams p) {
   }
 }
 
-template <int NB>
-static cudaError_t launch_nb(const ActParams& p, cudaStream_t s) {
+// Grid = exactly the resident capacity (one wave, no tail): blocks per SM
+// from the occupancy calculator x SM count, capped by the work.
+template <int NB, int MODE>
+static cudaError_t launch_mode(const ActParams& p, cudaStream_t s) {
+  static int per_sm = [] {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, act_kernel<NB, MODE>, 256, 0);
+    return n > 0 ? n : 1;
+  }();
   long long blocks = (p.n_mv + 256LL * 4 - 1) / (256LL * 4);
-  const long long cap = (long long)num_sms() * 8;  // 8 x 256 threads resident per SM
+  const long long cap = (long long)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  switch (p.mode) {
-    case 0: act_kernel<NB, 0><<<(unsigned)blocks, 256, 0, s>>>(p); break;
-    case 1: act_kernel<NB, 1><<<(unsigned)blocks, 256, 0, s>>>(p); break;
-    default: act_kernel<NB, 2><<<(unsigned)blocks, 256, 0, s>>>(p); break;
-  }
+  act_kernel<NB, MODE><<<(unsigned)blocks, 256, 0, s>>>(p);
   count_launch();
   return cudaGetLastError();
+}
+
+template <int NB>
+static cudaError_t launch_nb(const ActParams& p, cudaStream_t s) {
+  switch (p.mode) {
+    case 0: return launch_mode<NB, 0>(p, s);
+    case 1: return launch_mode<NB, 1>(p, s);
+    default: return launch_mode<NB, 2>(p, s);
+  }
 }
 
 cudaError_t launch_act(int nb, const ActParams& p, cudaStream_t s) {
