@@ -33,6 +33,36 @@ __device__ __forceinline__ void st_stream(float4* p, float4 v) {
                : "memory");
 }
 
+// 1-D (N_B = 2): 8-byte multivectors, 8 in flight per thread.
+template <int MODE>
+__global__ void __launch_bounds__(256) act_kernel_nb2(ActParams p) {
+  constexpr int U = 8;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const float2* __restrict__ x = reinterpret_cast<const float2*>(p.x);
+  float2* __restrict__ y = reinterpret_cast<float2*>(p.y);
+  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < p.n_mv; base += stride * U) {
+    float2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = base + u * stride;
+      if (i < p.n_mv) v[u] = __ldcs(x + i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = base + u * stride;
+      if (i < p.n_mv) {
+        const int c = (int)((i / p.P) % p.C);
+        float s = fmaf(v[u].x, __ldg(p.w + 2 * c), 0.f);
+        s = fmaf(v[u].y, __ldg(p.w + 2 * c + 1), s);
+        if (MODE == 0) s += __ldg(p.b + c);
+        if (MODE == 2) s = s / p.Kf;
+        const float gte = 1.f / (1.f + expf(-s));
+        __stcs(y + i, make_float2(v[u].x * gte, v[u].y * gte));
+      }
+    }
+  }
+}
+
 template <int NB, int MODE>
 __global__ void __launch_bounds__(256) act_kernel(ActParams p) {
   constexpr int V = NB / 4;  // float4 per multivector
@@ -97,6 +127,22 @@ static cudaError_t launch_mode(const ActParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int MODE>
+static cudaError_t launch_nb2_mode(const ActParams& p, cudaStream_t s) {
+  static int per_sm = [] {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, act_kernel_nb2<MODE>, 256, 0);
+    return n > 0 ? n : 1;
+  }();
+  long long blocks = (p.n_mv + 256LL * 8 - 1) / (256LL * 8);
+  const long long cap = (long long)num_sms() * per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  act_kernel_nb2<MODE><<<(unsigned)blocks, 256, 0, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
 template <int NB>
 static cudaError_t launch_nb(const ActParams& p, cudaStream_t s) {
   switch (p.mode) {
@@ -108,6 +154,13 @@ static cudaError_t launch_nb(const ActParams& p, cudaStream_t s) {
 
 cudaError_t launch_act(int nb, const ActParams& p, cudaStream_t s) {
   if (p.n_mv == 0) return cudaSuccess;
+  if (nb == 2) {
+    switch (p.mode) {
+      case 0: return launch_nb2_mode<0>(p, s);
+      case 1: return launch_nb2_mode<1>(p, s);
+      default: return launch_nb2_mode<2>(p, s);
+    }
+  }
   return nb == 4 ? launch_nb<4>(p, s) : launch_nb<8>(p, s);
 }
 

@@ -109,23 +109,22 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
   pl.prec = prec;
   const bool i8 = prec == kPrecFp32;
   pl.esize = i8 ? 1 : (prec == kPrecBf16 ? 2 : 4);
-  pl.rb = (prec == kPrecBf16 || i8) ? 16 : nb * 4;
+  // A operand: int8 digit planes (i8), a packed 16-byte-group copy (bf16; fp32
+  // in 1-D where a multivector is only 8 B), or the protocol tensor itself
+  pl.packed = !i8 && (prec == kPrecBf16 || nb == 2);
+  pl.rb = (pl.packed || i8) ? 16 : nb * 4;
   pl.epg = pl.rb / pl.esize;
+  pl.cpg = std::max(1, pl.epg / nb);
   pl.merged_bc = (k == 3);
   pl.d_filter = d_filter;
   pl.Q = ipow(d_filter, k);
-  // row-groups per sample: int8 groups hold 16/nb channels, bf16 2-D groups
-  // a channel pair, otherwise one channel
-  int G_real;
-  if (i8) G_real = (C_in * nb + 15) / 16;
-  else if (prec == kPrecBf16 && nb == 4) G_real = (C_in + 1) / 2;
-  else G_real = C_in;
+  const int G_real = (C_in + pl.cpg - 1) / pl.cpg;  // row-groups per sample
   const int gpk = 32 / pl.rb;  // row-groups per 32-byte K step
 
-  // spatial tile (tx * ty * tz == 128)
+  // output tile (tx * ty * tz == 128); in 1-D the rows span (position, sample)
   int tx = std::min(128, std::max(8, pow2_at_least(d_out)));
   int ty, tz;
-  if (k == 2) {
+  if (k == 1 || k == 2) {
     ty = 128 / tx;
     tz = 1;
   } else {
@@ -155,7 +154,7 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
     if (gs > G_pad_min) continue;
     int G, n_gs;
     if (pl.merged_bc) {
-      if (prec == kPrecBf16 || i8) {
+      if (pl.packed || i8) {
         G = ((G_real + gs - 1) / gs) * gs;  // the pack / slice pass zero-pads groups
       } else {
         if (G_real % gs) continue;
@@ -350,8 +349,6 @@ int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, in
   if (d_out < 1)
     return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch",
                 "d_filter " + std::to_string(d_filter) + " exceeds d_image " + std::to_string(d_image));
-  if (k == 1)
-    return fail(CL_ERR_UNSUPPORTED, "Unsupported", "k=1 (1-D) convolution is not implemented on the B200 path yet");
   if (!filters || !bias) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "filters and bias are required");
   setup_pool();
   cudaStream_t s = (cudaStream_t)stream;
@@ -422,7 +419,7 @@ struct Epi {
   const float* resid = nullptr;
   int res_side = 0, res_crop = 0;
   __nv_bfloat16* y_bf16 = nullptr;  // write bf16 A-ready output for a following bf16 conv
-  int ybf_groups = 0, ybf_pairs = 0;
+  int ybf_groups = 0;
 };
 
 static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUtensorMap* map) {
@@ -437,36 +434,48 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
   cuuint32_t box[5];
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   const cuuint64_t rowb = (cuuint64_t)pl.rb;
-  const bool bf = pl.prec == kPrecBf16;
   const bool i8 = pl.prec == kPrecFp32;
+  const bool own = pl.packed || i8;  // operand written by our pack / slice pass: G groups per sample
   const cuuint64_t planes = (cuuint64_t)pl.n_tma_a;  // int8 digit planes stacked over the batch
+  const cuuint64_t Gt = own ? (cuuint64_t)pl.G : (cuuint64_t)h->C_in;
   dims[0] = (cuuint64_t)pl.epg;
-  dims[1] = D;
-  dims[2] = D;
   box[0] = (cuuint32_t)pl.epg;
   box[1] = (cuuint32_t)pl.tx;
   box[2] = (cuuint32_t)pl.ty;
   strides[0] = rowb;
-  strides[1] = rowb * D;
-  if (pl.merged_bc) {
+  dims[1] = D;
+  if (h->k == 1) {
+    // (e, x, sample, group, plane) over a (plane, B, G, D, 16 B) tensor
+    dims[2] = (cuuint64_t)B;
+    dims[3] = Gt;
+    dims[4] = planes;
+    strides[1] = rowb * D * Gt;          // sample
+    strides[2] = rowb * D;               // group
+    strides[3] = rowb * D * Gt * (cuuint64_t)B;  // plane
+    box[3] = (cuuint32_t)pl.gs;
+    box[4] = 1;
+  } else if (pl.merged_bc) {
+    dims[2] = D;
     dims[3] = D;
-    dims[4] = planes * (cuuint64_t)B * (cuuint64_t)pl.G;
+    dims[4] = planes * (cuuint64_t)B * Gt;
+    strides[1] = rowb * D;
     strides[2] = rowb * D * D;
     strides[3] = rowb * D * D * D;
     box[3] = (cuuint32_t)pl.tz;
     box[4] = (cuuint32_t)pl.gs;
   } else {
-    const cuuint64_t Gt = (bf || i8) ? (cuuint64_t)pl.G : (cuuint64_t)h->C_in;
+    dims[2] = D;
     dims[3] = Gt;
     dims[4] = planes * (cuuint64_t)B;
+    strides[1] = rowb * D;
     strides[2] = rowb * D * D;
     strides[3] = rowb * D * D * Gt;
     box[3] = (cuuint32_t)pl.gs;
     box[4] = 1;
   }
-  CUresult r = enc(map, i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
-                           : (bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32), 5,
-                   const_cast<void*>(xsrc), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+  const CUtensorMapDataType dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                    : (pl.esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+  CUresult r = enc(map, dt, 5, const_cast<void*>(xsrc), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    pl.rb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CL_ERR_CUDA, "CudaError", "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
@@ -479,7 +488,7 @@ static size_t conv_ws_bytes(const cl_conv* h, long long B, bool prepacked) {
   const ConvPlan& pl = h->plan;
   const size_t P_in = (size_t)ipow(h->d_image, h->k);
   if (pl.prec == kPrecFp32) return align_up((size_t)kDigitsA * B * pl.G * P_in * 16, 256) + align_up((size_t)B * 8, 256);
-  if (pl.prec == kPrecBf16 && !prepacked) return align_up((size_t)B * pl.G * P_in * 16, 256);
+  if (pl.packed && !prepacked) return align_up((size_t)B * pl.G * P_in * 16, 256);
   return 0;
 }
 
@@ -505,13 +514,12 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
       CL_CUDA(launch_slice_input(x, amax, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G, s), "slice_input");
     }
     src = digits;
-  } else if (pl.prec == kPrecBf16) {
+  } else if (pl.packed) {
     if (xbf) {
       src = xbf;
     } else {
-      __nv_bfloat16* packed = reinterpret_cast<__nv_bfloat16*>(ws);
-      if (prep) CL_CUDA(launch_pack_bf16(x, packed, h->nb, B, h->C_in, P_in, pl.G, h->nb == 4, s), "pack_bf16");
-      src = packed;
+      if (prep) CL_CUDA(launch_pack_rows(x, ws, h->nb, pl.esize, B, h->C_in, P_in, pl.G, s), "pack_rows");
+      src = ws;
     }
   }
   CUtensorMap map;
@@ -527,13 +535,13 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.ty = pl.ty;
   p.tz = pl.tz;
   p.ntx = (h->d_out + pl.tx - 1) / pl.tx;
-  p.nty = (h->d_out + pl.ty - 1) / pl.ty;
+  p.nty = h->k == 1 ? (int)((B + pl.ty - 1) / pl.ty) : (h->d_out + pl.ty - 1) / pl.ty;  // 1-D: tiles along the batch
   p.ntz = h->k == 3 ? (h->d_out + pl.tz - 1) / pl.tz : 1;
   p.n_ntiles = pl.n_ntiles;
   p.n_tile = pl.n_tile;
   p.N = pl.N;
   p.C_out = h->C_out;
-  p.num_m_tiles = (long long)B * p.ntz * p.nty * p.ntx;
+  p.num_m_tiles = (h->k == 1 ? 1LL : (long long)B) * p.ntz * p.nty * p.ntx;
   // CTA pairs share each B stage by TMA multicast where it pays (measured:
   // +4-6% for the int8 and bf16 modes; the tf32 modes run faster unpaired)
   p.cs = (p.num_m_tiles >= 2 && !g_no_cluster && (pl.prec == kPrecFp32 || pl.prec == kPrecBf16)) ? 2 : 1;
@@ -563,7 +571,6 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.y = y;
   p.y_bf16 = epi.y_bf16;
   p.ybf_groups = epi.ybf_groups;
-  p.ybf_pairs = epi.ybf_pairs;
   p.resid = epi.resid;
   p.res_side = epi.res_side;
   p.res_crop = epi.res_crop;
@@ -715,7 +722,6 @@ int cl_act_create(const int32_t* g, int k, int mode, const int32_t* ki, int K, i
     return fail(CL_ERR_MODE_CONFIG_MISMATCH, "ModeConfigMismatch",
                 std::string(mode == 1 ? "SUM" : "MEAN") + " mode forbids weight/bias");
   if (C < 1) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "C must be >= 1");
-  if (k == 1) return fail(CL_ERR_UNSUPPORTED, "Unsupported", "k=1 activation is not implemented on the B200 path yet");
   setup_pool();
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<float> wk((size_t)C * nb, 0.f), bk((size_t)C, 0.f);
@@ -845,14 +851,12 @@ static int block_run(const cl_block* h, const float* x, float* y, long long B, v
     e2.res_crop = h->res_crop;
   }
   if (c1->prec == kPrecBf16) {
-    // conv1's epilogue writes conv2's packed bf16 operand directly
-    const bool pairs = c2->nb == 4;
-    const int real_groups = pairs ? (c2->C_in + 1) / 2 : c2->C_in;
-    if (c2->plan.G != real_groups || (pairs && (c2->C_in & 1)))
-      CL_CUDA(cudaMemsetAsync(mid, 0, mid_bytes, s), "block mid memset");
+    // conv1's epilogue writes conv2's packed bf16 operand directly (zero the
+    // padding channels/groups the epilogue never touches)
+    const int cpg = c2->plan.cpg;
+    if (c2->plan.G * cpg != c2->C_in) CL_CUDA(cudaMemsetAsync(mid, 0, mid_bytes, s), "block mid memset");
     e1.y_bf16 = (__nv_bfloat16*)mid;
     e1.ybf_groups = c2->plan.G;
-    e1.ybf_pairs = pairs ? 1 : 0;
     if (int rc = conv_run(c1, x, nullptr, nullptr, B, e1, cws, s)) return rc;
     return conv_run(c2, nullptr, (const __nv_bfloat16*)mid, y, B, e2, cws, s);
   }

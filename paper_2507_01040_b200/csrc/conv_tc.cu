@@ -50,6 +50,13 @@ __device__ __forceinline__ bool decode_tile(const ConvKParams& p, long long t, i
   long long m = (c / p.n_ntiles) * p.cs + crank;
   const bool real = m < p.num_m_tiles;
   if (!real) m = p.num_m_tiles - 1;
+  if (p.k == 1) {  // 1-D: tile rows span (position x, sample): b = first sample of the tile
+    tx = (int)(m % p.ntx);
+    ty = (int)(m / p.ntx);
+    tz = 0;
+    b = ty * p.ty;
+    return real;
+  }
   tx = (int)(m % p.ntx); m /= p.ntx;
   ty = (int)(m % p.nty); m /= p.nty;
   tz = (int)(m % p.ntz);
@@ -62,7 +69,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ConvKParams p) {
   constexpr bool kSplit = (PREC == kPrec3xTf32);
   constexpr bool kInt8 = (PREC == kPrecFp32);
-  constexpr int RB = (PREC == kPrecBf16 || kInt8) ? 16 : NB * 4;
+  // A row-group bytes: packed 16-byte groups for bf16 / int8 digits / 1-D,
+  // otherwise one protocol multivector (16 B in 2-D, 32 B in 3-D)
+  constexpr int RB = (PREC == kPrecBf16 || kInt8 || NB == 2) ? 16 : NB * 4;
   constexpr uint32_t kLayoutA = (RB == 32) ? kSwizzle32B : kSwizzleNone;
 
   extern __shared__ uint8_t smem_raw[];
@@ -131,6 +140,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             const int bb = d * p.B + b;  // digit planes are stacked over the batch
             if (p.merged_bc)
               tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, y0 + qy, z0 + qz, bb * p.G + g0);
+            else if (p.k == 1)  // dims (e, x, sample, group, plane)
+              tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, b, g0, d);
             else
               tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, y0 + qy, g0, bb);
           }
@@ -217,25 +228,32 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const int row = ew * 32 + lane;
     const int lx = row % p.tx, ly = (row / p.tx) % p.ty, lz = row / (p.tx * p.ty);
     const int d_out = p.d_out;
-    const long long P_out = (p.k == 3) ? (long long)d_out * d_out * d_out : (long long)d_out * d_out;
+    const long long P_out = (p.k == 3) ? (long long)d_out * d_out * d_out
+                                       : (p.k == 2 ? (long long)d_out * d_out : (long long)d_out);
     const long long P_res = (p.k == 3) ? (long long)p.res_side * p.res_side * p.res_side
-                                       : (long long)p.res_side * p.res_side;
+                                       : (p.k == 2 ? (long long)p.res_side * p.res_side : (long long)p.res_side);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int nt, tx, ty, tz, b;
       const bool real = decode_tile(p, t, crank, nt, tx, ty, tz, b);
       const int ox = tx * p.tx + lx, oy = ty * p.ty + ly, oz = tz * p.tz + lz;
-      const bool valid = real && ox < d_out && oy < d_out && oz < ((p.k == 3) ? d_out : 1);
-      const long long pix = (p.k == 3) ? ((long long)oz * d_out + oy) * d_out + ox : (long long)oy * d_out + ox;
-      long long pres = 0;
-      if (p.resid) {
-        const int rs = p.res_side, cr = p.res_crop;
+      bool valid;
+      long long pix, pres = 0;
+      const int rs = p.res_side, cr = p.res_crop;
+      if (p.k == 1) {  // row = (sample b + ly, position ox)
+        b += ly;
+        valid = real && ox < d_out && b < p.B;
+        pix = ox;
+        pres = ox + cr;
+      } else {
+        valid = real && ox < d_out && oy < d_out && oz < ((p.k == 3) ? d_out : 1);
+        pix = (p.k == 3) ? ((long long)oz * d_out + oy) * d_out + ox : (long long)oy * d_out + ox;
         pres = (p.k == 3) ? ((long long)(oz + cr) * rs + (oy + cr)) * rs + (ox + cr)
                           : (long long)(oy + cr) * rs + (ox + cr);
       }
       double a_sc = 0.0;
-      if constexpr (kInt8) if (real) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
+      if constexpr (kInt8) if (valid) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)acc * slot_cols;
@@ -285,37 +303,41 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 for (int j = 0; j < NB; ++j) v[j] *= gte;
               }
               if (p.resid) {
-                const float4* rp = reinterpret_cast<const float4*>(p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB);
+                const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB;
+                if constexpr (NB == 2) {
+                  const float2 q2 = __ldg(reinterpret_cast<const float2*>(rp));
+                  v[0] += q2.x; v[1] += q2.y;
+                } else {
 #pragma unroll
-                for (int j = 0; j < NB / 4; ++j) {
-                  const float4 q4 = __ldg(rp + j);
-                  v[4 * j] += q4.x; v[4 * j + 1] += q4.y; v[4 * j + 2] += q4.z; v[4 * j + 3] += q4.w;
+                  for (int j = 0; j < NB / 4; ++j) {
+                    const float4 q4 = __ldg(reinterpret_cast<const float4*>(rp) + j);
+                    v[4 * j] += q4.x; v[4 * j + 1] += q4.y; v[4 * j + 2] += q4.z; v[4 * j + 3] += q4.w;
+                  }
                 }
               }
               if (p.y) {
-                float4* yp = reinterpret_cast<float4*>(p.y + (((long long)b * p.C_out + co) * P_out + pix) * NB);
+                float* yp = p.y + (((long long)b * p.C_out + co) * P_out + pix) * NB;
+                if constexpr (NB == 2) {
+                  *reinterpret_cast<float2*>(yp) = make_float2(v[0], v[1]);
+                } else {
 #pragma unroll
-                for (int j = 0; j < NB / 4; ++j) yp[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                  for (int j = 0; j < NB / 4; ++j)
+                    reinterpret_cast<float4*>(yp)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                }
               }
               if (p.y_bf16) {
-                if (p.ybf_pairs) {  // 2-D: (B, Gy, P, [2 ch x 4 blades])
-                  __nv_bfloat16* yp = p.y_bf16 + (((long long)b * p.ybf_groups + (co >> 1)) * P_out + pix) * 8 + (co & 1) * 4;
-                  __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]);
-                  __nv_bfloat162 h1 = __floats2bfloat162_rn(v[2], v[3]);
-                  uint2 u;
-                  u.x = *reinterpret_cast<uint32_t*>(&h0);
-                  u.y = *reinterpret_cast<uint32_t*>(&h1);
-                  *reinterpret_cast<uint2*>(yp) = u;
-                } else {  // 3-D: (B, Gy, P, 8 blades)
-                  __nv_bfloat16* yp = p.y_bf16 + (((long long)b * p.ybf_groups + co) * P_out + pix) * 8;
-                  uint4 u;
-                  __nv_bfloat162 h;
-                  h = __floats2bfloat162_rn(v[0], v[1]); u.x = *reinterpret_cast<uint32_t*>(&h);
-                  h = __floats2bfloat162_rn(v[2], v[3]); u.y = *reinterpret_cast<uint32_t*>(&h);
-                  h = __floats2bfloat162_rn(v[4 % NB], v[5 % NB]); u.z = *reinterpret_cast<uint32_t*>(&h);
-                  h = __floats2bfloat162_rn(v[6 % NB], v[7 % NB]); u.w = *reinterpret_cast<uint32_t*>(&h);
-                  *reinterpret_cast<uint4*>(yp) = u;
+                // next conv's packed bf16 operand: (B, Gy, P, 16 B), cpg = 8 / NB channels per group
+                constexpr int cpg = 8 / NB;
+                __nv_bfloat16* yp = p.y_bf16 + (((long long)b * p.ybf_groups + co / cpg) * P_out + pix) * 8 + (co % cpg) * NB;
+                uint32_t u[NB / 2];
+#pragma unroll
+                for (int j = 0; j < NB / 2; ++j) {
+                  __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+                  u[j] = *reinterpret_cast<uint32_t*>(&h);
                 }
+                if constexpr (NB == 2) *reinterpret_cast<uint32_t*>(yp) = u[0];
+                else if constexpr (NB == 4) *reinterpret_cast<uint2*>(yp) = make_uint2(u[0], u[1]);
+                else *reinterpret_cast<uint4*>(yp) = make_uint4(u[0], u[1 % (NB / 2)], u[2 % (NB / 2)], u[3 % (NB / 2)]);
               }
             }
           }
@@ -393,6 +415,14 @@ static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const
 
 cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const ConvKParams& p,
                         int grid, cudaStream_t s) {
+  if (plan.nb == 2) {
+    switch (plan.prec) {
+      case kPrecFp32: return launch_t<2, kPrecFp32>(plan, tmap, p, grid, s);
+      case kPrec3xTf32: return launch_t<2, kPrec3xTf32>(plan, tmap, p, grid, s);
+      case kPrecTf32: return launch_t<2, kPrecTf32>(plan, tmap, p, grid, s);
+      default: return launch_t<2, kPrecBf16>(plan, tmap, p, grid, s);
+    }
+  }
   if (plan.nb == 4) {
     switch (plan.prec) {
       case kPrecFp32: return launch_t<4, kPrecFp32>(plan, tmap, p, grid, s);
@@ -409,12 +439,13 @@ cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const Con
   }
 }
 
-// fp32 protocol (B, C, P, NB) -> bf16 A-ready layout (B, G, P, 8):
-//   NB == 8: group = channel (G >= C, padding channels zero);
-//   NB == 4: group = channel pair, element (g, p, h*4 + t) = x[2g+h, p, t].
-__global__ void pack_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int nb,
-                                 long long B, int C, long long P, int G, int pairs) {
-  const long long total = B * G * P;  // one 16-byte output row per thread
+// fp32 protocol (B, C, P, NB) -> packed 16-byte row groups (B, G, P, 16 B):
+// group g holds channels g*cpg .. g*cpg+cpg-1 (zero beyond C), NB values each,
+// as bf16 (esize 2, cpg = 8/NB) or fp32 (esize 4, cpg = 4/NB; the 1-D tf32 modes).
+__global__ void pack_rows_kernel(const float* __restrict__ x, uint4* __restrict__ out, int nb, int esize,
+                                 long long B, int C, long long P, int G) {
+  const long long total = B * G * P;
+  const int nvals = 16 / esize, cpg = nvals / nb;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long pp = i % P;
@@ -422,43 +453,46 @@ __global__ void pack_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __r
     const int g = (int)(bg % G);
     const long long b = bg / G;
     float v[8];
-    if (pairs) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = 2 * g + h;
-        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (c < C) q = __ldg(reinterpret_cast<const float4*>(x + ((b * C + c) * P + pp) * 4));
-        v[4 * h] = q.x; v[4 * h + 1] = q.y; v[4 * h + 2] = q.z; v[4 * h + 3] = q.w;
-      }
-    } else {
-      if (g < C) {
-        const float4* src = reinterpret_cast<const float4*>(x + ((b * C + g) * P + pp) * 8);
-        const float4 q0 = __ldg(src), q1 = __ldg(src + 1);
+    for (int j = 0; j < 8; ++j) v[j] = 0.f;
+    for (int cl = 0; cl < cpg; ++cl) {
+      const int c = g * cpg + cl;
+      if (c >= C) break;
+      const float* src = x + ((b * C + c) * P + pp) * nb;
+      if (nb == 2) {
+        const float2 q = __ldg(reinterpret_cast<const float2*>(src));
+        v[cl * 2] = q.x; v[cl * 2 + 1] = q.y;
+      } else if (nb == 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(src));
+        v[cl * 4] = q.x; v[cl * 4 + 1] = q.y; v[cl * 4 + 2] = q.z; v[cl * 4 + 3] = q.w;
+      } else {
+        const float4 q0 = __ldg(reinterpret_cast<const float4*>(src)), q1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
         v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w;
         v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = 0.f;
       }
     }
     uint4 u;
-    __nv_bfloat162 h;
-    h = __floats2bfloat162_rn(v[0], v[1]); u.x = *reinterpret_cast<uint32_t*>(&h);
-    h = __floats2bfloat162_rn(v[2], v[3]); u.y = *reinterpret_cast<uint32_t*>(&h);
-    h = __floats2bfloat162_rn(v[4], v[5]); u.z = *reinterpret_cast<uint32_t*>(&h);
-    h = __floats2bfloat162_rn(v[6], v[7]); u.w = *reinterpret_cast<uint32_t*>(&h);
-    reinterpret_cast<uint4*>(out)[i] = u;
+    if (esize == 4) {
+      u = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
+    } else {
+      __nv_bfloat162 h;
+      h = __floats2bfloat162_rn(v[0], v[1]); u.x = *reinterpret_cast<uint32_t*>(&h);
+      h = __floats2bfloat162_rn(v[2], v[3]); u.y = *reinterpret_cast<uint32_t*>(&h);
+      h = __floats2bfloat162_rn(v[4], v[5]); u.z = *reinterpret_cast<uint32_t*>(&h);
+      h = __floats2bfloat162_rn(v[6], v[7]); u.w = *reinterpret_cast<uint32_t*>(&h);
+    }
+    out[i] = u;
   }
 }
 
-cudaError_t launch_pack_bf16(const float* x, __nv_bfloat16* out, int nb, long long B, int C,
-                             long long P, int G, int pairs, cudaStream_t s) {
+cudaError_t launch_pack_rows(const float* x, void* out, int nb, int esize, long long B, int C, long long P,
+                             int G, cudaStream_t s) {
   const long long total = B * G * P;
+  if (total == 0) return cudaSuccess;
   long long blocks = (total + 255) / 256;
   const long long cap = (long long)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  pack_bf16_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, out, nb, B, C, P, G, pairs);
+  pack_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, reinterpret_cast<uint4*>(out), nb, esize, B, C, P, G);
   count_launch();
   return cudaGetLastError();
 }

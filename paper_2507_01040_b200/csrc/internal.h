@@ -32,6 +32,8 @@ struct ConvPlan {
   int rb;               // bytes of one A row-group (16 or 32)
   int epg;              // operand elements per row-group (rb / esize)
   int merged_bc;        // tensor-map dim 4 = b*G + g (3-D) instead of separate (g, b) dims
+  int packed;           // operand is a packed 16-byte-group copy (bf16, or fp32 in 1-D)
+  int cpg;              // channels per row-group of the A operand
   int G;                // row-groups per sample in the A tensor (padded)
   int gs;               // row-groups per pipeline stage
   int ks;               // MMA K-steps (32 B of K per row) per stage
@@ -70,8 +72,7 @@ struct ConvKParams {
   const float* bias;          // (NB, C_out)
   float* y;                   // fp32 protocol output (or null)
   __nv_bfloat16* y_bf16;      // bf16 A-ready output (or null)
-  int ybf_pairs;              // 1: 2-D channel-pair interleave (B, Gy, P, 8)
-  int ybf_groups;             // groups per sample of the bf16 output tensor
+  int ybf_groups;             // groups per sample of the packed bf16 output tensor (B, Gy, P, 16 B)
   const float* resid;         // residual source (protocol layout) or null
   int res_side, res_crop;     // residual spatial side and centre-crop offset
   int act_mode;               // -1 none, 0 Linear, 1 Sum, 2 Mean
@@ -99,8 +100,8 @@ cudaError_t launch_expand_ref(const int* g, int k, const float* f, int C_in, int
                               float* out, cudaStream_t s);
 cudaError_t launch_expand_images(const int* g, const ConvPlan& plan, const float* f, int C_in,
                                  int C_out, const float* w_scale, uint8_t* img, cudaStream_t s);
-cudaError_t launch_pack_bf16(const float* x, __nv_bfloat16* out, int nb, long long B, int C,
-                             long long P, int G, int pairs, cudaStream_t s);
+cudaError_t launch_pack_rows(const float* x, void* out, int nb, int esize, long long B, int C, long long P,
+                             int G, cudaStream_t s);
 cudaError_t launch_act(int nb, const ActParams& p, cudaStream_t s);
 // kPrecFp32 operand preparation (slice.cu)
 cudaError_t launch_sample_absmax(const float* x, long long B, long long per_sample, unsigned* amax,

@@ -63,22 +63,24 @@ __global__ void slice_input_kernel(const float* __restrict__ x, const unsigned* 
     if (g == 0 && pp == 0) scale[b] = sc;
     const float inv = 1.f / sc;  // exact (power of two)
     int8_t dg[4][16];
-#pragma unroll
-    for (int cl = 0; cl < 4; ++cl) {
-      if (cl >= cpg) break;
+    for (int cl = 0; cl < cpg; ++cl) {
       const int c = g * cpg + cl;
       float v[8];
-      if (c < C) {
-        const float4* src = reinterpret_cast<const float4*>(x + ((b * C + c) * P + pp) * nb);
-        const float4 q0 = __ldg(src);
-        v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w;
-        if (nb == 8) {
-          const float4 q1 = __ldg(src + 1);
-          v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
-        }
-      } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = 0.f;
+      for (int j = 0; j < 8; ++j) v[j] = 0.f;
+      if (c < C) {
+        const float* src = x + ((b * C + c) * P + pp) * nb;
+        if (nb == 2) {
+          const float2 q = __ldg(reinterpret_cast<const float2*>(src));
+          v[0] = q.x; v[1] = q.y;
+        } else {
+          const float4 q0 = __ldg(reinterpret_cast<const float4*>(src));
+          v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w;
+          if (nb == 8) {
+            const float4 q1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
+            v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
+          }
+        }
       }
       for (int j = 0; j < nb; ++j) {
         int8_t d[4];

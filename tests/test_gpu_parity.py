@@ -85,15 +85,13 @@ def test_conv_golden_cases(golden, prec):
     for n in range(10):
         g = tuple(int(v) for v in golden[f"conv{n}_g"])
         B, ci, co, di, df, k = (int(v) for v in golden[f"conv{n}_dims"])
-        if k == 1:
-            continue
         layer = M.make_conv_layer(M.Dims(B, ci, co, di, df, k), M.Signature(g),
                                   golden[f"conv{n}_f"], golden[f"conv{n}_b"], precision=prec)
         y = run_dev(M.conv_forward, golden[f"conv{n}_x"], layer)
         assert_conv_close(y, golden[f"conv{n}_y"], prec)
 
 
-SIGS = [(1, 1), (-1, 1), (0, 1), (1, 1, 1), (1, -1, 0), (-1, 0, 1), (0, 0, 1)]
+SIGS = [(1,), (-1,), (1, 1), (-1, 1), (0, 1), (1, 1, 1), (1, -1, 0), (-1, 0, 1), (0, 0, 1)]
 
 
 @pytest.mark.parametrize("prec", ["fp32", "3xtf32", "tf32", "bf16"])
@@ -102,7 +100,7 @@ SIGS = [(1, 1), (-1, 1), (0, 1), (1, 1, 1), (1, -1, 0), (-1, 0, 1), (0, 0, 1)]
 def test_conv_signatures(prec, g, padding):
     rng = np.random.default_rng(7)
     k = len(g)
-    d = 9 if k == 2 else 6
+    d = {1: 40, 2: 9, 3: 6}[k]
     x, f, b, layer, pad = make_conv(rng, g, 2, 5, 6, d, 3, prec, padding)
     y = run_dev(M.conv_forward, x, layer)
     assert_conv_close(y, O.conv_ref(x, f, b, g, d, 3, pad), prec)
@@ -118,6 +116,8 @@ def test_conv_signatures(prec, g, padding):
     ((1, 1, 1), 2, 16, 16, 9, 3),
     ((1, 1, 1), 1, 5, 3, 4, 4),   # even filter, valid
     ((1, -1), 3, 33, 17, 11, 3),  # N not a multiple of 32
+    ((1,), 37, 3, 5, 9, 3),       # 1-D: tile rows span samples; odd channels
+    ((-1,), 3, 16, 16, 300, 5),   # 1-D: several position tiles
 ])
 def test_conv_edge_shapes(prec, shape):
     g, B, ci, co, d, df = shape
@@ -201,8 +201,6 @@ def test_conv_shape_errors():
 def test_activation_golden(golden):
     for n in range(int(golden["act_count"])):
         k, mode, K = (int(v) for v in golden[f"act{n}_meta"])
-        if k == 1:
-            continue
         ki = tuple(int(v) for v in golden[f"act{n}_ki"])
         w = golden[f"act{n}_w"] if mode == 0 else None
         b = golden[f"act{n}_bias"] if mode == 0 else None
@@ -220,7 +218,7 @@ def test_activation_spatial_golden(golden):
         assert O.max_abs_error(y, golden[f"sact{mode}_y"]) <= 1e-5
 
 
-@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("k", [1, 2, 3])
 @pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("C,P,B", [(1, 1, 1), (13, 7, 3), (64, 1000, 2), (3, 4097, 1)])
 def test_activation_shapes(k, mode, C, P, B):
@@ -281,14 +279,15 @@ def test_block_golden(golden, name, prec):
     assert_conv_close(y, ref, prec)
 
 
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
 @pytest.mark.parametrize("g,mode,padding,residual", [
     ((1, 1), 0, "same", True), ((1, 1, 1), 2, "same", True), ((1, 1), 1, "valid", False),
-    ((1, -1, 0), 0, "valid", True)])
-def test_block_random(g, mode, padding, residual):
+    ((1, -1, 0), 0, "valid", True), ((1,), 0, "same", True), ((-1,), 1, "valid", False)])
+def test_block_random(g, mode, padding, residual, prec):
     rng = np.random.default_rng(4)
     k = len(g)
     nb = 1 << k
-    B, C, d = 2, 6, 10 if k == 2 else 8
+    B, C, d = 2, 6, {1: 30, 2: 10, 3: 8}[k]
     fan = C * nb * 3 ** k
     f1 = rng.uniform(-1, 1, (nb, C, C, 3 ** k)).astype(np.float32) / np.float32(np.sqrt(fan))
     f2 = rng.uniform(-1, 1, (nb, C, C, 3 ** k)).astype(np.float32) / np.float32(np.sqrt(fan))
@@ -298,10 +297,10 @@ def test_block_random(g, mode, padding, residual):
     ab = (rng.standard_normal(C) * 0.1).astype(np.float32) if mode == 0 else None
     x = rng.standard_normal((B, C, d ** k, nb)).astype(np.float32)
     blk = M.make_basic_block(M.Signature(g), B, C, C, C, d, f1, b1, mode, f2, b2, act_weight=aw, act_bias=ab,
-                             padding=padding, residual=residual)
+                             padding=padding, residual=residual, precision=prec)
     y = run_dev(M.block_forward, x, blk)
     ref = O.block_ref(x, g, d, f1, b1, mode, tuple(range(nb)), aw, ab, f2, b2, padding=padding, residual=residual)
-    assert_conv_close(y, ref, "fp32")
+    assert_conv_close(y, ref, prec)
     yh = M.block_forward(x, blk)  # host path, chunked
     assert np.array_equal(yh, y)
 
