@@ -19,15 +19,17 @@ __global__ void absmax_kernel(const float* __restrict__ x, long long per_sample,
   const int b = blockIdx.y;
   const float* xs = x + (long long)b * per_sample;
   float m = 0.f;
-  const long long n4 = per_sample / 4;
-  const float4* x4 = reinterpret_cast<const float4*>(xs);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+  // samples need not start 16-byte aligned (1-D tensors): scalar head, float4 body, scalar tail
+  const long long head = min<long long>(per_sample, (long long)((16 - (reinterpret_cast<uintptr_t>(xs) & 15)) & 15) / 4);
+  const long long n4 = (per_sample - head) / 4;
+  const float4* x4 = reinterpret_cast<const float4*>(xs + head);
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n4; i += nth) {
     const float4 v = __ldg(x4 + i);
     m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
   }
-  for (long long i = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per_sample;
-       i += (long long)gridDim.x * blockDim.x)
-    m = fmaxf(m, fabsf(xs[i]));
+  if (tid < head) m = fmaxf(m, fabsf(xs[tid]));
+  for (long long i = head + n4 * 4 + tid; i < per_sample; i += nth) m = fmaxf(m, fabsf(xs[i]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(amax + b, __float_as_uint(m));
