@@ -20,7 +20,8 @@ __global__ void absmax_kernel(const float* __restrict__ x, long long per_sample,
   const float* xs = x + (long long)b * per_sample;
   float m = 0.f;
   // samples need not start 16-byte aligned (1-D tensors): scalar head, float4 body, scalar tail
-  const long long head = min<long long>(per_sample, (long long)((16 - (reinterpret_cast<uintptr_t>(xs) & 15)) & 15) / 4);
+  long long head = (long long)((16 - (reinterpret_cast<uintptr_t>(xs) & 15)) & 15) / 4;
+  if (head > per_sample) head = per_sample;
   const long long n4 = (per_sample - head) / 4;
   const float4* x4 = reinterpret_cast<const float4*>(xs + head);
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
