@@ -15,6 +15,7 @@
  *   cl_conv_create         <- conv.make_conv_layer                 conv.py:101-140
  *   cl_conv_forward        <- conv.conv_forward(x, layer, variant) conv.py:371-381
  *   cl_conv_forward_host   <- serve "forward" on a conv handle     serve.py:151-158
+ *   cl_linear_create/forward <- linear.make_linear_layer / linear_forward  linear.py:32-102
  *   cl_act_create          <- activation.make_activation_config    activation.py:57-89
  *   cl_act_forward         <- activation.activation_forward + the
  *                             spatial fold of serve._forward       activation.py:400-416, serve.py:102-119
@@ -72,6 +73,7 @@ typedef enum { CL_PAD_VALID = 0, CL_PAD_SAME = 1 } cl_padding;
 typedef enum { CL_AGG_LINEAR = 0, CL_AGG_SUM = 1, CL_AGG_MEAN = 2 } cl_agg_mode;
 
 typedef struct cl_conv cl_conv;
+typedef struct cl_conv cl_linear; /* a linear layer is a 1x1 conv over samples */
 typedef struct cl_act cl_act;
 typedef struct cl_block cl_block;
 
@@ -109,6 +111,14 @@ int cl_conv_time_kernel(const cl_conv* h, const float* x_dev, float* y_dev, int6
 int cl_conv_forward_host(const cl_conv* h, const float* x_host, float* y_host, int64_t B,
                          void* stream);
 void cl_conv_destroy(cl_conv* h);
+
+/* ---- Clifford linear layer (linear.py:22-107) --------------- */
+/* weight (N_B, C_out, C_in), bias (N_B, C_out); x (B, C_in, N_B) -> y (B, C_out, N_B) */
+int cl_linear_create(const int32_t* g, int k, int C_in, int C_out, const float* weight, const float* bias,
+                     int precision, void* stream, cl_linear** out);
+int cl_linear_forward(const cl_linear* h, const float* x_dev, float* y_dev, int64_t B, void* stream);
+int cl_linear_forward_host(const cl_linear* h, const float* x_host, float* y_host, int64_t B, void* stream);
+void cl_linear_destroy(cl_linear* h);
 
 /* ---- (3) multivector activation ---------------------------------------- */
 int cl_act_create(const int32_t* g, int k, int mode, const int32_t* kernel_indices, int K, int C,

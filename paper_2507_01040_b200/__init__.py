@@ -10,6 +10,7 @@ from .algebra import (Signature, all_valid_signatures, blade_product, product_ta
 from .block import BasicBlock, block_forward, make_basic_block
 from .conv import ConvLayer, build_expanded_kernel, conv_flops, conv_forward, make_conv_layer
 from .layout import Dims, LayoutTag, read_tensor, write_tensor
+from .linear import LinearLayer, linear_flops, linear_forward, make_linear_layer
 from . import errors
 
 __version__ = "0.1.0"

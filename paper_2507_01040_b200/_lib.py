@@ -21,7 +21,8 @@ EXPORTS = (
     "cl_validate_signature", "cl_blade_product", "cl_schedule_terms", "cl_expand_kernel",
     "cl_conv_create", "cl_conv_out_side", "cl_conv_forward", "cl_conv_forward_host",
     "cl_conv_workspace_bytes", "cl_conv_time_kernel", "cl_conv_forward_ws", "cl_block_workspace_bytes", "cl_block_forward_ws",
-    "cl_conv_destroy", "cl_act_create", "cl_act_forward", "cl_act_forward_host",
+    "cl_conv_destroy", "cl_linear_create", "cl_linear_forward", "cl_linear_forward_host",
+    "cl_linear_destroy", "cl_act_create", "cl_act_forward", "cl_act_forward_host",
     "cl_act_destroy", "cl_block_create", "cl_block_forward", "cl_block_forward_host",
     "cl_block_destroy", "cl_last_error", "cl_launch_count", "cl_version",
 )
@@ -56,6 +57,10 @@ def load():
         "cl_block_workspace_bytes": (C.c_size_t, [P, C.c_int64]),
         "cl_block_forward_ws": (C.c_int, [P, P, P, C.c_int64, P, C.c_size_t, P]),
         "cl_conv_destroy": (None, [P]),
+        "cl_linear_create": (C.c_int, [I32P, C.c_int, C.c_int, C.c_int, P, P, C.c_int, P, C.POINTER(P)]),
+        "cl_linear_forward": (C.c_int, [P, P, P, C.c_int64, P]),
+        "cl_linear_forward_host": (C.c_int, [P, P, P, C.c_int64, P]),
+        "cl_linear_destroy": (None, [P]),
         "cl_act_create": (C.c_int, [I32P, C.c_int, C.c_int, I32P, C.c_int, C.c_int, P, P, P, C.POINTER(P)]),
         "cl_act_forward": (C.c_int, [P, P, P, C.c_int64, C.c_int64, P]),
         "cl_act_forward_host": (C.c_int, [P, P, P, C.c_int64, C.c_int64, P]),

@@ -106,6 +106,7 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
   pl = ConvPlan{};
   pl.k = k;
   pl.nb = nb;
+  pl.ka = nb == 2 ? 1 : (nb == 4 ? 2 : 3);
   pl.prec = prec;
   const bool i8 = prec == kPrecFp32;
   pl.esize = i8 ? 1 : (prec == kPrecBf16 ? 2 : 4);
@@ -122,7 +123,8 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
   const int gpk = 32 / pl.rb;  // row-groups per 32-byte K step
 
   // output tile (tx * ty * tz == 128); in 1-D the rows span (position, sample)
-  int tx = std::min(128, std::max(8, pow2_at_least(d_out)));
+  // (d_out = 1, the linear layer: 128 samples per tile)
+  int tx = std::min(128, std::max(k == 1 ? 1 : 8, pow2_at_least(d_out)));
   int ty, tz;
   if (k == 1 || k == 2) {
     ty = 128 / tx;
@@ -258,6 +260,7 @@ struct HostPipe {
 struct cl_conv {
   int g[3];
   int k, nb, C_in, C_out, d_image, d_filter, pad, d_out, prec;
+  int sk;  // spatial rank (== k for convolutions, 1 for the linear layer)
   float* filters = nullptr;  // (NB, C_in, C_out, Q) device copy
   float* bias = nullptr;     // (NB, C_out)
   uint8_t* img = nullptr;    // tensor-core operand images
@@ -328,10 +331,13 @@ int cl_expand_kernel(const int32_t* g, int k, const float* filters_dev, int C_in
   return CL_OK;
 }
 
+}  // extern "C"
+
 // ---- conv ------------------------------------------------------------------
-int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, int d_filter,
-                   int padding, int precision, const float* filters, const float* bias,
-                   void* stream, cl_conv** out) {
+// k = algebra rank (N_B = 2^k), sk = spatial rank of the layer
+static int conv_create_impl(const int32_t* g, int k, int sk, int C_in, int C_out, int d_image, int d_filter,
+                            int padding, int precision, const float* filters, const float* bias, void* stream,
+                            cl_conv** out) {
   if (!out) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null output handle pointer");
   *out = nullptr;
   if (int st = check_sig(g, k)) return st;
@@ -355,6 +361,7 @@ int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, in
   cl_conv* h = new cl_conv();
   for (int a = 0; a < 3; ++a) h->g[a] = a < k ? g[a] : 0;
   h->k = k;
+  h->sk = sk;
   h->nb = 1 << k;
   h->C_in = C_in;
   h->C_out = C_out;
@@ -363,11 +370,11 @@ int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, in
   h->pad = pad;
   h->d_out = d_out;
   h->prec = precision;
-  if (precision == CL_PREC_FP32 && (long long)ipow(d_filter, k) * C_in * (1 << k) > 32000) {
+  if (precision == CL_PREC_FP32 && (long long)ipow(d_filter, sk) * C_in * (1 << k) > 32000) {
     delete h;  // s32 level accumulators: 4 pairs x 128 x 128 x K must stay below 2^31
     return fail(CL_ERR_UNSUPPORTED, "Unsupported", "fp32 mode supports K = d_filter^k * C_in * N_B <= 32000");
   }
-  if (!plan_conv(k, h->nb, precision, C_in, C_out, d_out, d_filter, h->plan)) {
+  if (!plan_conv(sk, h->nb, precision, C_in, C_out, d_out, d_filter, h->plan)) {
     delete h;
     return fail(CL_ERR_UNSUPPORTED, "Unsupported", "no shared-memory plan fits this layer");
   }
@@ -393,6 +400,42 @@ int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, in
   *out = h;
   return CL_OK;
 }
+
+extern "C" {
+
+int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, int d_filter, int padding,
+                   int precision, const float* filters, const float* bias, void* stream, cl_conv** out) {
+  return conv_create_impl(g, k, k, C_in, C_out, d_image, d_filter, padding, precision, filters, bias, stream, out);
+}
+
+// Clifford linear layer (linear.py:22-107): out[b, co] = bias[co] + sum_ci w[co, ci] * x[b, ci]
+// (geometric product, weight first) == a 1x1 "conv" whose 1-D rows are the
+// samples: spatial rank 1, d_image = d_filter = 1, weight (N_B, C_out, C_in)
+// transposed to the filter layout (N_B, C_in, C_out, 1).
+int cl_linear_create(const int32_t* g, int k, int C_in, int C_out, const float* weight, const float* bias,
+                     int precision, void* stream, cl_linear** out) {
+  if (int st = check_sig(g, k)) return st;
+  if (C_in < 1 || C_out < 1 || !weight || !bias)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "C_in, C_out >= 1 and weight/bias required");
+  const int nb = 1 << k;
+  std::vector<float> w((size_t)nb * C_out * C_in), f((size_t)nb * C_in * C_out);
+  CL_CUDA(cudaMemcpy(w.data(), weight, w.size() * 4, cudaMemcpyDefault), "linear weight copy");
+  for (int i = 0; i < nb; ++i)
+    for (int co = 0; co < C_out; ++co)
+      for (int ci = 0; ci < C_in; ++ci)
+        f[((size_t)i * C_in + ci) * C_out + co] = w[((size_t)i * C_out + co) * C_in + ci];
+  return conv_create_impl(g, k, 1, C_in, C_out, 1, 1, CL_PAD_VALID, precision, f.data(), bias, stream, out);
+}
+
+int cl_linear_forward(const cl_linear* h, const float* x, float* y, int64_t B, void* stream) {
+  return cl_conv_forward(h, x, y, B, stream);
+}
+
+int cl_linear_forward_host(const cl_linear* h, const float* x, float* y, int64_t B, void* stream) {
+  return cl_conv_forward_host(h, x, y, B, stream);
+}
+
+void cl_linear_destroy(cl_linear* h) { cl_conv_destroy(h); }
 
 int cl_conv_out_side(const cl_conv* h, int* d_out) {
   if (!h || !d_out) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null handle");
@@ -444,7 +487,7 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
   box[2] = (cuuint32_t)pl.ty;
   strides[0] = rowb;
   dims[1] = D;
-  if (h->k == 1) {
+  if (h->sk == 1) {
     // (e, x, sample, group, plane) over a (plane, B, G, D, 16 B) tensor
     dims[2] = (cuuint64_t)B;
     dims[3] = Gt;
@@ -486,7 +529,7 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
 // amax/scale (fp32 mode) or the packed bf16 input (bf16 mode).
 static size_t conv_ws_bytes(const cl_conv* h, long long B, bool prepacked) {
   const ConvPlan& pl = h->plan;
-  const size_t P_in = (size_t)ipow(h->d_image, h->k);
+  const size_t P_in = (size_t)ipow(h->d_image, h->sk);
   if (pl.prec == kPrecFp32) return align_up((size_t)kDigitsA * B * pl.G * P_in * 16, 256) + align_up((size_t)B * 8, 256);
   if (pl.packed && !prepacked) return align_up((size_t)B * pl.G * P_in * 16, 256);
   return 0;
@@ -499,7 +542,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
                     const Epi& epi, void* ws, cudaStream_t s) {
   const ConvPlan& pl = h->plan;
   if (B == 0) return CL_OK;
-  const long long P_in = (long long)ipow(h->d_image, h->k);
+  const long long P_in = (long long)ipow(h->d_image, h->sk);
   float* a_scale = nullptr;
   const void* src = x;
   const bool prep = !g_time_kernel_only;
@@ -526,7 +569,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   if (int st = encode_input_map(h, src, B, &map)) return st;
   ConvKParams p{};
   p.B = (int)B;
-  p.k = h->k;
+  p.k = h->sk;
   p.nb = h->nb;
   p.d_in = h->d_image;
   p.d_out = h->d_out;
@@ -535,13 +578,13 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.ty = pl.ty;
   p.tz = pl.tz;
   p.ntx = (h->d_out + pl.tx - 1) / pl.tx;
-  p.nty = h->k == 1 ? (int)((B + pl.ty - 1) / pl.ty) : (h->d_out + pl.ty - 1) / pl.ty;  // 1-D: tiles along the batch
-  p.ntz = h->k == 3 ? (h->d_out + pl.tz - 1) / pl.tz : 1;
+  p.nty = h->sk == 1 ? (int)((B + pl.ty - 1) / pl.ty) : (h->d_out + pl.ty - 1) / pl.ty;  // 1-D: tiles along the batch
+  p.ntz = h->sk == 3 ? (h->d_out + pl.tz - 1) / pl.tz : 1;
   p.n_ntiles = pl.n_ntiles;
   p.n_tile = pl.n_tile;
   p.N = pl.N;
   p.C_out = h->C_out;
-  p.num_m_tiles = (h->k == 1 ? 1LL : (long long)B) * p.ntz * p.nty * p.ntx;
+  p.num_m_tiles = (h->sk == 1 ? 1LL : (long long)B) * p.ntz * p.nty * p.ntx;
   // CTA pairs share each B stage by TMA multicast where it pays (measured:
   // +4-6% for the int8 and bf16 modes; the tf32 modes run faster unpaired)
   p.cs = (p.num_m_tiles >= 2 && !g_no_cluster && (pl.prec == kPrecFp32 || pl.prec == kPrecBf16)) ? 2 : 1;
@@ -690,8 +733,8 @@ int cl_conv_time_kernel(const cl_conv* h, const float* x, float* y, int64_t B, i
 
 int cl_conv_forward_host(const cl_conv* h, const float* xh, float* yh, int64_t B, void* stream) {
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null conv handle");
-  const size_t in_per = (size_t)h->C_in * ipow(h->d_image, h->k) * h->nb * 4;
-  const size_t out_per = (size_t)h->C_out * ipow(h->d_out, h->k) * h->nb * 4;
+  const size_t in_per = (size_t)h->C_in * ipow(h->d_image, h->sk) * h->nb * 4;
+  const size_t out_per = (size_t)h->C_out * ipow(h->d_out, h->sk) * h->nb * 4;
   return host_chunked(
       h->host, B, in_per, out_per, 0, xh, yh, (cudaStream_t)stream,
       [&](long long nb) { return conv_ws_bytes(h, nb, false); },
@@ -795,7 +838,7 @@ int cl_block_create(const cl_conv* c1, const cl_act* act, const cl_conv* c2, int
   if (!out) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null output handle pointer");
   *out = nullptr;
   if (!c1 || !act || !c2) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "block needs conv1, act and conv2");
-  if (c1->k != c2->k || act->k != c1->k)
+  if (c1->k != c2->k || act->k != c1->k || c1->sk != c1->k || c2->sk != c2->k)
     return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "block layers disagree on k");
   for (int a = 0; a < c1->k; ++a)
     if (c1->g[a] != c2->g[a]) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "block convs disagree on signature");

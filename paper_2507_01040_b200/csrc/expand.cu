@@ -117,8 +117,8 @@ cudaError_t launch_expand_ref(const int* g, int k, const float* f, int C_in, int
 
 cudaError_t launch_expand_images(const int* g, const ConvPlan& pl, const float* f, int C_in,
                                  int C_out, const float* w_scale, uint8_t* img, cudaStream_t s) {
-  Sig sg{{0, 0, 0}, pl.k};
-  for (int i = 0; i < pl.k; ++i) sg.g[i] = g[i];
+  Sig sg{{0, 0, 0}, pl.ka};
+  for (int i = 0; i < pl.ka; ++i) sg.g[i] = g[i];
   const long long total =
       (long long)pl.n_ntiles * pl.k_iters * (pl.ks * 32 / pl.esize) * pl.n_tile;
   expand_img_kernel<<<grid_for(total), 256, 0, s>>>(sg, f, C_in, C_out, pl, w_scale, img);

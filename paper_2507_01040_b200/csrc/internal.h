@@ -27,6 +27,7 @@ constexpr int kMaxSmem = 232448;     // 227 KB opt-in dynamic shared memory per 
 // its CPU kernel parameters at the same point).
 struct ConvPlan {
   int k, nb;            // spatial rank, blades
+  int ka;               // algebra rank (nb = 2^ka); differs from k for the linear layer
   int prec;             // Prec
   int esize;            // operand element bytes (4 fp32/tf32, 2 bf16)
   int rb;               // bytes of one A row-group (16 or 32)

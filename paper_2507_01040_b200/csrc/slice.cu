@@ -149,7 +149,7 @@ __global__ void weight_colscale_kernel(int g0, int g1, int g2, int k, const floa
 cudaError_t launch_weight_colscale(const int* g, const ConvPlan& pl, const float* f, int C_in, int C_out,
                                    float* w_scale, cudaStream_t s) {
   const int N_pad = pl.n_ntiles * pl.n_tile;
-  weight_colscale_kernel<<<N_pad, 256, 0, s>>>(g[0], g[1], g[2], pl.k, f, C_in, C_out, pl.Q, N_pad, w_scale);
+  weight_colscale_kernel<<<N_pad, 256, 0, s>>>(g[0], g[1], g[2], pl.ka, f, C_in, C_out, pl.Q, N_pad, w_scale);
   count_launch();
   return cudaGetLastError();
 }

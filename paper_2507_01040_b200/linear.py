@@ -1,0 +1,103 @@
+"""Clifford linear layer on the B200.
+
+Drop-in for linear.py:22-107 of the reference: `make_linear_layer(sig,
+weight (N_B, C_out, C_in), bias (N_B, C_out))`, `linear_forward(x (B, C_in,
+N_B), layer, variant)` and `linear_flops`. The layer runs on the same
+tcgen05 implicit-GEMM kernel as the convolution (a 1x1 conv whose rows are
+the samples, 128 samples per tile), in any of the four precision modes.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device, _lib
+from .algebra import Signature, schedule_flop_count
+from .conv import PRECISIONS, _out
+from .errors import ShapeMismatch
+
+VARIANTS = ("b200", "reference", "gemm")
+
+
+@dataclass(frozen=True, eq=False)
+class LinearLayer:
+    sig: Signature
+    C_in: int
+    C_out: int
+    weight: np.ndarray  # (N_B, C_out, C_in) float32, frozen
+    bias: np.ndarray    # (N_B, C_out) float32, frozen
+    precision: str = "fp32"
+    _handles: dict = field(default_factory=dict, repr=False)
+
+    def handle(self) -> int:
+        dev = _device.current_device()
+        h = self._handles.get(dev)
+        if h is None:
+            lib = _lib.load()
+            out = C.c_void_p()
+            w = np.ascontiguousarray(self.weight)
+            b = np.ascontiguousarray(self.bias)
+            _lib.check(lib.cl_linear_create(
+                _lib.int32_array(self.sig.g), self.sig.k, self.C_in, self.C_out,
+                C.c_void_p(w.ctypes.data), C.c_void_p(b.ctypes.data), PRECISIONS[self.precision],
+                C.c_void_p(_device.stream_ptr()), C.byref(out)))
+            h = _device.Handle(out.value, lib.cl_linear_destroy)
+            self._handles[dev] = h
+        return h.ptr
+
+
+def make_linear_layer(sig: Signature, weight, bias, *, precision: str = "fp32") -> LinearLayer:
+    """Checks of linear.py:32-47 (same exceptions)."""
+    if not 1 <= sig.k <= 3:
+        raise ShapeMismatch(f"linear layer supports k in {{1,2,3}}, got k={sig.k}")
+    w = np.asarray(weight.detach().cpu().numpy() if hasattr(weight, "detach") else weight)
+    b = np.asarray(bias.detach().cpu().numpy() if hasattr(bias, "detach") else bias)
+    nb = sig.n_blades
+    if w.ndim != 3 or w.shape[0] != nb:
+        raise ShapeMismatch(f"weight shape {w.shape}, expected (N_B={nb}, C_out, C_in)")
+    _, c_out, c_in = w.shape
+    if b.shape != (nb, c_out):
+        raise ShapeMismatch(f"bias shape {b.shape}, expected {(nb, c_out)}")
+    if precision not in PRECISIONS:
+        raise ValueError(f"unknown precision {precision!r}")
+    return LinearLayer(sig, c_in, c_out, _device.frozen_f32(w), _device.frozen_f32(b), precision)
+
+
+def linear_forward(x, layer: LinearLayer, variant: str = "b200", out=None):
+    """(B, C_in, N_B) -> (B, C_out, N_B) (linear.py:97-102) on the B200."""
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown linear variant {variant!r}")
+    nb = layer.sig.n_blades
+    if x.ndim != 3 or x.shape[1] != layer.C_in or x.shape[2] != nb:
+        raise ShapeMismatch(f"input shape {tuple(x.shape)}, expected (B, {layer.C_in}, {nb})")
+    B = int(x.shape[0])
+    shape = (B, layer.C_out, nb)
+    lib = _lib.load()
+    if _device.is_cuda_tensor(x):
+        torch = _device.torch_mod()
+        with torch.cuda.device(x.device):
+            xc = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
+            y = _out(out, shape, x.device)
+            _lib.check(lib.cl_linear_forward(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
+                                             C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
+        return y
+    if _device.is_cpu_tensor(x):
+        xc = x.float().contiguous()
+        y = _out(out, shape, None, pinned=xc.is_pinned())
+        _lib.check(lib.cl_linear_forward_host(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
+                                              C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
+        return y
+    xa = np.ascontiguousarray(x, dtype=np.float32)
+    y = out if out is not None else np.empty(shape, dtype=np.float32)
+    _lib.check(lib.cl_linear_forward_host(C.c_void_p(layer.handle()), C.c_void_p(xa.ctypes.data),
+                                          C.c_void_p(y.ctypes.data), B, C.c_void_p(_device.stream_ptr())))
+    return y
+
+
+def linear_flops(B: int, C_in: int, C_out: int, sig_or_layer) -> int:
+    """B * C_out * (C_in * 2*terms + N_B) (linear.py:105-107)."""
+    sig = getattr(sig_or_layer, "sig", sig_or_layer)
+    return B * C_out * (C_in * schedule_flop_count(sig) + sig.n_blades)

@@ -202,6 +202,26 @@ def main():
         out["mvtf_arr"] = arr
         out["mvtf_bytes"] = np.frombuffer(open(p, "rb").read(), dtype=np.uint8)
 
+    # 9. Clifford linear layer (linear.py:58-102): fp64 oracle and the gemm variant
+    lrng = np.random.default_rng(7)
+    lin_cases = [((1,), 5, 3, 4), ((1, 1), 7, 6, 5), ((0, 1), 3, 2, 3), ((1, 1, 1), 9, 5, 4),
+                 ((1, -1, 0), 4, 3, 6), ((-1, 0, 1), 2, 8, 8)]
+    for n, (g, B, ci, co) in enumerate(lin_cases):
+        sig = mk.Signature(g)
+        nb = sig.n_blades
+        w = (lrng.standard_normal((nb, co, ci)) / np.sqrt(ci * nb)).astype(np.float32)
+        b = (lrng.standard_normal((nb, co)) * 0.1).astype(np.float32)
+        x = lrng.standard_normal((B, ci, nb)).astype(np.float32)
+        layer = mk.make_linear_layer(sig, w, b)
+        out[f"lin{n}_g"] = np.array(g, dtype=np.int64)
+        out[f"lin{n}_x"] = x
+        out[f"lin{n}_w"] = w
+        out[f"lin{n}_b"] = b
+        out[f"lin{n}_y"] = mk.linear_reference(x, layer)
+        out[f"lin{n}_y_gemm"] = mk.linear_forward(x, layer, "gemm")
+        out[f"lin{n}_flops"] = np.array(mk.linear_flops(B, ci, co, layer.schedule))
+    out["lin_count"] = np.array(len(lin_cases))
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
     print("wrote", len(out), "arrays")
 

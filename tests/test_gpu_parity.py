@@ -312,3 +312,29 @@ def test_launch_counter_moves():
     M.activation_forward(torch.zeros((1, 1, 4), device="cuda"), cfg)
     torch.cuda.synchronize()
     assert _lib.launch_count() > n0
+
+
+# ---- Clifford linear layer --------------------------------------------
+
+@pytest.mark.parametrize("prec", ["fp32", "3xtf32", "tf32", "bf16"])
+def test_linear_golden(golden, prec):
+    for n in range(int(golden["lin_count"])):
+        g = tuple(int(v) for v in golden[f"lin{n}_g"])
+        layer = M.make_linear_layer(M.Signature(g), golden[f"lin{n}_w"], golden[f"lin{n}_b"], precision=prec)
+        y = run_dev(M.linear_forward, golden[f"lin{n}_x"], layer)
+        assert_conv_close(y, golden[f"lin{n}_y"], prec)
+
+
+@pytest.mark.parametrize("g", [(1,), (1, 1), (1, 1, 1), (0, 1, -1)])
+@pytest.mark.parametrize("B,ci,co", [(1, 1, 1), (300, 64, 48), (129, 7, 33)])
+def test_linear_shapes(g, B, ci, co):
+    rng = np.random.default_rng(B + ci)
+    nb = 1 << len(g)
+    w = (rng.standard_normal((nb, co, ci)) / np.sqrt(ci * nb)).astype(np.float32)
+    b = (rng.standard_normal((nb, co)) * 0.1).astype(np.float32)
+    x = rng.standard_normal((B, ci, nb)).astype(np.float32)
+    layer = M.make_linear_layer(M.Signature(g), w, b)
+    y = run_dev(M.linear_forward, x, layer)
+    assert_conv_close(y, O.linear_ref(x, w, b, g), "fp32")
+    yh = M.linear_forward(x, layer)  # host path
+    np.testing.assert_array_equal(yh, y)

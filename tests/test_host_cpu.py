@@ -147,3 +147,17 @@ def test_no_oracle_in_product():
             if f.endswith(".py"):
                 src = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_linear_validation_and_flops(golden):
+    s2 = M.Signature((1, 1))
+    with pytest.raises(E.ShapeMismatch):
+        M.make_linear_layer(s2, np.zeros((3, 2, 2)), np.zeros((4, 2)))
+    with pytest.raises(E.ShapeMismatch):
+        M.make_linear_layer(s2, np.zeros((4, 2, 3)), np.zeros((4, 3)))
+    layer = M.make_linear_layer(s2, np.zeros((4, 2, 3)), np.zeros((4, 2)))
+    assert (layer.C_in, layer.C_out) == (3, 2)
+    for n in range(int(golden["lin_count"])):
+        g = tuple(int(v) for v in golden[f"lin{n}_g"])
+        x, w = golden[f"lin{n}_x"], golden[f"lin{n}_w"]
+        assert M.linear_flops(x.shape[0], x.shape[1], w.shape[1], M.Signature(g)) == int(golden[f"lin{n}_flops"])

@@ -132,3 +132,13 @@ def test_mvtf_bytes(golden):
     data, tag, k = O.mvtf_decode(raw)
     np.testing.assert_array_equal(data, golden["mvtf_arr"])
     assert (tag, k) == (1, 2)
+
+
+def test_linear_oracle_matches_reference(golden):
+    for n in range(int(golden["lin_count"])):
+        g = tuple(int(v) for v in golden[f"lin{n}_g"])
+        x, w, b = golden[f"lin{n}_x"], golden[f"lin{n}_w"], golden[f"lin{n}_b"]
+        y = O.linear_ref(x, w, b, g)
+        np.testing.assert_allclose(y, golden[f"lin{n}_y"], rtol=2e-7, atol=1e-9)
+        assert O.max_rel_error(y, golden[f"lin{n}_y_gemm"]) <= 1e-4
+        assert O.linear_flops(x.shape[0], x.shape[1], w.shape[1], g) == int(golden[f"lin{n}_flops"])
