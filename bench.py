@@ -136,17 +136,35 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("BENCH_SHARE_GPU"):
+            # validation of the multi-rank code path on a 1-GPU box: every rank on
+            # cuda:0, gloo for the (host-side) broadcast / max-reduce; no kernel of
+            # one rank ever waits on another rank
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     return world, rank, local
 
 
+def _gloo():
+    import torch.distributed as dist
+    return dist.get_backend() == "gloo"
+
+
 def bcast(t, world):
     if world > 1:
         import torch.distributed as dist
-        dist.broadcast(t, src=0)
+        if _gloo():
+            c = t.cpu()
+            dist.broadcast(c, src=0)
+            t.copy_(c)
+        else:
+            dist.broadcast(t, src=0)
     return t
 
 
@@ -161,7 +179,7 @@ def max_over_ranks(v, world):
     if world == 1:
         return v
     import torch.distributed as dist
-    t = torch.tensor([v], device="cuda", dtype=torch.float64)
+    t = torch.tensor([v], device="cpu" if _gloo() else "cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
