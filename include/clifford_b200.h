@@ -82,6 +82,10 @@ int cl_validate_signature(const int32_t* g, int k);
 int cl_blade_product(int i_mask, int j_mask, const int32_t* g, int k, int* target, int* coeff);
 /* number of surviving FMA terms of the signature schedule, or -status */
 int cl_schedule_terms(const int32_t* g, int k);
+/* change of basis used by the conv for this signature:
+ * returns 1 and fills ncol, w and the 8x8 row-major transform T (x' = T x,
+ * T T^T = 2 I) if the algebra is a full 2x2 matrix algebra, 0 if none, -status */
+int cl_basis_info(const int32_t* g, int k, int* ncol, int* w, int8_t* T64);
 
 /* ---- (1) on-device Clifford kernel construction ----------------------- */
 /* Writes the (C_out*N_B, C_in*N_B, Q) real filter of conv.py:188-202 from

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libclifford_b200.so")
 _lib = None
 
 EXPORTS = (
-    "cl_validate_signature", "cl_blade_product", "cl_schedule_terms", "cl_expand_kernel",
+    "cl_validate_signature", "cl_blade_product", "cl_schedule_terms", "cl_basis_info", "cl_expand_kernel",
     "cl_conv_create", "cl_conv_out_side", "cl_conv_forward", "cl_conv_forward_host",
     "cl_conv_workspace_bytes", "cl_conv_time_kernel", "cl_conv_forward_ws", "cl_block_workspace_bytes", "cl_block_forward_ws",
     "cl_conv_destroy", "cl_linear_create", "cl_linear_forward", "cl_linear_forward_host",
@@ -45,6 +45,7 @@ def load():
         "cl_validate_signature": (C.c_int, [I32P, C.c_int]),
         "cl_blade_product": (C.c_int, [C.c_int, C.c_int, I32P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "cl_schedule_terms": (C.c_int, [I32P, C.c_int]),
+        "cl_basis_info": (C.c_int, [I32P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int8)]),
         "cl_expand_kernel": (C.c_int, [I32P, C.c_int, P, C.c_int, C.c_int, C.c_int, P, P]),
         "cl_conv_create": (C.c_int, [I32P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                      P, P, P, C.POINTER(P)]),

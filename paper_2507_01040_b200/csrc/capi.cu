@@ -22,6 +22,7 @@ namespace cl {
 static thread_local std::string g_last_error;
 static thread_local bool g_time_kernel_only = false;  // cl_conv_time_kernel: skip operand preparation
 static bool g_no_cluster = getenv("CL_NO_CLUSTER") != nullptr;  // debug: disable B multicast
+static bool g_no_basis = getenv("CL_NO_BASIS") != nullptr;      // A/B: disable the change of basis
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -101,37 +102,42 @@ static int pow2_at_least(int v) {
 // ---------------------------------------------------------------------------
 // planning
 // ---------------------------------------------------------------------------
-static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, int d_filter,
+static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, int d_filter, const Basis& bs,
                       ConvPlan& pl) {
   pl = ConvPlan{};
   pl.k = k;
   pl.nb = nb;
   pl.ka = nb == 2 ? 1 : (nb == 4 ? 2 : 3);
   pl.prec = prec;
+  pl.bs = bs;
   const bool i8 = prec == kPrecFp32;
+  const int wk = bs.on ? bs.w : nb;          // K (and N) elements per channel
+  const int ncol = bs.on ? bs.ncol : 1;      // GEMM rows per output pixel
   pl.esize = i8 ? 1 : (prec == kPrecBf16 ? 2 : 4);
   // A operand: int8 digit planes (i8), a packed 16-byte-group copy (bf16; fp32
-  // in 1-D where a multivector is only 8 B), or the protocol tensor itself
-  pl.packed = !i8 && (prec == kPrecBf16 || nb == 2);
+  // in 1-D where a multivector is only 8 B; any mode in a changed basis), or
+  // the protocol tensor itself
+  pl.packed = !i8 && (prec == kPrecBf16 || nb == 2 || bs.on);
   pl.rb = (pl.packed || i8) ? 16 : nb * 4;
   pl.epg = pl.rb / pl.esize;
-  pl.cpg = std::max(1, pl.epg / nb);
+  pl.cpg = std::max(1, pl.epg / wk);
   pl.merged_bc = (k == 3);
   pl.d_filter = d_filter;
   pl.Q = ipow(d_filter, k);
   const int G_real = (C_in + pl.cpg - 1) / pl.cpg;  // row-groups per sample
   const int gpk = 32 / pl.rb;  // row-groups per 32-byte K step
 
-  // output tile (tx * ty * tz == 128); in 1-D the rows span (position, sample)
-  // (d_out = 1, the linear layer: 128 samples per tile)
-  int tx = std::min(128, std::max(k == 1 ? 1 : 8, pow2_at_least(d_out)));
+  // output tile (tx * ty * tz == 128 / ncol pixels); in 1-D the rows span
+  // (position, sample) (d_out = 1, the linear layer: 128 samples per tile)
+  const int tpix = kTileM / ncol;
+  int tx = std::min(tpix, std::max(k == 1 ? 1 : 8, pow2_at_least(d_out)));
   int ty, tz;
   if (k == 1 || k == 2) {
-    ty = 128 / tx;
+    ty = tpix / tx;
     tz = 1;
   } else {
-    ty = std::min(128 / tx, pow2_at_least(d_out));
-    tz = 128 / (tx * ty);
+    ty = std::min(tpix / tx, pow2_at_least(d_out));
+    tz = tpix / (tx * ty);
   }
   pl.tx = tx;
   pl.ty = ty;
@@ -143,7 +149,7 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
   pl.levels = i8 ? kLevels : 1;
   pl.acc_slots = i8 ? 1 : 2;
   const int max_tile = i8 ? 128 : 256;  // levels x n_tile x slots <= 512 TMEM columns
-  pl.N = C_out * nb;
+  pl.N = C_out * wk;
   pl.n_ntiles = (pl.N + max_tile - 1) / max_tile;
   const int per = (pl.N + pl.n_ntiles - 1) / pl.n_ntiles;
   pl.n_tile = ((per + 31) / 32) * 32;
@@ -172,7 +178,7 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
     c.gs = gs;
     c.G = G;
     c.n_gs = n_gs;
-    c.cps = gs * c.epg / nb;
+    c.cps = gs * c.epg / wk;
     c.k_iters = pl.Q * n_gs;
     c.a_bytes = (uint32_t)(kTileM * gs * pl.rb);
     c.b_img_bytes = (uint32_t)(ks * pl.n_tile * 32);
@@ -308,6 +314,18 @@ int cl_blade_product(int i, int j, const int32_t* g, int k, int* target, int* co
   return CL_OK;
 }
 
+int cl_basis_info(const int32_t* g, int k, int* ncol, int* w, int8_t* T64) {
+  if (int st = check_sig(g, k)) return -st;
+  int gi[3] = {0, 0, 0};
+  for (int a = 0; a < k; ++a) gi[a] = g[a];
+  Basis bs{};
+  if (!find_basis(gi, k, &bs)) return 0;
+  if (ncol) *ncol = bs.ncol;
+  if (w) *w = bs.w;
+  if (T64) memcpy(T64, bs.T, 64);
+  return 1;
+}
+
 int cl_schedule_terms(const int32_t* g, int k) {
   if (int st = check_sig(g, k)) return -st;
   int gi[3] = {0, 0, 0};
@@ -374,7 +392,9 @@ static int conv_create_impl(const int32_t* g, int k, int sk, int C_in, int C_out
     delete h;  // s32 level accumulators: 4 pairs x 128 x 128 x K must stay below 2^31
     return fail(CL_ERR_UNSUPPORTED, "Unsupported", "fp32 mode supports K = d_filter^k * C_in * N_B <= 32000");
   }
-  if (!plan_conv(sk, h->nb, precision, C_in, C_out, d_out, d_filter, h->plan)) {
+  Basis bs{};
+  if (sk >= 2 && sk == k && !g_no_basis) find_basis(h->g, k, &bs);
+  if (!plan_conv(sk, h->nb, precision, C_in, C_out, d_out, d_filter, bs, h->plan)) {
     delete h;
     return fail(CL_ERR_UNSUPPORTED, "Unsupported", "no shared-memory plan fits this layer");
   }
@@ -476,13 +496,14 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
   cuuint64_t strides[4];
   cuuint32_t box[5];
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  const cuuint64_t rowb = (cuuint64_t)pl.rb;
+  const int ncol = pl.bs.on ? pl.bs.ncol : 1;
+  const cuuint64_t rowb = (cuuint64_t)pl.rb * ncol;  // bytes per pixel of one row-group
   const bool i8 = pl.prec == kPrecFp32;
   const bool own = pl.packed || i8;  // operand written by our pack / slice pass: G groups per sample
   const cuuint64_t planes = (cuuint64_t)pl.n_tma_a;  // int8 digit planes stacked over the batch
   const cuuint64_t Gt = own ? (cuuint64_t)pl.G : (cuuint64_t)h->C_in;
-  dims[0] = (cuuint64_t)pl.epg;
-  box[0] = (cuuint32_t)pl.epg;
+  dims[0] = (cuuint64_t)pl.epg * ncol;
+  box[0] = (cuuint32_t)(pl.epg * ncol);
   box[1] = (cuuint32_t)pl.tx;
   box[2] = (cuuint32_t)pl.ty;
   strides[0] = rowb;
@@ -519,7 +540,7 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
   const CUtensorMapDataType dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                     : (pl.esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
   CUresult r = enc(map, dt, 5, const_cast<void*>(xsrc), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   pl.rb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   (pl.rb == 32 && ncol == 1) ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CL_ERR_CUDA, "CudaError", "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return CL_OK;
@@ -529,7 +550,7 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
 // amax/scale (fp32 mode) or the packed bf16 input (bf16 mode).
 static size_t conv_ws_bytes(const cl_conv* h, long long B, bool prepacked) {
   const ConvPlan& pl = h->plan;
-  const size_t P_in = (size_t)ipow(h->d_image, h->sk);
+  const size_t P_in = (size_t)ipow(h->d_image, h->sk) * (pl.bs.on ? pl.bs.ncol : 1);  // rows per sample
   if (pl.prec == kPrecFp32) return align_up((size_t)kDigitsA * B * pl.G * P_in * 16, 256) + align_up((size_t)B * 8, 256);
   if (pl.packed && !prepacked) return align_up((size_t)B * pl.G * P_in * 16, 256);
   return 0;
@@ -547,21 +568,21 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   const void* src = x;
   const bool prep = !g_time_kernel_only;
   if (pl.prec == kPrecFp32) {
-    const size_t bytes = align_up((size_t)kDigitsA * B * pl.G * P_in * 16, 256);
+    const size_t bytes = align_up((size_t)kDigitsA * B * pl.G * P_in * (pl.bs.on ? pl.bs.ncol : 1) * 16, 256);
     int8_t* digits = reinterpret_cast<int8_t*>(ws);
     unsigned* amax = reinterpret_cast<unsigned*>(digits + bytes);
     a_scale = reinterpret_cast<float*>(digits + bytes + (size_t)B * 4);
     const long long per_sample = (long long)h->C_in * P_in * h->nb;
     if (prep) {
       CL_CUDA(launch_sample_absmax(x, B, per_sample, amax, s), "absmax");
-      CL_CUDA(launch_slice_input(x, amax, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G, s), "slice_input");
+      CL_CUDA(launch_slice_input(x, amax, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G, pl.bs, s), "slice_input");
     }
     src = digits;
   } else if (pl.packed) {
     if (xbf) {
       src = xbf;
     } else {
-      if (prep) CL_CUDA(launch_pack_rows(x, ws, h->nb, pl.esize, B, h->C_in, P_in, pl.G, s), "pack_rows");
+      if (prep) CL_CUDA(launch_pack_rows(x, ws, h->nb, pl.esize, B, h->C_in, P_in, pl.G, pl.bs, s), "pack_rows");
       src = ws;
     }
   }
@@ -609,6 +630,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.acc_slots = pl.acc_slots;
   p.a_scale = a_scale;
   p.w_scale = h->w_scale;
+  p.bs = pl.bs;
   p.b_img = h->img;
   p.bias = h->bias;
   p.y = y;
@@ -865,16 +887,22 @@ int cl_block_create(const cl_conv* c1, const cl_act* act, const cl_conv* c2, int
 }  // extern "C"
 
 namespace cl {
+// bf16 blocks hand conv2 its packed operand straight from conv1's epilogue
+// (protocol basis only; with a change of basis conv2 packs conv1's fp32 output)
+static bool bf16_handoff(const cl_block* h) {
+  return h->c1->prec == kPrecBf16 && !h->c1->plan.bs.on && !h->c2->plan.bs.on;
+}
+
 // block workspace: [mid activation | conv workspace (max of both convs)]
 static size_t block_mid_bytes(const cl_block* h, long long B) {
   const cl_conv* c1 = h->c1;
   const cl_conv* c2 = h->c2;
   const size_t P1 = (size_t)ipow(c1->d_out, c1->k);
-  if (c1->prec == kPrecBf16) return align_up((size_t)B * c2->plan.G * P1 * 16, 256);
+  if (bf16_handoff(h)) return align_up((size_t)B * c2->plan.G * P1 * 16, 256);
   return align_up((size_t)B * c1->C_out * P1 * c1->nb * 4, 256);
 }
 static size_t block_ws_bytes(const cl_block* h, long long B) {
-  const bool bf = h->c1->prec == kPrecBf16;
+  const bool bf = bf16_handoff(h);
   return block_mid_bytes(h, B) + std::max(conv_ws_bytes(h->c1, B, false), conv_ws_bytes(h->c2, B, bf));
 }
 
@@ -893,7 +921,7 @@ static int block_run(const cl_block* h, const float* x, float* y, long long B, v
     e2.res_side = c1->d_image;
     e2.res_crop = h->res_crop;
   }
-  if (c1->prec == kPrecBf16) {
+  if (bf16_handoff(h)) {
     // conv1's epilogue writes conv2's packed bf16 operand directly (zero the
     // padding channels/groups the epilogue never touches)
     const int cpg = c2->plan.cpg;

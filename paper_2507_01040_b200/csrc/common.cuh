@@ -241,6 +241,18 @@ __device__ __forceinline__ void digits_b256(float u, int8_t (&d)[ND]) {
   }
   d[0] = (int8_t)X;
 }
+// double-precision input (transformed operands are exact sums of two fp32)
+template <int ND>
+__device__ __forceinline__ void digits_b256_d(double u, int8_t (&d)[ND]) {
+  long long X = __double2ll_rn(ldexp(u, 8 * ND - 1));
+#pragma unroll
+  for (int i = ND - 1; i > 0; --i) {
+    const long long lo = (long long)(int8_t)(X & 0xFF);
+    d[i] = (int8_t)lo;
+    X = (X - lo) >> 8;
+  }
+  d[0] = (int8_t)X;
+}
 #endif
 
 // ---- UMMA descriptors (layouts: cute/arch/mma_sm100_desc.hpp conventions) ---

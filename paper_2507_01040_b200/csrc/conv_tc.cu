@@ -163,7 +163,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // 14-bit field, and CTA-local shared addresses < 2^18 never carry out of it.
     const uint32_t idesc = kInt8 ? instr_desc_i8(128u, (uint32_t)p.n_tile)
                                  : instr_desc(PREC == kPrecBf16 ? 1u : 2u, 128u, (uint32_t)p.n_tile);
-    const uint64_t a_tmpl = (RB == 32) ? smem_desc(0, 16, 256, kLayoutA) : smem_desc(0, 2048, 128, kLayoutA);
+    // 32-byte swizzled protocol rows (3-D tf32 modes) unless a changed basis packs 16-byte rows
+    const bool rb32 = (RB == 32) && !p.bs.on;
+    const uint64_t a_tmpl = rb32 ? smem_desc(0, 16, 256, kSwizzle32B) : smem_desc(0, 2048, 128, kSwizzleNone);
     const uint64_t b_tmpl = smem_desc(0, (uint32_t)p.n_tile * 16u, 128, kSwizzleNone);
     const uint32_t a_img4 = p.a_bytes >> 4, b_img4 = p.b_img_bytes >> 4;
     const uint32_t b_ks4 = ((uint32_t)p.n_tile * 32u) >> 4;
@@ -226,7 +228,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // ===================== epilogue =====================
     const int ew = warp - 4;
     const int row = ew * 32 + lane;
-    const int lx = row % p.tx, ly = (row / p.tx) % p.ty, lz = row / (p.tx * p.ty);
+    // with a change of basis a pixel owns ncol = 2 adjacent rows (lanes), one per matrix column
+    const int bcol = p.bs.on ? (row & 1) : 0;
+    const int prow = p.bs.on ? (row >> 1) : row;
+    const int lx = prow % p.tx, ly = (prow / p.tx) % p.ty, lz = prow / (p.tx * p.ty);
     const int d_out = p.d_out;
     const long long P_out = (p.k == 3) ? (long long)d_out * d_out * d_out
                                        : (p.k == 2 ? (long long)d_out * d_out : (long long)d_out);
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       for (int c0 = 0; c0 < p.n_tile; c0 += 16) {
         const int n0 = nt * p.n_tile + c0;
         if (n0 >= p.N) break;
-        float vv[16];
+        double dv[16];  // accumulator values of this chunk (bias not yet added)
         if constexpr (kInt8) {
           uint32_t l0[16], l1[16], l2[16], l3[16];
           tmem_ld16(taddr + (uint32_t)c0, l0);
@@ -274,19 +279,78 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             const double s = (double)(int)l0[c] + (double)(int)l1[c] * (1.0 / 256.0) +
                              (double)(int)l2[c] * (1.0 / 65536.0) + (double)(int)l3[c] * (1.0 / 16777216.0);
             const int n = min(n0 + c, p.N - 1);
-            const int co = n / NB, tb = n % NB;
-            const double v = s * a_sc * (double)__ldg(p.w_scale + n) + (double)__ldg(p.bias + tb * p.C_out + co);
-            vv[c] = (float)v;
+            dv[c] = s * a_sc * (double)__ldg(p.w_scale + n);
           }
         } else {
           uint32_t rr[16];
           tmem_ld16(taddr + (uint32_t)c0, rr);
           tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const int n = min(n0 + c, p.N - 1);
-            vv[c] = __uint_as_float(rr[c]) + __ldg(p.bias + (n % NB) * p.C_out + n / NB);
+          for (int c = 0; c < 16; ++c) dv[c] = (double)__uint_as_float(rr[c]);
+        }
+        if (p.bs.on) {
+          if constexpr (NB >= 4) {
+            // change of basis: lanes (2i, 2i+1) hold columns 0 / 1 of pixel i; exchange,
+            // invert x = T^T x' / 2 in fp64, then bias / activation / residual in the
+            // protocol basis; lane of column c stores blades [c NB/2, (c+1) NB/2)
+            constexpr int W = NB / 2;
+#pragma unroll
+            for (int cc = 0; cc < 16 / W; ++cc) {
+              double xs[NB];
+#pragma unroll
+              for (int r = 0; r < W; ++r) {
+                const double mine = dv[cc * W + r];
+                const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
+                xs[bcol * W + r] = mine;
+                xs[(1 - bcol) * W + r] = other;
+              }
+              const int co = n0 / W + cc;
+              if (valid && co < p.C_out) {
+                float v[NB];
+#pragma unroll
+                for (int t2 = 0; t2 < NB; ++t2) {
+                  double y = 0.0;
+#pragma unroll
+                  for (int s2 = 0; s2 < NB; ++s2) {
+                    const int tt = p.bs.T[s2 * 8 + t2];
+                    y += tt > 0 ? xs[s2] : (tt < 0 ? -xs[s2] : 0.0);
+                  }
+                  v[t2] = (float)(0.5 * y + (double)__ldg(p.bias + t2 * p.C_out + co));
+                }
+                if (p.act_mode >= 0) {
+                  const float gte = act_gate<NB>(v, p.act_mode, p.act_w + co * NB,
+                                                 p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K);
+#pragma unroll
+                  for (int j = 0; j < NB; ++j) v[j] *= gte;
+                }
+                float h[W];
+#pragma unroll
+                for (int j = 0; j < W; ++j) h[j] = bcol ? v[W + j] : v[j];
+                if (p.resid) {
+                  const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB + bcol * W;
+                  if constexpr (W == 2) {
+                    const float2 q2 = __ldg(reinterpret_cast<const float2*>(rp));
+                    h[0] += q2.x; h[1] += q2.y;
+                  } else {
+                    const float4 q4 = __ldg(reinterpret_cast<const float4*>(rp));
+                    h[0] += q4.x; h[1] += q4.y; h[2 % W] += q4.z; h[3 % W] += q4.w;
+                  }
+                }
+                if (p.y) {
+                  float* yp = p.y + (((long long)b * p.C_out + co) * P_out + pix) * NB + bcol * W;
+                  if constexpr (W == 2) *reinterpret_cast<float2*>(yp) = make_float2(h[0], h[1]);
+                  else *reinterpret_cast<float4*>(yp) = make_float4(h[0], h[1], h[2 % W], h[3 % W]);
+                }
+              }
+            }
           }
+          continue;
+        }
+        float vv[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int n = min(n0 + c, p.N - 1);
+          vv[c] = (float)(dv[c] + (double)__ldg(p.bias + (n % NB) * p.C_out + n / NB));
         }
         if (valid) {
 #pragma unroll
@@ -439,60 +503,80 @@ cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const Con
   }
 }
 
-// fp32 protocol (B, C, P, NB) -> packed 16-byte row groups (B, G, P, 16 B):
-// group g holds channels g*cpg .. g*cpg+cpg-1 (zero beyond C), NB values each,
-// as bf16 (esize 2, cpg = 8/NB) or fp32 (esize 4, cpg = 4/NB; the 1-D tf32 modes).
+// fp32 protocol (B, C, P, NB) -> packed 16-byte row groups (B, G, P, [ncol x] 16 B):
+// group g holds channels g*cpg .. g*cpg+cpg-1 (zero beyond C), w values each,
+// as bf16 (esize 2) or fp32 (esize 4); cpg = 16 / (w * esize). Without a change
+// of basis w = NB (the blades); with one, each pixel yields ncol rows of the
+// transformed components x'[c*w + r] = sum_I T[c*w + r][I] x[I].
 __global__ void pack_rows_kernel(const float* __restrict__ x, uint4* __restrict__ out, int nb, int esize,
-                                 long long B, int C, long long P, int G) {
+                                 long long B, int C, long long P, int G, Basis bs) {
   const long long total = B * G * P;
-  const int nvals = 16 / esize, cpg = nvals / nb;
+  const int ncol = bs.on ? bs.ncol : 1;
+  const int w = bs.on ? bs.w : nb;
+  const int nvals = 16 / esize, cpg = nvals / w;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long pp = i % P;
     const long long bg = i / P;
     const int g = (int)(bg % G);
     const long long b = bg / G;
-    float v[8];
+    for (int col = 0; col < ncol; ++col) {
+      float v[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = 0.f;
-    for (int cl = 0; cl < cpg; ++cl) {
-      const int c = g * cpg + cl;
-      if (c >= C) break;
-      const float* src = x + ((b * C + c) * P + pp) * nb;
-      if (nb == 2) {
-        const float2 q = __ldg(reinterpret_cast<const float2*>(src));
-        v[cl * 2] = q.x; v[cl * 2 + 1] = q.y;
-      } else if (nb == 4) {
-        const float4 q = __ldg(reinterpret_cast<const float4*>(src));
-        v[cl * 4] = q.x; v[cl * 4 + 1] = q.y; v[cl * 4 + 2] = q.z; v[cl * 4 + 3] = q.w;
-      } else {
-        const float4 q0 = __ldg(reinterpret_cast<const float4*>(src)), q1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
-        v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w;
-        v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
+      for (int j = 0; j < 8; ++j) v[j] = 0.f;
+      for (int cl = 0; cl < cpg; ++cl) {
+        const int c = g * cpg + cl;
+        if (c >= C) break;
+        const float* src = x + ((b * C + c) * P + pp) * nb;
+        float m[8];
+        if (nb == 2) {
+          const float2 q = __ldg(reinterpret_cast<const float2*>(src));
+          m[0] = q.x; m[1] = q.y;
+        } else {
+          const float4 q0 = __ldg(reinterpret_cast<const float4*>(src));
+          m[0] = q0.x; m[1] = q0.y; m[2] = q0.z; m[3] = q0.w;
+          if (nb == 8) {
+            const float4 q1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
+            m[4] = q1.x; m[5] = q1.y; m[6] = q1.z; m[7] = q1.w;
+          }
+        }
+        for (int r = 0; r < w; ++r) {
+          float xv;
+          if (bs.on) {
+            xv = 0.f;
+            for (int I = 0; I < nb; ++I) {
+              const int t = bs.T[(col * w + r) * 8 + I];
+              if (t) xv += t > 0 ? m[I] : -m[I];
+            }
+          } else {
+            xv = m[r];
+          }
+          v[cl * w + r] = xv;
+        }
       }
+      uint4 u;
+      if (esize == 4) {
+        u = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
+      } else {
+        __nv_bfloat162 h;
+        h = __floats2bfloat162_rn(v[0], v[1]); u.x = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(v[2], v[3]); u.y = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(v[4], v[5]); u.z = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(v[6], v[7]); u.w = *reinterpret_cast<uint32_t*>(&h);
+      }
+      out[i * ncol + col] = u;
     }
-    uint4 u;
-    if (esize == 4) {
-      u = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
-    } else {
-      __nv_bfloat162 h;
-      h = __floats2bfloat162_rn(v[0], v[1]); u.x = *reinterpret_cast<uint32_t*>(&h);
-      h = __floats2bfloat162_rn(v[2], v[3]); u.y = *reinterpret_cast<uint32_t*>(&h);
-      h = __floats2bfloat162_rn(v[4], v[5]); u.z = *reinterpret_cast<uint32_t*>(&h);
-      h = __floats2bfloat162_rn(v[6], v[7]); u.w = *reinterpret_cast<uint32_t*>(&h);
-    }
-    out[i] = u;
   }
 }
 
 cudaError_t launch_pack_rows(const float* x, void* out, int nb, int esize, long long B, int C, long long P,
-                             int G, cudaStream_t s) {
+                             int G, const Basis& bs, cudaStream_t s) {
   const long long total = B * G * P;
   if (total == 0) return cudaSuccess;
   long long blocks = (total + 255) / 256;
   const long long cap = (long long)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  pack_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, reinterpret_cast<uint4*>(out), nb, esize, B, C, P, G);
+  pack_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, reinterpret_cast<uint4*>(out), nb, esize, B, C, P, G, bs);
   count_launch();
   return cudaGetLastError();
 }

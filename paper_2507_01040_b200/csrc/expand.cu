@@ -18,20 +18,6 @@
 
 namespace cl {
 
-struct Sig {
-  int g[3];
-  int k;
-};
-
-__device__ __forceinline__ float expanded_entry(const Sig& sg, const float* __restrict__ f, int nb,
-                                                int C_in, int C_out, int Q, int co, int t, int ci,
-                                                int j, int q) {
-  const int i = t ^ j;
-  const int c = blade_coeff(i, j, sg.g, sg.k);
-  if (c == 0) return 0.f;
-  const float v = __ldg(f + (((long long)i * C_in + ci) * C_out + co) * Q + q);
-  return c > 0 ? v : -v;
-}
 
 __global__ void expand_ref_kernel(Sig sg, const float* __restrict__ f, int C_in, int C_out, int Q,
                                   float* __restrict__ out) {
@@ -70,10 +56,14 @@ __global__ void expand_img_kernel(Sig sg, const float* __restrict__ f, int C_in,
     const int nt = (int)(r / pl.k_iters);
     const int q = kit / pl.n_gs, gsi = kit % pl.n_gs;
     const int n = nt * pl.n_tile + row;
-    const int co = n / nb, t = n % nb;
-    const int ci = gsi * pl.cps + kl / nb, j = kl % nb;
-    float w = 0.f;
-    if (co < C_out && ci < C_in) w = expanded_entry(sg, f, nb, C_in, C_out, pl.Q, co, t, ci, j, q);
+    const int wd = pl.bs.on ? pl.bs.w : nb;  // components per channel in the operand basis
+    const int co = n / wd, t = n % wd;
+    const int ci = gsi * pl.cps + kl / wd, j = kl % wd;
+    double wv = 0.0;
+    if (co < C_out && ci < C_in)
+      wv = pl.bs.on ? basis_entry(sg, pl.bs, f, C_in, C_out, pl.Q, co, t, ci, j, q)
+                    : (double)expanded_entry(sg, f, nb, C_in, C_out, pl.Q, co, t, ci, j, q);
+    const float w = (float)wv;
     // position inside the stage image
     const int byte_k = kl * pl.esize;
     const int s = byte_k >> 5, h = (byte_k >> 4) & 1, e = (byte_k & 15) / pl.esize;
@@ -82,13 +72,13 @@ __global__ void expand_img_kernel(Sig sg, const float* __restrict__ f, int C_in,
                        (size_t)e * pl.esize;
     if (pl.prec == kPrecFp32) {
       int8_t d[kDigitsW];
-      digits_b256<kDigitsW>(w / __ldg(w_scale + n), d);
+      digits_b256_d<kDigitsW>(wv / (double)__ldg(w_scale + n), d);
 #pragma unroll
       for (int k = 0; k < kDigitsW; ++k) *reinterpret_cast<int8_t*>(base + (size_t)k * pl.b_img_bytes + off) = d[k];
     } else if (pl.prec == kPrec3xTf32) {
       const float hi = __uint_as_float(__float_as_uint(w) & 0xFFFFE000u);
       *reinterpret_cast<float*>(base + off) = hi;
-      *reinterpret_cast<float*>(base + pl.b_img_bytes + off) = w - hi;
+      *reinterpret_cast<float*>(base + pl.b_img_bytes + off) = (float)(wv - (double)hi);
     } else if (pl.prec == kPrecTf32) {
       *reinterpret_cast<float*>(base + off) = tf32_rna(w);
     } else {

@@ -19,7 +19,51 @@ constexpr int kDigitsA = 4;  // int8 digits per activation value in kPrecFp32 (3
 constexpr int kDigitsW = 4;  // int8 digits per filter value (31 bits, per-column scale)
 constexpr int kLevels = 4;   // digit-pair levels kept: i + j <= 3 (0-based)
 
-constexpr int kTileM = 128;          // output pixels per tile (= TMEM lanes)
+constexpr int kTileM = 128;          // GEMM rows per tile (= TMEM lanes)
+
+// Change of basis (basis.cu): x' = T x splits the conv into ncol independent
+// GEMMs sharing a w x w filter; T rows = (column, component), entries +-1/0,
+// T T^T = 2 I.
+struct Basis {
+  int on;
+  int ncol, w;
+  int8_t T[64];  // row-major [s][blade], 8 x 8 (unused rows/cols zero)
+};
+bool find_basis(const int* g, int k, Basis* bs);
+
+struct Sig {
+  int g[3];
+  int k;
+};
+
+#if defined(__CUDACC__)
+// W[(co,t),(ci,j),q] = coeff(t^j, j) f[t^j, ci, co, q]  (conv.py:188-202)
+__device__ __forceinline__ float expanded_entry(const Sig& sg, const float* __restrict__ f, int nb, int C_in,
+                                                int C_out, int Q, int co, int t, int ci, int j, int q) {
+  const int i = t ^ j;
+  const int c = blade_coeff(i, j, sg.g, sg.k);
+  if (c == 0) return 0.f;
+  const float v = __ldg(f + (((long long)i * C_in + ci) * C_out + co) * Q + q);
+  return c > 0 ? v : -v;
+}
+// Filter in the changed basis: R(f)[r][m] = (T L_f T^T)[r][m] / 2 (first
+// w x w block), L_f the expanded N_B x N_B block above; exact in fp64.
+__device__ __forceinline__ double basis_entry(const Sig& sg, const Basis& bs, const float* __restrict__ f,
+                                              int C_in, int C_out, int Q, int co, int r, int ci, int m, int q) {
+  const int nb = 1 << sg.k;
+  double s = 0.0;
+  for (int a = 0; a < nb; ++a) {
+    const int ta = bs.T[r * 8 + a];
+    if (!ta) continue;
+    for (int b = 0; b < nb; ++b) {
+      const int tb = bs.T[m * 8 + b];
+      if (!tb) continue;
+      s += (double)(ta * tb) * (double)expanded_entry(sg, f, nb, C_in, C_out, Q, co, a, ci, b, q);
+    }
+  }
+  return 0.5 * s;
+}
+#endif
 constexpr int kConvThreads = 384;    // 12 warps, see conv_tc.cu
 constexpr int kMaxSmem = 232448;     // 227 KB opt-in dynamic shared memory per CTA
 
@@ -28,6 +72,7 @@ constexpr int kMaxSmem = 232448;     // 227 KB opt-in dynamic shared memory per 
 struct ConvPlan {
   int k, nb;            // spatial rank, blades
   int ka;               // algebra rank (nb = 2^ka); differs from k for the linear layer
+  Basis bs;             // change of basis (bs.on) for M2(R) / M2(C) signatures
   int prec;             // Prec
   int esize;            // operand element bytes (4 fp32/tf32, 2 bf16)
   int rb;               // bytes of one A row-group (16 or 32)
@@ -65,6 +110,7 @@ struct ConvKParams {
   uint32_t a_bytes, b_bytes, b_img_bytes, stage_bytes, tmem_cols;
   int stages, n_a, n_tma_a, levels, acc_slots;
   int cs;                     // cluster size: CTAs sharing each B stage by multicast (1 or 2)
+  Basis bs;                   // change of basis: rows = (pixel, column), epilogue inverse transform
   long long num_m_tiles;      // real pixel tiles (tiles beyond are cluster padding)
   int dbg_nomc;               // debug: cluster launch without B multicast
   const uint8_t* b_img;
@@ -102,13 +148,13 @@ cudaError_t launch_expand_ref(const int* g, int k, const float* f, int C_in, int
 cudaError_t launch_expand_images(const int* g, const ConvPlan& plan, const float* f, int C_in,
                                  int C_out, const float* w_scale, uint8_t* img, cudaStream_t s);
 cudaError_t launch_pack_rows(const float* x, void* out, int nb, int esize, long long B, int C, long long P,
-                             int G, cudaStream_t s);
+                             int G, const Basis& bs, cudaStream_t s);
 cudaError_t launch_act(int nb, const ActParams& p, cudaStream_t s);
 // kPrecFp32 operand preparation (slice.cu)
 cudaError_t launch_sample_absmax(const float* x, long long B, long long per_sample, unsigned* amax,
                                  cudaStream_t s);
 cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* digits, float* scale,
-                               int nb, long long B, int C, long long P, int G, cudaStream_t s);
+                               int nb, long long B, int C, long long P, int G, const Basis& bs, cudaStream_t s);
 cudaError_t launch_weight_colscale(const int* g, const ConvPlan& pl, const float* f, int C_in, int C_out,
                                    float* w_scale, cudaStream_t s);
 

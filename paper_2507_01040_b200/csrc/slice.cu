@@ -49,90 +49,110 @@ cudaError_t launch_sample_absmax(const float* x, long long B, long long per_samp
   return cudaGetLastError();
 }
 
-// One thread per (b, g, p): the 16 K-elements of group g at pixel p
-// (16/nb channels x nb blades) -> 4 digit planes (digit, b, g, p, 16 B).
+// One thread per (b, g, p): the 16 K-elements of group g at pixel p -> 4
+// digit planes (digit, b, g, p, [ncol x] 16 B). Without a change of basis a
+// group is 16/nb channels x nb blades; with one (bs.on) each pixel yields ncol
+// rows, row c holding 16/w channels x the w transformed components
+// x'[c*w + r] = sum_I T[c*w + r][I] x[I] (exact in fp64).
 __global__ void slice_input_kernel(const float* __restrict__ x, const unsigned* __restrict__ amax,
                                    int8_t* __restrict__ out, float* __restrict__ scale, int nb, long long B,
-                                   int C, long long P, int G) {
+                                   int C, long long P, int G, Basis bs) {
   const long long total = B * G * P;
-  const int cpg = 16 / nb;  // channels per group
+  const int ncol = bs.on ? bs.ncol : 1;
+  const int w = bs.on ? bs.w : nb;
+  const int cpg = 16 / w;  // channels per group
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long pp = i % P;
     const long long bg = i / P;
     const int g = (int)(bg % G);
     const long long b = bg / G;
-    const float sc = pow2_scale_for(__uint_as_float(__ldg(amax + b)));
+    const float amx = __uint_as_float(__ldg(amax + b));
+    const float sc = pow2_scale_for(bs.on ? 2.f * amx : amx);  // |x'| <= 2 max|x|
     if (g == 0 && pp == 0) scale[b] = sc;
-    const float inv = 1.f / sc;  // exact (power of two)
-    int8_t dg[4][16];
-    for (int cl = 0; cl < cpg; ++cl) {
-      const int c = g * cpg + cl;
-      float v[8];
+    const double inv = 1.0 / (double)sc;  // exact (power of two)
+    for (int col = 0; col < ncol; ++col) {
+      int8_t dg[4][16];
+      for (int cl = 0; cl < cpg; ++cl) {
+        const int c = g * cpg + cl;
+        float v[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = 0.f;
-      if (c < C) {
-        const float* src = x + ((b * C + c) * P + pp) * nb;
-        if (nb == 2) {
-          const float2 q = __ldg(reinterpret_cast<const float2*>(src));
-          v[0] = q.x; v[1] = q.y;
-        } else {
-          const float4 q0 = __ldg(reinterpret_cast<const float4*>(src));
-          v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w;
-          if (nb == 8) {
-            const float4 q1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
-            v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
+        for (int j = 0; j < 8; ++j) v[j] = 0.f;
+        if (c < C) {
+          const float* src = x + ((b * C + c) * P + pp) * nb;
+          if (nb == 2) {
+            const float2 q = __ldg(reinterpret_cast<const float2*>(src));
+            v[0] = q.x; v[1] = q.y;
+          } else {
+            const float4 q0 = __ldg(reinterpret_cast<const float4*>(src));
+            v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w;
+            if (nb == 8) {
+              const float4 q1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
+              v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
+            }
           }
         }
-      }
-      for (int j = 0; j < nb; ++j) {
-        int8_t d[4];
-        digits_b256<4>(v[j] * inv, d);
+        for (int r = 0; r < w; ++r) {
+          double xv;
+          if (bs.on) {
+            xv = 0.0;
+            for (int I = 0; I < nb; ++I) {
+              const int t = bs.T[(col * w + r) * 8 + I];
+              if (t) xv += t > 0 ? (double)v[I] : -(double)v[I];
+            }
+          } else {
+            xv = (double)v[r];
+          }
+          int8_t d[4];
+          digits_b256_d<4>(xv * inv, d);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) dg[k][cl * nb + j] = d[k];
+          for (int k = 0; k < 4; ++k) dg[k][cl * w + r] = d[k];
+        }
       }
-    }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint4 u;
-      u.x = (uint32_t)(uint8_t)dg[k][0] | ((uint32_t)(uint8_t)dg[k][1] << 8) | ((uint32_t)(uint8_t)dg[k][2] << 16) | ((uint32_t)(uint8_t)dg[k][3] << 24);
-      u.y = (uint32_t)(uint8_t)dg[k][4] | ((uint32_t)(uint8_t)dg[k][5] << 8) | ((uint32_t)(uint8_t)dg[k][6] << 16) | ((uint32_t)(uint8_t)dg[k][7] << 24);
-      u.z = (uint32_t)(uint8_t)dg[k][8] | ((uint32_t)(uint8_t)dg[k][9] << 8) | ((uint32_t)(uint8_t)dg[k][10] << 16) | ((uint32_t)(uint8_t)dg[k][11] << 24);
-      u.w = (uint32_t)(uint8_t)dg[k][12] | ((uint32_t)(uint8_t)dg[k][13] << 8) | ((uint32_t)(uint8_t)dg[k][14] << 16) | ((uint32_t)(uint8_t)dg[k][15] << 24);
-      reinterpret_cast<uint4*>(out)[(long long)k * total + i] = u;
+      for (int k = 0; k < 4; ++k) {
+        uint32_t wd[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          wd[q] = (uint32_t)(uint8_t)dg[k][4 * q] | ((uint32_t)(uint8_t)dg[k][4 * q + 1] << 8) |
+                  ((uint32_t)(uint8_t)dg[k][4 * q + 2] << 16) | ((uint32_t)(uint8_t)dg[k][4 * q + 3] << 24);
+        reinterpret_cast<uint4*>(out)[((long long)k * total + i) * ncol + col] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+      }
     }
   }
 }
 
 cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* digits, float* scale, int nb,
-                               long long B, int C, long long P, int G, cudaStream_t s) {
+                               long long B, int C, long long P, int G, const Basis& bs, cudaStream_t s) {
   const long long total = B * G * P;
   if (total == 0) return cudaSuccess;
   long long blocks = (total + 255) / 256;
   const long long cap = (long long)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  slice_input_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, amax, digits, scale, nb, B, C, P, G);
+  slice_input_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, amax, digits, scale, nb, B, C, P, G, bs);
   count_launch();
   return cudaGetLastError();
 }
 
-// Per output column n = (co, t) of the expanded filter: power-of-two scale
-// covering max_k |W[n, k]| (W entries are signed filter values, conv.py:188-202).
-__global__ void weight_colscale_kernel(int g0, int g1, int g2, int k, const float* __restrict__ f, int C_in,
-                                       int C_out, int Q, int N_pad, float* __restrict__ w_scale) {
-  const int nb = 1 << k;
-  const int gg[3] = {g0, g1, g2};
+// Per output column n of the B operand: power-of-two scale covering
+// max_k |W[n, k]|. Without a change of basis W is the expanded filter
+// (conv.py:188-202, entries are signed filter values); with one, n = (co, r)
+// and W[n, (q, ci, m)] = R(f[ci, co, q])[r][m] (see expand.cu).
+__global__ void weight_colscale_kernel(Sig sg, const float* __restrict__ f, int C_in, int C_out, int Q,
+                                       Basis bs, float* __restrict__ w_scale) {
+  const int nb = 1 << sg.k;
+  const int w = bs.on ? bs.w : nb;
   const int n = blockIdx.x;
-  const int co = n / nb, t = n % nb;
+  const int co = n / w, t = n % w;
   float m = 0.f;
   if (co < C_out) {
-    for (int idx = threadIdx.x; idx < C_in * nb * Q; idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < C_in * w * Q; idx += blockDim.x) {
       const int q = idx % Q;
-      const int j = (idx / Q) % nb;
-      const int ci = idx / (Q * nb);
-      const int i = t ^ j;
-      if (blade_coeff(i, j, gg, k) != 0)
-        m = fmaxf(m, fabsf(__ldg(f + (((long long)i * C_in + ci) * C_out + co) * Q + q)));
+      const int j = (idx / Q) % w;
+      const int ci = idx / (Q * w);
+      const double e = bs.on ? basis_entry(sg, bs, f, C_in, C_out, Q, co, t, ci, j, q)
+                             : (double)expanded_entry(sg, f, nb, C_in, C_out, Q, co, t, ci, j, q);
+      m = fmaxf(m, (float)fabs(e));
     }
   }
   __shared__ float red[32];
@@ -141,15 +161,18 @@ __global__ void weight_colscale_kernel(int g0, int g1, int g2, int k, const floa
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
-    w_scale[n] = pow2_scale_for(m);
+    for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww) m = fmaxf(m, red[ww]);
+    // float rounding of |e| may round down: one more power of two of headroom is free
+    w_scale[n] = pow2_scale_for(m * 1.0000002f);
   }
 }
 
 cudaError_t launch_weight_colscale(const int* g, const ConvPlan& pl, const float* f, int C_in, int C_out,
                                    float* w_scale, cudaStream_t s) {
   const int N_pad = pl.n_ntiles * pl.n_tile;
-  weight_colscale_kernel<<<N_pad, 256, 0, s>>>(g[0], g[1], g[2], pl.ka, f, C_in, C_out, pl.Q, N_pad, w_scale);
+  Sig sg{{0, 0, 0}, pl.ka};
+  for (int i = 0; i < pl.ka; ++i) sg.g[i] = g[i];
+  weight_colscale_kernel<<<N_pad, 256, 0, s>>>(sg, f, C_in, C_out, pl.Q, pl.bs, w_scale);
   count_launch();
   return cudaGetLastError();
 }

@@ -161,3 +161,38 @@ def test_linear_validation_and_flops(golden):
         g = tuple(int(v) for v in golden[f"lin{n}_g"])
         x, w = golden[f"lin{n}_x"], golden[f"lin{n}_w"]
         assert M.linear_flops(x.shape[0], x.shape[1], w.shape[1], M.Signature(g)) == int(golden[f"lin{n}_flops"])
+
+
+def _basis(g):
+    lib = _lib.load()
+    ncol, w = _lib.C.c_int(), _lib.C.c_int()
+    T = (_lib.C.c_int8 * 64)()
+    ok = lib.cl_basis_info(_lib.int32_array(g), len(g), _lib.C.byref(ncol), _lib.C.byref(w), T)
+    return ok, ncol.value, w.value, np.array(list(T), np.int64).reshape(8, 8)
+
+
+@pytest.mark.parametrize("g", O.all_signatures(3))
+def test_change_of_basis_is_exact_block_diagonalisation(g):
+    """x' = T x turns left multiplication by any multivector into
+    ncol identical w x w blocks (checked against the oracle's Cayley tensor)."""
+    ok, ncol, w, T = _basis(g)
+    k = len(g)
+    expect = k >= 2 and all(g) and not (k == 2 and g == (-1, -1)) and g not in [(-1, -1, -1), (1, 1, -1), (1, -1, 1), (-1, 1, 1)]
+    if not ok:
+        assert not expect, f"no basis found for {g}"
+        return
+    nb = 1 << k
+    T = T[:nb, :nb]
+    np.testing.assert_array_equal(T @ T.T, 2 * np.eye(nb, dtype=np.int64))
+    cay = O.cayley(g)
+    rng = np.random.default_rng(0)
+    f = rng.standard_normal(nb)
+    L = np.einsum("i,ijt->tj", f, cay)  # (f x)[t] = sum_j L[t, j] x[j]
+    A = T @ L @ T.T / 2
+    for c in range(ncol):
+        for c2 in range(ncol):
+            blk = A[c * w:(c + 1) * w, c2 * w:(c2 + 1) * w]
+            if c == c2:
+                np.testing.assert_allclose(blk, A[:w, :w], atol=1e-12)
+            else:
+                np.testing.assert_allclose(blk, 0, atol=1e-12)
