@@ -140,6 +140,23 @@ bool build_and_check(const int* g, int k, const std::vector<C2>& gen, Basis* bs)
   bs->w = w;
   for (int a = 0; a < 8; ++a)
     for (int I = 0; I < 8; ++I) bs->T[a * 8 + I] = (int8_t)((a < nb && I < nb) ? T[a][I] : 0);
+  // two-term forms of T (rows) and T^T (columns)
+  for (int a = 0; a < nb; ++a) {
+    int n = 0, m = 0;
+    for (int I = 0; I < nb; ++I) {
+      if (T[a][I]) {
+        if (n == 2) return false;
+        bs->fwd[a][n] = (int8_t)I;
+        bs->fwd_sgn[a][n++] = (int8_t)T[a][I];
+      }
+      if (T[I][a]) {
+        if (m == 2) return false;
+        bs->inv[a][m] = (int8_t)I;
+        bs->inv_sgn[a][m++] = (int8_t)T[I][a];
+      }
+    }
+    if (n != 2 || m != 2) return false;
+  }
   return true;
 }
 

@@ -231,6 +231,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // with a change of basis a pixel owns ncol = 2 adjacent rows (lanes), one per matrix column
     const int bcol = p.bs.on ? (row & 1) : 0;
     const int prow = p.bs.on ? (row >> 1) : row;
+    int inv_i0[NB], inv_i1[NB], inv_s0[NB], inv_s1[NB];  // two-term inverse transform (registers)
+#pragma unroll
+    for (int t2 = 0; t2 < NB; ++t2) {
+      inv_i0[t2] = p.bs.inv[t2 % 8][0];
+      inv_i1[t2] = p.bs.inv[t2 % 8][1];
+      inv_s0[t2] = p.bs.inv_sgn[t2 % 8][0];
+      inv_s1[t2] = p.bs.inv_sgn[t2 % 8][1];
+    }
     const int lx = prow % p.tx, ly = (prow / p.tx) % p.ty, lz = prow / (p.tx * p.ty);
     const int d_out = p.d_out;
     const long long P_out = (p.k == 3) ? (long long)d_out * d_out * d_out
@@ -291,32 +299,43 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (p.bs.on) {
           if constexpr (NB >= 4) {
             // change of basis: lanes (2i, 2i+1) hold columns 0 / 1 of pixel i; exchange,
-            // invert x = T^T x' / 2 in fp64, then bias / activation / residual in the
-            // protocol basis; lane of column c stores blades [c NB/2, (c+1) NB/2)
+            // invert x[t] = (+-x'[a_t] +- x'[b_t]) / 2 (fp64 for the exact mode), then bias /
+            // activation / residual in the protocol basis; the lane of column c stores
+            // blades [c NB/2, (c+1) NB/2)
             constexpr int W = NB / 2;
 #pragma unroll
             for (int cc = 0; cc < 16 / W; ++cc) {
-              double xs[NB];
-#pragma unroll
-              for (int r = 0; r < W; ++r) {
-                const double mine = dv[cc * W + r];
-                const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
-                xs[bcol * W + r] = mine;
-                xs[(1 - bcol) * W + r] = other;
-              }
               const int co = n0 / W + cc;
-              if (valid && co < p.C_out) {
-                float v[NB];
+              float v[NB];
+              if constexpr (kInt8) {
+                double xs[NB];
+#pragma unroll
+                for (int r = 0; r < W; ++r) {
+                  const double mine = dv[cc * W + r];
+                  const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
+                  xs[bcol * W + r] = mine;
+                  xs[(1 - bcol) * W + r] = other;
+                }
 #pragma unroll
                 for (int t2 = 0; t2 < NB; ++t2) {
-                  double y = 0.0;
-#pragma unroll
-                  for (int s2 = 0; s2 < NB; ++s2) {
-                    const int tt = p.bs.T[s2 * 8 + t2];
-                    y += tt > 0 ? xs[s2] : (tt < 0 ? -xs[s2] : 0.0);
-                  }
-                  v[t2] = (float)(0.5 * y + (double)__ldg(p.bias + t2 * p.C_out + co));
+                  const double y = 0.5 * ((double)inv_s0[t2] * xs[inv_i0[t2]] + (double)inv_s1[t2] * xs[inv_i1[t2]]);
+                  v[t2] = (float)(y + (double)__ldg(p.bias + t2 * p.C_out + min(co, p.C_out - 1)));
                 }
+              } else {
+                float xs[NB];
+#pragma unroll
+                for (int r = 0; r < W; ++r) {
+                  const float mine = (float)dv[cc * W + r];
+                  const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
+                  xs[bcol * W + r] = mine;
+                  xs[(1 - bcol) * W + r] = other;
+                }
+#pragma unroll
+                for (int t2 = 0; t2 < NB; ++t2)
+                  v[t2] = 0.5f * ((float)inv_s0[t2] * xs[inv_i0[t2]] + (float)inv_s1[t2] * xs[inv_i1[t2]]) +
+                          __ldg(p.bias + t2 * p.C_out + min(co, p.C_out - 1));
+              }
+              if (valid && co < p.C_out) {
                 if (p.act_mode >= 0) {
                   const float gte = act_gate<NB>(v, p.act_mode, p.act_w + co * NB,
                                                  p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K);

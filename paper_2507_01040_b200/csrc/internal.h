@@ -27,7 +27,11 @@ constexpr int kTileM = 128;          // GEMM rows per tile (= TMEM lanes)
 struct Basis {
   int on;
   int ncol, w;
-  int8_t T[64];  // row-major [s][blade], 8 x 8 (unused rows/cols zero)
+  int8_t T[64];   // row-major [s][blade], 8 x 8 (unused rows/cols zero)
+  // every row of T and every column of T (blade) has exactly two +-1 entries:
+  // x'[s] = sgn * x[fwd[s][0]] + sgn * x[fwd[s][1]], x[t] = (+-x'[inv[t][0]] +- x'[inv[t][1]]) / 2
+  int8_t fwd[8][2], fwd_sgn[8][2];
+  int8_t inv[8][2], inv_sgn[8][2];
 };
 bool find_basis(const int* g, int k, Basis* bs);
 
