@@ -97,6 +97,11 @@ int cl_expand_kernel(const int32_t* g, int k, const float* filters_dev, int C_in
 int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, int d_filter,
                    int padding, int precision, const float* filters_dev, const float* bias_dev,
                    void* stream, cl_conv** out);
+/* FLOPs of one forward of B samples: the reference's algorithmic count
+ * (conv_flops, conv.py:384-387) and the dense tensor-core GEMM actually
+ * issued (half of the expanded one under a change of basis); basis = 1 if the
+ * layer runs in a changed (matrix-algebra) basis */
+int cl_conv_gemm_flops(const cl_conv* h, int64_t B, double* algorithmic, double* executed, int* basis);
 /* spatial output side d_out of the layer */
 int cl_conv_out_side(const cl_conv* h, int* d_out);
 /* x_dev (B, C_in, d_image^k, N_B) -> y_dev (B, C_out, d_out^k, N_B) */

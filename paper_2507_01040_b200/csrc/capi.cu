@@ -23,6 +23,7 @@ static thread_local std::string g_last_error;
 static thread_local bool g_time_kernel_only = false;  // cl_conv_time_kernel: skip operand preparation
 static bool g_no_cluster = getenv("CL_NO_CLUSTER") != nullptr;  // debug: disable B multicast
 static bool g_no_basis = getenv("CL_NO_BASIS") != nullptr;      // A/B: disable the change of basis
+static bool g_basis_2d = getenv("CL_BASIS_2D") != nullptr;      // A/B: enable it for 2-D layers
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -393,7 +394,10 @@ static int conv_create_impl(const int32_t* g, int k, int sk, int C_in, int C_out
     return fail(CL_ERR_UNSUPPORTED, "Unsupported", "fp32 mode supports K = d_filter^k * C_in * N_B <= 32000");
   }
   Basis bs{};
-  if (sk >= 2 && sk == k && !g_no_basis) find_basis(h->g, k, &bs);
+  // M2(C) change of basis for 3-D layers (measured 2.0x on cfg5);
+  // the 2-D M2(R) basis is available (CL_BASIS_2D=1) but measured slower on
+  // cfg1/cfg3, whose per-tile MMA work is too small to hide its epilogue
+  if (sk == k && !g_no_basis && (sk == 3 || (sk == 2 && g_basis_2d))) find_basis(h->g, k, &bs);
   if (!plan_conv(sk, h->nb, precision, C_in, C_out, d_out, d_filter, bs, h->plan)) {
     delete h;
     return fail(CL_ERR_UNSUPPORTED, "Unsupported", "no shared-memory plan fits this layer");
@@ -456,6 +460,22 @@ int cl_linear_forward_host(const cl_linear* h, const float* x, float* y, int64_t
 }
 
 void cl_linear_destroy(cl_linear* h) { cl_conv_destroy(h); }
+
+int cl_conv_gemm_flops(const cl_conv* h, int64_t B, double* algorithmic, double* executed, int* basis) {
+  if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null conv handle");
+  int gi[3] = {h->g[0], h->g[1], h->g[2]};
+  int terms = 0;
+  for (int t = 0; t < h->nb; ++t)
+    for (int a = 0; a < h->nb; ++a) terms += blade_coeff(a, t ^ a, gi, h->k) != 0;
+  const double P = (double)ipow(h->d_out, h->sk), Q = (double)ipow(h->d_filter, h->sk);
+  // conv_flops (conv.py:384-387) and the dense tensor-core GEMM actually issued
+  if (algorithmic) *algorithmic = (double)B * h->C_out * P * (h->C_in * Q * 2.0 * terms + h->nb);
+  const Basis& bs = h->plan.bs;
+  const double ncol = bs.on ? bs.ncol : 1, w = bs.on ? bs.w : h->nb;
+  if (executed) *executed = 2.0 * ((double)B * P * ncol) * (h->C_out * w) * (Q * h->C_in * w);
+  if (basis) *basis = bs.on;
+  return CL_OK;
+}
 
 int cl_conv_out_side(const cl_conv* h, int* d_out) {
   if (!h || !d_out) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null handle");
