@@ -51,16 +51,21 @@ cudaError_t launch_sample_absmax(const float* x, long long B, long long per_samp
 
 // One thread per (b, g, p): the 16 K-elements of group g at pixel p -> 4
 // digit planes (digit, b, g, p, [ncol x] 16 B). Without a change of basis a
-// group is 16/nb channels x nb blades; with one (bs.on) each pixel yields ncol
-// rows, row c holding 16/w channels x the w transformed components
-// x'[c*w + r] = sum_I T[c*w + r][I] x[I] (exact in fp64).
-__global__ void slice_input_kernel(const float* __restrict__ x, const unsigned* __restrict__ amax,
-                                   int8_t* __restrict__ out, float* __restrict__ scale, int nb, long long B,
-                                   int C, long long P, int G, Basis bs) {
+// group is 16/NB channels x NB blades; with one (BASIS) each pixel yields 2
+// rows, row c holding 16/W channels x the W = NB/2 transformed components
+// x'[c*W + r] = sum_I T[c*W + r][I] x[I].
+// Integer-exact: X_I = rint(x_I 2^31 / s) (power-of-two scaling, one rounding),
+// X' = sum_I T X_I in int32 (|X'| < 2^31 since s >= 2 max|x| 1.016), and the
+// balanced base-256 digits are the two's-complement bytes of X'.
+template <int NB, bool BASIS>
+__global__ void __launch_bounds__(256) slice_input_kernel(const float* __restrict__ x,
+                                                          const unsigned* __restrict__ amax,
+                                                          int8_t* __restrict__ out, float* __restrict__ scale,
+                                                          long long B, int C, long long P, int G, Basis bs) {
+  constexpr int W = BASIS ? NB / 2 : NB;
+  constexpr int NCOL = BASIS ? 2 : 1;
+  constexpr int CPG = 16 / W;  // channels per group
   const long long total = B * G * P;
-  const int ncol = bs.on ? bs.ncol : 1;
-  const int w = bs.on ? bs.w : nb;
-  const int cpg = 16 / w;  // channels per group
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long pp = i % P;
@@ -68,57 +73,70 @@ __global__ void slice_input_kernel(const float* __restrict__ x, const unsigned* 
     const int g = (int)(bg % G);
     const long long b = bg / G;
     const float amx = __uint_as_float(__ldg(amax + b));
-    const float sc = pow2_scale_for(bs.on ? 2.f * amx : amx);  // |x'| <= 2 max|x|
+    const float sc = pow2_scale_for(BASIS ? 2.f * amx : amx);  // |x'| <= 2 max|x|
     if (g == 0 && pp == 0) scale[b] = sc;
-    const double inv = 1.0 / (double)sc;  // exact (power of two)
-    for (int col = 0; col < ncol; ++col) {
-      int8_t dg[4][16];
-      for (int cl = 0; cl < cpg; ++cl) {
-        const int c = g * cpg + cl;
-        float v[8];
+    const float mult = 2147483648.f / sc;  // 2^31 / s, exact power of two
+    uint32_t word[NCOL][4][4];  // [col][digit plane][4 bytes x 4 words]
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = 0.f;
-        if (c < C) {
-          const float* src = x + ((b * C + c) * P + pp) * nb;
-          if (nb == 2) {
-            const float2 q = __ldg(reinterpret_cast<const float2*>(src));
-            v[0] = q.x; v[1] = q.y;
-          } else {
-            const float4 q0 = __ldg(reinterpret_cast<const float4*>(src));
-            v[0] = q0.x; v[1] = q0.y; v[2] = q0.z; v[3] = q0.w;
-            if (nb == 8) {
-              const float4 q1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
-              v[4] = q1.x; v[5] = q1.y; v[6] = q1.z; v[7] = q1.w;
-            }
+    for (int cl = 0; cl < CPG; ++cl) {
+      const int c = g * CPG + cl;
+      int X[NB];
+      if (c < C) {
+        const float* src = x + ((b * C + c) * P + pp) * NB;
+        float v[NB];
+        if constexpr (NB == 2) {
+          const float2 q = __ldg(reinterpret_cast<const float2*>(src));
+          v[0] = q.x; v[1] = q.y;
+        } else {
+#pragma unroll
+          for (int h = 0; h < NB / 4; ++h) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(src) + h);
+            v[4 * h] = q.x; v[4 * h + 1] = q.y; v[4 * h + 2] = q.z; v[4 * h + 3] = q.w;
           }
         }
-        for (int r = 0; r < w; ++r) {
-          double xv;
-          if (bs.on) {
-            xv = 0.0;
-            for (int I = 0; I < nb; ++I) {
-              const int t = bs.T[(col * w + r) * 8 + I];
-              if (t) xv += t > 0 ? (double)v[I] : -(double)v[I];
-            }
-          } else {
-            xv = (double)v[r];
-          }
-          int8_t d[4];
-          digits_b256_d<4>(xv * inv, d);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) dg[k][cl * w + r] = d[k];
-        }
+        for (int I = 0; I < NB; ++I) X[I] = __float2int_rn(v[I] * mult);
+      } else {
+#pragma unroll
+        for (int I = 0; I < NB; ++I) X[I] = 0;
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        uint32_t wd[4];
+      for (int col = 0; col < NCOL; ++col) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          wd[q] = (uint32_t)(uint8_t)dg[k][4 * q] | ((uint32_t)(uint8_t)dg[k][4 * q + 1] << 8) |
-                  ((uint32_t)(uint8_t)dg[k][4 * q + 2] << 16) | ((uint32_t)(uint8_t)dg[k][4 * q + 3] << 24);
-        reinterpret_cast<uint4*>(out)[((long long)k * total + i) * ncol + col] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+        for (int r = 0; r < W; ++r) {
+          int Xs;
+          if constexpr (BASIS) {
+            Xs = 0;
+#pragma unroll
+            for (int I = 0; I < NB; ++I) Xs += (int)bs.T[(col * W + r) * 8 + I] * X[I];
+          } else {
+            Xs = X[r];
+          }
+          // balanced base-256 digits, least significant first
+          const int e = cl * W + r;  // byte position inside the 16-byte row
+          const int shift = (e & 3) * 8;
+#pragma unroll
+          for (int k = 3; k >= 0; --k) {
+            int d;
+            if (k > 0) {
+              d = (int)(int8_t)(Xs & 0xFF);
+              Xs = (Xs - d) >> 8;
+            } else {
+              d = Xs;
+            }
+            uint32_t& wd = word[col][k][e >> 2];
+            const uint32_t byte = (uint32_t)(uint8_t)d << shift;
+            wd = (shift == 0) ? byte : (wd | byte);
+          }
+        }
       }
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int col = 0; col < NCOL; ++col)
+        reinterpret_cast<uint4*>(out)[((long long)k * total + i) * NCOL + col] =
+            make_uint4(word[col][k][0], word[col][k][1], word[col][k][2], word[col][k][3]);
   }
 }
 
@@ -129,7 +147,15 @@ cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* dig
   long long blocks = (total + 255) / 256;
   const long long cap = (long long)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  slice_input_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, amax, digits, scale, nb, B, C, P, G, bs);
+  const unsigned gb = (unsigned)blocks;
+  if (bs.on) {
+    if (nb == 4) slice_input_kernel<4, true><<<gb, 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
+    else slice_input_kernel<8, true><<<gb, 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
+  } else {
+    if (nb == 2) slice_input_kernel<2, false><<<gb, 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
+    else if (nb == 4) slice_input_kernel<4, false><<<gb, 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
+    else slice_input_kernel<8, false><<<gb, 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
+  }
   count_launch();
   return cudaGetLastError();
 }
