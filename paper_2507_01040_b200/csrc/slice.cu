@@ -144,17 +144,21 @@ cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* dig
                                long long B, int C, long long P, int G, const Basis& bs, cudaStream_t s) {
   const long long total = B * G * P;
   if (total == 0) return cudaSuccess;
-  long long blocks = (total + 255) / 256;
-  const long long cap = (long long)num_sms() * 8;
-  if (blocks > cap) blocks = cap;
-  const unsigned gb = (unsigned)blocks;
+  // one wave: blocks per SM from the occupancy calculator (the basis variants are register-heavy)
+  auto grid = [&](auto kern) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+    long long blocks = (total + 255) / 256;
+    const long long cap = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
+    return (unsigned)(blocks > cap ? cap : blocks);
+  };
   if (bs.on) {
-    if (nb == 4) slice_input_kernel<4, true><<<gb, 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
-    else slice_input_kernel<8, true><<<gb, 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
+    if (nb == 4) slice_input_kernel<4, true><<<grid(slice_input_kernel<4, true>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
+    else slice_input_kernel<8, true><<<grid(slice_input_kernel<8, true>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
   } else {
-    if (nb == 2) slice_input_kernel<2, false><<<gb, 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
-    else if (nb == 4) slice_input_kernel<4, false><<<gb, 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
-    else slice_input_kernel<8, false><<<gb, 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
+    if (nb == 2) slice_input_kernel<2, false><<<grid(slice_input_kernel<2, false>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
+    else if (nb == 4) slice_input_kernel<4, false><<<grid(slice_input_kernel<4, false>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
+    else slice_input_kernel<8, false><<<grid(slice_input_kernel<8, false>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
   }
   count_launch();
   return cudaGetLastError();
