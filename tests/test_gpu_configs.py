@@ -1,0 +1,117 @@
+"""BASELINE.json configs at their full sizes on the B200, checked against the
+CPU oracle on sampled items (the fp64 oracle costs ~5 s per cfg5 sample)
+plus size-independent properties: per-sample batch independence (bit-exact)
+and the max_rel_error bound (bench.py:74-88) with the value printed."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2507_01040_b200 as M  # noqa: E402
+from paper_2507_01040_b200 import workloads as W  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _block(spec, B, prec="fp32"):
+    f1, b1 = W.conv_params(spec, 1)
+    f2, b2 = W.conv_params(spec, 2)
+    aw, ab = W.act_params(spec)
+    blk = M.make_basic_block(M.Signature(spec.g), B, spec.C, spec.C, spec.C, spec.d, f1, b1, spec.mode, f2, b2,
+                             act_weight=aw, act_bias=ab, padding=spec.padding, residual=True, precision=prec)
+    ref = lambda x: O.block_ref(x, spec.g, spec.d, f1, b1, spec.mode, tuple(range(spec.nb)), aw, ab, f2, b2,  # noqa: E731
+                                padding=spec.padding, residual=True)
+    return blk, ref
+
+
+def test_cfg1_full_oracle():
+    spec = W.CONFIGS[1]
+    f, b = W.conv_params(spec, 1)
+    layer = M.make_conv_layer(M.Dims(spec.B, spec.C, spec.C, spec.d, 3, 2), M.Signature(spec.g), f, b)
+    x = W.make_input(spec, 0, spec.B)
+    y = M.conv_forward(x, layer).cpu().numpy()
+    e = O.max_rel_error(y, O.conv_ref(x.cpu().numpy(), f, b, spec.g, spec.d, 3))
+    print(f"cfg1 max_rel_error {e:.3e}")
+    assert e <= 1e-4
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_cfg2_full_oracle(mode):
+    spec = W.CONFIGS[2]
+    wgt, bias = W.act_params(spec)
+    cfg = M.make_activation_config(M.Signature(spec.g), mode, (0, 1, 2, 3),
+                                   wgt if mode == 0 else None, bias if mode == 0 else None)
+    x = W.make_input(spec, 0, spec.B)
+    y = M.activation_forward(x, cfg).cpu().numpy()
+    e = O.max_abs_error(y, O.activation_ref(x.cpu().numpy(), mode, (0, 1, 2, 3),
+                                            wgt if mode == 0 else None, bias if mode == 0 else None))
+    print(f"cfg2 mode {mode} max_abs_error {e:.3e}")
+    assert e <= 1e-5
+
+
+@pytest.mark.parametrize("cfg", [4, 40])
+def test_cfg4_full_batch_sampled_oracle(cfg):
+    spec = W.CONFIGS[cfg]
+    f, b = W.conv_params(spec, 1)
+    layer = M.make_conv_layer(M.Dims(spec.B, spec.C, spec.C, spec.d, 3, 3), M.Signature(spec.g), f, b)
+    x = W.make_input(spec, 0, spec.B)
+    y = M.conv_forward(x, layer)
+    for i in (0, spec.B - 1):
+        xi = x[i:i + 1].cpu().numpy()
+        e = O.max_rel_error(y[i:i + 1].cpu().numpy(), O.conv_ref(xi, f, b, spec.g, spec.d, 3))
+        print(f"cfg{cfg} sample {i} max_rel_error {e:.3e}")
+        assert e <= 1e-4
+    # per-sample batch independence, bit-exact
+    one = M.make_conv_layer(M.Dims(1, spec.C, spec.C, spec.d, 3, 3), M.Signature(spec.g), f, b)
+    assert torch.equal(M.conv_forward(x[5:6].contiguous(), one)[0], y[5])
+
+
+def test_cfg3_block_sampled_oracle():
+    spec = W.CONFIGS[3]
+    blk, ref = _block(spec, spec.B)
+    x = W.make_input(spec, 0, spec.B)
+    y = M.block_forward(x, blk)
+    for i in (0, spec.B - 1):
+        e = O.max_rel_error(y[i:i + 1].cpu().numpy(), ref(x[i:i + 1].cpu().numpy()))
+        print(f"cfg3 sample {i} max_rel_error {e:.3e}")
+        assert e <= 1e-4
+
+
+@pytest.mark.slow
+def test_cfg5_full_batch_sampled_oracle():
+    spec = W.CONFIGS[5]
+    blk, ref = _block(spec, spec.B)
+    x = W.make_input(spec, 0, spec.B)
+    y = M.block_forward(x, blk)
+    torch.cuda.synchronize()
+    for i in (0, spec.B - 1):
+        e = O.max_rel_error(y[i:i + 1].cpu().numpy(), ref(x[i:i + 1].cpu().numpy()))
+        print(f"cfg5 sample {i} max_rel_error {e:.3e}")
+        assert e <= 1e-4
+    # per-sample batch independence, bit-exact (a 2-sample block over samples 7, 8)
+    blk2, _ = _block(spec, 2)
+    y2 = M.block_forward(x[7:9].contiguous(), blk2)
+    assert torch.equal(y2, y[7:9])
+    del x, y
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("prec,tol", [("3xtf32", 1e-5), ("tf32", 2e-2), ("bf16", 2e-2)])
+def test_cfg5_shape_other_modes(prec, tol):
+    spec = W.CONFIGS[5]
+    blk, ref = _block(spec, 2, prec)
+    x = W.make_input(spec, 0, 2)
+    y = M.block_forward(x, blk)[:1].cpu().numpy()
+    r = ref(x[:1].cpu().numpy())
+    e = O.max_rel_error(y, r, floor=float(np.abs(r).max()))
+    print(f"cfg5 {prec} normwise max_rel_error {e:.3e}")
+    assert e <= tol
