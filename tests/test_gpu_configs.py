@@ -105,7 +105,7 @@ def test_cfg5_full_batch_sampled_oracle():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("prec,tol", [("3xtf32", 1e-5), ("tf32", 2e-2), ("bf16", 2e-2)])
+@pytest.mark.parametrize("prec,tol", [("3xtf32", 5e-5), ("tf32", 2e-2), ("bf16", 2e-2)])
 def test_cfg5_shape_other_modes(prec, tol):
     spec = W.CONFIGS[5]
     blk, ref = _block(spec, 2, prec)
