@@ -24,6 +24,7 @@ static thread_local bool g_time_kernel_only = false;  // cl_conv_time_kernel: sk
 static bool g_no_cluster = getenv("CL_NO_CLUSTER") != nullptr;  // debug: disable B multicast
 static bool g_no_basis = getenv("CL_NO_BASIS") != nullptr;      // A/B: disable the change of basis
 static bool g_basis_2d = getenv("CL_BASIS_2D") != nullptr;      // A/B: enable it for 2-D layers
+static bool g_no_halo = getenv("CL_NO_HALO") != nullptr;        // A/B: disable halo reuse of the A tile
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -140,6 +141,19 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
     ty = std::min(tpix / tx, pow2_at_least(d_out));
     tz = tpix / (tx * ty);
   }
+  // halo reuse (16-byte-row operands, 2-D / 3-D, filters wider than 1): the
+  // tile is one core-matrix group wide (8 rows = 8/ncol pixels) so every
+  // filter tap is a plain descriptor offset into one loaded halo
+  pl.halo = !i8 && pl.rb == 16 && (k == 2 || k == 3) && d_filter >= 2 && !g_no_halo;
+  if (pl.halo) {
+    tx = 8 / ncol;
+    ty = tpix / tx;
+    tz = 1;
+    pl.hx = tx + d_filter - 1;
+    pl.hy = ty + d_filter - 1;
+    pl.hz = k == 3 ? d_filter : 1;
+    pl.hs = 2;
+  }
   pl.tx = tx;
   pl.ty = ty;
   pl.tz = tz;
@@ -185,14 +199,23 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
     c.b_img_bytes = (uint32_t)(ks * pl.n_tile * 32);
     c.b_bytes = c.b_img_bytes * pl.n_img;
     c.stage_bytes = c.a_bytes * pl.n_a + c.b_bytes;
-    c.stages = std::min(8, (int)((kMaxSmem - 2048) / c.stage_bytes));
+    if (pl.halo) {
+      if (pl.hx > 256 || pl.hy > 256 || pl.hz > 256) return false;
+      c.halo_bytes = (uint32_t)(pl.hx * pl.hy * pl.hz * ncol * 16 * gs);
+      c.a_bytes = c.halo_bytes;
+      c.halo_slot = (uint32_t)(((size_t)pl.n_a * c.halo_bytes + 1023) / 1024 * 1024);
+      c.ring_off = (uint32_t)pl.hs * c.halo_slot;
+      c.stage_bytes = c.b_bytes;
+      if (c.ring_off + 2048 >= (size_t)kMaxSmem) continue;
+    }
+    c.stages = std::min(8, (int)((kMaxSmem - 2048 - c.ring_off) / c.stage_bytes));
     if (c.stages >= 4 || (i8 && c.stages >= 3)) { bestp = c; best = 4; break; }
     if (c.stages >= 2 && best < c.stages) { bestp = c; best = c.stages; }
   }
   if (best < 0) return false;
   pl = bestp;
   pl.tmem_cols = (uint32_t)std::max(32, pow2_at_least(pl.levels * pl.n_tile * pl.acc_slots));
-  pl.smem_bytes = (size_t)pl.stages * pl.stage_bytes + 1024 + 256;
+  pl.smem_bytes = (size_t)pl.ring_off + (size_t)pl.stages * pl.stage_bytes + 1024 + 512;
   return pl.tmem_cols <= 512;
 }
 
@@ -524,8 +547,8 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
   const cuuint64_t Gt = own ? (cuuint64_t)pl.G : (cuuint64_t)h->C_in;
   dims[0] = (cuuint64_t)pl.epg * ncol;
   box[0] = (cuuint32_t)(pl.epg * ncol);
-  box[1] = (cuuint32_t)pl.tx;
-  box[2] = (cuuint32_t)pl.ty;
+  box[1] = (cuuint32_t)(pl.halo ? pl.hx : pl.tx);
+  box[2] = (cuuint32_t)(pl.halo ? pl.hy : pl.ty);
   strides[0] = rowb;
   dims[1] = D;
   if (h->sk == 1) {
@@ -545,7 +568,7 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
     strides[1] = rowb * D;
     strides[2] = rowb * D * D;
     strides[3] = rowb * D * D * D;
-    box[3] = (cuuint32_t)pl.tz;
+    box[3] = (cuuint32_t)(pl.halo ? pl.hz : pl.tz);
     box[4] = (cuuint32_t)pl.gs;
   } else {
     dims[2] = D;
@@ -639,6 +662,14 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.k_iters = pl.k_iters;
   p.ks = pl.ks;
   p.a_bytes = pl.a_bytes;
+  p.halo = pl.halo;
+  p.hx = pl.hx;
+  p.hy = pl.hy;
+  p.hz = pl.hz;
+  p.hs = pl.hs;
+  p.halo_bytes = pl.halo_bytes;
+  p.halo_slot = pl.halo_slot;
+  p.ring_off = pl.ring_off;
   p.b_bytes = pl.b_bytes;
   p.b_img_bytes = pl.b_img_bytes;
   p.stage_bytes = pl.stage_bytes;

@@ -69,6 +69,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ConvKParams p) {
   constexpr bool kSplit = (PREC == kPrec3xTf32);
   constexpr bool kInt8 = (PREC == kPrecFp32);
+  // epilogue warp groups: warps 4-7, plus warps 8-11 when they are not the
+  // 3xTF32 splitter (each group drains half of the accumulator columns)
+  constexpr int kEpiGroups = kSplit ? 1 : 2;
   // A row-group bytes: packed 16-byte groups for bf16 / int8 digits / 1-D,
   // otherwise one protocol multivector (16 B in 2-D, 32 B in 3-D)
   constexpr int RB = (PREC == kPrecBf16 || kInt8 || NB == 2) ? 16 : NB * 4;
@@ -77,12 +80,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = p.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * p.stage_bytes);
+  const int HS = p.halo ? p.hs : 0;
+  uint8_t* ring = smem + p.ring_off;  // pipeline stages (after the halo buffers in halo mode)
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)S * p.stage_bytes);
   uint64_t* empty = full + S;
   uint64_t* lo_ready = empty + S;
   uint64_t* tfull = lo_ready + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* hfull = tempty + 2;   // halo buffers: loaded
+  uint64_t* hempty = hfull + 2;   //               consumed by the last tap's MMAs
+  uint64_t* hlo = hempty + 2;     //               3xTF32 split done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hlo + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -97,7 +105,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 128 * kEpiGroups);
+      mbar_init(&hfull[a], 1);
+      mbar_init(&hempty[a], 1);
+      mbar_init(&hlo[a], 128);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmap);
@@ -111,6 +122,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int crank = cs > 1 ? (int)cluster_ctarank() : 0;
 
   const long long num_tiles = p.num_tiles;
+  const int nQ = p.k_iters / p.n_gs;  // filter taps
   const uint32_t a_total = p.a_bytes * (uint32_t)p.n_a;
   const int slots = p.acc_slots;
   const uint32_t slot_cols = (uint32_t)(p.levels * p.n_tile);
@@ -120,21 +132,52 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int hsl = 0;
+      uint32_t hphase = 0;
       const int df = p.d_filter;
-      const uint32_t tx_bytes = p.a_bytes * (uint32_t)p.n_tma_a + p.b_bytes;
+      const uint32_t tx_bytes = p.halo ? p.b_bytes : p.a_bytes * (uint32_t)p.n_tma_a + p.b_bytes;
+      auto load_b = [&](const uint8_t* bsrc, int kit) {
+        uint8_t* sB = ring + (size_t)stage * p.stage_bytes + (p.halo ? 0u : a_total);
+        if (cs == 1 || p.dbg_nomc) {
+          bulk_load(sB, bsrc + (size_t)kit * p.b_bytes, p.b_bytes, &full[stage]);
+        } else {  // this CTA's slice of the stage, multicast to the whole cluster
+          const uint32_t sl = p.b_bytes / (uint32_t)cs;
+          bulk_load_multicast(sB + crank * sl, bsrc + (size_t)kit * p.b_bytes + crank * sl, sl, &full[stage], cmask);
+        }
+      };
       for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int nt, tx, ty, tz, b;
         decode_tile(p, t, crank, nt, tx, ty, tz, b);
         const int x0 = tx * p.tx - p.pad, y0 = ty * p.ty - p.pad, z0 = tz * p.tz - p.pad;
         const uint8_t* bsrc = p.b_img + (size_t)nt * p.k_iters * p.b_bytes;
+        if (p.halo) {
+          // one halo box per channel group, then the B stage of every tap
+          for (int gsi = 0; gsi < p.n_gs; ++gsi) {
+            const int g0 = gsi * p.gs;
+            mbar_wait(&hempty[hsl], hphase ^ 1);
+            uint8_t* hA = smem + (size_t)hsl * p.halo_slot;
+            mbar_arrive_expect_tx(&hfull[hsl], p.halo_bytes);
+            if (p.merged_bc)
+              tma_load_5d(hA, &tmap, &hfull[hsl], 0, x0, y0, z0, b * p.G + g0);
+            else
+              tma_load_5d(hA, &tmap, &hfull[hsl], 0, x0, y0, g0, b);
+            if (++hsl == HS) { hsl = 0; hphase ^= 1; }
+            for (int q = 0; q < nQ; ++q) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              mbar_arrive_expect_tx(&full[stage], tx_bytes);
+              load_b(bsrc, q * p.n_gs + gsi);
+              if (++stage == S) { stage = 0; phase ^= 1; }
+            }
+          }
+          continue;
+        }
         for (int kit = 0; kit < p.k_iters; ++kit) {
           const int q = kit / p.n_gs, g0 = (kit - q * p.n_gs) * p.gs;
           int qx, qy, qz;
           if (p.k == 3) { qz = q / (df * df); qy = (q / df) % df; qx = q % df; }
           else { qz = 0; qy = q / df; qx = q % df; }
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sA = smem + (size_t)stage * p.stage_bytes;
-          uint8_t* sB = sA + a_total;
+          uint8_t* sA = ring + (size_t)stage * p.stage_bytes;
           mbar_arrive_expect_tx(&full[stage], tx_bytes);
           for (int d = 0; d < p.n_tma_a; ++d) {
             const int bb = d * p.B + b;  // digit planes are stacked over the batch
@@ -145,12 +188,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             else
               tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, y0 + qy, g0, bb);
           }
-          if (cs == 1 || p.dbg_nomc) {
-            bulk_load(sB, bsrc + (size_t)kit * p.b_bytes, p.b_bytes, &full[stage]);
-          } else {  // this CTA's slice of the stage, multicast to the whole cluster
-            const uint32_t sl = p.b_bytes / (uint32_t)cs;
-            bulk_load_multicast(sB + crank * sl, bsrc + (size_t)kit * p.b_bytes + crank * sl, sl, &full[stage], cmask);
-          }
+          load_b(bsrc, kit);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
@@ -174,17 +212,76 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int hsl = 0;
+    uint32_t hphase = 0;
+    const int df = p.d_filter;
+    const int ncol = p.bs.on ? p.bs.ncol : 1;
+    // halo mode: K-major SWIZZLE_NONE, SBO = halo row pitch (the tile is one
+    // 8-row core-matrix group wide), LBO = one channel-group plane of the halo
+    const uint32_t h_plane = (uint32_t)(p.hx * p.hy * p.hz * ncol * 16);
+    const uint64_t h_tmpl = smem_desc(0, h_plane, (uint32_t)(p.hx * ncol * 16), kSwizzleNone);
+    const uint32_t h_img4 = p.halo_bytes >> 4, h_plane4 = h_plane >> 4;
+    const uint32_t h_dx = (uint32_t)ncol;                                  // next tap along x
+    const uint32_t h_wrap_x = (uint32_t)((p.hx - df) * ncol);              // x wrapped: next halo row
+    const uint32_t h_wrap_y = (uint32_t)((p.hy - df) * p.hx * ncol);       // y wrapped: next halo plane
     for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)acc * slot_cols;
+      if (p.halo) {
+        for (int gsi = 0; gsi < p.n_gs; ++gsi) {
+          if (kSplit) mbar_wait(&hlo[hsl], hphase);
+          else mbar_wait(&hfull[hsl], hphase);
+          tc_fence_after();
+          const uint32_t hA4 = (smem_u32(smem + (size_t)hsl * p.halo_slot) & 0x3FFFFu) >> 4;
+          // tap (qx, qy, qz) -> halo offset in 16-byte rows, stepped without divisions
+          uint32_t tap4 = 0;
+          int qx = 0, qy = 0;
+          for (int q = 0; q < nQ; ++q) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sB4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
+            if (elect_one()) {
+              for (int s = 0; s < p.ks; ++s) {
+                const uint64_t a0 = h_tmpl + (uint64_t)(hA4 + tap4 + (uint32_t)s * 2u * h_plane4);
+                const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)s * b_ks4);
+                const uint32_t first = (gsi == 0 && q == 0 && s == 0) ? 1u : 0u;
+                if constexpr (kSplit) {
+                  mma_tf32(d_tmem, a0 + h_img4, b0, idesc, first ? 0u : 1u);  // A_lo * B_hi
+                  mma_tf32(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
+                  mma_tf32(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
+                } else if constexpr (PREC == kPrecTf32) {
+                  mma_tf32(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+                } else if constexpr (PREC == kPrecBf16) {
+                  mma_bf16(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+                }
+              }
+              if (cs == 1 || p.dbg_nomc) mma_commit(&empty[stage]);
+              else mma_commit_multicast(&empty[stage], cmask);
+              if (q == nQ - 1) mma_commit(&hempty[hsl]);  // halo reusable once the last tap retires
+              if (q == nQ - 1 && gsi == p.n_gs - 1) mma_commit(&tfull[acc]);
+            }
+            __syncwarp();
+            if (++stage == S) { stage = 0; phase ^= 1; }
+            tap4 += h_dx;
+            if (++qx == df) {
+              qx = 0;
+              tap4 += h_wrap_x;
+              if (++qy == df) { qy = 0; tap4 += h_wrap_y; }
+            }
+          }
+          if (++hsl == HS) { hsl = 0; hphase ^= 1; }
+        }
+        if (++acc == slots) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
       for (int kit = 0; kit < p.k_iters; ++kit) {
         if (kSplit) mbar_wait(&lo_ready[stage], phase);
         else mbar_wait(&full[stage], phase);
         tc_fence_after();
         // (cluster launches return cluster-window shared addresses: keep the
         // CTA-local 18 bits so nothing carries past the 14-bit start field)
-        const uint32_t sA4 = (smem_u32(smem + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
+        const uint32_t sA4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
         const uint32_t sB4 = sA4 + a_tot4;
         if (elect_one()) {
           for (int s = 0; s < p.ks; ++s) {
@@ -224,9 +321,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       if (++acc == slots) { acc = 0; acc_phase ^= 1; }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && (warp < 8 || !kSplit)) {
     // ===================== epilogue =====================
-    const int ew = warp - 4;
+    const int ew = warp & 3;  // TMEM lane quarter this warp may access
+    const int eg = (warp >> 2) - 1;
+    const int c_half = ((p.n_tile / kEpiGroups + 15) / 16) * 16;
+    const int c_beg = eg * c_half, c_end = min(p.n_tile, c_beg + c_half);
     const int row = ew * 32 + lane;
     // with a change of basis a pixel owns ncol = 2 adjacent rows (lanes), one per matrix column
     const int bcol = p.bs.on ? (row & 1) : 0;
@@ -270,7 +370,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)acc * slot_cols;
-      for (int c0 = 0; c0 < p.n_tile; c0 += 16) {
+      for (int c0 = c_beg; c0 < c_end; c0 += 16) {
         const int n0 = nt * p.n_tile + c0;
         if (n0 >= p.N) break;
         double dv[16];  // accumulator values of this chunk (bias not yet added)
@@ -434,27 +534,41 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // ===================== 3xTF32 splitter =====================
     if constexpr (kSplit) {
       const int tid = threadIdx.x - 256;
+      auto split = [&](uint8_t* buf, uint32_t bytes) {
+        uint4* a = reinterpret_cast<uint4*>(buf);
+        float4* lo = reinterpret_cast<float4*>(buf + bytes);
+        const int n4 = (int)(bytes / 16);
+        for (int i = tid; i < n4; i += 128) {
+          uint4 v = a[i];
+          uint4 h;
+          h.x = v.x & 0xFFFFE000u; h.y = v.y & 0xFFFFE000u; h.z = v.z & 0xFFFFE000u; h.w = v.w & 0xFFFFE000u;
+          float4 l;
+          l.x = __uint_as_float(v.x) - __uint_as_float(h.x);
+          l.y = __uint_as_float(v.y) - __uint_as_float(h.y);
+          l.z = __uint_as_float(v.z) - __uint_as_float(h.z);
+          l.w = __uint_as_float(v.w) - __uint_as_float(h.w);
+          a[i] = h;
+          lo[i] = l;
+        }
+        fence_proxy_async_smem();
+      };
       int stage = 0;
       uint32_t phase = 0;
-      const int n4 = (int)(p.a_bytes / 16);
+      int hsl = 0;
+      uint32_t hphase = 0;
       for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        if (p.halo) {
+          for (int gsi = 0; gsi < p.n_gs; ++gsi) {
+            mbar_wait(&hfull[hsl], hphase);
+            split(smem + (size_t)hsl * p.halo_slot, p.halo_bytes);
+            mbar_arrive(&hlo[hsl]);
+            if (++hsl == HS) { hsl = 0; hphase ^= 1; }
+          }
+          continue;
+        }
         for (int kit = 0; kit < p.k_iters; ++kit) {
           mbar_wait(&full[stage], phase);
-          uint4* a = reinterpret_cast<uint4*>(smem + (size_t)stage * p.stage_bytes);
-          float4* lo = reinterpret_cast<float4*>(smem + (size_t)stage * p.stage_bytes + p.a_bytes);
-          for (int i = tid; i < n4; i += 128) {
-            uint4 v = a[i];
-            uint4 h;
-            h.x = v.x & 0xFFFFE000u; h.y = v.y & 0xFFFFE000u; h.z = v.z & 0xFFFFE000u; h.w = v.w & 0xFFFFE000u;
-            float4 l;
-            l.x = __uint_as_float(v.x) - __uint_as_float(h.x);
-            l.y = __uint_as_float(v.y) - __uint_as_float(h.y);
-            l.z = __uint_as_float(v.z) - __uint_as_float(h.z);
-            l.w = __uint_as_float(v.w) - __uint_as_float(h.w);
-            a[i] = h;
-            lo[i] = l;
-          }
-          fence_proxy_async_smem();
+          split(ring + (size_t)stage * p.stage_bytes, p.a_bytes);
           mbar_arrive(&lo_ready[stage]);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }

@@ -102,6 +102,10 @@ struct ConvPlan {
   int stages;
   uint32_t tmem_cols;
   size_t smem_bytes;
+  // halo mode: each channel group's input halo (hx x hy x hz pixels) is loaded
+  // once and reused by every filter tap through descriptor offsets
+  int halo, hx, hy, hz, hs;
+  uint32_t halo_bytes, halo_slot, ring_off;
 };
 
 struct ConvKParams {
@@ -114,6 +118,8 @@ struct ConvKParams {
   uint32_t a_bytes, b_bytes, b_img_bytes, stage_bytes, tmem_cols;
   int stages, n_a, n_tma_a, levels, acc_slots;
   int cs;                     // cluster size: CTAs sharing each B stage by multicast (1 or 2)
+  int halo, hx, hy, hz, hs;   // halo mode (see ConvPlan)
+  uint32_t halo_bytes, halo_slot, ring_off;
   Basis bs;                   // change of basis: rows = (pixel, column), epilogue inverse transform
   long long num_m_tiles;      // real pixel tiles (tiles beyond are cluster padding)
   int dbg_nomc;               // debug: cluster launch without B multicast
