@@ -87,28 +87,12 @@ std::vector<C2> candidates(bool real_only, int square) {
   return out;
 }
 
-bool build_and_check(const int* g, int k, const std::vector<C2>& gen, Basis* bs) {
+// Exact validation of a candidate T (rows = (column, component), ncol = 2
+// identical w x w blocks) and fill of the Basis record: T T^T = 2 I, every
+// blade's left multiplication block-diagonal with identical blocks, and the
+// two-term forms of T and T^T used by the device kernels.
+bool validate_and_fill(const int* g, int k, const int (&T)[8][8], int w, Basis* bs) {
   const int nb = 1 << k;
-  const bool cplx = (k == 3);
-  const int w = cplx ? 4 : 2;
-  std::vector<C2> M(nb);
-  for (int I = 0; I < nb; ++I) {
-    C2 m = ident();
-    for (int bit = 0; bit < k; ++bit)
-      if ((I >> bit) & 1) m = mul(m, gen[bit]);
-    M[I] = m;
-  }
-  int T[8][8] = {};
-  for (int c = 0; c < 2; ++c)
-    for (int r = 0; r < 2; ++r)
-      for (int part = 0; part < (cplx ? 2 : 1); ++part) {
-        const int s = c * w + r * (cplx ? 2 : 1) + part;
-        for (int I = 0; I < nb; ++I) {
-          const double v = part ? M[I].im[r][c] : M[I].re[r][c];
-          if (v != 0 && v != 1 && v != -1) return false;
-          T[s][I] = (int)v;
-        }
-      }
   // T T^T == 2 I
   for (int a = 0; a < nb; ++a)
     for (int b = 0; b < nb; ++b) {
@@ -160,13 +144,83 @@ bool build_and_check(const int* g, int k, const std::vector<C2>& gen, Basis* bs)
   return true;
 }
 
+
+bool build_and_check(const int* g, int k, const std::vector<C2>& gen, Basis* bs) {
+  const int nb = 1 << k;
+  const bool cplx = (k == 3);
+  const int w = cplx ? 4 : 2;
+  std::vector<C2> M(nb);
+  for (int I = 0; I < nb; ++I) {
+    C2 m = ident();
+    for (int bit = 0; bit < k; ++bit)
+      if ((I >> bit) & 1) m = mul(m, gen[bit]);
+    M[I] = m;
+  }
+  int T[8][8] = {};
+  for (int c = 0; c < 2; ++c)
+    for (int r = 0; r < 2; ++r)
+      for (int part = 0; part < (cplx ? 2 : 1); ++part) {
+        const int s = c * w + r * (cplx ? 2 : 1) + part;
+        for (int I = 0; I < nb; ++I) {
+          const double v = part ? M[I].im[r][c] : M[I].re[r][c];
+          if (v != 0 && v != 1 && v != -1) return false;
+          T[s][I] = (int)v;
+        }
+      }
+  return validate_and_fill(g, k, T, w, bs);
+}
+
 }  // namespace
+
+// Degenerate k = 3 signature with exactly one null generator e_z whose other
+// two generators span M2(R) (Cl(2,0), Cl(1,1)): x = a + b e_z with a, b in
+// that M2(R), and since e_z e_z = 0 and e_z c = c^ e_z (grade involution),
+//   f x = f_a x_a + (f_a x_b + f_b x_a^) e_z.
+// With c^ = E c E^-1 (E = the pair's pseudoscalar matrix) and Z = X_b E, each
+// column of (X_a, Z) transforms by the same lower block-triangular operator
+// [[F_a, 0], [F_b E, F_a]]: two identical 4 x 4 blocks, half the multiply-adds
+// of the 8 x 8 expanded kernel (SURVEY 8f f4 extended to H4's signatures).
+// T is assembled from the pair's 2-D basis; the column swap and signs that
+// realise Z are searched and the result validated exactly.
+static bool find_degenerate_basis(const int* g, int k, Basis* bs) {
+  if (k != 3) return false;
+  int z = -1, nz = 0;
+  for (int i = 0; i < 3; ++i)
+    if (g[i] == 0) { z = i; ++nz; }
+  if (nz != 1) return false;
+  int gi[2], pos[2], n = 0;
+  for (int i = 0; i < 3; ++i)
+    if (i != z) { pos[n] = i; gi[n++] = g[i]; }
+  Basis pb;
+  if (!find_basis(gi, 2, &pb)) return false;  // pair must be M2(R)
+  auto full = [&](int m) {  // pair blade (2-bit) -> full blade mask
+    return ((m & 1) ? (1 << pos[0]) : 0) | ((m & 2) ? (1 << pos[1]) : 0);
+  };
+  for (int swap = 0; swap < 2; ++swap)
+    for (int sg = 0; sg < 16; ++sg) {
+      int T[8][8] = {};
+      for (int c = 0; c < 2; ++c)
+        for (int r = 0; r < 2; ++r) {
+          const int sA = c * 4 + r, sB = c * 4 + 2 + r;
+          const int sgn = ((sg >> (c * 2 + r)) & 1) ? -1 : 1;
+          for (int m = 0; m < 4; ++m) {
+            const int I = full(m);
+            T[sA][I] = pb.T[(c * 2 + r) * 8 + m];
+            // coefficient of e_I e_z = reorder sign * x_{I | z}
+            T[sB][I | (1 << z)] = sgn * pb.T[((c ^ swap) * 2 + r) * 8 + m] * blade_coeff(I, 1 << z, g, k);
+          }
+        }
+      if (validate_and_fill(g, k, T, 4, bs)) return true;
+    }
+  *bs = Basis{};
+  return false;
+}
 
 bool find_basis(const int* g, int k, Basis* bs) {
   *bs = Basis{};
   if (k != 2 && k != 3) return false;
   for (int i = 0; i < k; ++i)
-    if (g[i] == 0) return false;  // degenerate: not semisimple, no matrix algebra
+    if (g[i] == 0) return find_degenerate_basis(g, k, bs);  // not semisimple: see above
   std::vector<std::vector<C2>> cand(k);
   for (int i = 0; i < k; ++i) cand[i] = candidates(k == 2, g[i]);
   std::vector<C2> gen(k);

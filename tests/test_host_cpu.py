@@ -174,10 +174,13 @@ def _basis(g):
 @pytest.mark.parametrize("g", O.all_signatures(3))
 def test_change_of_basis_is_exact_block_diagonalisation(g):
     """x' = T x turns left multiplication by any multivector into
-    ncol identical w x w blocks (checked against the oracle's Cayley tensor)."""
+    ncol identical w x w blocks (checked against the oracle's Cayley tensor);
+    for the degenerate signatures the blocks are lower block-triangular."""
     ok, ncol, w, T = _basis(g)
     k = len(g)
     expect = k >= 2 and all(g) and not (k == 2 and g == (-1, -1)) and g not in [(-1, -1, -1), (1, 1, -1), (1, -1, 1), (-1, 1, 1)]
+    # degenerate k = 3 with one null generator whose complement pair is M2(R) (not the quaternions)
+    expect = expect or (k == 3 and g.count(0) == 1 and tuple(v for v in g if v) != (-1, -1))
     if not ok:
         assert not expect, f"no basis found for {g}"
         return
