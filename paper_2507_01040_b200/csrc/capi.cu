@@ -25,6 +25,8 @@ static bool g_no_cluster = getenv("CL_NO_CLUSTER") != nullptr;  // debug: disabl
 static bool g_no_basis = getenv("CL_NO_BASIS") != nullptr;      // A/B: disable the change of basis
 static bool g_basis_2d = getenv("CL_BASIS_2D") != nullptr;      // A/B: enable it for 2-D layers
 static bool g_no_halo = getenv("CL_NO_HALO") != nullptr;        // A/B: disable halo reuse of the A tile
+static bool g_no_halo_i8 = getenv("CL_NO_HALO_I8") != nullptr;  // A/B: halo off for the int8 mode only
+static int g_force_ks = getenv("CL_KS") ? atoi(getenv("CL_KS")) : 0;  // A/B: force the K steps per stage
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -104,8 +106,8 @@ static int pow2_at_least(int v) {
 // ---------------------------------------------------------------------------
 // planning
 // ---------------------------------------------------------------------------
-static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, int d_filter, const Basis& bs,
-                      ConvPlan& pl) {
+static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_out, int d_filter, const Basis& bs,
+                           bool allow_halo, ConvPlan& pl) {
   pl = ConvPlan{};
   pl.k = k;
   pl.nb = nb;
@@ -144,7 +146,7 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
   // halo reuse (16-byte-row operands, 2-D / 3-D, filters wider than 1): the
   // tile is one core-matrix group wide (8 rows = 8/ncol pixels) so every
   // filter tap is a plain descriptor offset into one loaded halo
-  pl.halo = !i8 && pl.rb == 16 && (k == 2 || k == 3) && d_filter >= 2 && !g_no_halo;
+  pl.halo = allow_halo && pl.rb == 16 && (k == 2 || k == 3) && d_filter >= 2 && !g_no_halo && !(i8 && g_no_halo_i8);
   if (pl.halo) {
     tx = 8 / ncol;
     ty = tpix / tx;
@@ -173,6 +175,7 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
   int best = -1;
   ConvPlan bestp;
   for (int ks : {8, 4, 2, 1}) {
+    if (g_force_ks && ks != g_force_ks) continue;
     const int gs = ks * gpk;
     if (gs > G_pad_min) continue;
     int G, n_gs;
@@ -201,9 +204,9 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
     c.stage_bytes = c.a_bytes * pl.n_a + c.b_bytes;
     if (pl.halo) {
       if (pl.hx > 256 || pl.hy > 256 || pl.hz > 256) return false;
-      c.halo_bytes = (uint32_t)(pl.hx * pl.hy * pl.hz * ncol * 16 * gs);
-      c.a_bytes = c.halo_bytes;
-      c.halo_slot = (uint32_t)(((size_t)pl.n_a * c.halo_bytes + 1023) / 1024 * 1024);
+      c.halo_bytes = (uint32_t)(pl.hx * pl.hy * pl.hz * ncol * 16 * gs);  // one plane's TMA bytes
+      c.a_bytes = (c.halo_bytes + 127u) / 128u * 128u;                     // plane stride (TMA dst alignment)
+      c.halo_slot = (uint32_t)(((size_t)pl.n_a * c.a_bytes + 1023) / 1024 * 1024);
       c.ring_off = (uint32_t)pl.hs * c.halo_slot;
       c.stage_bytes = c.b_bytes;
       if (c.ring_off + 2048 >= (size_t)kMaxSmem) continue;
@@ -217,6 +220,16 @@ static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, i
   pl.tmem_cols = (uint32_t)std::max(32, pow2_at_least(pl.levels * pl.n_tile * pl.acc_slots));
   pl.smem_bytes = (size_t)pl.ring_off + (size_t)pl.stages * pl.stage_bytes + 1024 + 512;
   return pl.tmem_cols <= 512;
+}
+
+// Halo reuse when it plans a pipeline at least 4 stages deep; the int8 mode's
+// four digit planes leave 3-D halos only 3 short B stages (measured slower),
+// so those fall back to per-tap A loads.
+static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, int d_filter, const Basis& bs,
+                      ConvPlan& pl) {
+  if (plan_conv_impl(k, nb, prec, C_in, C_out, d_out, d_filter, bs, true, pl) && (!pl.halo || pl.stages >= 4))
+    return true;
+  return plan_conv_impl(k, nb, prec, C_in, C_out, d_out, d_filter, bs, false, pl);
 }
 
 }  // namespace cl
@@ -269,14 +282,15 @@ struct WsCache {
   }
 };
 
-// Host-buffer pipeline state of one handle: two streams and their staging
+// Host-buffer pipeline state of one handle: kPipe streams and their staging
 // buffers + workspaces, reused across calls (host calls on one handle are
 // serialised by the mutex; they are synchronous anyway).
+constexpr int kPipe = 3;
 struct HostPipe {
   std::mutex m;
-  cudaStream_t st[2] = {nullptr, nullptr};
-  WsCache stage[2];
-  WsCache ws[2];
+  cudaStream_t st[kPipe] = {};
+  WsCache stage[kPipe];
+  WsCache ws[kPipe];
   ~HostPipe() {
     for (auto& x : st)
       if (x) cudaStreamDestroy(x);
@@ -654,6 +668,9 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.cs = (p.num_m_tiles >= 2 && !g_no_cluster && (pl.prec == kPrecFp32 || pl.prec == kPrecBf16)) ? 2 : 1;
   p.num_tiles = ((p.num_m_tiles + p.cs - 1) / p.cs) * p.cs * p.n_ntiles;
   p.dbg_nomc = getenv("CL_DBG_NOMC") != nullptr;
+  p.dbg_skip = getenv("CL_DBG_SKIP") ? atoi(getenv("CL_DBG_SKIP")) : 0;
+  p.sleep_prod = getenv("CL_SLEEP_PROD") ? (uint32_t)atoi(getenv("CL_SLEEP_PROD")) : 0u;
+  p.sleep_epi = getenv("CL_SLEEP_EPI") ? (uint32_t)atoi(getenv("CL_SLEEP_EPI")) : 0u;
   p.d_filter = h->d_filter;
   p.n_gs = pl.n_gs;
   p.gs = pl.gs;
@@ -702,9 +719,12 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
 }
 
 // Generic host-buffer runner: the batch is streamed through the device in
-// chunks on two streams, so chunk i+1's H2D copy overlaps chunk i's compute
-// and chunk i-1's D2H copy (copy engines and SMs work concurrently). Streams,
-// staging buffers and workspaces persist in the handle's HostPipe.
+// chunks round-robin over kPipe streams, so chunk i+1's H2D copy overlaps
+// chunk i's compute and chunk i-1's D2H copy (copy engines and SMs work
+// concurrently). With three streams a stream's H2D -> compute -> D2H cycle
+// (longer than one chunk's compute when copies are slow) spans three chunks
+// of compute, so the SMs stay busy. Streams, staging buffers and workspaces
+// persist in the handle's HostPipe.
 template <class WsFn, class F>
 static int host_chunked(HostPipe& hp, long long B, size_t in_per, size_t out_per, long long chunk,
                         const float* xh, float* yh, cudaStream_t user, WsFn&& ws_bytes, F&& fwd) {
@@ -713,18 +733,19 @@ static int host_chunked(HostPipe& hp, long long B, size_t in_per, size_t out_per
   if (chunk <= 0) {
     const size_t target = (size_t)512 << 20;  // ~512 MB of input per chunk
     chunk = std::max<long long>(1, (long long)(target / std::max<size_t>(in_per, 1)));
-    chunk = std::min<long long>(chunk, std::max<long long>(1, (B + 1) / 2));
+    chunk = std::min<long long>(chunk, std::max<long long>(1, (B + kPipe - 1) / kPipe));
   }
   chunk = std::min(chunk, B);
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < kPipe; ++i)
     if (!hp.st[i]) CL_CUDA(cudaStreamCreateWithFlags(&hp.st[i], cudaStreamNonBlocking), "stream create");
   cudaEvent_t start;
   CL_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming), "event");
   CL_CUDA(cudaEventRecord(start, user), "event record");
-  void* stg[2];
-  void* wsp[2];
+  void* stg[kPipe];
+  void* wsp[kPipe];
+  const int npipe = (int)std::min<long long>(kPipe, (B + chunk - 1) / chunk);
   int rc = CL_OK;
-  for (int i = 0; i < 2 && rc == CL_OK; ++i) {
+  for (int i = 0; i < npipe && rc == CL_OK; ++i) {
     cudaStreamWaitEvent(hp.st[i], start, 0);
     rc = hp.stage[i].get(hp.st[i], align_up(in_per * chunk, 256) + out_per * chunk, &stg[i]);
     if (rc == CL_OK) rc = hp.ws[i].get(hp.st[i], ws_bytes(chunk), &wsp[i]);
@@ -732,7 +753,7 @@ static int host_chunked(HostPipe& hp, long long B, size_t in_per, size_t out_per
   int it = 0;
   for (long long b0 = 0; b0 < B && rc == CL_OK; b0 += chunk, ++it) {
     const long long nb = std::min(chunk, B - b0);
-    const int i = it & 1;
+    const int i = it % npipe;
     float* dx = reinterpret_cast<float*>(stg[i]);
     float* dy = reinterpret_cast<float*>(reinterpret_cast<char*>(stg[i]) + align_up(in_per * chunk, 256));
     cudaError_t e = cudaMemcpyAsync(dx, reinterpret_cast<const char*>(xh) + (size_t)b0 * in_per,
@@ -744,11 +765,12 @@ static int host_chunked(HostPipe& hp, long long B, size_t in_per, size_t out_per
                         cudaMemcpyDeviceToHost, hp.st[i]);
     if (e != cudaSuccess) { rc = cuda_fail(e, "D2H"); break; }
   }
-  cudaError_t e0 = cudaStreamSynchronize(hp.st[0]);
-  cudaError_t e1 = cudaStreamSynchronize(hp.st[1]);
+  for (int i = 0; i < kPipe; ++i) {
+    if (!hp.st[i]) continue;
+    const cudaError_t e = cudaStreamSynchronize(hp.st[i]);
+    if (rc == CL_OK && e != cudaSuccess) rc = cuda_fail(e, "host path");
+  }
   cudaEventDestroy(start);
-  if (rc == CL_OK && e0 != cudaSuccess) rc = cuda_fail(e0, "host path");
-  if (rc == CL_OK && e1 != cudaSuccess) rc = cuda_fail(e1, "host path");
   return rc;
 }
 

@@ -73,6 +73,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait with back-off for warps that are off the critical path (the epilogue
+// waiting for an accumulator, the producer waiting for a free slot): a tight
+// try_wait spin from many warps floods the MIO queue that tcgen05.mma issue
+// shares, so sleep between polls.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t done;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(ns);
+  }
+}
+
 // one lane of a converged warp (elect.sync): the MMA issuer idiom
 __device__ __forceinline__ uint32_t elect_one() {
   uint32_t pred = 0;

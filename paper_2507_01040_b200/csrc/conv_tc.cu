@@ -39,6 +39,14 @@ __device__ __forceinline__ float act_gate(const float (&v)[NB], int mode, const 
   return 1.f / (1.f + expf(-s));
 }
 
+// register-array pick with a runtime index (selects, no local memory)
+template <int W>
+__device__ __forceinline__ long long pick_w(const long long (&a)[W], int i) {
+  if constexpr (W == 1) return a[0];
+  else if constexpr (W == 2) return i ? a[1] : a[0];
+  else return (i & 2) ? ((i & 1) ? a[3] : a[2]) : ((i & 1) ? a[1] : a[0]);
+}
+
 // Persistent tile order: CTAs of one cluster (consecutive blockIdx, rank r)
 // take consecutive pixel tiles of the SAME N tile so they can share each B
 // stage by multicast; N tiles of one pixel-tile group run back to back (A
@@ -154,16 +162,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           // one halo box per channel group, then the B stage of every tap
           for (int gsi = 0; gsi < p.n_gs; ++gsi) {
             const int g0 = gsi * p.gs;
-            mbar_wait(&hempty[hsl], hphase ^ 1);
+            mbar_wait_sleep(&hempty[hsl], hphase ^ 1, p.sleep_prod);
             uint8_t* hA = smem + (size_t)hsl * p.halo_slot;
-            mbar_arrive_expect_tx(&hfull[hsl], p.halo_bytes);
-            if (p.merged_bc)
-              tma_load_5d(hA, &tmap, &hfull[hsl], 0, x0, y0, z0, b * p.G + g0);
-            else
-              tma_load_5d(hA, &tmap, &hfull[hsl], 0, x0, y0, g0, b);
+            mbar_arrive_expect_tx(&hfull[hsl], p.halo_bytes * (uint32_t)p.n_tma_a);
+            for (int d = 0; d < p.n_tma_a; ++d) {  // int8: one halo per digit plane (planes stacked over the batch)
+              const int bb = d * p.B + b;
+              if (p.merged_bc)
+                tma_load_5d(hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], 0, x0, y0, z0, bb * p.G + g0);
+              else
+                tma_load_5d(hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], 0, x0, y0, g0, bb);
+            }
             if (++hsl == HS) { hsl = 0; hphase ^= 1; }
             for (int q = 0; q < nQ; ++q) {
-              mbar_wait(&empty[stage], phase ^ 1);
+              mbar_wait_sleep(&empty[stage], phase ^ 1, p.sleep_prod);
               mbar_arrive_expect_tx(&full[stage], tx_bytes);
               load_b(bsrc, q * p.n_gs + gsi);
               if (++stage == S) { stage = 0; phase ^= 1; }
@@ -176,8 +187,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           int qx, qy, qz;
           if (p.k == 3) { qz = q / (df * df); qy = (q / df) % df; qx = q % df; }
           else { qz = 0; qy = q / df; qx = q % df; }
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_sleep(&empty[stage], phase ^ 1, p.sleep_prod);
           uint8_t* sA = ring + (size_t)stage * p.stage_bytes;
+          if (p.dbg_skip) {  // timing experiment: drop A and/or B traffic
+            const uint32_t txb = ((p.dbg_skip & 1) ? 0u : p.a_bytes * (uint32_t)p.n_tma_a) + ((p.dbg_skip & 2) ? 0u : p.b_bytes);
+            if (txb) mbar_arrive_expect_tx(&full[stage], txb); else mbar_arrive(&full[stage]);
+            if (!(p.dbg_skip & 1))
+              for (int d = 0; d < p.n_tma_a; ++d)
+                tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, y0 + qy, z0 + qz, (d * p.B + b) * p.G + g0);
+            if (!(p.dbg_skip & 2)) load_b(bsrc, kit);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_arrive_expect_tx(&full[stage], tx_bytes);
           for (int d = 0; d < p.n_tma_a; ++d) {
             const int bb = d * p.B + b;  // digit planes are stacked over the batch
@@ -220,7 +241,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // 8-row core-matrix group wide), LBO = one channel-group plane of the halo
     const uint32_t h_plane = (uint32_t)(p.hx * p.hy * p.hz * ncol * 16);
     const uint64_t h_tmpl = smem_desc(0, h_plane, (uint32_t)(p.hx * ncol * 16), kSwizzleNone);
-    const uint32_t h_img4 = p.halo_bytes >> 4, h_plane4 = h_plane >> 4;
+    const uint32_t h_img4 = p.a_bytes >> 4, h_plane4 = h_plane >> 4;  // digit / lo plane stride
     const uint32_t h_dx = (uint32_t)ncol;                                  // next tap along x
     const uint32_t h_wrap_x = (uint32_t)((p.hx - df) * ncol);              // x wrapped: next halo row
     const uint32_t h_wrap_y = (uint32_t)((p.hy - df) * p.hx * ncol);       // y wrapped: next halo plane
@@ -246,7 +267,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 const uint64_t a0 = h_tmpl + (uint64_t)(hA4 + tap4 + (uint32_t)s * 2u * h_plane4);
                 const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)s * b_ks4);
                 const uint32_t first = (gsi == 0 && q == 0 && s == 0) ? 1u : 0u;
-                if constexpr (kSplit) {
+                if constexpr (kInt8) {
+#pragma unroll
+                  for (int L = 0; L < kLevels; ++L) {
+                    const int i0 = L > kDigitsW - 1 ? L - (kDigitsW - 1) : 0;
+#pragma unroll
+                    for (int i = i0; i <= L && i < kDigitsA; ++i) {
+                      const int j = L - i;
+                      mma_i8(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * h_img4),
+                             b0 + (uint64_t)(j * b_img4), idesc, (first && i == i0) ? 0u : 1u);
+                    }
+                  }
+                } else if constexpr (kSplit) {
                   mma_tf32(d_tmem, a0 + h_img4, b0, idesc, first ? 0u : 1u);  // A_lo * B_hi
                   mma_tf32(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
                   mma_tf32(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
@@ -339,6 +371,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       inv_s0[t2] = p.bs.inv_sgn[t2 % 8][0];
       inv_s1[t2] = p.bs.inv_sgn[t2 % 8][1];
     }
+    // int8 epilogue: the two terms of each of this lane's blades, own column / partner column
+    constexpr int WL = (NB >= 4) ? NB / 2 : 1;
+    int inv_o[WL], inv_p[WL], inv_os[WL], inv_ps[WL];
+#pragma unroll
+    for (int j = 0; j < WL; ++j) {
+      const int t = bcol * WL + j;
+      const int a0 = p.bs.inv[t % 8][0], a1 = p.bs.inv[t % 8][1];
+      const bool first_own = (a0 / WL) == bcol;
+      inv_o[j] = (first_own ? a0 : a1) % WL;
+      inv_p[j] = (first_own ? a1 : a0) % WL;
+      inv_os[j] = first_own ? p.bs.inv_sgn[t % 8][0] : p.bs.inv_sgn[t % 8][1];
+      inv_ps[j] = first_own ? p.bs.inv_sgn[t % 8][1] : p.bs.inv_sgn[t % 8][0];
+    }
     const int lx = prow % p.tx, ly = (prow / p.tx) % p.ty, lz = prow / (p.tx * p.ty);
     const int d_out = p.d_out;
     const long long P_out = (p.k == 3) ? (long long)d_out * d_out * d_out
@@ -367,10 +412,170 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       double a_sc = 0.0;
       if constexpr (kInt8) if (valid) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
-      mbar_wait(&tfull[acc], acc_phase);
+      mbar_wait_sleep(&tfull[acc], acc_phase, p.sleep_epi);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)acc * slot_cols;
-      for (int c0 = c_beg; c0 < c_end; c0 += 16) {
+      if constexpr (kInt8) {
+        // Two-phase epilogue: this mode has ONE accumulator slot (4 exact
+        // levels x N_TILE fill TMEM), so the next tile's MMAs wait for it.
+        // Phase 1 drains TMEM into registers (level combine, change-of-basis
+        // inverse, bias, activation gate) and releases the slot; phase 2 adds
+        // the residual and stores while the next tile's MMAs run.
+        constexpr int kHold = 64;  // columns per thread: N_TILE <= 128 over 2 warp groups
+        float hv[kHold];
+#pragma unroll
+        for (int ci = 0; ci < kHold / 16; ++ci) {
+          const int c0 = c_beg + ci * 16;
+          const int n0 = nt * p.n_tile + c0;
+          if (c0 < c_end && n0 < p.N && !(p.dbg_skip & 4)) {
+            long long sv[16];  // exact: S = L0 2^24 + L1 2^16 + L2 2^8 + L3 (|S| < 2^53 for K <= 32000)
+            {
+              uint32_t l0[16], l1[16], l2[16], l3[16];
+              tmem_ld16(taddr + (uint32_t)c0, l0);
+              tmem_ld16(taddr + (uint32_t)(p.n_tile + c0), l1);
+              tmem_ld16(taddr + (uint32_t)(2 * p.n_tile + c0), l2);
+              tmem_ld16(taddr + (uint32_t)(3 * p.n_tile + c0), l3);
+              tmem_ld_wait();
+#pragma unroll
+              for (int c = 0; c < 16; ++c)
+                sv[c] = ((long long)(int)l0[c] << 24) + ((long long)(int)l1[c] << 16) +
+                        ((long long)(int)l2[c] << 8) + (long long)(int)l3[c];
+            }
+            if (p.bs.on) {
+              if constexpr (NB >= 4) {
+                // lane (column bcol) produces blades bcol*W + j: x = (s_o own[o_j] + s_p partner[p_j]) / 2,
+                // combined exactly in int64 (one weight scale per channel), rounded once
+                constexpr int W = NB / 2;
+#pragma unroll
+                for (int cc = 0; cc < 16 / W; ++cc) {
+                  const int co = n0 / W + cc;
+                  const int cq = min(co, p.C_out - 1);
+                  long long own[W], oth[W];
+#pragma unroll
+                  for (int r = 0; r < W; ++r) {
+                    own[r] = sv[cc * W + r];
+                    const int lo = __shfl_xor_sync(0xffffffffu, (int)(own[r] & 0xffffffffll), 1);
+                    const int hi = __shfl_xor_sync(0xffffffffu, (int)(own[r] >> 32), 1);
+                    oth[r] = ((long long)hi << 32) | (long long)(unsigned)lo;
+                  }
+                  const double sc = a_sc * (0.5 / 16777216.0) * (double)__ldg(p.w_scale + nt * p.n_tile + cc * W + c0);
+                  float v[W];
+                  float part = 0.f;
+#pragma unroll
+                  for (int j = 0; j < W; ++j) {
+                    const long long a = pick_w<W>(own, inv_o[j]), bq = pick_w<W>(oth, inv_p[j]);
+                    const long long xs = (inv_os[j] > 0 ? a : -a) + (inv_ps[j] > 0 ? bq : -bq);
+                    const int t = bcol * W + j;
+                    v[j] = (float)fma((double)xs, sc, (double)__ldg(p.bias + t * p.C_out + cq));
+                    if (p.act_mode >= 0) part = fmaf(v[j], __ldg(p.act_w + cq * NB + t), part);
+                  }
+                  if (p.act_mode >= 0) {
+                    float sg = part + __shfl_xor_sync(0xffffffffu, part, 1);
+                    if (p.act_mode == 0) sg += __ldg(p.act_b + cq);
+                    else if (p.act_mode == 2) sg = sg / p.act_K;
+                    const float gte = 1.f / (1.f + expf(-sg));
+#pragma unroll
+                    for (int j = 0; j < W; ++j) v[j] *= gte;
+                  }
+#pragma unroll
+                  for (int j = 0; j < W; ++j) hv[ci * 16 + cc * W + j] = v[j];
+                }
+              }
+            } else {
+#pragma unroll
+              for (int cc = 0; cc < 16 / NB; ++cc) {
+                const int co = n0 / NB + cc;
+                const int cq = min(co, p.C_out - 1);
+                float v[NB];
+#pragma unroll
+                for (int j = 0; j < NB; ++j) {
+                  const double sc = a_sc * (1.0 / 16777216.0) * (double)__ldg(p.w_scale + min(n0 + cc * NB + j, p.N - 1));
+                  v[j] = (float)fma((double)sv[cc * NB + j], sc, (double)__ldg(p.bias + j * p.C_out + cq));
+                }
+                if (p.act_mode >= 0 && co < p.C_out) {
+                  const float gte = act_gate<NB>(v, p.act_mode, p.act_w + co * NB,
+                                                 p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K);
+#pragma unroll
+                  for (int j = 0; j < NB; ++j) v[j] *= gte;
+                }
+#pragma unroll
+                for (int j = 0; j < NB; ++j) hv[ci * 16 + cc * NB + j] = v[j];
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == slots) { acc = 0; acc_phase ^= 1; }
+        if (!valid || (p.dbg_skip & 4)) continue;
+#pragma unroll
+        for (int ci = 0; ci < kHold / 16; ++ci) {
+          const int c0 = c_beg + ci * 16;
+          const int n0 = nt * p.n_tile + c0;
+          if (c0 < c_end && n0 < p.N) {
+            // W blades of one channel per store: the lane's half (change of basis) or all N_B
+            constexpr int W = (NB >= 4) ? NB / 2 : NB;
+            const int wv = p.bs.on ? W : NB;
+#pragma unroll
+            for (int cc = 0; cc < 16 / W; ++cc) {
+              if (cc * wv >= 16) break;
+              const int co = n0 / wv + cc;
+              if (co >= p.C_out) break;
+              const long long off = p.bs.on ? (long long)bcol * W : 0;
+              if (p.bs.on) {
+                float h[W];
+#pragma unroll
+                for (int j = 0; j < W; ++j) h[j] = hv[ci * 16 + cc * W + j];
+                if (p.resid) {
+                  const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB + off;
+                  if constexpr (W == 2) {
+                    const float2 q2 = __ldg(reinterpret_cast<const float2*>(rp));
+                    h[0] += q2.x; h[1 % W] += q2.y;
+                  } else {
+                    const float4 q4 = __ldg(reinterpret_cast<const float4*>(rp));
+                    h[0] += q4.x; h[1 % W] += q4.y; h[2 % W] += q4.z; h[3 % W] += q4.w;
+                  }
+                }
+                if (p.y) {
+                  float* yp = p.y + (((long long)b * p.C_out + co) * P_out + pix) * NB + off;
+                  if constexpr (W == 2) *reinterpret_cast<float2*>(yp) = make_float2(h[0], h[1 % W]);
+                  else *reinterpret_cast<float4*>(yp) = make_float4(h[0], h[1 % W], h[2 % W], h[3 % W]);
+                }
+              } else {
+                if (cc >= 16 / NB) break;
+                float v[NB];
+#pragma unroll
+                for (int j = 0; j < NB; ++j) v[j] = hv[ci * 16 + cc * NB + j];
+                if (p.resid) {
+                  const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB;
+                  if constexpr (NB == 2) {
+                    const float2 q2 = __ldg(reinterpret_cast<const float2*>(rp));
+                    v[0] += q2.x; v[1] += q2.y;
+                  } else {
+#pragma unroll
+                    for (int j = 0; j < NB / 4; ++j) {
+                      const float4 q4 = __ldg(reinterpret_cast<const float4*>(rp) + j);
+                      v[4 * j] += q4.x; v[4 * j + 1] += q4.y; v[4 * j + 2] += q4.z; v[4 * j + 3] += q4.w;
+                    }
+                  }
+                }
+                if (p.y) {
+                  float* yp = p.y + (((long long)b * p.C_out + co) * P_out + pix) * NB;
+                  if constexpr (NB == 2) {
+                    *reinterpret_cast<float2*>(yp) = make_float2(v[0], v[1]);
+                  } else {
+#pragma unroll
+                    for (int j = 0; j < NB / 4; ++j)
+                      reinterpret_cast<float4*>(yp)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                  }
+                }
+              }
+            }
+          }
+        }
+        continue;
+      }
+      for (int c0 = c_beg; c0 < ((p.dbg_skip & 4) ? c_beg : c_end); c0 += 16) {
         const int n0 = nt * p.n_tile + c0;
         if (n0 >= p.N) break;
         double dv[16];  // accumulator values of this chunk (bias not yet added)
@@ -534,9 +739,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // ===================== 3xTF32 splitter =====================
     if constexpr (kSplit) {
       const int tid = threadIdx.x - 256;
-      auto split = [&](uint8_t* buf, uint32_t bytes) {
+      auto split = [&](uint8_t* buf, uint32_t bytes, uint32_t lo_off) {
         uint4* a = reinterpret_cast<uint4*>(buf);
-        float4* lo = reinterpret_cast<float4*>(buf + bytes);
+        float4* lo = reinterpret_cast<float4*>(buf + lo_off);
         const int n4 = (int)(bytes / 16);
         for (int i = tid; i < n4; i += 128) {
           uint4 v = a[i];
@@ -560,7 +765,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (p.halo) {
           for (int gsi = 0; gsi < p.n_gs; ++gsi) {
             mbar_wait(&hfull[hsl], hphase);
-            split(smem + (size_t)hsl * p.halo_slot, p.halo_bytes);
+            split(smem + (size_t)hsl * p.halo_slot, p.halo_bytes, p.a_bytes);
             mbar_arrive(&hlo[hsl]);
             if (++hsl == HS) { hsl = 0; hphase ^= 1; }
           }
@@ -568,7 +773,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
         for (int kit = 0; kit < p.k_iters; ++kit) {
           mbar_wait(&full[stage], phase);
-          split(ring + (size_t)stage * p.stage_bytes, p.a_bytes);
+          split(ring + (size_t)stage * p.stage_bytes, p.a_bytes, p.a_bytes);
           mbar_arrive(&lo_ready[stage]);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }

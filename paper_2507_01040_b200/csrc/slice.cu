@@ -175,15 +175,19 @@ __global__ void weight_colscale_kernel(Sig sg, const float* __restrict__ f, int 
   const int n = blockIdx.x;
   const int co = n / w, t = n % w;
   float m = 0.f;
+  // under a change of basis all w columns of a channel share one scale, so the
+  // epilogue can combine the two column terms of the inverse as exact integers
+  const int t0 = bs.on ? 0 : t, t1 = bs.on ? w : t + 1;
   if (co < C_out) {
-    for (int idx = threadIdx.x; idx < C_in * w * Q; idx += blockDim.x) {
-      const int q = idx % Q;
-      const int j = (idx / Q) % w;
-      const int ci = idx / (Q * w);
-      const double e = bs.on ? basis_entry(sg, bs, f, C_in, C_out, Q, co, t, ci, j, q)
-                             : (double)expanded_entry(sg, f, nb, C_in, C_out, Q, co, t, ci, j, q);
-      m = fmaxf(m, (float)fabs(e));
-    }
+    for (int tt = t0; tt < t1; ++tt)
+      for (int idx = threadIdx.x; idx < C_in * w * Q; idx += blockDim.x) {
+        const int q = idx % Q;
+        const int j = (idx / Q) % w;
+        const int ci = idx / (Q * w);
+        const double e = bs.on ? basis_entry(sg, bs, f, C_in, C_out, Q, co, tt, ci, j, q)
+                               : (double)expanded_entry(sg, f, nb, C_in, C_out, Q, co, tt, ci, j, q);
+        m = fmaxf(m, (float)fabs(e));
+      }
   }
   __shared__ float red[32];
 #pragma unroll
