@@ -26,6 +26,7 @@ static bool g_no_basis = getenv("CL_NO_BASIS") != nullptr;      // A/B: disable 
 static bool g_basis_2d = getenv("CL_BASIS_2D") != nullptr;      // A/B: enable it for 2-D layers
 static bool g_no_halo = getenv("CL_NO_HALO") != nullptr;        // A/B: disable halo reuse of the A tile
 static bool g_no_halo_i8 = getenv("CL_NO_HALO_I8") != nullptr;  // A/B: halo off for the int8 mode only
+static bool g_no_tma_merge = getenv("CL_NO_TMA_MERGE") != nullptr;  // A/B: one TMA line per pixel
 static int g_force_ks = getenv("CL_KS") ? atoi(getenv("CL_KS")) : 0;  // A/B: force the K steps per stage
 static std::atomic<uint64_t> g_launches{0};
 
@@ -542,6 +543,14 @@ struct Epi {
   int ybf_groups = 0;
 };
 
+// 8-byte elements per pixel of the A tensor map's merged (pixel, row) inner
+// dimension, or 0 for the per-pixel-line map (32-byte swizzled protocol rows).
+static int tma_epx(const ConvPlan& pl) {
+  const int ncol = pl.bs.on ? pl.bs.ncol : 1;
+  if (g_no_tma_merge || (pl.rb == 32 && ncol == 1)) return 0;
+  return pl.rb * ncol / 8;
+}
+
 static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUtensorMap* map) {
   const ConvPlan& pl = h->plan;
   auto enc = get_encode();
@@ -559,43 +568,42 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
   const bool own = pl.packed || i8;  // operand written by our pack / slice pass: G groups per sample
   const cuuint64_t planes = (cuuint64_t)pl.n_tma_a;  // int8 digit planes stacked over the batch
   const cuuint64_t Gt = own ? (cuuint64_t)pl.G : (cuuint64_t)h->C_in;
-  dims[0] = (cuuint64_t)pl.epg * ncol;
-  box[0] = (cuuint32_t)(pl.epg * ncol);
-  box[1] = (cuuint32_t)(pl.halo ? pl.hx : pl.tx);
-  box[2] = (cuuint32_t)(pl.halo ? pl.hy : pl.ty);
-  strides[0] = rowb;
-  dims[1] = D;
-  if (h->sk == 1) {
-    // (e, x, sample, group, plane) over a (plane, B, G, D, 16 B) tensor
-    dims[2] = (cuuint64_t)B;
-    dims[3] = Gt;
-    dims[4] = planes;
-    strides[1] = rowb * D * Gt;          // sample
-    strides[2] = rowb * D;               // group
-    strides[3] = rowb * D * Gt * (cuuint64_t)B;  // plane
-    box[3] = (cuuint32_t)pl.gs;
-    box[4] = 1;
-  } else if (pl.merged_bc) {
-    dims[2] = D;
-    dims[3] = D;
-    dims[4] = planes * (cuuint64_t)B * Gt;
-    strides[1] = rowb * D;
-    strides[2] = rowb * D * D;
-    strides[3] = rowb * D * D * D;
-    box[3] = (cuuint32_t)(pl.halo ? pl.hz : pl.tz);
-    box[4] = (cuuint32_t)pl.gs;
-  } else {
-    dims[2] = D;
-    dims[3] = Gt;
-    dims[4] = planes * (cuuint64_t)B;
-    strides[1] = rowb * D;
-    strides[2] = rowb * D * D;
-    strides[3] = rowb * D * D * Gt;
-    box[3] = (cuuint32_t)pl.gs;
-    box[4] = 1;
+  const cuuint32_t bx = (cuuint32_t)(pl.halo ? pl.hx : pl.tx);
+  // logical dims after x: (d1, d2, d3) with byte strides (s1, s2, s3), boxes (b1, b2, b3)
+  cuuint64_t d1, d2, d3, s1, s2, s3;
+  cuuint32_t b1, b2, b3;
+  if (h->sk == 1) {  // (x, sample, group, plane) over a (plane, B, G, D, row) tensor
+    d1 = (cuuint64_t)B; s1 = rowb * D * Gt; b1 = (cuuint32_t)pl.ty;
+    d2 = Gt; s2 = rowb * D; b2 = (cuuint32_t)pl.gs;
+    d3 = planes; s3 = rowb * D * Gt * (cuuint64_t)B; b3 = 1;
+  } else if (pl.merged_bc) {  // (x, y, z, plane*B*G)
+    d1 = D; s1 = rowb * D; b1 = (cuuint32_t)(pl.halo ? pl.hy : pl.ty);
+    d2 = D; s2 = rowb * D * D; b2 = (cuuint32_t)(pl.halo ? pl.hz : pl.tz);
+    d3 = planes * (cuuint64_t)B * Gt; s3 = rowb * D * D * D; b3 = (cuuint32_t)pl.gs;
+  } else {  // (x, y, group, plane*B)
+    d1 = D; s1 = rowb * D; b1 = (cuuint32_t)(pl.halo ? pl.hy : pl.ty);
+    d2 = Gt; s2 = rowb * D * D; b2 = (cuuint32_t)pl.gs;
+    d3 = planes * (cuuint64_t)B; s3 = rowb * D * D * Gt; b3 = 1;
   }
-  const CUtensorMapDataType dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
-                                    : (pl.esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+  const int epx = tma_epx(pl);
+  CUtensorMapDataType dt;
+  if (epx) {
+    // merged inner dimension: (pixel x, row bytes) as 8-byte elements, so a
+    // tile row is one TMA line; zero fill still lands on whole pixels
+    dims[0] = D * (cuuint64_t)epx; box[0] = bx * (cuuint32_t)epx;
+    dims[1] = d1; dims[2] = d2; dims[3] = d3; dims[4] = 1;
+    strides[0] = s1; strides[1] = s2; strides[2] = s3; strides[3] = s3 * d3;
+    box[1] = b1; box[2] = b2; box[3] = b3; box[4] = 1;
+    dt = CU_TENSOR_MAP_DATA_TYPE_UINT64;
+  } else {
+    dims[0] = (cuuint64_t)pl.epg * ncol; box[0] = (cuuint32_t)(pl.epg * ncol);
+    dims[1] = D; box[1] = bx; strides[0] = rowb;
+    dims[2] = d1; dims[3] = d2; dims[4] = d3;
+    strides[1] = s1; strides[2] = s2; strides[3] = s3;
+    box[2] = b1; box[3] = b2; box[4] = b3;
+    dt = i8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+            : (pl.esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+  }
   CUresult r = enc(map, dt, 5, const_cast<void*>(xsrc), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    (pl.rb == 32 && ncol == 1) ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -680,6 +688,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.ks = pl.ks;
   p.a_bytes = pl.a_bytes;
   p.halo = pl.halo;
+  p.epx = tma_epx(pl);
   p.hx = pl.hx;
   p.hy = pl.hy;
   p.hz = pl.hz;

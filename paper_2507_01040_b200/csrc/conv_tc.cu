@@ -39,6 +39,15 @@ __device__ __forceinline__ float act_gate(const float (&v)[NB], int mode, const 
   return 1.f / (1.f + expf(-s));
 }
 
+// A-operand TMA box at (x, c1, c2, c3). With a merged (pixel x row-bytes)
+// inner dimension of 8-byte elements (p.epx per pixel; one TMA line per tile
+// row instead of one per pixel) the coordinates shift left by one.
+__device__ __forceinline__ void load_a_box(const ConvKParams& p, void* dst, const CUtensorMap* map, uint64_t* bar,
+                                           int x, int c1, int c2, int c3) {
+  if (p.epx) tma_load_5d(dst, map, bar, x * p.epx, c1, c2, c3, 0);
+  else tma_load_5d(dst, map, bar, 0, x, c1, c2, c3);
+}
+
 // register-array pick with a runtime index (selects, no local memory)
 template <int W>
 __device__ __forceinline__ long long pick_w(const long long (&a)[W], int i) {
@@ -168,9 +177,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             for (int d = 0; d < p.n_tma_a; ++d) {  // int8: one halo per digit plane (planes stacked over the batch)
               const int bb = d * p.B + b;
               if (p.merged_bc)
-                tma_load_5d(hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], 0, x0, y0, z0, bb * p.G + g0);
+                load_a_box(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, z0, bb * p.G + g0);
               else
-                tma_load_5d(hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], 0, x0, y0, g0, bb);
+                load_a_box(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, g0, bb);
             }
             if (++hsl == HS) { hsl = 0; hphase ^= 1; }
             for (int q = 0; q < nQ; ++q) {
@@ -194,7 +203,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             if (txb) mbar_arrive_expect_tx(&full[stage], txb); else mbar_arrive(&full[stage]);
             if (!(p.dbg_skip & 1))
               for (int d = 0; d < p.n_tma_a; ++d)
-                tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, y0 + qy, z0 + qz, (d * p.B + b) * p.G + g0);
+                load_a_box(p, sA + d * p.a_bytes, &tmap, &full[stage], x0 + qx, y0 + qy, z0 + qz, (d * p.B + b) * p.G + g0);
             if (!(p.dbg_skip & 2)) load_b(bsrc, kit);
             if (++stage == S) { stage = 0; phase ^= 1; }
             continue;
@@ -203,11 +212,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           for (int d = 0; d < p.n_tma_a; ++d) {
             const int bb = d * p.B + b;  // digit planes are stacked over the batch
             if (p.merged_bc)
-              tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, y0 + qy, z0 + qz, bb * p.G + g0);
+              load_a_box(p, sA + d * p.a_bytes, &tmap, &full[stage], x0 + qx, y0 + qy, z0 + qz, bb * p.G + g0);
             else if (p.k == 1)  // dims (e, x, sample, group, plane)
-              tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, b, g0, d);
+              load_a_box(p, sA + d * p.a_bytes, &tmap, &full[stage], x0 + qx, b, g0, d);
             else
-              tma_load_5d(sA + d * p.a_bytes, &tmap, &full[stage], 0, x0 + qx, y0 + qy, g0, bb);
+              load_a_box(p, sA + d * p.a_bytes, &tmap, &full[stage], x0 + qx, y0 + qy, g0, bb);
           }
           load_b(bsrc, kit);
           if (++stage == S) { stage = 0; phase ^= 1; }

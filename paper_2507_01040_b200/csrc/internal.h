@@ -119,6 +119,7 @@ struct ConvKParams {
   int stages, n_a, n_tma_a, levels, acc_slots;
   int cs;                     // cluster size: CTAs sharing each B stage by multicast (1 or 2)
   int halo, hx, hy, hz, hs;   // halo mode (see ConvPlan)
+  int epx;                    // A tensor map with merged (pixel, row) inner dim: 8-byte elements per pixel, else 0
   uint32_t halo_bytes, halo_slot, ring_off;
   Basis bs;                   // change of basis: rows = (pixel, column), epilogue inverse transform
   long long num_m_tiles;      // real pixel tiles (tiles beyond are cluster padding)
