@@ -424,7 +424,7 @@ def run_ours(args):
         e2e = {"value": spec.B / t_e2e, "unit": "samples/s",
                "h2d_bytes_per_step": int(x.numel() * 4) * world,
                "d2h_bytes_per_step": int(y.numel() * 4) * world,
-               "path": "block_forward(pinned host tensor) -> cl_block_forward_host (chunked H2D/compute/D2H over 2 streams)"}
+               "path": "block_forward(pinned host tensor) -> cl_block_forward_host (chunked H2D/compute/D2H over 3 streams)"}
         del xh, yh
 
     cpu = None

@@ -25,27 +25,35 @@ layer = M.make_conv_layer(M.Dims(B, spec.C, spec.C, spec.d, spec.d_filter, spec.
                           precision=a.precision, padding=spec.padding)
 
 
-def timeit(fn):
+from bench import ClockSampler  # noqa: E402
+
+clocks = {}
+
+
+def timeit(fn, name):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(a.iters):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
+    with ClockSampler(0) as cs:
+        e0.record()
+        for _ in range(a.iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+    clocks[name] = cs.summary().get("sm_mhz")
     return e0.elapsed_time(e1) / a.iters
 
 
 y = torch.empty(layer.output_shape(), device="cuda")
-res = {"conv_ms": timeit(lambda: M.conv_forward(x, layer, out=y))}
+res = {"conv_ms": timeit(lambda: M.conv_forward(x, layer, out=y), "conv")}
 if spec.kind == "block":
     f2, b2 = W.conv_params(spec, 2)
     aw, ab = W.act_params(spec)
     blk = M.make_basic_block(M.Signature(spec.g), B, spec.C, spec.C, spec.C, spec.d, f1, b1, spec.mode, f2, b2,
                              act_weight=aw, act_bias=ab, padding=spec.padding, residual=True, precision=a.precision)
     yb = torch.empty_like(x)
-    res["block_ms"] = timeit(lambda: M.block_forward(x, blk, out=yb))
+    res["block_ms"] = timeit(lambda: M.block_forward(x, blk, out=yb), "block")
 tag = "halo=off" if os.environ.get("CL_NO_HALO") else "halo=on"
-print(f"cfg{a.config} {a.precision} B={B} {tag}", " ".join(f"{k}={v:.3f}" for k, v in res.items()), flush=True)
+print(f"cfg{a.config} {a.precision} B={B} {tag}", " ".join(f"{k}={v:.3f}" for k, v in res.items()),
+      "sm_mhz", clocks, flush=True)
