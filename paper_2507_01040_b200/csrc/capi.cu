@@ -21,7 +21,7 @@ namespace cl {
 
 static thread_local std::string g_last_error;
 static thread_local bool g_time_kernel_only = false;  // cl_conv_time_kernel: skip operand preparation
-static bool g_no_cluster = getenv("CL_NO_CLUSTER") != nullptr;  // debug: disable B multicast
+static bool g_no_pair = getenv("CL_NO_PAIR") != nullptr || getenv("CL_NO_CLUSTER") != nullptr;  // A/B: 1-SM MMA
 static bool g_no_basis = getenv("CL_NO_BASIS") != nullptr;      // A/B: disable the change of basis
 static bool g_basis_2d = getenv("CL_BASIS_2D") != nullptr;      // A/B: enable it for 2-D layers
 static bool g_no_halo = getenv("CL_NO_HALO") != nullptr;        // A/B: disable halo reuse of the A tile
@@ -161,6 +161,9 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
   pl.ty = ty;
   pl.tz = tz;
 
+  // 2-SM MMA for every mode but 3xTF32 (its A splitter would need the pair's
+  // two halves split before the leader's MMA)
+  pl.pair = prec != kPrec3xTf32 && !g_no_pair;
   pl.n_img = i8 ? kDigitsW : (prec == kPrec3xTf32 ? 2 : 1);
   pl.n_a = i8 ? kDigitsA : pl.n_img;
   pl.n_tma_a = i8 ? kDigitsA : 1;
@@ -202,14 +205,16 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
     c.a_bytes = (uint32_t)(kTileM * gs * pl.rb);
     c.b_img_bytes = (uint32_t)(ks * pl.n_tile * 32);
     c.b_bytes = c.b_img_bytes * pl.n_img;
-    c.stage_bytes = c.a_bytes * pl.n_a + c.b_bytes;
+    const uint32_t b_cta = pl.pair ? c.b_bytes / 2 : c.b_bytes;  // B bytes each CTA holds
+    if (pl.pair && (b_cta % 512 || b_cta / 512 > 256)) continue;  // B half = one 2-D TMA box of 512-byte rows
+    c.stage_bytes = c.a_bytes * pl.n_a + b_cta;
     if (pl.halo) {
       if (pl.hx > 256 || pl.hy > 256 || pl.hz > 256) return false;
       c.halo_bytes = (uint32_t)(pl.hx * pl.hy * pl.hz * ncol * 16 * gs);  // one plane's TMA bytes
       c.a_bytes = (c.halo_bytes + 127u) / 128u * 128u;                     // plane stride (TMA dst alignment)
       c.halo_slot = (uint32_t)(((size_t)pl.n_a * c.a_bytes + 1023) / 1024 * 1024);
       c.ring_off = (uint32_t)pl.hs * c.halo_slot;
-      c.stage_bytes = c.b_bytes;
+      c.stage_bytes = b_cta;
       if (c.ring_off + 2048 >= (size_t)kMaxSmem) continue;
     }
     c.stages = std::min(8, (int)((kMaxSmem - 2048 - c.ring_off) / c.stage_bytes));
@@ -671,11 +676,11 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.N = pl.N;
   p.C_out = h->C_out;
   p.num_m_tiles = (h->sk == 1 ? 1LL : (long long)B) * p.ntz * p.nty * p.ntx;
-  // CTA pairs share each B stage by TMA multicast where it pays (measured:
-  // +4-6% for the int8 and bf16 modes; the tf32 modes run faster unpaired)
-  p.cs = (p.num_m_tiles >= 2 && !g_no_cluster && (pl.prec == kPrecFp32 || pl.prec == kPrecBf16)) ? 2 : 1;
+  // 2-SM pairs take consecutive M tiles of the same N tile (an odd last one
+  // is paired with a ghost tile that computes but stores nothing)
+  p.pair = pl.pair;
+  p.cs = pl.pair ? 2 : 1;
   p.num_tiles = ((p.num_m_tiles + p.cs - 1) / p.cs) * p.cs * p.n_ntiles;
-  p.dbg_nomc = getenv("CL_DBG_NOMC") != nullptr;
   p.dbg_skip = getenv("CL_DBG_SKIP") ? atoi(getenv("CL_DBG_SKIP")) : 0;
   p.sleep_prod = getenv("CL_SLEEP_PROD") ? (uint32_t)atoi(getenv("CL_SLEEP_PROD")) : 0u;
   p.sleep_epi = getenv("CL_SLEEP_EPI") ? (uint32_t)atoi(getenv("CL_SLEEP_EPI")) : 0u;
@@ -722,7 +727,22 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.act_K = epi.act ? (float)epi.act->K : 1.f;
   int grid = (int)std::min<long long>(p.num_tiles, (long long)num_sms());
   grid -= grid % p.cs;
-  cudaError_t e = launch_conv(pl, map, p, grid, s);
+  CUtensorMap bmap = map;  // unused unless paired
+  if (pl.pair) {
+    // the filter images as 512-byte rows; each CTA of a pair loads its half
+    // of a stage as one (64 x 8 B, half / 512) box
+    auto enc = get_encode();
+    const cuuint64_t total = (cuuint64_t)pl.n_ntiles * pl.k_iters * pl.b_bytes;
+    cuuint64_t bd[2] = {64, total / 512};
+    cuuint64_t bst[1] = {512};
+    cuuint32_t bbox[2] = {64, (cuuint32_t)(pl.b_bytes / 2 / 512)};
+    cuuint32_t bes[2] = {1, 1};
+    CUresult r = enc(&bmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint8_t*>(h->img), bd, bst, bbox, bes,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(CL_ERR_CUDA, "CudaError", "filter tensor map: " + std::to_string((int)r));
+  }
+  cudaError_t e = launch_conv(pl, map, bmap, p, grid, s);
   if (e != cudaSuccess) return cuda_fail(e, "conv_tc launch");
   return CL_OK;
 }

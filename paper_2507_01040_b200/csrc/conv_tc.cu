@@ -39,13 +39,31 @@ __device__ __forceinline__ float act_gate(const float (&v)[NB], int mode, const 
   return 1.f / (1.f + expf(-s));
 }
 
+// MMA of the precision mode, 1-SM or 2-SM (pair leader).
+template <int PREC, bool PAIR>
+__device__ __forceinline__ void mma_mode(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (PREC == kPrecFp32) {
+    if constexpr (PAIR) mma_i8_cg2(d, a, b, idesc, acc); else mma_i8(d, a, b, idesc, acc);
+  } else if constexpr (PREC == kPrecBf16) {
+    if constexpr (PAIR) mma_bf16_cg2(d, a, b, idesc, acc); else mma_bf16(d, a, b, idesc, acc);
+  } else {
+    if constexpr (PAIR) mma_tf32_cg2(d, a, b, idesc, acc); else mma_tf32(d, a, b, idesc, acc);
+  }
+}
+
 // A-operand TMA box at (x, c1, c2, c3). With a merged (pixel x row-bytes)
 // inner dimension of 8-byte elements (p.epx per pixel; one TMA line per tile
 // row instead of one per pixel) the coordinates shift left by one.
+template <bool PAIR>
 __device__ __forceinline__ void load_a_box(const ConvKParams& p, void* dst, const CUtensorMap* map, uint64_t* bar,
                                            int x, int c1, int c2, int c3) {
-  if (p.epx) tma_load_5d(dst, map, bar, x * p.epx, c1, c2, c3, 0);
-  else tma_load_5d(dst, map, bar, 0, x, c1, c2, c3);
+  if constexpr (PAIR) {  // bytes complete on the pair leader's barrier
+    if (p.epx) tma_load_5d_cg2(dst, map, bar, x * p.epx, c1, c2, c3, 0);
+    else tma_load_5d_cg2(dst, map, bar, 0, x, c1, c2, c3);
+  } else {
+    if (p.epx) tma_load_5d(dst, map, bar, x * p.epx, c1, c2, c3, 0);
+    else tma_load_5d(dst, map, bar, 0, x, c1, c2, c3);
+  }
 }
 
 // register-array pick with a runtime index (selects, no local memory)
@@ -81,11 +99,13 @@ __device__ __forceinline__ bool decode_tile(const ConvKParams& p, long long t, i
   return real;
 }
 
-template <int NB, int PREC>
+template <int NB, int PREC, bool PAIR>
 __global__ void __launch_bounds__(kConvThreads, 1)
-    conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ConvKParams p) {
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap bmap,
+                   const __grid_constant__ ConvKParams p) {
   constexpr bool kSplit = (PREC == kPrec3xTf32);
   constexpr bool kInt8 = (PREC == kPrecFp32);
+  static_assert(!(PAIR && kSplit), "the 3xTF32 splitter runs unpaired");
   // epilogue warp groups: warps 4-7, plus warps 8-11 when they are not the
   // 3xTF32 splitter (each group drains half of the accumulator columns)
   constexpr int kEpiGroups = kSplit ? 1 : 2;
@@ -113,27 +133,30 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int lane = threadIdx.x & 31;
 
   const int cs = p.cs;
-  const uint16_t cmask = (uint16_t)((1u << cs) - 1u);
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], p.dbg_nomc ? 1u : (uint32_t)cs);  // one MMA commit from every CTA of the cluster
+      mbar_init(&empty[s], 1);  // one MMA commit (the pair leader's reaches both CTAs)
       mbar_init(&lo_ready[s], 128);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128 * kEpiGroups);
+      mbar_init(&tempty[a], 128 * kEpiGroups * (PAIR ? 2 : 1));  // pair: both CTAs' epilogues, on the leader
       mbar_init(&hfull[a], 1);
       mbar_init(&hempty[a], 1);
       mbar_init(&hlo[a], 128);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmap);
+    if constexpr (PAIR) tma_prefetch_desc(&bmap);
   }
-  if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_alloc_cg2(tmem_slot, p.tmem_cols);
+    else tmem_alloc(tmem_slot, p.tmem_cols);
+  }
   tc_fence_before();
   __syncthreads();
-  if (cs > 1) cluster_sync();  // peers' barriers initialised before any multicast
+  if (cs > 1) cluster_sync();  // the pair's barriers and TMEM exist before any cross-CTA traffic
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int crank = cs > 1 ? (int)cluster_ctarank() : 0;
@@ -152,40 +175,40 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       int hsl = 0;
       uint32_t hphase = 0;
       const int df = p.d_filter;
-      const uint32_t tx_bytes = p.halo ? p.b_bytes : p.a_bytes * (uint32_t)p.n_tma_a + p.b_bytes;
-      auto load_b = [&](const uint8_t* bsrc, int kit) {
+      // pair: each CTA loads its own A rows and its half of the B columns; the
+      // leader alone arms its barriers for the bytes of both CTAs
+      const bool arm = !PAIR || crank == 0;
+      const uint32_t b_cta = PAIR ? p.b_bytes / 2 : p.b_bytes;
+      const uint32_t tx_bytes = (PAIR ? 2u : 1u) * (p.halo ? b_cta : p.a_bytes * (uint32_t)p.n_tma_a + b_cta);
+      auto load_b = [&](int nt, int kit) {
         uint8_t* sB = ring + (size_t)stage * p.stage_bytes + (p.halo ? 0u : a_total);
-        if (cs == 1 || p.dbg_nomc) {
-          bulk_load(sB, bsrc + (size_t)kit * p.b_bytes, p.b_bytes, &full[stage]);
-        } else {  // this CTA's slice of the stage, multicast to the whole cluster
-          const uint32_t sl = p.b_bytes / (uint32_t)cs;
-          bulk_load_multicast(sB + crank * sl, bsrc + (size_t)kit * p.b_bytes + crank * sl, sl, &full[stage], cmask);
-        }
+        const size_t off = ((size_t)nt * p.k_iters + kit) * p.b_bytes;
+        if constexpr (PAIR) tma_load_2d_cg2(sB, &bmap, &full[stage], 0, (int)((off + (size_t)crank * b_cta) >> 9));
+        else bulk_load(sB, p.b_img + off, p.b_bytes, &full[stage]);
       };
       for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int nt, tx, ty, tz, b;
         decode_tile(p, t, crank, nt, tx, ty, tz, b);
         const int x0 = tx * p.tx - p.pad, y0 = ty * p.ty - p.pad, z0 = tz * p.tz - p.pad;
-        const uint8_t* bsrc = p.b_img + (size_t)nt * p.k_iters * p.b_bytes;
         if (p.halo) {
           // one halo box per channel group, then the B stage of every tap
           for (int gsi = 0; gsi < p.n_gs; ++gsi) {
             const int g0 = gsi * p.gs;
             mbar_wait_sleep(&hempty[hsl], hphase ^ 1, p.sleep_prod);
             uint8_t* hA = smem + (size_t)hsl * p.halo_slot;
-            mbar_arrive_expect_tx(&hfull[hsl], p.halo_bytes * (uint32_t)p.n_tma_a);
+            if (arm) mbar_arrive_expect_tx(&hfull[hsl], (PAIR ? 2u : 1u) * p.halo_bytes * (uint32_t)p.n_tma_a);
             for (int d = 0; d < p.n_tma_a; ++d) {  // int8: one halo per digit plane (planes stacked over the batch)
               const int bb = d * p.B + b;
               if (p.merged_bc)
-                load_a_box(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, z0, bb * p.G + g0);
+                load_a_box<PAIR>(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, z0, bb * p.G + g0);
               else
-                load_a_box(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, g0, bb);
+                load_a_box<PAIR>(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, g0, bb);
             }
             if (++hsl == HS) { hsl = 0; hphase ^= 1; }
             for (int q = 0; q < nQ; ++q) {
               mbar_wait_sleep(&empty[stage], phase ^ 1, p.sleep_prod);
-              mbar_arrive_expect_tx(&full[stage], tx_bytes);
-              load_b(bsrc, q * p.n_gs + gsi);
+              if (arm) mbar_arrive_expect_tx(&full[stage], tx_bytes);
+              load_b(nt, q * p.n_gs + gsi);
               if (++stage == S) { stage = 0; phase ^= 1; }
             }
           }
@@ -198,45 +221,37 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           else { qz = 0; qy = q / df; qx = q % df; }
           mbar_wait_sleep(&empty[stage], phase ^ 1, p.sleep_prod);
           uint8_t* sA = ring + (size_t)stage * p.stage_bytes;
-          if (p.dbg_skip) {  // timing experiment: drop A and/or B traffic
-            const uint32_t txb = ((p.dbg_skip & 1) ? 0u : p.a_bytes * (uint32_t)p.n_tma_a) + ((p.dbg_skip & 2) ? 0u : p.b_bytes);
-            if (txb) mbar_arrive_expect_tx(&full[stage], txb); else mbar_arrive(&full[stage]);
-            if (!(p.dbg_skip & 1))
-              for (int d = 0; d < p.n_tma_a; ++d)
-                load_a_box(p, sA + d * p.a_bytes, &tmap, &full[stage], x0 + qx, y0 + qy, z0 + qz, (d * p.B + b) * p.G + g0);
-            if (!(p.dbg_skip & 2)) load_b(bsrc, kit);
-            if (++stage == S) { stage = 0; phase ^= 1; }
-            continue;
-          }
-          mbar_arrive_expect_tx(&full[stage], tx_bytes);
+          if (arm) mbar_arrive_expect_tx(&full[stage], tx_bytes);
           for (int d = 0; d < p.n_tma_a; ++d) {
             const int bb = d * p.B + b;  // digit planes are stacked over the batch
             if (p.merged_bc)
-              load_a_box(p, sA + d * p.a_bytes, &tmap, &full[stage], x0 + qx, y0 + qy, z0 + qz, bb * p.G + g0);
+              load_a_box<PAIR>(p, sA + d * p.a_bytes, &tmap, &full[stage], x0 + qx, y0 + qy, z0 + qz, bb * p.G + g0);
             else if (p.k == 1)  // dims (e, x, sample, group, plane)
-              load_a_box(p, sA + d * p.a_bytes, &tmap, &full[stage], x0 + qx, b, g0, d);
+              load_a_box<PAIR>(p, sA + d * p.a_bytes, &tmap, &full[stage], x0 + qx, b, g0, d);
             else
-              load_a_box(p, sA + d * p.a_bytes, &tmap, &full[stage], x0 + qx, y0 + qy, g0, bb);
+              load_a_box<PAIR>(p, sA + d * p.a_bytes, &tmap, &full[stage], x0 + qx, y0 + qy, g0, bb);
           }
-          load_b(bsrc, kit);
+          load_b(nt, kit);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
+  } else if (warp == 1 && (!PAIR || crank == 0)) {
+    // ===================== MMA issuer (the pair leader's in 2-SM mode) =====================
     // The warp runs the loop converged (all lanes wait on the barriers, all
     // values warp-uniform); one elected lane issues tcgen05.mma + commit.
     // Descriptors are template + (address >> 4): start address is the low
     // 14-bit field, and CTA-local shared addresses < 2^18 never carry out of it.
-    const uint32_t idesc = kInt8 ? instr_desc_i8(128u, (uint32_t)p.n_tile)
-                                 : instr_desc(PREC == kPrecBf16 ? 1u : 2u, 128u, (uint32_t)p.n_tile);
+    constexpr uint32_t kM = PAIR ? 256u : 128u;
+    const uint32_t idesc = kInt8 ? instr_desc_i8(kM, (uint32_t)p.n_tile)
+                                 : instr_desc(PREC == kPrecBf16 ? 1u : 2u, kM, (uint32_t)p.n_tile);
+    const uint32_t n_cta = PAIR ? (uint32_t)p.n_tile / 2u : (uint32_t)p.n_tile;  // B rows in this CTA
     // 32-byte swizzled protocol rows (3-D tf32 modes) unless a changed basis packs 16-byte rows
     const bool rb32 = (RB == 32) && !p.bs.on;
     const uint64_t a_tmpl = rb32 ? smem_desc(0, 16, 256, kSwizzle32B) : smem_desc(0, 2048, 128, kSwizzleNone);
-    const uint64_t b_tmpl = smem_desc(0, (uint32_t)p.n_tile * 16u, 128, kSwizzleNone);
-    const uint32_t a_img4 = p.a_bytes >> 4, b_img4 = p.b_img_bytes >> 4;
-    const uint32_t b_ks4 = ((uint32_t)p.n_tile * 32u) >> 4;
+    const uint64_t b_tmpl = smem_desc(0, n_cta * 16u, 128, kSwizzleNone);
+    const uint32_t a_img4 = p.a_bytes >> 4, b_img4 = (PAIR ? p.b_img_bytes / 2 : p.b_img_bytes) >> 4;
+    const uint32_t b_ks4 = (n_cta * 32u) >> 4;
     const uint32_t a_tot4 = a_total >> 4;
     int stage = 0;
     uint32_t phase = 0;
@@ -283,8 +298,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
                     for (int i = i0; i <= L && i < kDigitsA; ++i) {
                       const int j = L - i;
-                      mma_i8(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * h_img4),
-                             b0 + (uint64_t)(j * b_img4), idesc, (first && i == i0) ? 0u : 1u);
+                      mma_mode<PREC, PAIR>(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * h_img4),
+                                           b0 + (uint64_t)(j * b_img4), idesc, (first && i == i0) ? 0u : 1u);
                     }
                   }
                 } else if constexpr (kSplit) {
@@ -292,15 +307,20 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                   mma_tf32(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
                   mma_tf32(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
                 } else if constexpr (PREC == kPrecTf32) {
-                  mma_tf32(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+                  mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
                 } else if constexpr (PREC == kPrecBf16) {
-                  mma_bf16(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+                  mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
                 }
               }
-              if (cs == 1 || p.dbg_nomc) mma_commit(&empty[stage]);
-              else mma_commit_multicast(&empty[stage], cmask);
-              if (q == nQ - 1) mma_commit(&hempty[hsl]);  // halo reusable once the last tap retires
-              if (q == nQ - 1 && gsi == p.n_gs - 1) mma_commit(&tfull[acc]);
+              if constexpr (PAIR) {
+                mma_commit_cg2(&empty[stage]);
+                if (q == nQ - 1) mma_commit_cg2(&hempty[hsl]);  // halo reusable once the last tap retires
+                if (q == nQ - 1 && gsi == p.n_gs - 1) mma_commit_cg2(&tfull[acc]);
+              } else {
+                mma_commit(&empty[stage]);
+                if (q == nQ - 1) mma_commit(&hempty[hsl]);
+                if (q == nQ - 1 && gsi == p.n_gs - 1) mma_commit(&tfull[acc]);
+              }
             }
             __syncwarp();
             if (++stage == S) { stage = 0; phase ^= 1; }
@@ -338,8 +358,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
                 for (int i = i0; i <= L && i < kDigitsA; ++i) {
                   const int j = L - i;
-                  mma_i8(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * a_img4),
-                         b0 + (uint64_t)(j * b_img4), idesc, (first && i == i0) ? 0u : 1u);
+                  mma_mode<PREC, PAIR>(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * a_img4),
+                                       b0 + (uint64_t)(j * b_img4), idesc, (first && i == i0) ? 0u : 1u);
                 }
               }
             } else if constexpr (kSplit) {
@@ -347,15 +367,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               mma_tf32(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
               mma_tf32(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
             } else if constexpr (PREC == kPrecTf32) {
-              mma_tf32(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+              mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
             } else {
-              mma_bf16(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+              mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
             }
           }
-          // smem slot free (in every CTA of the cluster) once these MMAs retire
-          if (cs == 1 || p.dbg_nomc) mma_commit(&empty[stage]);
-          else mma_commit_multicast(&empty[stage], cmask);
-          if (kit == p.k_iters - 1) mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+          // smem slot free (in both CTAs of a pair) once these MMAs retire
+          if constexpr (PAIR) {
+            mma_commit_cg2(&empty[stage]);
+            if (kit == p.k_iters - 1) mma_commit_cg2(&tfull[acc]);  // accumulator ready for the epilogues
+          } else {
+            mma_commit(&empty[stage]);
+            if (kit == p.k_iters - 1) mma_commit(&tfull[acc]);
+          }
         }
         __syncwarp();
         if (++stage == S) { stage = 0; phase ^= 1; }
@@ -514,7 +538,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
         if (++acc == slots) { acc = 0; acc_phase ^= 1; }
         if (!valid || (p.dbg_skip & 4)) continue;
 #pragma unroll
@@ -741,7 +765,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
       if (++acc == slots) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 8) {
@@ -792,17 +816,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (cs > 1) cluster_sync();  // no CTA leaves while a peer may still multicast into it
+  if (cs > 1) cluster_sync();  // no CTA leaves while its pair may still touch its smem / TMEM
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, p.tmem_cols);
+    if constexpr (PAIR) tmem_dealloc_cg2(tmem_base, p.tmem_cols);
+    else tmem_dealloc(tmem_base, p.tmem_cols);
   }
 }
 
-template <int NB, int PREC>
-static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const ConvKParams& p,
-                            int grid, cudaStream_t s) {
-  auto kfn = conv_tc_kernel<NB, PREC>;
+template <int NB, int PREC, bool PAIR>
+static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const CUtensorMap& bmap,
+                            const ConvKParams& p, int grid, cudaStream_t s) {
+  auto kfn = conv_tc_kernel<NB, PREC, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)plan.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -818,36 +843,36 @@ static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kfn, tmap, p);
+  e = cudaLaunchKernelEx(&cfg, kfn, tmap, bmap, p);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const ConvKParams& p,
-                        int grid, cudaStream_t s) {
-  if (plan.nb == 2) {
+template <int NB>
+static cudaError_t launch_nb(const ConvPlan& plan, const CUtensorMap& tmap, const CUtensorMap& bmap,
+                             const ConvKParams& p, int grid, cudaStream_t s) {
+  if (p.pair) {
     switch (plan.prec) {
-      case kPrecFp32: return launch_t<2, kPrecFp32>(plan, tmap, p, grid, s);
-      case kPrec3xTf32: return launch_t<2, kPrec3xTf32>(plan, tmap, p, grid, s);
-      case kPrecTf32: return launch_t<2, kPrecTf32>(plan, tmap, p, grid, s);
-      default: return launch_t<2, kPrecBf16>(plan, tmap, p, grid, s);
-    }
-  }
-  if (plan.nb == 4) {
-    switch (plan.prec) {
-      case kPrecFp32: return launch_t<4, kPrecFp32>(plan, tmap, p, grid, s);
-      case kPrec3xTf32: return launch_t<4, kPrec3xTf32>(plan, tmap, p, grid, s);
-      case kPrecTf32: return launch_t<4, kPrecTf32>(plan, tmap, p, grid, s);
-      default: return launch_t<4, kPrecBf16>(plan, tmap, p, grid, s);
+      case kPrecFp32: return launch_t<NB, kPrecFp32, true>(plan, tmap, bmap, p, grid, s);
+      case kPrecTf32: return launch_t<NB, kPrecTf32, true>(plan, tmap, bmap, p, grid, s);
+      case kPrecBf16: return launch_t<NB, kPrecBf16, true>(plan, tmap, bmap, p, grid, s);
+      default: return cudaErrorInvalidValue;
     }
   }
   switch (plan.prec) {
-    case kPrecFp32: return launch_t<8, kPrecFp32>(plan, tmap, p, grid, s);
-    case kPrec3xTf32: return launch_t<8, kPrec3xTf32>(plan, tmap, p, grid, s);
-    case kPrecTf32: return launch_t<8, kPrecTf32>(plan, tmap, p, grid, s);
-    default: return launch_t<8, kPrecBf16>(plan, tmap, p, grid, s);
+    case kPrecFp32: return launch_t<NB, kPrecFp32, false>(plan, tmap, bmap, p, grid, s);
+    case kPrec3xTf32: return launch_t<NB, kPrec3xTf32, false>(plan, tmap, bmap, p, grid, s);
+    case kPrecTf32: return launch_t<NB, kPrecTf32, false>(plan, tmap, bmap, p, grid, s);
+    default: return launch_t<NB, kPrecBf16, false>(plan, tmap, bmap, p, grid, s);
   }
+}
+
+cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const CUtensorMap& bmap,
+                        const ConvKParams& p, int grid, cudaStream_t s) {
+  if (plan.nb == 2) return launch_nb<2>(plan, tmap, bmap, p, grid, s);
+  if (plan.nb == 4) return launch_nb<4>(plan, tmap, bmap, p, grid, s);
+  return launch_nb<8>(plan, tmap, bmap, p, grid, s);
 }
 
 // fp32 protocol (B, C, P, NB) -> packed 16-byte row groups (B, G, P, [ncol x] 16 B):

@@ -67,18 +67,22 @@ __global__ void expand_img_kernel(Sig sg, const float* __restrict__ f, int C_in,
     // position inside the stage image
     const int byte_k = kl * pl.esize;
     const int s = byte_k >> 5, h = (byte_k >> 4) & 1, e = (byte_k & 15) / pl.esize;
-    uint8_t* base = img + ((size_t)nt * pl.k_iters + kit) * pl.b_bytes;
-    const size_t off = (size_t)s * pl.n_tile * 32 + (size_t)h * pl.n_tile * 16 + (size_t)row * 16 +
-                       (size_t)e * pl.esize;
+    // 2-SM pair: the stage holds two contiguous column halves, one per CTA,
+    // each laid out like a full stage of n_tile / 2 rows
+    const int nrow = pl.pair ? pl.n_tile / 2 : pl.n_tile;
+    const int half = row / nrow, rr = row % nrow;
+    const size_t img_stride = pl.pair ? pl.b_img_bytes / 2 : pl.b_img_bytes;
+    uint8_t* base = img + ((size_t)nt * pl.k_iters + kit) * pl.b_bytes + (size_t)half * (pl.b_bytes / 2);
+    const size_t off = (size_t)s * nrow * 32 + (size_t)h * nrow * 16 + (size_t)rr * 16 + (size_t)e * pl.esize;
     if (pl.prec == kPrecFp32) {
       int8_t d[kDigitsW];
       digits_b256_d<kDigitsW>(wv / (double)__ldg(w_scale + n), d);
 #pragma unroll
-      for (int k = 0; k < kDigitsW; ++k) *reinterpret_cast<int8_t*>(base + (size_t)k * pl.b_img_bytes + off) = d[k];
+      for (int k = 0; k < kDigitsW; ++k) *reinterpret_cast<int8_t*>(base + (size_t)k * img_stride + off) = d[k];
     } else if (pl.prec == kPrec3xTf32) {
       const float hi = __uint_as_float(__float_as_uint(w) & 0xFFFFE000u);
       *reinterpret_cast<float*>(base + off) = hi;
-      *reinterpret_cast<float*>(base + pl.b_img_bytes + off) = (float)(wv - (double)hi);
+      *reinterpret_cast<float*>(base + img_stride + off) = (float)(wv - (double)hi);
     } else if (pl.prec == kPrecTf32) {
       *reinterpret_cast<float*>(base + off) = tf32_rna(w);
     } else {

@@ -106,6 +106,10 @@ struct ConvPlan {
   // once and reused by every filter tap through descriptor offsets
   int halo, hx, hy, hz, hs;
   uint32_t halo_bytes, halo_slot, ring_off;
+  // 2-SM MMA (cta_group::2): a CTA pair computes M = 256 rows; each CTA holds
+  // its 128 A rows and half of the B columns (the filter images are laid out
+  // as two contiguous column halves per stage)
+  int pair;
 };
 
 struct ConvKParams {
@@ -117,13 +121,13 @@ struct ConvKParams {
   int d_filter, n_gs, gs, G, merged_bc, k_iters, ks;
   uint32_t a_bytes, b_bytes, b_img_bytes, stage_bytes, tmem_cols;
   int stages, n_a, n_tma_a, levels, acc_slots;
-  int cs;                     // cluster size: CTAs sharing each B stage by multicast (1 or 2)
+  int cs;                     // cluster size: 2 for a 2-SM (cta_group::2) pair, else 1
+  int pair;                   // 2-SM MMA: M = 256 over the pair, B columns split between the two CTAs
   int halo, hx, hy, hz, hs;   // halo mode (see ConvPlan)
   int epx;                    // A tensor map with merged (pixel, row) inner dim: 8-byte elements per pixel, else 0
   uint32_t halo_bytes, halo_slot, ring_off;
   Basis bs;                   // change of basis: rows = (pixel, column), epilogue inverse transform
   long long num_m_tiles;      // real pixel tiles (tiles beyond are cluster padding)
-  int dbg_nomc;               // debug: cluster launch without B multicast
   uint32_t sleep_prod, sleep_epi;  // back-off (ns) of the producer / epilogue barrier polls
   int dbg_skip;               // timing experiments only: bit 0 skips A loads, bit 1 skips B loads (garbage results)
   const uint8_t* b_img;
@@ -154,8 +158,8 @@ struct ActParams {
 };
 
 // launchers (conv_tc.cu / expand.cu / activation.cu)
-cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const ConvKParams& p,
-                        int grid, cudaStream_t s);
+cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const CUtensorMap& bmap,
+                        const ConvKParams& p, int grid, cudaStream_t s);
 cudaError_t launch_expand_ref(const int* g, int k, const float* f, int C_in, int C_out, int Q,
                               float* out, cudaStream_t s);
 cudaError_t launch_expand_images(const int* g, const ConvPlan& plan, const float* f, int C_in,
