@@ -13,7 +13,7 @@ import os
 from .errors import STATUS_TO_ERROR, ConfigInvalid, MvkernelsError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libclifford_b200.so")
+LIB_PATH = os.environ.get("CL_LIB_PATH") or os.path.join(_HERE, "lib", "libclifford_b200.so")  # override: A/B builds
 
 _lib = None
 

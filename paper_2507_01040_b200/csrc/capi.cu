@@ -27,6 +27,7 @@ static bool g_basis_2d = getenv("CL_BASIS_2D") != nullptr;      // A/B: enable i
 static bool g_no_halo = getenv("CL_NO_HALO") != nullptr;        // A/B: disable halo reuse of the A tile
 static bool g_no_halo_i8 = getenv("CL_NO_HALO_I8") != nullptr;  // A/B: halo off for the int8 mode only
 static bool g_no_tma_merge = getenv("CL_NO_TMA_MERGE") != nullptr;  // A/B: one TMA line per pixel
+static int g_force_tps = getenv("CL_TPS") ? atoi(getenv("CL_TPS")) : 0;  // A/B: taps per stage (halo)
 static int g_force_ks = getenv("CL_KS") ? atoi(getenv("CL_KS")) : 0;  // A/B: force the K steps per stage
 static std::atomic<uint64_t> g_launches{0};
 
@@ -216,6 +217,16 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
       c.ring_off = (uint32_t)pl.hs * c.halo_slot;
       c.stage_bytes = b_cta;
       if (c.ring_off + 2048 >= (size_t)kMaxSmem) continue;
+    }
+    c.tps = 1;
+    if (pl.halo) {
+      // several taps' B images per stage when that keeps the ring >= 4 deep
+      // (fewer barrier round trips per MMA; bf16 / tf32 stages are short)
+      for (int tps : {4, 2}) {
+        if (g_force_tps && tps != g_force_tps) continue;
+        const int st = (int)((kMaxSmem - 2048 - c.ring_off) / (c.stage_bytes * tps));
+        if (st >= 4) { c.tps = tps; c.stage_bytes *= tps; break; }
+      }
     }
     c.stages = std::min(8, (int)((kMaxSmem - 2048 - c.ring_off) / c.stage_bytes));
     if (c.stages >= 4 || (i8 && c.stages >= 3)) { bestp = c; best = 4; break; }
@@ -693,6 +704,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.ks = pl.ks;
   p.a_bytes = pl.a_bytes;
   p.halo = pl.halo;
+  p.tps = pl.tps;
   p.epx = tma_epx(pl);
   p.hx = pl.hx;
   p.hy = pl.hy;

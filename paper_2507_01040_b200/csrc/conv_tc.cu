@@ -180,8 +180,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const bool arm = !PAIR || crank == 0;
       const uint32_t b_cta = PAIR ? p.b_bytes / 2 : p.b_bytes;
       const uint32_t tx_bytes = (PAIR ? 2u : 1u) * (p.halo ? b_cta : p.a_bytes * (uint32_t)p.n_tma_a + b_cta);
-      auto load_b = [&](int nt, int kit) {
-        uint8_t* sB = ring + (size_t)stage * p.stage_bytes + (p.halo ? 0u : a_total);
+      auto load_b = [&](int nt, int kit, uint32_t sub = 0) {
+        uint8_t* sB = ring + (size_t)stage * p.stage_bytes + (p.halo ? 0u : a_total) + sub;
         const size_t off = ((size_t)nt * p.k_iters + kit) * p.b_bytes;
         if constexpr (PAIR) tma_load_2d_cg2(sB, &bmap, &full[stage], 0, (int)((off + (size_t)crank * b_cta) >> 9));
         else bulk_load(sB, p.b_img + off, p.b_bytes, &full[stage]);
@@ -205,10 +205,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 load_a_box<PAIR>(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, g0, bb);
             }
             if (++hsl == HS) { hsl = 0; hphase ^= 1; }
-            for (int q = 0; q < nQ; ++q) {
+            for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
+              const int nq = min(p.tps, nQ - q0);
               mbar_wait_sleep(&empty[stage], phase ^ 1, p.sleep_prod);
-              if (arm) mbar_arrive_expect_tx(&full[stage], tx_bytes);
-              load_b(nt, q * p.n_gs + gsi);
+              if (arm) mbar_arrive_expect_tx(&full[stage], tx_bytes * (uint32_t)nq);
+              for (int i = 0; i < nq; ++i) load_b(nt, (q0 + i) * p.n_gs + gsi, (uint32_t)i * b_cta);
               if (++stage == S) { stage = 0; phase ^= 1; }
             }
           }
@@ -252,6 +253,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const uint64_t b_tmpl = smem_desc(0, n_cta * 16u, 128, kSwizzleNone);
     const uint32_t a_img4 = p.a_bytes >> 4, b_img4 = (PAIR ? p.b_img_bytes / 2 : p.b_img_bytes) >> 4;
     const uint32_t b_ks4 = (n_cta * 32u) >> 4;
+    const uint32_t b_cta4 = (PAIR ? p.b_bytes / 2 : p.b_bytes) >> 4;  // one tap's B image in a multi-tap stage
     const uint32_t a_tot4 = a_total >> 4;
     int stage = 0;
     uint32_t phase = 0;
@@ -282,53 +284,117 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           // tap (qx, qy, qz) -> halo offset in 16-byte rows, stepped without divisions
           uint32_t tap4 = 0;
           int qx = 0, qy = 0;
-          for (int q = 0; q < nQ; ++q) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint32_t sB4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
-            if (elect_one()) {
-              for (int s = 0; s < p.ks; ++s) {
-                const uint64_t a0 = h_tmpl + (uint64_t)(hA4 + tap4 + (uint32_t)s * 2u * h_plane4);
-                const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)s * b_ks4);
-                const uint32_t first = (gsi == 0 && q == 0 && s == 0) ? 1u : 0u;
-                if constexpr (kInt8) {
-#pragma unroll
-                  for (int L = 0; L < kLevels; ++L) {
-                    const int i0 = L > kDigitsW - 1 ? L - (kDigitsW - 1) : 0;
-#pragma unroll
-                    for (int i = i0; i <= L && i < kDigitsA; ++i) {
-                      const int j = L - i;
-                      mma_mode<PREC, PAIR>(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * h_img4),
-                                           b0 + (uint64_t)(j * b_img4), idesc, (first && i == i0) ? 0u : 1u);
+          if (p.tps == 1) {  // one tap per stage (kept separate: the multi-tap loop's codegen costs 20% here)
+            for (int q = 0; q < nQ; ++q) {
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint32_t sB4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
+              if (elect_one()) {
+                for (int s = 0; s < p.ks; ++s) {
+                  const uint64_t a0 = h_tmpl + (uint64_t)(hA4 + tap4 + (uint32_t)s * 2u * h_plane4);
+                  const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)s * b_ks4);
+                  const uint32_t first = (gsi == 0 && q == 0 && s == 0) ? 1u : 0u;
+                  if constexpr (kInt8) {
+  #pragma unroll
+                    for (int L = 0; L < kLevels; ++L) {
+                      const int i0 = L > kDigitsW - 1 ? L - (kDigitsW - 1) : 0;
+  #pragma unroll
+                      for (int i = i0; i <= L && i < kDigitsA; ++i) {
+                        const int j = L - i;
+                        mma_mode<PREC, PAIR>(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * h_img4),
+                                             b0 + (uint64_t)(j * b_img4), idesc, (first && i == i0) ? 0u : 1u);
+                      }
                     }
+                  } else if constexpr (kSplit) {
+                    mma_tf32(d_tmem, a0 + h_img4, b0, idesc, first ? 0u : 1u);  // A_lo * B_hi
+                    mma_tf32(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
+                    mma_tf32(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
+                  } else if constexpr (PREC == kPrecTf32) {
+                    mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+                  } else if constexpr (PREC == kPrecBf16) {
+                    mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
                   }
-                } else if constexpr (kSplit) {
-                  mma_tf32(d_tmem, a0 + h_img4, b0, idesc, first ? 0u : 1u);  // A_lo * B_hi
-                  mma_tf32(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
-                  mma_tf32(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
-                } else if constexpr (PREC == kPrecTf32) {
-                  mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
-                } else if constexpr (PREC == kPrecBf16) {
-                  mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+                }
+                if constexpr (PAIR) {
+                  mma_commit_cg2(&empty[stage]);
+                  if (q == nQ - 1) mma_commit_cg2(&hempty[hsl]);  // halo reusable once the last tap retires
+                  if (q == nQ - 1 && gsi == p.n_gs - 1) mma_commit_cg2(&tfull[acc]);
+                } else {
+                  mma_commit(&empty[stage]);
+                  if (q == nQ - 1) mma_commit(&hempty[hsl]);
+                  if (q == nQ - 1 && gsi == p.n_gs - 1) mma_commit(&tfull[acc]);
                 }
               }
-              if constexpr (PAIR) {
-                mma_commit_cg2(&empty[stage]);
-                if (q == nQ - 1) mma_commit_cg2(&hempty[hsl]);  // halo reusable once the last tap retires
-                if (q == nQ - 1 && gsi == p.n_gs - 1) mma_commit_cg2(&tfull[acc]);
-              } else {
-                mma_commit(&empty[stage]);
-                if (q == nQ - 1) mma_commit(&hempty[hsl]);
-                if (q == nQ - 1 && gsi == p.n_gs - 1) mma_commit(&tfull[acc]);
+              __syncwarp();
+              if (++stage == S) { stage = 0; phase ^= 1; }
+              tap4 += h_dx;
+              if (++qx == df) {
+                qx = 0;
+                tap4 += h_wrap_x;
+                if (++qy == df) { qy = 0; tap4 += h_wrap_y; }
               }
             }
-            __syncwarp();
-            if (++stage == S) { stage = 0; phase ^= 1; }
-            tap4 += h_dx;
-            if (++qx == df) {
-              qx = 0;
-              tap4 += h_wrap_x;
-              if (++qy == df) { qy = 0; tap4 += h_wrap_y; }
+          } else {
+            for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
+              const int nq = min(p.tps, nQ - q0);
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint32_t sB4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
+              if (elect_one()) {
+                uint32_t t4 = tap4;
+                int x = qx, y = qy;
+                for (int i = 0; i < nq; ++i) {
+                  for (int s = 0; s < p.ks; ++s) {
+                    const uint64_t a0 = h_tmpl + (uint64_t)(hA4 + t4 + (uint32_t)s * 2u * h_plane4);
+                    const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)i * b_cta4 + (uint32_t)s * b_ks4);
+                    const uint32_t first = (gsi == 0 && q0 + i == 0 && s == 0) ? 1u : 0u;
+                    if constexpr (kInt8) {
+  #pragma unroll
+                      for (int L = 0; L < kLevels; ++L) {
+                        const int i0 = L > kDigitsW - 1 ? L - (kDigitsW - 1) : 0;
+  #pragma unroll
+                        for (int ii = i0; ii <= L && ii < kDigitsA; ++ii) {
+                          const int j = L - ii;
+                          mma_mode<PREC, PAIR>(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(ii * h_img4),
+                                               b0 + (uint64_t)(j * b_img4), idesc, (first && ii == i0) ? 0u : 1u);
+                        }
+                      }
+                    } else if constexpr (kSplit) {
+                      mma_tf32(d_tmem, a0 + h_img4, b0, idesc, first ? 0u : 1u);  // A_lo * B_hi
+                      mma_tf32(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
+                      mma_tf32(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
+                    } else {
+                      mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+                    }
+                  }
+                  t4 += h_dx;
+                  if (++x == df) {
+                    x = 0;
+                    t4 += h_wrap_x;
+                    if (++y == df) { y = 0; t4 += h_wrap_y; }
+                  }
+                }
+                const bool last = q0 + nq == nQ;
+                if constexpr (PAIR) {
+                  mma_commit_cg2(&empty[stage]);
+                  if (last) mma_commit_cg2(&hempty[hsl]);  // halo reusable once the last tap retires
+                  if (last && gsi == p.n_gs - 1) mma_commit_cg2(&tfull[acc]);
+                } else {
+                  mma_commit(&empty[stage]);
+                  if (last) mma_commit(&hempty[hsl]);
+                  if (last && gsi == p.n_gs - 1) mma_commit(&tfull[acc]);
+                }
+              }
+              __syncwarp();
+              if (++stage == S) { stage = 0; phase ^= 1; }
+              for (int i = 0; i < nq; ++i) {  // advance the warp-uniform tap state
+                tap4 += h_dx;
+                if (++qx == df) {
+                  qx = 0;
+                  tap4 += h_wrap_x;
+                  if (++qy == df) { qy = 0; tap4 += h_wrap_y; }
+                }
+              }
             }
           }
           if (++hsl == HS) { hsl = 0; hphase ^= 1; }

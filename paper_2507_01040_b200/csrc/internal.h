@@ -106,6 +106,7 @@ struct ConvPlan {
   // once and reused by every filter tap through descriptor offsets
   int halo, hx, hy, hz, hs;
   uint32_t halo_bytes, halo_slot, ring_off;
+  int tps;  // halo mode: filter taps (B images) per pipeline stage
   // 2-SM MMA (cta_group::2): a CTA pair computes M = 256 rows; each CTA holds
   // its 128 A rows and half of the B columns (the filter images are laid out
   // as two contiguous column halves per stage)
@@ -124,6 +125,7 @@ struct ConvKParams {
   int cs;                     // cluster size: 2 for a 2-SM (cta_group::2) pair, else 1
   int pair;                   // 2-SM MMA: M = 256 over the pair, B columns split between the two CTAs
   int halo, hx, hy, hz, hs;   // halo mode (see ConvPlan)
+  int tps;                    // halo mode: filter taps per B stage
   int epx;                    // A tensor map with merged (pixel, row) inner dim: 8-byte elements per pixel, else 0
   uint32_t halo_bytes, halo_slot, ring_off;
   Basis bs;                   // change of basis: rows = (pixel, column), epilogue inverse transform

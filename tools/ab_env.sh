@@ -5,6 +5,6 @@ IFS='|' read -ra VARS <<< "${ENVS:--}"
 for v in "${VARS[@]}"; do
   for c in ${CFGS:-5}; do
     B=$([ $c = 5 ] && echo 64 || echo 0)
-    env $([ "$v" = "-" ] || echo $v) python tools/ab_conv.py --config $c --precision ${PREC:-fp32} --B $B | sed "s/^/[$v] /"
+    env $([ "$v" = "-" ] || echo $v) python tools/ab_conv.py --config $c --precision ${PREC:-fp32} --B $B | sed "s|^|[$v] |"
   done
 done

@@ -12,15 +12,6 @@
 #include "../../paper_2507_01040_b200/csrc/common.cuh"
 using namespace cl;
 
-__device__ __forceinline__ void mma_i8_cg2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                           uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
 template <int KIND>
 __global__ void __launch_bounds__(128, 1) rate(int n, int iters, unsigned long long* out, const uint8_t* gsrc,
                                                volatile int* stop) {
@@ -179,9 +170,9 @@ int main(int argc, char** argv) {
     return 0;
   }
   run<0>(128, iters);
-  run<3>(128, iters);
-  run<4>(128, iters * 4);
-  run<3>(256, iters / 2);
+  run<0>(64, iters);
   run<2>(128, iters);
+  run<2>(64, iters);
+  run<2>(32, iters);
   return 0;
 }
