@@ -74,6 +74,17 @@ def mode_peak(precision, peaks, sustained=True):
     return val, basis + (" sustained" if sustained else " burst")
 
 
+def ncu_traffic(spec, prec, batch):
+    """roofline.traffic: DRAM bytes of one conv launch from a committed ncu --set full capture
+    (profiles/ncu_traffic.json), when one exists for this config / precision / batch."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")) as f:
+            ent = json.load(f).get(f"cfg{spec.cfg}:{prec}:{batch}")
+        return int(ent["bytes"]) if ent else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 class ClockSampler:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -447,7 +458,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (%.1f GB per rank)" % (x.numel() * 4 / 1e9)},
             "tflops": flops_per_sample * spec.B / t_step / 1e12,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": ncu_traffic(spec, prec, conv_layer.dims.B),
                          "kernel": "conv_tc_kernel (conv2 of the block)",
                          "peak_basis": f"{prec}: {peak_basis}" + (
                              "; x2 algorithmic/executed (M2(C) change of basis, SURVEY 8f f4)" if basis_on.value else ""),
