@@ -1,0 +1,51 @@
+"""GPU parity of the kernel variants the planner can switch off (1-SM MMA,
+per-tap A loads, per-pixel TMA lines, one tap per B stage). The switches are
+read once when the library loads, so each variant runs in a fresh process;
+the default variant is covered by test_gpu_parity.py. Same tolerances."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SNIPPET = r"""
+import sys
+import numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import torch
+import oracle as O
+from test_gpu_parity import make_conv, run_dev, assert_conv_close
+import paper_2507_01040_b200 as M
+torch.cuda.set_device(0)
+rng = np.random.default_rng(11)
+cases = [((1, 1, 1), 2, 5, 6, 6, 3, "same"), ((1, -1, 0), 1, 3, 4, 5, 3, "valid"), ((1, 1), 3, 6, 5, 9, 3, "same"),
+         ((0, 0, 1), 2, 4, 3, 5, 2, "valid"), ((1,), 3, 4, 4, 40, 3, "valid")]
+for prec in ("fp32", "3xtf32", "tf32", "bf16"):
+    for g, B, ci, co, d, df, padding in cases:
+        x, f, b, layer, pad = make_conv(rng, g, B, ci, co, d, df, prec, padding)
+        y = run_dev(M.conv_forward, x, layer)
+        assert_conv_close(y, O.conv_ref(x, f, b, g, d, df, pad), prec)
+print("ok")
+"""
+
+
+def _run(env_extra):
+    env = dict(os.environ, **env_extra)
+    code = SNIPPET.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("flags", [{"CL_NO_PAIR": "1"}, {"CL_NO_HALO": "1"}, {"CL_NO_TMA_MERGE": "1"},
+                                   {"CL_TPS": "1"}, {"CL_BASIS_2D": "1"}, {"CL_NO_BASIS": "1"}],
+                         ids=lambda f: ",".join(f))
+def test_variant_parity(flags):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    _run(flags)
