@@ -225,7 +225,7 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
       for (int tps : {4, 2}) {
         if (g_force_tps && tps != g_force_tps) continue;
         const int st = (int)((kMaxSmem - 2048 - c.ring_off) / (c.stage_bytes * tps));
-        if (st >= 4) { c.tps = tps; c.stage_bytes *= tps; break; }
+        if (st >= (g_force_tps ? 2 : 4)) { c.tps = tps; c.stage_bytes *= tps; break; }
       }
     }
     c.stages = std::min(8, (int)((kMaxSmem - 2048 - c.ring_off) / c.stage_bytes));

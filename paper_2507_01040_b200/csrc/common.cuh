@@ -253,6 +253,41 @@ __device__ __forceinline__ void mma_i8_cg2(uint32_t d_tmem, uint64_t adesc, uint
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-converged issue: every lane runs the issue loop on warp-uniform values
+// (descriptors stay on the uniform datapath) and the instruction is guarded so
+// only the lane with `issue` set performs it.
+#define CL_MMA_GUARDED(NAME, KIND, GROUP)                                                                  \
+  __device__ __forceinline__ void NAME(uint32_t issue, uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,   \
+                                       uint32_t idesc, uint32_t accumulate) {                             \
+    asm volatile(                                                                                         \
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 q, %5, 0;\n\t"                 \
+        "@q tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),        \
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(issue)                                   \
+        : "memory");                                                                                      \
+  }
+CL_MMA_GUARDED(mma_tf32_g, "tf32", "1")
+CL_MMA_GUARDED(mma_bf16_g, "f16", "1")
+CL_MMA_GUARDED(mma_i8_g, "i8", "1")
+CL_MMA_GUARDED(mma_tf32_cg2_g, "tf32", "2")
+CL_MMA_GUARDED(mma_bf16_cg2_g, "f16", "2")
+CL_MMA_GUARDED(mma_i8_cg2_g, "i8", "2")
+#undef CL_MMA_GUARDED
+__device__ __forceinline__ void mma_commit_g(uint32_t issue, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_u32(bar)),
+      "r"(issue)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_cg2_g(uint32_t issue, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %2;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(issue), "h"((uint16_t)3)
+      : "memory");
+}
+
 // Commit the pair's MMAs to the barrier at the same offset in both CTAs.
 __device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
   asm volatile(
@@ -276,6 +311,16 @@ __device__ __forceinline__ void mma_commit_multicast(uint64_t* bar, uint16_t cta
           smem_u32(bar)),
       "h"(cta_mask)
       : "memory");
+}
+// tcgen05.wait::ld that also ties the loaded registers to the wait, so the
+// compiler cannot move their uses above it (for loads left in flight while
+// other work runs).
+__device__ __forceinline__ void tmem_ld_wait_dep16(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
 }
 // 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {

@@ -51,6 +51,22 @@ __device__ __forceinline__ void mma_mode(uint32_t d, uint64_t a, uint64_t b, uin
   }
 }
 
+template <int PREC, bool PAIR>
+__device__ __forceinline__ void mma_mode_g(uint32_t issue, uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t acc) {
+  if constexpr (PREC == kPrecFp32) {
+    if constexpr (PAIR) mma_i8_cg2_g(issue, d, a, b, idesc, acc); else mma_i8_g(issue, d, a, b, idesc, acc);
+  } else if constexpr (PREC == kPrecBf16) {
+    if constexpr (PAIR) mma_bf16_cg2_g(issue, d, a, b, idesc, acc); else mma_bf16_g(issue, d, a, b, idesc, acc);
+  } else {
+    if constexpr (PAIR) mma_tf32_cg2_g(issue, d, a, b, idesc, acc); else mma_tf32_g(issue, d, a, b, idesc, acc);
+  }
+}
+template <bool PAIR>
+__device__ __forceinline__ void commit_g(uint32_t issue, uint64_t* bar) {
+  if constexpr (PAIR) mma_commit_cg2_g(issue, bar); else mma_commit_g(issue, bar);
+}
+
 // A-operand TMA box at (x, c1, c2, c3). With a merged (pixel x row-bytes)
 // inner dimension of 8-byte elements (p.epx per pixel; one TMA line per tile
 // row instead of one per pixel) the coordinates shift left by one.
@@ -66,7 +82,13 @@ __device__ __forceinline__ void load_a_box(const ConvKParams& p, void* dst, cons
   }
 }
 
-// register-array pick with a runtime index (selects, no local memory)
+// register-array picks with a runtime index (selects, no local memory)
+template <int W>
+__device__ __forceinline__ float pick_wf(const float (&a)[W], int i) {
+  if constexpr (W == 1) return a[0];
+  else if constexpr (W == 2) return i ? a[1] : a[0];
+  else return (i & 2) ? ((i & 1) ? a[3] : a[2]) : ((i & 1) ? a[1] : a[0]);
+}
 template <int W>
 __device__ __forceinline__ long long pick_w(const long long (&a)[W], int i) {
   if constexpr (W == 1) return a[0];
@@ -243,6 +265,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // values warp-uniform); one elected lane issues tcgen05.mma + commit.
     // Descriptors are template + (address >> 4): start address is the low
     // 14-bit field, and CTA-local shared addresses < 2^18 never carry out of it.
+    const uint32_t issuer = elect_one();  // the lane whose guarded tcgen05 instructions issue
     constexpr uint32_t kM = PAIR ? 256u : 128u;
     const uint32_t idesc = kInt8 ? instr_desc_i8(kM, (uint32_t)p.n_tile)
                                  : instr_desc(PREC == kPrecBf16 ? 1u : 2u, kM, (uint32_t)p.n_tile);
@@ -268,6 +291,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const uint32_t h_plane = (uint32_t)(p.hx * p.hy * p.hz * ncol * 16);
     const uint64_t h_tmpl = smem_desc(0, h_plane, (uint32_t)(p.hx * ncol * 16), kSwizzleNone);
     const uint32_t h_img4 = p.a_bytes >> 4, h_plane4 = h_plane >> 4;  // digit / lo plane stride
+    const uint64_t a_kstep = 2u * h_plane4;                                // next K step: 2 groups
     const uint32_t h_dx = (uint32_t)ncol;                                  // next tap along x
     const uint32_t h_wrap_x = (uint32_t)((p.hx - df) * ncol);              // x wrapped: next halo row
     const uint32_t h_wrap_y = (uint32_t)((p.hy - df) * p.hx * ncol);       // y wrapped: next halo plane
@@ -340,50 +364,50 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               mbar_wait(&full[stage], phase);
               tc_fence_after();
               const uint32_t sB4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
-              if (elect_one()) {
-                uint32_t t4 = tap4;
+              {
+                // converged issue (every lane computes the warp-uniform descriptors,
+                // one lane's guard is set): the descriptors stay in uniform registers
+                uint64_t a_tap = h_tmpl + (uint64_t)(hA4 + tap4);
+                uint64_t b_cur = b_tmpl + (uint64_t)sB4;
+                uint32_t accf = (gsi == 0 && q0 == 0) ? 0u : 1u;
                 int x = qx, y = qy;
                 for (int i = 0; i < nq; ++i) {
+                  uint64_t a0 = a_tap, b0 = b_cur;
                   for (int s = 0; s < p.ks; ++s) {
-                    const uint64_t a0 = h_tmpl + (uint64_t)(hA4 + t4 + (uint32_t)s * 2u * h_plane4);
-                    const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)i * b_cta4 + (uint32_t)s * b_ks4);
-                    const uint32_t first = (gsi == 0 && q0 + i == 0 && s == 0) ? 1u : 0u;
                     if constexpr (kInt8) {
-  #pragma unroll
+#pragma unroll
                       for (int L = 0; L < kLevels; ++L) {
                         const int i0 = L > kDigitsW - 1 ? L - (kDigitsW - 1) : 0;
-  #pragma unroll
+#pragma unroll
                         for (int ii = i0; ii <= L && ii < kDigitsA; ++ii) {
                           const int j = L - ii;
-                          mma_mode<PREC, PAIR>(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(ii * h_img4),
-                                               b0 + (uint64_t)(j * b_img4), idesc, (first && ii == i0) ? 0u : 1u);
+                          mma_mode_g<PREC, PAIR>(issuer, d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(ii * h_img4),
+                                                 b0 + (uint64_t)(j * b_img4), idesc, ii == i0 ? accf : 1u);
                         }
                       }
                     } else if constexpr (kSplit) {
-                      mma_tf32(d_tmem, a0 + h_img4, b0, idesc, first ? 0u : 1u);  // A_lo * B_hi
-                      mma_tf32(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
-                      mma_tf32(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
+                      mma_tf32_g(issuer, d_tmem, a0 + h_img4, b0, idesc, accf);  // A_lo * B_hi
+                      mma_tf32_g(issuer, d_tmem, a0, b0 + b_img4, idesc, 1u);   // A_hi * B_lo
+                      mma_tf32_g(issuer, d_tmem, a0, b0, idesc, 1u);            // A_hi * B_hi
                     } else {
-                      mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+                      mma_mode_g<PREC, PAIR>(issuer, d_tmem, a0, b0, idesc, accf);
                     }
+                    accf = 1u;
+                    a0 += a_kstep;
+                    b0 += b_ks4;
                   }
-                  t4 += h_dx;
+                  b_cur += b_cta4;
+                  a_tap += h_dx;
                   if (++x == df) {
                     x = 0;
-                    t4 += h_wrap_x;
-                    if (++y == df) { y = 0; t4 += h_wrap_y; }
+                    a_tap += h_wrap_x;
+                    if (++y == df) { y = 0; a_tap += h_wrap_y; }
                   }
                 }
                 const bool last = q0 + nq == nQ;
-                if constexpr (PAIR) {
-                  mma_commit_cg2(&empty[stage]);
-                  if (last) mma_commit_cg2(&hempty[hsl]);  // halo reusable once the last tap retires
-                  if (last && gsi == p.n_gs - 1) mma_commit_cg2(&tfull[acc]);
-                } else {
-                  mma_commit(&empty[stage]);
-                  if (last) mma_commit(&hempty[hsl]);
-                  if (last && gsi == p.n_gs - 1) mma_commit(&tfull[acc]);
-                }
+                commit_g<PAIR>(issuer, &empty[stage]);
+                if (last) commit_g<PAIR>(issuer, &hempty[hsl]);  // halo reusable once the last tap retires
+                if (last && gsi == p.n_gs - 1) commit_g<PAIR>(issuer, &tfull[acc]);
               }
               __syncwarp();
               if (++stage == S) { stage = 0; phase ^= 1; }
@@ -674,160 +698,150 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
         continue;
       }
-      for (int c0 = c_beg; c0 < ((p.dbg_skip & 4) ? c_beg : c_end); c0 += 16) {
+      // fp32-accumulator modes (tf32 / 3xTF32 / bf16): fp32 math, the next
+      // chunk's TMEM load in flight while this one is processed
+      const int c_stop = (p.dbg_skip & 4) ? c_beg : c_end;
+      uint32_t cur[16], nxt[16];
+      bool have = c_beg < c_stop && nt * p.n_tile + c_beg < p.N;
+      if (have) {
+        tmem_ld16(taddr + (uint32_t)c_beg, cur);
+        tmem_ld_wait_dep16(cur);
+      }
+      for (int c0 = c_beg; have; c0 += 16) {
         const int n0 = nt * p.n_tile + c0;
-        if (n0 >= p.N) break;
-        double dv[16];  // accumulator values of this chunk (bias not yet added)
-        if constexpr (kInt8) {
-          uint32_t l0[16], l1[16], l2[16], l3[16];
-          tmem_ld16(taddr + (uint32_t)c0, l0);
-          tmem_ld16(taddr + (uint32_t)(p.n_tile + c0), l1);
-          tmem_ld16(taddr + (uint32_t)(2 * p.n_tile + c0), l2);
-          tmem_ld16(taddr + (uint32_t)(3 * p.n_tile + c0), l3);
-          tmem_ld_wait();
+        const bool more = c0 + 16 < c_stop && n0 + 16 < p.N;
+        if (more) tmem_ld16(taddr + (uint32_t)(c0 + 16), nxt);
+        // the chunk's residual values, loaded up front so their latencies overlap
+        float4 rq[4];
+        const bool use_res = p.resid != nullptr && valid;
+        if (use_res) {
+          const int wv = p.bs.on ? NB / 2 : NB;  // floats of one channel this lane adds
+          const int nch = 16 / wv;
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            // exact integer levels combined in fp64: L0 + L1 2^-8 + L2 2^-16 + L3 2^-24
-            const double s = (double)(int)l0[c] + (double)(int)l1[c] * (1.0 / 256.0) +
-                             (double)(int)l2[c] * (1.0 / 65536.0) + (double)(int)l3[c] * (1.0 / 16777216.0);
-            const int n = min(n0 + c, p.N - 1);
-            dv[c] = s * a_sc * (double)__ldg(p.w_scale + n);
+          for (int cc = 0; cc < 4; ++cc) {
+            rq[cc] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!p.bs.on && NB != 4) break;  // NB = 8: 2 float4 per channel, NB = 2: 8 channels; loaded in place below
+            const int co = n0 / wv + cc;
+            if (cc < nch && co < p.C_out) {
+              const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB + (p.bs.on ? bcol * wv : 0);
+              if (wv == 2) {
+                const float2 q2 = __ldg(reinterpret_cast<const float2*>(rp));
+                rq[cc] = make_float4(q2.x, q2.y, 0.f, 0.f);
+              } else {
+                rq[cc] = __ldg(reinterpret_cast<const float4*>(rp));
+              }
+            }
           }
-        } else {
-          uint32_t rr[16];
-          tmem_ld16(taddr + (uint32_t)c0, rr);
-          tmem_ld_wait();
-#pragma unroll
-          for (int c = 0; c < 16; ++c) dv[c] = (double)__uint_as_float(rr[c]);
         }
         if (p.bs.on) {
           if constexpr (NB >= 4) {
-            // change of basis: lanes (2i, 2i+1) hold columns 0 / 1 of pixel i; exchange,
-            // invert x[t] = (+-x'[a_t] +- x'[b_t]) / 2 (fp64 for the exact mode), then bias /
-            // activation / residual in the protocol basis; the lane of column c stores
-            // blades [c NB/2, (c+1) NB/2)
+            // change of basis: lane (column bcol) produces blades bcol*W + j as
+            // (s_o own[o_j] + s_p partner[p_j]) / 2; the gate sums over both lanes
             constexpr int W = NB / 2;
 #pragma unroll
             for (int cc = 0; cc < 16 / W; ++cc) {
               const int co = n0 / W + cc;
-              float v[NB];
-              if constexpr (kInt8) {
-                double xs[NB];
+              const int cq = min(co, p.C_out - 1);
+              float own[W], oth[W];
 #pragma unroll
-                for (int r = 0; r < W; ++r) {
-                  const double mine = dv[cc * W + r];
-                  const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
-                  xs[bcol * W + r] = mine;
-                  xs[(1 - bcol) * W + r] = other;
-                }
+              for (int r = 0; r < W; ++r) {
+                own[r] = __uint_as_float(cur[cc * W + r]);
+                oth[r] = __shfl_xor_sync(0xffffffffu, own[r], 1);
+              }
+              float h[W];
+              float part = 0.f;
 #pragma unroll
-                for (int t2 = 0; t2 < NB; ++t2) {
-                  const double y = 0.5 * ((double)inv_s0[t2] * xs[inv_i0[t2]] + (double)inv_s1[t2] * xs[inv_i1[t2]]);
-                  v[t2] = (float)(y + (double)__ldg(p.bias + t2 * p.C_out + min(co, p.C_out - 1)));
-                }
-              } else {
-                float xs[NB];
+              for (int j = 0; j < W; ++j) {
+                const float a = pick_wf<W>(own, inv_o[j]), bq = pick_wf<W>(oth, inv_p[j]);
+                const int t = bcol * W + j;
+                h[j] = 0.5f * ((inv_os[j] > 0 ? a : -a) + (inv_ps[j] > 0 ? bq : -bq)) + __ldg(p.bias + t * p.C_out + cq);
+                if (p.act_mode >= 0) part = fmaf(h[j], __ldg(p.act_w + cq * NB + t), part);
+              }
+              if (p.act_mode >= 0) {
+                float sg = part + __shfl_xor_sync(0xffffffffu, part, 1);
+                if (p.act_mode == 0) sg += __ldg(p.act_b + cq);
+                else if (p.act_mode == 2) sg = sg / p.act_K;
+                const float gte = 1.f / (1.f + expf(-sg));
 #pragma unroll
-                for (int r = 0; r < W; ++r) {
-                  const float mine = (float)dv[cc * W + r];
-                  const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
-                  xs[bcol * W + r] = mine;
-                  xs[(1 - bcol) * W + r] = other;
-                }
-#pragma unroll
-                for (int t2 = 0; t2 < NB; ++t2)
-                  v[t2] = 0.5f * ((float)inv_s0[t2] * xs[inv_i0[t2]] + (float)inv_s1[t2] * xs[inv_i1[t2]]) +
-                          __ldg(p.bias + t2 * p.C_out + min(co, p.C_out - 1));
+                for (int j = 0; j < W; ++j) h[j] *= gte;
               }
               if (valid && co < p.C_out) {
-                if (p.act_mode >= 0) {
-                  const float gte = act_gate<NB>(v, p.act_mode, p.act_w + co * NB,
-                                                 p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K);
-#pragma unroll
-                  for (int j = 0; j < NB; ++j) v[j] *= gte;
-                }
-                float h[W];
-#pragma unroll
-                for (int j = 0; j < W; ++j) h[j] = bcol ? v[W + j] : v[j];
-                if (p.resid) {
-                  const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB + bcol * W;
-                  if constexpr (W == 2) {
-                    const float2 q2 = __ldg(reinterpret_cast<const float2*>(rp));
-                    h[0] += q2.x; h[1] += q2.y;
-                  } else {
-                    const float4 q4 = __ldg(reinterpret_cast<const float4*>(rp));
-                    h[0] += q4.x; h[1] += q4.y; h[2 % W] += q4.z; h[3 % W] += q4.w;
-                  }
+                if (use_res) {
+                  const float4 q4 = rq[cc % 4];
+                  h[0] += q4.x; h[1 % W] += q4.y;
+                  if constexpr (W == 4) { h[2 % W] += q4.z; h[3 % W] += q4.w; }
                 }
                 if (p.y) {
                   float* yp = p.y + (((long long)b * p.C_out + co) * P_out + pix) * NB + bcol * W;
-                  if constexpr (W == 2) *reinterpret_cast<float2*>(yp) = make_float2(h[0], h[1]);
-                  else *reinterpret_cast<float4*>(yp) = make_float4(h[0], h[1], h[2 % W], h[3 % W]);
+                  if constexpr (W == 2) *reinterpret_cast<float2*>(yp) = make_float2(h[0], h[1 % W]);
+                  else *reinterpret_cast<float4*>(yp) = make_float4(h[0], h[1 % W], h[2 % W], h[3 % W]);
                 }
               }
             }
           }
-          continue;
-        }
-        float vv[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int n = min(n0 + c, p.N - 1);
-          vv[c] = (float)(dv[c] + (double)__ldg(p.bias + (n % NB) * p.C_out + n / NB));
-        }
-        if (valid) {
+        } else {
 #pragma unroll
           for (int cc = 0; cc < 16 / NB; ++cc) {
             const int co = n0 / NB + cc;
-            if (co < p.C_out) {
-              float v[NB];
+            const int cq = min(co, p.C_out - 1);
+            float v[NB];
 #pragma unroll
-              for (int j = 0; j < NB; ++j) v[j] = vv[cc * NB + j];
-              if (p.act_mode >= 0) {
-                const float gte = act_gate<NB>(v, p.act_mode, p.act_w + co * NB,
-                                               p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K);
+            for (int j = 0; j < NB; ++j) v[j] = __uint_as_float(cur[cc * NB + j]) + __ldg(p.bias + j * p.C_out + cq);
+            if (!valid || co >= p.C_out) continue;
+            if (p.act_mode >= 0) {
+              const float gte = act_gate<NB>(v, p.act_mode, p.act_w + co * NB,
+                                             p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K);
 #pragma unroll
-                for (int j = 0; j < NB; ++j) v[j] *= gte;
-              }
-              if (p.resid) {
+              for (int j = 0; j < NB; ++j) v[j] *= gte;
+            }
+            if (use_res) {
+              if constexpr (NB == 4) {
+                const float4 q4 = rq[cc % 4];
+                v[0] += q4.x; v[1 % NB] += q4.y; v[2 % NB] += q4.z; v[3 % NB] += q4.w;
+              } else if constexpr (NB == 2) {
+                const float2 q2 = __ldg(reinterpret_cast<const float2*>(
+                    p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB));
+                v[0] += q2.x; v[1 % NB] += q2.y;
+              } else {
                 const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB;
-                if constexpr (NB == 2) {
-                  const float2 q2 = __ldg(reinterpret_cast<const float2*>(rp));
-                  v[0] += q2.x; v[1] += q2.y;
-                } else {
 #pragma unroll
-                  for (int j = 0; j < NB / 4; ++j) {
-                    const float4 q4 = __ldg(reinterpret_cast<const float4*>(rp) + j);
-                    v[4 * j] += q4.x; v[4 * j + 1] += q4.y; v[4 * j + 2] += q4.z; v[4 * j + 3] += q4.w;
-                  }
+                for (int j = 0; j < NB / 4; ++j) {
+                  const float4 q4 = __ldg(reinterpret_cast<const float4*>(rp) + j);
+                  v[4 * j] += q4.x; v[(4 * j + 1) % NB] += q4.y; v[(4 * j + 2) % NB] += q4.z; v[(4 * j + 3) % NB] += q4.w;
                 }
-              }
-              if (p.y) {
-                float* yp = p.y + (((long long)b * p.C_out + co) * P_out + pix) * NB;
-                if constexpr (NB == 2) {
-                  *reinterpret_cast<float2*>(yp) = make_float2(v[0], v[1]);
-                } else {
-#pragma unroll
-                  for (int j = 0; j < NB / 4; ++j)
-                    reinterpret_cast<float4*>(yp)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                }
-              }
-              if (p.y_bf16) {
-                // next conv's packed bf16 operand: (B, Gy, P, 16 B), cpg = 8 / NB channels per group
-                constexpr int cpg = 8 / NB;
-                __nv_bfloat16* yp = p.y_bf16 + (((long long)b * p.ybf_groups + co / cpg) * P_out + pix) * 8 + (co % cpg) * NB;
-                uint32_t u[NB / 2];
-#pragma unroll
-                for (int j = 0; j < NB / 2; ++j) {
-                  __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-                  u[j] = *reinterpret_cast<uint32_t*>(&h);
-                }
-                if constexpr (NB == 2) *reinterpret_cast<uint32_t*>(yp) = u[0];
-                else if constexpr (NB == 4) *reinterpret_cast<uint2*>(yp) = make_uint2(u[0], u[1]);
-                else *reinterpret_cast<uint4*>(yp) = make_uint4(u[0], u[1 % (NB / 2)], u[2 % (NB / 2)], u[3 % (NB / 2)]);
               }
             }
+            if (p.y) {
+              float* yp = p.y + (((long long)b * p.C_out + co) * P_out + pix) * NB;
+              if constexpr (NB == 2) {
+                *reinterpret_cast<float2*>(yp) = make_float2(v[0], v[1]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < NB / 4; ++j)
+                  reinterpret_cast<float4*>(yp)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              }
+            }
+            if (p.y_bf16) {
+              // next conv's packed bf16 operand: (B, Gy, P, 16 B), cpg = 8 / NB channels per group
+              constexpr int cpg = 8 / NB;
+              __nv_bfloat16* yp = p.y_bf16 + (((long long)b * p.ybf_groups + co / cpg) * P_out + pix) * 8 + (co % cpg) * NB;
+              uint32_t u[NB / 2];
+#pragma unroll
+              for (int j = 0; j < NB / 2; ++j) {
+                __nv_bfloat162 hh = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+                u[j] = *reinterpret_cast<uint32_t*>(&hh);
+              }
+              if constexpr (NB == 2) *reinterpret_cast<uint32_t*>(yp) = u[0];
+              else if constexpr (NB == 4) *reinterpret_cast<uint2*>(yp) = make_uint2(u[0], u[1]);
+              else *reinterpret_cast<uint4*>(yp) = make_uint4(u[0], u[1 % (NB / 2)], u[2 % (NB / 2)], u[3 % (NB / 2)]);
+            }
           }
+        }
+        have = more;
+        if (more) {
+          tmem_ld_wait_dep16(nxt);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) cur[c] = nxt[c];
         }
       }
       tc_fence_before();

@@ -14,14 +14,14 @@ using namespace cl;
 
 template <int KIND>
 __global__ void __launch_bounds__(128, 1) rate(int n, int iters, unsigned long long* out, const uint8_t* gsrc,
-                                               volatile int* stop) {
+                                               volatile int* stop, int a_sbo) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
   __shared__ uint64_t cbar[4];
   __shared__ int done_flag;
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
-  const bool cg2 = KIND == 2;
+  const bool cg2 = KIND == 2 || KIND == 5;
   const uint32_t rank = cg2 ? cluster_ctarank() : 0;
   for (int i = threadIdx.x; i < 131072 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = i * 2654435761u;
   if (threadIdx.x == 0) {
@@ -66,14 +66,24 @@ __global__ void __launch_bounds__(128, 1) rate(int n, int iters, unsigned long l
   }
   if (KIND != 4 && threadIdx.x == 0 && rank == 0) {
     const uint32_t a4 = (smem_u32(sm) & 0x3FFFFu) >> 4, b4 = (smem_u32(sm + 32768) & 0x3FFFFu) >> 4;
-    const uint64_t at = smem_desc(0, 2048, 128, kSwizzleNone), bt = smem_desc(0, (uint32_t)n * 16u, 128, kSwizzleNone);
-    const uint32_t m = cg2 ? 256u : 128u;
-    const uint32_t idesc = (KIND == 1) ? instr_desc(1u, m, (uint32_t)n) : instr_desc_i8(m, (uint32_t)n);
+    const uint64_t at = smem_desc(0, 4096, (uint32_t)a_sbo, kSwizzleNone), bt = smem_desc(0, (uint32_t)n * 16u, 128, kSwizzleNone);
+    const uint32_t m = (cg2 || KIND == 5) ? 256u : 128u;
+    const uint32_t idesc = (KIND == 1 || KIND == 5) ? instr_desc(1u, m, (uint32_t)n) : instr_desc_i8(m, (uint32_t)n);
     const int nacc = (KIND == 1) ? 512 / n : (4 * n <= 512 ? 4 : 512 / n);
     unsigned long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
-      if (KIND == 1) {
-        mma_bf16(tmem + (uint32_t)((it % nacc) * n), at + a4, bt + b4, idesc, 1u);
+      if (KIND == 1 || KIND == 5) {  // 8 bf16 MMAs per iteration, 2 accumulators
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint64_t a = at + a4 + (uint32_t)((q & 1) * 2), b = bt + b4 + (uint32_t)((q & 1) * 2);
+          if (KIND == 5) {
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (uint32_t)((q & 1) * n)),
+                         "l"(a), "l"(b), "r"(idesc), "r"(1u) : "memory");
+          } else {
+            mma_bf16(tmem + (uint32_t)((q & 1) * n), a, b, idesc, 1u);
+          }
+        }
       } else {
         // 10 MMAs / K step into nacc accumulators (level L = i + j)
 #pragma unroll
@@ -112,7 +122,7 @@ __global__ void __launch_bounds__(128, 1) rate(int n, int iters, unsigned long l
 }
 
 template <int KIND>
-void run(int n, int iters) {
+void run(int n, int iters, int a_sbo = 128) {
   unsigned long long* d;
   const int grid = 148;
   cudaMalloc(&d, 2 * grid * sizeof(unsigned long long));
@@ -129,7 +139,7 @@ void run(int n, int iters) {
   cfg.dynamicSmemBytes = 131072 + 2048;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = KIND == 2 ? 2 : 1;
+  at[0].val.clusterDim.x = (KIND == 2 || KIND == 5) ? 2 : 1;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
@@ -137,9 +147,9 @@ void run(int n, int iters) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  cudaLaunchKernelEx(&cfg, rate<KIND>, n, iters, d, (const uint8_t*)g, stop);  // warm
+  cudaLaunchKernelEx(&cfg, rate<KIND>, n, iters, d, (const uint8_t*)g, stop, a_sbo);  // warm
   cudaEventRecord(e0);
-  cudaLaunchKernelEx(&cfg, rate<KIND>, n, iters, d, (const uint8_t*)g, stop);
+  cudaLaunchKernelEx(&cfg, rate<KIND>, n, iters, d, (const uint8_t*)g, stop, a_sbo);
   cudaEventRecord(e1);
   cudaError_t e = cudaDeviceSynchronize();
   float ms;
@@ -150,12 +160,12 @@ void run(int n, int iters) {
   for (int i = 0; i < grid; ++i) wr += h[148 + i] / 1000.0 / grid;
   unsigned long long mx = 0;
   for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
-  const double nmma = (double)iters * (KIND == 1 ? 1 : 10);
-  const double m = KIND == 2 ? 256 : 128;
-  const double kel = KIND == 1 ? 16 : 32;
-  const int issuers = KIND == 2 ? grid / 2 : grid;
+  const double nmma = (double)iters * ((KIND == 1 || KIND == 5) ? 8 : 10);
+  const double m = (KIND == 2 || KIND == 5) ? 256 : 128;
+  const double kel = (KIND == 1 || KIND == 5) ? 16 : 32;
+  const int issuers = (KIND == 2 || KIND == 5) ? grid / 2 : grid;
   const double ops = 2.0 * m * n * kel * nmma * issuers;
-  printf("kind %d n %3d: %s  %.1f cyc/MMA (leader)  %.0f TOPS over %.3f ms  writer %.1f B/clk\n", KIND, n,
+  printf("sbo %d kind %d n %3d: %s  %.1f cyc/MMA (leader)  %.0f TOPS over %.3f ms  writer %.1f B/clk\n", a_sbo, KIND, n,
          cudaGetErrorString(e), (double)mx / nmma, ops / (ms * 1e-3) / 1e12, ms, wr);
   cudaFree(d);
   cudaFree(g);
@@ -169,10 +179,12 @@ int main(int argc, char** argv) {
     run<0>(128, iters);
     return 0;
   }
-  run<0>(128, iters);
-  run<0>(64, iters);
-  run<2>(128, iters);
-  run<2>(64, iters);
-  run<2>(32, iters);
+  run<5>(256, iters, 128);
+  run<5>(256, iters, 192);
+  run<1>(256, iters, 128);
+  run<0>(128, iters, 128);
+  run<0>(128, iters, 192);
+  run<2>(128, iters, 128);
+  run<2>(128, iters, 192);
   return 0;
 }
