@@ -960,75 +960,107 @@ cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const CUt
 // as bf16 (esize 2) or fp32 (esize 4); cpg = 16 / (w * esize). Without a change
 // of basis w = NB (the blades); with one, each pixel yields ncol rows of the
 // transformed components x'[c*w + r] = sum_I T[c*w + r][I] x[I].
-__global__ void pack_rows_kernel(const float* __restrict__ x, uint4* __restrict__ out, int nb, int esize,
-                                 long long B, int C, long long P, int G, Basis bs) {
+template <int NB, int ESIZE, bool BASIS>
+__global__ void __launch_bounds__(256) pack_rows_kernel(const float* __restrict__ x, uint4* __restrict__ out,
+                                                        long long B, int C, long long P, int G, Basis bs) {
+  constexpr int NCOL = BASIS ? 2 : 1;
+  constexpr int W = BASIS ? NB / 2 : NB;   // components per channel and row
+  constexpr int NV = 16 / ESIZE;           // values per 16-byte row
+  constexpr int CPG = NV / W;              // channels per row group
+  float T[BASIS ? NB * NB : 1];            // x'[c*W + r] = sum_I T[c*W + r][I] x[I] (entries 0, +-1)
+  if constexpr (BASIS) {
+#pragma unroll
+    for (int a = 0; a < NB; ++a)
+#pragma unroll
+      for (int I = 0; I < NB; ++I) T[a * NB + I] = (float)bs.T[a * 8 + I];
+  }
   const long long total = B * G * P;
-  const int ncol = bs.on ? bs.ncol : 1;
-  const int w = bs.on ? bs.w : nb;
-  const int nvals = 16 / esize, cpg = nvals / w;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long pp = i % P;
     const long long bg = i / P;
     const int g = (int)(bg % G);
     const long long b = bg / G;
-    for (int col = 0; col < ncol; ++col) {
-      float v[8];
+    float v[NCOL][NV];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = 0.f;
-      for (int cl = 0; cl < cpg; ++cl) {
-        const int c = g * cpg + cl;
-        if (c >= C) break;
-        const float* src = x + ((b * C + c) * P + pp) * nb;
-        float m[8];
-        if (nb == 2) {
+    for (int cl = 0; cl < CPG; ++cl) {
+      const int c = g * CPG + cl;
+      float m[NB];
+      if (c < C) {
+        const float* src = x + ((b * C + c) * P + pp) * NB;
+        if constexpr (NB == 2) {
           const float2 q = __ldg(reinterpret_cast<const float2*>(src));
           m[0] = q.x; m[1] = q.y;
         } else {
-          const float4 q0 = __ldg(reinterpret_cast<const float4*>(src));
-          m[0] = q0.x; m[1] = q0.y; m[2] = q0.z; m[3] = q0.w;
-          if (nb == 8) {
-            const float4 q1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
-            m[4] = q1.x; m[5] = q1.y; m[6] = q1.z; m[7] = q1.w;
+#pragma unroll
+          for (int h = 0; h < NB / 4; ++h) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(src) + h);
+            m[4 * h] = q.x; m[4 * h + 1] = q.y; m[4 * h + 2] = q.z; m[4 * h + 3] = q.w;
           }
         }
-        for (int r = 0; r < w; ++r) {
+      } else {
+#pragma unroll
+        for (int I = 0; I < NB; ++I) m[I] = 0.f;
+      }
+#pragma unroll
+      for (int col = 0; col < NCOL; ++col)
+#pragma unroll
+        for (int r = 0; r < W; ++r) {
           float xv;
-          if (bs.on) {
+          if constexpr (BASIS) {
             xv = 0.f;
-            for (int I = 0; I < nb; ++I) {
-              const int t = bs.T[(col * w + r) * 8 + I];
-              if (t) xv += t > 0 ? m[I] : -m[I];
-            }
+#pragma unroll
+            for (int I = 0; I < NB; ++I) xv = fmaf(T[(col * W + r) * NB + I], m[I], xv);  // exact: +-1 / 0 terms
           } else {
             xv = m[r];
           }
-          v[cl * w + r] = xv;
+          v[col][cl * W + r] = xv;
         }
-      }
+    }
+#pragma unroll
+    for (int col = 0; col < NCOL; ++col) {
       uint4 u;
-      if (esize == 4) {
-        u = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
+      if constexpr (ESIZE == 4) {
+        u = make_uint4(__float_as_uint(v[col][0]), __float_as_uint(v[col][1]), __float_as_uint(v[col][2]),
+                       __float_as_uint(v[col][3]));
       } else {
         __nv_bfloat162 h;
-        h = __floats2bfloat162_rn(v[0], v[1]); u.x = *reinterpret_cast<uint32_t*>(&h);
-        h = __floats2bfloat162_rn(v[2], v[3]); u.y = *reinterpret_cast<uint32_t*>(&h);
-        h = __floats2bfloat162_rn(v[4], v[5]); u.z = *reinterpret_cast<uint32_t*>(&h);
-        h = __floats2bfloat162_rn(v[6], v[7]); u.w = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(v[col][0], v[col][1]); u.x = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(v[col][2], v[col][3]); u.y = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(v[col][4 % NV], v[col][5 % NV]); u.z = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(v[col][6 % NV], v[col][7 % NV]); u.w = *reinterpret_cast<uint32_t*>(&h);
       }
-      out[i * ncol + col] = u;
+      out[i * NCOL + col] = u;
     }
   }
 }
 
-cudaError_t launch_pack_rows(const float* x, void* out, int nb, int esize, long long B, int C, long long P,
-                             int G, const Basis& bs, cudaStream_t s) {
+template <int NB, int ESIZE, bool BASIS>
+static void launch_pack_t(const float* x, void* out, long long B, int C, long long P, int G, const Basis& bs,
+                          cudaStream_t s) {
+  auto kern = pack_rows_kernel<NB, ESIZE, BASIS>;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
   const long long total = B * G * P;
-  if (total == 0) return cudaSuccess;
   long long blocks = (total + 255) / 256;
-  const long long cap = (long long)num_sms() * 8;
+  const long long cap = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
   if (blocks > cap) blocks = cap;
-  pack_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, reinterpret_cast<uint4*>(out), nb, esize, B, C, P, G, bs);
+  kern<<<(unsigned)blocks, 256, 0, s>>>(x, reinterpret_cast<uint4*>(out), B, C, P, G, bs);
+}
+
+cudaError_t launch_pack_rows(const float* x, void* out, int nb, int esize, long long B, int C, long long P, int G,
+                             const Basis& bs, cudaStream_t s) {
+  if (B * G * P == 0) return cudaSuccess;
+  if (bs.on) {
+    if (nb == 4) { if (esize == 2) launch_pack_t<4, 2, true>(x, out, B, C, P, G, bs, s); else launch_pack_t<4, 4, true>(x, out, B, C, P, G, bs, s); }
+    else { if (esize == 2) launch_pack_t<8, 2, true>(x, out, B, C, P, G, bs, s); else launch_pack_t<8, 4, true>(x, out, B, C, P, G, bs, s); }
+  } else if (nb == 2) {
+    if (esize == 2) launch_pack_t<2, 2, false>(x, out, B, C, P, G, bs, s); else launch_pack_t<2, 4, false>(x, out, B, C, P, G, bs, s);
+  } else if (nb == 4) {
+    if (esize == 2) launch_pack_t<4, 2, false>(x, out, B, C, P, G, bs, s); else launch_pack_t<4, 4, false>(x, out, B, C, P, G, bs, s);
+  } else {
+    if (esize == 2) launch_pack_t<8, 2, false>(x, out, B, C, P, G, bs, s); else launch_pack_t<8, 4, false>(x, out, B, C, P, G, bs, s);
+  }
   count_launch();
   return cudaGetLastError();
 }
