@@ -45,12 +45,15 @@ def run_dev(fn, x, *a):
     return fn(torch.from_numpy(x).cuda(), *a).cpu().numpy()
 
 
-def assert_conv_close(y, ref, prec):
+def assert_conv_close(y, ref, prec, K=0):
+    """K = reduction length C_in * N_B * d_f^k: the 3xTF32 bound is 1e-5 up to
+    K = 2304 and 5e-5 beyond (its truncating fp32 accumulation grows with K,
+    DESIGN.md "Why the fp32 mode is int8 digits")."""
     if prec == "fp32":
         assert O.max_rel_error(y, ref) <= 1e-4, O.max_rel_error(y, ref)
     elif prec == "3xtf32":
         e = O.max_rel_error(y, ref, floor=float(np.abs(ref).max()) + 1e-30)
-        assert e <= 1e-5, e
+        assert e <= (1e-5 if K <= 2304 else 5e-5), (e, K)
     else:
         e = O.max_rel_error(y, ref, floor=float(np.abs(ref).max()) + 1e-30)
         assert e <= 2e-2, e
@@ -107,7 +110,7 @@ def test_conv_signatures(prec, g, padding):
     assert_conv_close(y, O.conv_ref(x, f, b, g, d, 3, pad), prec)
 
 
-@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+@pytest.mark.parametrize("prec", ["fp32", "3xtf32", "tf32", "bf16"])
 @pytest.mark.parametrize("shape", [
     ((1, 1), 1, 1, 1, 4, 1),      # 1x1 conv, single channel
     ((1, 1), 3, 7, 3, 5, 5),      # d_out = 1
@@ -119,13 +122,17 @@ def test_conv_signatures(prec, g, padding):
     ((1, -1), 3, 33, 17, 11, 3),  # N not a multiple of 32
     ((1,), 37, 3, 5, 9, 3),       # 1-D: tile rows span samples; odd channels
     ((-1,), 3, 16, 16, 300, 5),   # 1-D: several position tiles
+    ((1, 1), 3, 20, 12, 23, 7),   # 2-D wide filter: halo 14 x 22
+    ((1, 1, 1), 3, 9, 40, 10, 5), # 3-D d_f = 5 under the change of basis: halo 8 x 20 x 5
+    ((1, -1, 0), 1, 24, 72, 8, 3),  # degenerate basis, two N tiles (int8), ghost tile of a CTA pair
+    ((0, 0, 1), 2, 6, 10, 6, 2),  # no basis in 3-D: 32-byte protocol rows (tf32 modes)
 ])
 def test_conv_edge_shapes(prec, shape):
     g, B, ci, co, d, df = shape
     rng = np.random.default_rng(11)
     x, f, b, layer, pad = make_conv(rng, g, B, ci, co, d, df, prec)
     y = run_dev(M.conv_forward, x, layer)
-    assert_conv_close(y, O.conv_ref(x, f, b, g, d, df, pad), prec)
+    assert_conv_close(y, O.conv_ref(x, f, b, g, d, df, pad), prec, K=ci * (1 << len(g)) * df ** len(g))
 
 
 def test_conv_identity_filter():
