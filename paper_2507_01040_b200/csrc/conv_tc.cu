@@ -296,8 +296,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const uint32_t h_wrap_x = (uint32_t)((p.hx - df) * ncol);              // x wrapped: next halo row
     const uint32_t h_wrap_y = (uint32_t)((p.hy - df) * p.hx * ncol);       // y wrapped: next halo plane
     for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const long long dbg_w0 = p.dbg_acc ? clock64() : 0;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
+      if (p.dbg_acc && lane == 0) {  // timing instrumentation: MMA warp's wait for the accumulator
+        atomicAdd(p.dbg_acc + 2, (unsigned long long)(clock64() - dbg_w0));
+        atomicAdd(p.dbg_acc + 3, 1ull);
+      }
       const uint32_t d_tmem = tmem_base + (uint32_t)acc * slot_cols;
       if (p.halo) {
         for (int gsi = 0; gsi < p.n_gs; ++gsi) {
@@ -537,6 +542,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if constexpr (kInt8) if (valid) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
       mbar_wait_sleep(&tfull[acc], acc_phase, p.sleep_epi);
       tc_fence_after();
+      const long long dbg_t0 = p.dbg_acc ? clock64() : 0;
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)acc * slot_cols;
       if constexpr (kInt8) {
         // Two-phase epilogue: this mode has ONE accumulator slot (4 exact
@@ -629,6 +635,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
         tc_fence_before();
         if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
+        if (p.dbg_acc && threadIdx.x == 128) {  // timing instrumentation: phase-1 cycles per tile
+          atomicAdd(p.dbg_acc, (unsigned long long)(clock64() - dbg_t0));
+          atomicAdd(p.dbg_acc + 1, 1ull);
+        }
         if (++acc == slots) { acc = 0; acc_phase ^= 1; }
         if (!valid || (p.dbg_skip & 4)) continue;
 #pragma unroll

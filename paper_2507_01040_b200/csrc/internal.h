@@ -131,7 +131,8 @@ struct ConvKParams {
   Basis bs;                   // change of basis: rows = (pixel, column), epilogue inverse transform
   long long num_m_tiles;      // real pixel tiles (tiles beyond are cluster padding)
   uint32_t sleep_prod, sleep_epi;  // back-off (ns) of the producer / epilogue barrier polls
-  int dbg_skip;               // timing experiments only: bit 0 skips A loads, bit 1 skips B loads (garbage results)
+  int dbg_skip;
+  unsigned long long* dbg_acc;  // timing instrumentation (CL_DBG_CLK): cycle counters, else null               // timing experiments only: bit 0 skips A loads, bit 1 skips B loads (garbage results)
   const uint8_t* b_img;
   const float* a_scale;       // kPrecFp32: per-sample power-of-two scale of the A digits
   const float* w_scale;       // kPrecFp32: per-column power-of-two scale of the B digits
