@@ -324,6 +324,7 @@ struct cl_conv {
   int sk;  // spatial rank (== k for convolutions, 1 for the linear layer)
   float* filters = nullptr;  // (NB, C_in, C_out, Q) device copy
   float* bias = nullptr;     // (NB, C_out)
+  float* bias_t = nullptr;   // (C_out, NB): the epilogue's vector-loadable copy
   uint8_t* img = nullptr;    // tensor-core operand images
   float* w_scale = nullptr;  // kPrecFp32: per-column digit scales
   ConvPlan plan;
@@ -462,12 +463,14 @@ static int conv_create_impl(const int32_t* g, int k, int sk, int C_in, int C_out
   cudaError_t e;
   const size_t nscale = (size_t)h->plan.n_ntiles * h->plan.n_tile;
   if ((e = cudaMalloc(&h->filters, nf * 4)) != cudaSuccess || (e = cudaMalloc(&h->bias, nbias * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&h->bias_t, nbias * 4)) != cudaSuccess ||
       (e = cudaMalloc(&h->img, nimg)) != cudaSuccess || (e = cudaMalloc(&h->w_scale, nscale * 4)) != cudaSuccess) {
     cl_conv_destroy(h);
     return cuda_fail(e, "cl_conv_create alloc");
   }
   if ((e = cudaMemcpyAsync(h->filters, filters, nf * 4, cudaMemcpyDefault, s)) != cudaSuccess ||
       (e = cudaMemcpyAsync(h->bias, bias, nbias * 4, cudaMemcpyDefault, s)) != cudaSuccess ||
+      (e = launch_transpose(h->bias, h->bias_t, h->nb, C_out, s)) != cudaSuccess ||
       (precision == kPrecFp32 &&
        (e = launch_weight_colscale(h->g, h->plan, h->filters, C_in, C_out, h->w_scale, s)) != cudaSuccess) ||
       (e = launch_expand_images(h->g, h->plan, h->filters, C_in, C_out, h->w_scale, h->img, s)) != cudaSuccess ||
@@ -541,6 +544,7 @@ void cl_conv_destroy(cl_conv* h) {
   if (!h) return;
   cudaFree(h->filters);
   cudaFree(h->bias);
+  cudaFree(h->bias_t);
   cudaFree(h->img);
   cudaFree(h->w_scale);
   delete h;
@@ -727,6 +731,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.bs = pl.bs;
   p.b_img = h->img;
   p.bias = h->bias;
+  p.bias_t = h->bias_t;
   p.y = y;
   p.y_bf16 = epi.y_bf16;
   p.ybf_groups = epi.ybf_groups;

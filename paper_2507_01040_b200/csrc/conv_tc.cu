@@ -588,15 +588,32 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     oth[r] = ((long long)hi << 32) | (long long)(unsigned)lo;
                   }
                   const double sc = a_sc * (0.5 / 16777216.0) * (double)__ldg(p.w_scale + nt * p.n_tile + cc * W + c0);
+                  // this lane's W biases / activation weights: one vector load each
+                  float bw[W], aw[W];
+                  if constexpr (W == 4) {
+                    const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias_t + cq * NB + bcol * W));
+                    bw[0] = b4.x; bw[1 % W] = b4.y; bw[2 % W] = b4.z; bw[3 % W] = b4.w;
+                  } else {
+                    const float2 b2 = __ldg(reinterpret_cast<const float2*>(p.bias_t + cq * NB + bcol * W));
+                    bw[0] = b2.x; bw[1 % W] = b2.y;
+                  }
+                  if (p.act_mode >= 0) {
+                    if constexpr (W == 4) {
+                      const float4 a4 = __ldg(reinterpret_cast<const float4*>(p.act_w + cq * NB + bcol * W));
+                      aw[0] = a4.x; aw[1 % W] = a4.y; aw[2 % W] = a4.z; aw[3 % W] = a4.w;
+                    } else {
+                      const float2 a2 = __ldg(reinterpret_cast<const float2*>(p.act_w + cq * NB + bcol * W));
+                      aw[0] = a2.x; aw[1 % W] = a2.y;
+                    }
+                  }
                   float v[W];
                   float part = 0.f;
 #pragma unroll
                   for (int j = 0; j < W; ++j) {
                     const long long a = pick_w<W>(own, inv_o[j]), bq = pick_w<W>(oth, inv_p[j]);
                     const long long xs = (inv_os[j] > 0 ? a : -a) + (inv_ps[j] > 0 ? bq : -bq);
-                    const int t = bcol * W + j;
-                    v[j] = (float)fma((double)xs, sc, (double)__ldg(p.bias + t * p.C_out + cq));
-                    if (p.act_mode >= 0) part = fmaf(v[j], __ldg(p.act_w + cq * NB + t), part);
+                    v[j] = (float)fma((double)xs, sc, (double)bw[j]);
+                    if (p.act_mode >= 0) part = fmaf(v[j], aw[j], part);
                   }
                   if (p.act_mode >= 0) {
                     float sg = part + __shfl_xor_sync(0xffffffffu, part, 1);
@@ -970,6 +987,17 @@ cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const CUt
 // as bf16 (esize 2) or fp32 (esize 4); cpg = 16 / (w * esize). Without a change
 // of basis w = NB (the blades); with one, each pixel yields ncol rows of the
 // transformed components x'[c*w + r] = sum_I T[c*w + r][I] x[I].
+__global__ void transpose_kernel(const float* __restrict__ in, float* __restrict__ out, int rows, int cols) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * cols; i += gridDim.x * blockDim.x)
+    out[(i % cols) * rows + i / cols] = in[i];
+}
+cudaError_t launch_transpose(const float* in, float* out, int rows, int cols, cudaStream_t s) {
+  if (rows * cols == 0) return cudaSuccess;
+  transpose_kernel<<<(rows * cols + 255) / 256, 256, 0, s>>>(in, out, rows, cols);
+  count_launch();
+  return cudaGetLastError();
+}
+
 template <int NB, int ESIZE, bool BASIS>
 __global__ void __launch_bounds__(256) pack_rows_kernel(const float* __restrict__ x, uint4* __restrict__ out,
                                                         long long B, int C, long long P, int G, Basis bs) {

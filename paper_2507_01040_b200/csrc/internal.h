@@ -137,6 +137,7 @@ struct ConvKParams {
   const float* a_scale;       // kPrecFp32: per-sample power-of-two scale of the A digits
   const float* w_scale;       // kPrecFp32: per-column power-of-two scale of the B digits
   const float* bias;          // (NB, C_out)
+  const float* bias_t;        // (C_out, NB) copy: one vector load per (channel, lane)
   float* y;                   // fp32 protocol output (or null)
   __nv_bfloat16* y_bf16;      // bf16 A-ready output (or null)
   int ybf_groups;             // groups per sample of the packed bf16 output tensor (B, Gy, P, 16 B)
@@ -167,6 +168,7 @@ cudaError_t launch_expand_ref(const int* g, int k, const float* f, int C_in, int
                               float* out, cudaStream_t s);
 cudaError_t launch_expand_images(const int* g, const ConvPlan& plan, const float* f, int C_in,
                                  int C_out, const float* w_scale, uint8_t* img, cudaStream_t s);
+cudaError_t launch_transpose(const float* in, float* out, int rows, int cols, cudaStream_t s);
 cudaError_t launch_pack_rows(const float* x, void* out, int nb, int esize, long long B, int C, long long P,
                              int G, const Basis& bs, cudaStream_t s);
 cudaError_t launch_act(int nb, const ActParams& p, cudaStream_t s);
