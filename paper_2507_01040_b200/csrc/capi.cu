@@ -792,7 +792,9 @@ static int host_chunked(HostPipe& hp, long long B, size_t in_per, size_t out_per
   if (chunk <= 0) {
     const size_t target = (size_t)512 << 20;  // ~512 MB of input per chunk
     chunk = std::max<long long>(1, (long long)(target / std::max<size_t>(in_per, 1)));
-    chunk = std::min<long long>(chunk, std::max<long long>(1, (B + kPipe - 1) / kPipe));
+    // at least ~8 chunks when the batch allows: the first H2D and the last D2H
+    // are not overlapped, so their share shrinks with the chunk count
+    chunk = std::min<long long>(chunk, std::max<long long>(1, (B + 7) / 8));
   }
   chunk = std::min(chunk, B);
   for (int i = 0; i < kPipe; ++i)
