@@ -162,9 +162,9 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
   pl.ty = ty;
   pl.tz = tz;
 
-  // 2-SM MMA for every mode but 3xTF32 (its A splitter would need the pair's
-  // two halves split before the leader's MMA)
-  pl.pair = prec != kPrec3xTf32 && !g_no_pair;
+  // 2-SM MMA for every mode; 3xTF32 only with halo reuse (there each CTA's
+  // splitter works on its own halo and reports to the pair leader)
+  pl.pair = !g_no_pair && !(prec == kPrec3xTf32 && !pl.halo);
   pl.n_img = i8 ? kDigitsW : (prec == kPrec3xTf32 ? 2 : 1);
   pl.n_a = i8 ? kDigitsA : pl.n_img;
   pl.n_tma_a = i8 ? kDigitsA : 1;

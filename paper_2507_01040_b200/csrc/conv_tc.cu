@@ -127,7 +127,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                    const __grid_constant__ ConvKParams p) {
   constexpr bool kSplit = (PREC == kPrec3xTf32);
   constexpr bool kInt8 = (PREC == kPrecFp32);
-  static_assert(!(PAIR && kSplit), "the 3xTF32 splitter runs unpaired");
+  // 3xTF32 pairs (halo mode only): each CTA's A halo lands on its OWN barrier
+  // for its splitter, whose "split done" arrivals go to the leader's barrier
+  constexpr bool kAOwn = kSplit;
   // epilogue warp groups: warps 4-7, plus warps 8-11 when they are not the
   // 3xTF32 splitter (each group drains half of the accumulator columns)
   constexpr int kEpiGroups = kSplit ? 1 : 2;
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       mbar_init(&tempty[a], 128 * kEpiGroups * (PAIR ? 2 : 1));  // pair: both CTAs' epilogues, on the leader
       mbar_init(&hfull[a], 1);
       mbar_init(&hempty[a], 1);
-      mbar_init(&hlo[a], 128);
+      mbar_init(&hlo[a], 128 * (PAIR ? 2 : 1));
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmap);
@@ -218,13 +220,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             const int g0 = gsi * p.gs;
             mbar_wait_sleep(&hempty[hsl], hphase ^ 1, p.sleep_prod);
             uint8_t* hA = smem + (size_t)hsl * p.halo_slot;
-            if (arm) mbar_arrive_expect_tx(&hfull[hsl], (PAIR ? 2u : 1u) * p.halo_bytes * (uint32_t)p.n_tma_a);
+            if (kAOwn) mbar_arrive_expect_tx(&hfull[hsl], p.halo_bytes * (uint32_t)p.n_tma_a);
+            else if (arm) mbar_arrive_expect_tx(&hfull[hsl], (PAIR ? 2u : 1u) * p.halo_bytes * (uint32_t)p.n_tma_a);
             for (int d = 0; d < p.n_tma_a; ++d) {  // int8: one halo per digit plane (planes stacked over the batch)
               const int bb = d * p.B + b;
               if (p.merged_bc)
-                load_a_box<PAIR>(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, z0, bb * p.G + g0);
+                load_a_box<PAIR && !kAOwn>(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, z0, bb * p.G + g0);
               else
-                load_a_box<PAIR>(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, g0, bb);
+                load_a_box<PAIR && !kAOwn>(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, g0, bb);
             }
             if (++hsl == HS) { hsl = 0; hphase ^= 1; }
             for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
@@ -335,9 +338,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                       }
                     }
                   } else if constexpr (kSplit) {
-                    mma_tf32(d_tmem, a0 + h_img4, b0, idesc, first ? 0u : 1u);  // A_lo * B_hi
-                    mma_tf32(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
-                    mma_tf32(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
+                    mma_mode<kPrecTf32, PAIR>(d_tmem, a0 + h_img4, b0, idesc, first ? 0u : 1u);  // A_lo * B_hi
+                    mma_mode<kPrecTf32, PAIR>(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
+                    mma_mode<kPrecTf32, PAIR>(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
                   } else if constexpr (PREC == kPrecTf32) {
                     mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
                   } else if constexpr (PREC == kPrecBf16) {
@@ -391,9 +394,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                         }
                       }
                     } else if constexpr (kSplit) {
-                      mma_tf32_g(issuer, d_tmem, a0 + h_img4, b0, idesc, accf);  // A_lo * B_hi
-                      mma_tf32_g(issuer, d_tmem, a0, b0 + b_img4, idesc, 1u);   // A_hi * B_lo
-                      mma_tf32_g(issuer, d_tmem, a0, b0, idesc, 1u);            // A_hi * B_hi
+                      mma_mode_g<kPrecTf32, PAIR>(issuer, d_tmem, a0 + h_img4, b0, idesc, accf);  // A_lo * B_hi
+                      mma_mode_g<kPrecTf32, PAIR>(issuer, d_tmem, a0, b0 + b_img4, idesc, 1u);   // A_hi * B_lo
+                      mma_mode_g<kPrecTf32, PAIR>(issuer, d_tmem, a0, b0, idesc, 1u);            // A_hi * B_hi
                     } else {
                       mma_mode_g<PREC, PAIR>(issuer, d_tmem, a0, b0, idesc, accf);
                     }
@@ -906,7 +909,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           for (int gsi = 0; gsi < p.n_gs; ++gsi) {
             mbar_wait(&hfull[hsl], hphase);
             split(smem + (size_t)hsl * p.halo_slot, p.halo_bytes, p.a_bytes);
-            mbar_arrive(&hlo[hsl]);
+            if constexpr (PAIR) mbar_arrive_leader(&hlo[hsl]); else mbar_arrive(&hlo[hsl]);
             if (++hsl == HS) { hsl = 0; hphase ^= 1; }
           }
           continue;
@@ -964,7 +967,7 @@ static cudaError_t launch_nb(const ConvPlan& plan, const CUtensorMap& tmap, cons
       case kPrecFp32: return launch_t<NB, kPrecFp32, true>(plan, tmap, bmap, p, grid, s);
       case kPrecTf32: return launch_t<NB, kPrecTf32, true>(plan, tmap, bmap, p, grid, s);
       case kPrecBf16: return launch_t<NB, kPrecBf16, true>(plan, tmap, bmap, p, grid, s);
-      default: return cudaErrorInvalidValue;
+      default: return launch_t<NB, kPrec3xTf32, true>(plan, tmap, bmap, p, grid, s);
     }
   }
   switch (plan.prec) {
