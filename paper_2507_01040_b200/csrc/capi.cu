@@ -28,6 +28,7 @@ static bool g_no_halo = getenv("CL_NO_HALO") != nullptr;        // A/B: disable 
 static bool g_no_halo_i8 = getenv("CL_NO_HALO_I8") != nullptr;  // A/B: halo off for the int8 mode only
 static bool g_no_tma_merge = getenv("CL_NO_TMA_MERGE") != nullptr;  // A/B: one TMA line per pixel
 static int g_force_tps = getenv("CL_TPS") ? atoi(getenv("CL_TPS")) : 0;  // A/B: taps per stage (halo)
+static bool g_no_bcls = getenv("CL_NO_BCLS") != nullptr;  // A/B: generic basis-inverse picks
 static int g_force_ks = getenv("CL_KS") ? atoi(getenv("CL_KS")) : 0;  // A/B: force the K steps per stage
 static std::atomic<uint64_t> g_launches{0};
 
@@ -563,6 +564,23 @@ struct Epi {
   int ybf_groups = 0;
 };
 
+// Pattern class of the change-of-basis inverse for the int8 epilogue: 1 when
+// every lane's blade j uses own row {0,0,3,3}[j] and partner row {2,2,1,1}[j]
+// (the (1,1,1) family), else 0 (runtime picks). Mirrors the kernel's tables.
+static int basis_class(const Basis& bs, int nb) {
+  if (!bs.on || nb != 8 || bs.w != 4 || g_no_bcls) return 0;
+  static const int O[4] = {0, 0, 3, 3}, P[4] = {2, 2, 1, 1};
+  for (int c = 0; c < 2; ++c)
+    for (int j = 0; j < 4; ++j) {
+      const int t = c * 4 + j;
+      const int a0 = bs.inv[t][0], a1 = bs.inv[t][1];
+      const bool first_own = (a0 / 4) == c;
+      const int o = (first_own ? a0 : a1) % 4, pr = (first_own ? a1 : a0) % 4;
+      if (o != O[j] || pr != P[j]) return 0;
+    }
+  return 1;
+}
+
 // 8-byte elements per pixel of the A tensor map's merged (pixel, row) inner
 // dimension, or 0 for the per-pixel-line map (32-byte swizzled protocol rows).
 static int tma_epx(const ConvPlan& pl) {
@@ -709,6 +727,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.a_bytes = pl.a_bytes;
   p.halo = pl.halo;
   p.tps = pl.tps;
+  p.bcls = basis_class(pl.bs, h->nb);
   p.epx = tma_epx(pl);
   p.hx = pl.hx;
   p.hy = pl.hy;

@@ -121,7 +121,10 @@ __device__ __forceinline__ bool decode_tile(const ConvKParams& p, long long t, i
   return real;
 }
 
-template <int NB, int PREC, bool PAIR>
+// BCLS: change-of-basis pattern class of the int8 epilogue. 1 = the M2(C)
+// basis of the (1,1,1) family: each lane's blades use own rows {0,0,3,3} and
+// partner rows {2,2,1,1} (compile-time picks, 2 shuffles per channel); 0 = any.
+template <int NB, int PREC, bool PAIR, int BCLS = 0>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap bmap,
                    const __grid_constant__ ConvKParams p) {
@@ -586,9 +589,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
                   for (int r = 0; r < W; ++r) {
                     own[r] = sv[cc * W + r];
-                    const int lo = __shfl_xor_sync(0xffffffffu, (int)(own[r] & 0xffffffffll), 1);
-                    const int hi = __shfl_xor_sync(0xffffffffu, (int)(own[r] >> 32), 1);
-                    oth[r] = ((long long)hi << 32) | (long long)(unsigned)lo;
+                    oth[r] = 0;
+                    // BCLS 1: the partner only needs rows 1 and 2
+                    if (BCLS == 0 || r == 1 || r == 2) {
+                      const int lo = __shfl_xor_sync(0xffffffffu, (int)(own[r] & 0xffffffffll), 1);
+                      const int hi = __shfl_xor_sync(0xffffffffu, (int)(own[r] >> 32), 1);
+                      oth[r] = ((long long)hi << 32) | (long long)(unsigned)lo;
+                    }
                   }
                   const double sc = a_sc * (0.5 / 16777216.0) * (double)__ldg(p.w_scale + nt * p.n_tile + cc * W + c0);
                   // this lane's W biases / activation weights: one vector load each
@@ -613,7 +620,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                   float part = 0.f;
 #pragma unroll
                   for (int j = 0; j < W; ++j) {
-                    const long long a = pick_w<W>(own, inv_o[j]), bq = pick_w<W>(oth, inv_p[j]);
+                    long long a, bq;
+                    if constexpr (BCLS == 1 && W == 4) {
+                      a = own[(j >> 1) * 3];        // rows 0, 0, 3, 3
+                      bq = oth[2 - (j >> 1)];       // rows 2, 2, 1, 1
+                    } else {
+                      a = pick_w<W>(own, inv_o[j]);
+                      bq = pick_w<W>(oth, inv_p[j]);
+                    }
                     const long long xs = (inv_os[j] > 0 ? a : -a) + (inv_ps[j] > 0 ? bq : -bq);
                     v[j] = (float)fma((double)xs, sc, (double)bw[j]);
                     if (p.act_mode >= 0) part = fmaf(v[j], aw[j], part);
@@ -934,10 +948,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   }
 }
 
-template <int NB, int PREC, bool PAIR>
+template <int NB, int PREC, bool PAIR, int BCLS = 0>
 static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const CUtensorMap& bmap,
                             const ConvKParams& p, int grid, cudaStream_t s) {
-  auto kfn = conv_tc_kernel<NB, PREC, PAIR>;
+  auto kfn = conv_tc_kernel<NB, PREC, PAIR, BCLS>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)plan.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -964,7 +978,10 @@ static cudaError_t launch_nb(const ConvPlan& plan, const CUtensorMap& tmap, cons
                              const ConvKParams& p, int grid, cudaStream_t s) {
   if (p.pair) {
     switch (plan.prec) {
-      case kPrecFp32: return launch_t<NB, kPrecFp32, true>(plan, tmap, bmap, p, grid, s);
+      case kPrecFp32:
+        if constexpr (NB == 8)
+          if (p.bcls == 1) return launch_t<NB, kPrecFp32, true, 1>(plan, tmap, bmap, p, grid, s);
+        return launch_t<NB, kPrecFp32, true>(plan, tmap, bmap, p, grid, s);
       case kPrecTf32: return launch_t<NB, kPrecTf32, true>(plan, tmap, bmap, p, grid, s);
       case kPrecBf16: return launch_t<NB, kPrecBf16, true>(plan, tmap, bmap, p, grid, s);
       default: return launch_t<NB, kPrec3xTf32, true>(plan, tmap, bmap, p, grid, s);

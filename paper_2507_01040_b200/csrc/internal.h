@@ -126,6 +126,7 @@ struct ConvKParams {
   int pair;                   // 2-SM MMA: M = 256 over the pair, B columns split between the two CTAs
   int halo, hx, hy, hz, hs;   // halo mode (see ConvPlan)
   int tps;                    // halo mode: filter taps per B stage
+  int bcls;                   // int8 epilogue change-of-basis pattern class (see conv_tc.cu), 0 = generic
   int epx;                    // A tensor map with merged (pixel, row) inner dim: 8-byte elements per pixel, else 0
   uint32_t halo_bytes, halo_slot, ring_off;
   Basis bs;                   // change of basis: rows = (pixel, column), epilogue inverse transform
