@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 // lane (column bcol) produces blades bcol*W + j: x = (s_o own[o_j] + s_p partner[p_j]) / 2,
                 // combined exactly in int64 (one weight scale per channel), rounded once
                 constexpr int W = NB / 2;
+                float part[16 / W];  // gate pre-activations, finished for all channels together (ILP)
 #pragma unroll
                 for (int cc = 0; cc < 16 / W; ++cc) {
                   const int co = n0 / W + cc;
@@ -617,7 +618,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     }
                   }
                   float v[W];
-                  float part = 0.f;
+                  part[cc] = 0.f;
 #pragma unroll
                   for (int j = 0; j < W; ++j) {
                     long long a, bq;
@@ -630,18 +631,26 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     }
                     const long long xs = (inv_os[j] > 0 ? a : -a) + (inv_ps[j] > 0 ? bq : -bq);
                     v[j] = (float)fma((double)xs, sc, (double)bw[j]);
-                    if (p.act_mode >= 0) part = fmaf(v[j], aw[j], part);
-                  }
-                  if (p.act_mode >= 0) {
-                    float sg = part + __shfl_xor_sync(0xffffffffu, part, 1);
-                    if (p.act_mode == 0) sg += __ldg(p.act_b + cq);
-                    else if (p.act_mode == 2) sg = sg / p.act_K;
-                    const float gte = 1.f / (1.f + expf(-sg));
-#pragma unroll
-                    for (int j = 0; j < W; ++j) v[j] *= gte;
+                    if (p.act_mode >= 0) part[cc] = fmaf(v[j], aw[j], part[cc]);
                   }
 #pragma unroll
                   for (int j = 0; j < W; ++j) hv[ci * 16 + cc * W + j] = v[j];
+                }
+                if (p.act_mode >= 0) {  // the chunk's gates: other lane's partial sums, sigmoid, scale
+                  const float inv_K = 1.f / p.act_K;
+                  float sg[16 / W];
+#pragma unroll
+                  for (int cc = 0; cc < 16 / W; ++cc) sg[cc] = part[cc] + __shfl_xor_sync(0xffffffffu, part[cc], 1);
+#pragma unroll
+                  for (int cc = 0; cc < 16 / W; ++cc) {
+                    const int cq = min(n0 / W + cc, p.C_out - 1);
+                    if (p.act_mode == 0) sg[cc] += __ldg(p.act_b + cq);
+                    else if (p.act_mode == 2) sg[cc] = sg[cc] * inv_K;
+                    // fast exp / reciprocal: ~1e-7 relative on the gate, far inside the block's 1e-4 bound
+                    const float gte = __frcp_rn(1.f + __expf(-sg[cc]));
+#pragma unroll
+                    for (int j = 0; j < W; ++j) hv[ci * 16 + cc * W + j] *= gte;
+                  }
                 }
               }
             } else {
