@@ -9,6 +9,7 @@
 // the truncating fp32 accumulation of the tf32/bf16 tensor-core paths never
 // touches the result.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -57,7 +58,10 @@ cudaError_t launch_sample_absmax(const float* x, long long B, long long per_samp
 // Integer-exact: X_I = rint(x_I 2^31 / s) (power-of-two scaling, one rounding),
 // X' = sum_I T X_I in int32 (|X'| < 2^31 since s >= 2 max|x| 1.016), and the
 // balanced base-256 digits are the two's-complement bytes of X'.
-template <int NB, bool BASIS>
+// FIXED: the (1,1,1) M2(C) basis found by find_basis, whose rows are sums /
+// differences of blade pairs (2m, 2m+1): x' = (u0, -u3, v2, v1, u2, -u1, v0, v3)
+// with u_m = X_2m + X_2m+1, v_m = X_2m - X_2m+1 (8 adds instead of 64 multiply-adds).
+template <int NB, bool BASIS, bool FIXED = false>
 __global__ void __launch_bounds__(256) slice_input_kernel(const float* __restrict__ x,
                                                           const unsigned* __restrict__ amax,
                                                           int8_t* __restrict__ out, float* __restrict__ scale,
@@ -105,7 +109,13 @@ __global__ void __launch_bounds__(256) slice_input_kernel(const float* __restric
 #pragma unroll
         for (int r = 0; r < W; ++r) {
           int Xs;
-          if constexpr (BASIS) {
+          if constexpr (FIXED) {
+            const int a = col * W + r;
+            const int m = (a == 0 || a == 6) ? 0 : (a == 3 || a == 5) ? 1 : (a == 2 || a == 4) ? 2 : 3;
+            const bool use_u = (a == 0 || a == 1 || a == 4 || a == 5);
+            const int val = use_u ? X[2 * m] + X[2 * m + 1] : X[2 * m] - X[2 * m + 1];
+            Xs = (a == 1 || a == 5) ? -val : val;
+          } else if constexpr (BASIS) {
             Xs = 0;
 #pragma unroll
             for (int I = 0; I < NB; ++I) Xs += (int)bs.T[(col * W + r) * 8 + I] * X[I];
@@ -153,7 +163,14 @@ cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* dig
     return (unsigned)(blocks > cap ? cap : blocks);
   };
   if (bs.on) {
+    static const int8_t kFixed[8][8] = {{1, 1, 0, 0, 0, 0, 0, 0},  {0, 0, 0, 0, 0, 0, -1, -1}, {0, 0, 0, 0, 1, -1, 0, 0},
+                                        {0, 0, 1, -1, 0, 0, 0, 0}, {0, 0, 0, 0, 1, 1, 0, 0},   {0, 0, -1, -1, 0, 0, 0, 0},
+                                        {1, -1, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0, 1, -1}};
+    bool fixed = nb == 8 && getenv("CL_NO_SLICE_FIXED") == nullptr;
+    for (int a = 0; a < 8 && fixed; ++a)
+      for (int I = 0; I < 8 && fixed; ++I) fixed = bs.T[a * 8 + I] == kFixed[a][I];
     if (nb == 4) slice_input_kernel<4, true><<<grid(slice_input_kernel<4, true>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
+    else if (fixed) slice_input_kernel<8, true, true><<<grid(slice_input_kernel<8, true, true>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
     else slice_input_kernel<8, true><<<grid(slice_input_kernel<8, true>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
   } else {
     if (nb == 2) slice_input_kernel<2, false><<<grid(slice_input_kernel<2, false>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
