@@ -830,9 +830,28 @@ static int host_chunked(HostPipe& hp, long long B, size_t in_per, size_t out_per
     rc = hp.stage[i].get(hp.st[i], align_up(in_per * chunk, 256) + out_per * chunk, &stg[i]);
     if (rc == CL_OK) rc = hp.ws[i].get(hp.st[i], ws_bytes(chunk), &wsp[i]);
   }
+  // chunk sizes: small chunks first and last (1, 2, 4, ... up to `chunk`) so
+  // the unoverlapped first H2D and last D2H are short, full chunks between
+  std::vector<long long> sizes;
+  {
+    std::vector<long long> ramp;
+    long long used = 0;
+    for (long long r = 1; r < chunk && B - used - 2 * r >= 2 * chunk; r *= 2) {
+      ramp.push_back(r);
+      used += 2 * r;
+    }
+    sizes = ramp;
+    long long mid = B - used;
+    while (mid > 0) {
+      sizes.push_back(std::min(chunk, mid));
+      mid -= sizes.back();
+    }
+    for (auto r = ramp.rbegin(); r != ramp.rend(); ++r) sizes.push_back(*r);
+  }
   int it = 0;
-  for (long long b0 = 0; b0 < B && rc == CL_OK; b0 += chunk, ++it) {
-    const long long nb = std::min(chunk, B - b0);
+  long long b0 = 0;
+  for (size_t ci = 0; ci < sizes.size() && rc == CL_OK; b0 += sizes[ci], ++ci, ++it) {
+    const long long nb = sizes[ci];
     const int i = it % npipe;
     float* dx = reinterpret_cast<float*>(stg[i]);
     float* dy = reinterpret_cast<float*>(reinterpret_cast<char*>(stg[i]) + align_up(in_per * chunk, 256));

@@ -174,6 +174,17 @@ def test_conv_host_path_numpy():
     assert_conv_close(y, O.conv_ref(x, f, b, (1, 1, 1), 8, 3, pad), "fp32")
 
 
+def test_conv_host_path_ragged_chunks():
+    # B = 37 through the host pipeline: ramped chunks 1, 2, 4, 5 x 4, 3, 4, 2, 1
+    # over three streams; per-sample results are batch-independent, so bit-exact
+    rng = np.random.default_rng(6)
+    x, f, b, layer, pad = make_conv(rng, (1, 1), 37, 3, 5, 9, 3, "fp32", "same")
+    y_host = M.conv_forward(x, layer)
+    y_dev = run_dev(M.conv_forward, x, layer)
+    assert np.array_equal(y_host, y_dev)
+    assert_conv_close(y_host, O.conv_ref(x, f, b, (1, 1), 9, 3, pad), "fp32")
+
+
 def test_conv_batch_independence():
     rng = np.random.default_rng(9)
     x, f, b, layer, _ = make_conv(rng, (1, 1), 5, 4, 4, 12, 3)
