@@ -102,6 +102,15 @@ int cl_conv_create(const int32_t* g, int k, int C_in, int C_out, int d_image, in
  * issued (half of the expanded one under a change of basis); basis = 1 if the
  * layer runs in a changed (matrix-algebra) basis */
 int cl_conv_gemm_flops(const cl_conv* h, int64_t B, double* algorithmic, double* executed, int* basis);
+
+/* Host-only planner query (no device memory, no GPU needed): the kernel
+ * configuration cl_conv_create would choose. out[16] (int64): 0 basis_on,
+ * 1 halo reuse, 2 2-SM pair MMA, 3 K steps per stage, 4 row groups per stage,
+ * 5 filter taps per stage, 6 pipeline stages, 7 N tile, 8 N tiles, 9-11 tile
+ * extent (x, y, z), 12 dynamic shared memory bytes, 13 TMA line elements per
+ * pixel (0 = per-pixel lines), 14 epilogue basis class, 15 TMEM columns. */
+int cl_conv_plan_info(const int32_t* g, int k, int C_in, int C_out, int d_image, int d_filter, int padding,
+                      int precision, int64_t* out);
 /* spatial output side d_out of the layer */
 int cl_conv_out_side(const cl_conv* h, int* d_out);
 /* x_dev (B, C_in, d_image^k, N_B) -> y_dev (B, C_out, d_out^k, N_B) */

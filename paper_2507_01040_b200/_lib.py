@@ -19,7 +19,7 @@ _lib = None
 
 EXPORTS = (
     "cl_validate_signature", "cl_blade_product", "cl_schedule_terms", "cl_basis_info", "cl_expand_kernel",
-    "cl_conv_create", "cl_conv_gemm_flops", "cl_conv_out_side", "cl_conv_forward", "cl_conv_forward_host",
+    "cl_conv_create", "cl_conv_gemm_flops", "cl_conv_plan_info", "cl_conv_out_side", "cl_conv_forward", "cl_conv_forward_host",
     "cl_conv_workspace_bytes", "cl_conv_time_kernel", "cl_conv_forward_ws", "cl_block_workspace_bytes", "cl_block_forward_ws",
     "cl_conv_destroy", "cl_linear_create", "cl_linear_forward", "cl_linear_forward_host",
     "cl_linear_destroy", "cl_act_create", "cl_act_forward", "cl_act_forward_host",
@@ -50,6 +50,8 @@ def load():
         "cl_conv_create": (C.c_int, [I32P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                      P, P, P, C.POINTER(P)]),
         "cl_conv_out_side": (C.c_int, [P, C.POINTER(C.c_int)]),
+        "cl_conv_plan_info": (C.c_int, [I32P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(C.c_int64)]),
         "cl_conv_gemm_flops": (C.c_int, [P, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                          C.POINTER(C.c_int)]),
         "cl_conv_forward": (C.c_int, [P, P, P, C.c_int64, P]),

@@ -877,6 +877,34 @@ static int host_chunked(HostPipe& hp, long long B, size_t in_per, size_t out_per
 
 extern "C" {
 
+// Host-only planner query (no device memory): the kernel configuration
+// cl_conv_create would choose for this layer. Fields of `out` (int64):
+//   0 basis_on, 1 halo, 2 pair (2-SM MMA), 3 ks, 4 gs, 5 tps, 6 stages,
+//   7 n_tile, 8 n_ntiles, 9 tx, 10 ty, 11 tz, 12 smem_bytes, 13 tma line elements
+//   per pixel (0: per-pixel lines), 14 epilogue basis class, 15 tmem_cols
+int cl_conv_plan_info(const int32_t* g, int k, int C_in, int C_out, int d_image, int d_filter, int padding,
+                      int precision, int64_t* out) {
+  if (!out) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null output");
+  if (int st = cl_validate_signature(g, k)) return st;
+  if (C_in < 1 || C_out < 1 || d_image < 1 || d_filter < 1 || d_filter > d_image + 2 * ((d_filter - 1) / 2))
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "bad layer dimensions");
+  if (precision < 0 || precision > 3) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "unknown precision");
+  const int pad = padding == CL_PAD_SAME ? (d_filter - 1) / 2 : 0;
+  const int d_out = d_image + 2 * pad - d_filter + 1;
+  int gi[3] = {0, 0, 0};
+  for (int i = 0; i < k; ++i) gi[i] = g[i];
+  Basis bs{};
+  if (!g_no_basis && (k == 3 || (k == 2 && g_basis_2d))) find_basis(gi, k, &bs);
+  ConvPlan pl;
+  if (!plan_conv(k, 1 << k, precision, C_in, C_out, d_out, d_filter, bs, pl))
+    return fail(CL_ERR_UNSUPPORTED, "Unsupported", "no shared-memory plan fits this layer");
+  const int64_t v[16] = {pl.bs.on, pl.halo, pl.pair, pl.ks, pl.gs, pl.tps, pl.stages, pl.n_tile, pl.n_ntiles,
+                         pl.tx, pl.ty, pl.tz, (int64_t)pl.smem_bytes, tma_epx(pl),
+                         precision == CL_PREC_FP32 ? basis_class(pl.bs, 1 << k) : 0, pl.tmem_cols};
+  for (int i = 0; i < 16; ++i) out[i] = v[i];
+  return CL_OK;
+}
+
 size_t cl_conv_workspace_bytes(const cl_conv* h, int64_t B) { return h ? conv_ws_bytes(h, B, false) : 0; }
 
 int cl_conv_forward_ws(const cl_conv* h, const float* x, float* y, int64_t B, void* ws, size_t ws_bytes,

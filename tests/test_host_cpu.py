@@ -199,3 +199,46 @@ def test_change_of_basis_is_exact_block_diagonalisation(g):
                 np.testing.assert_allclose(blk, A[:w, :w], atol=1e-12)
             else:
                 np.testing.assert_allclose(blk, 0, atol=1e-12)
+
+
+PLAN_KEYS = ["basis", "halo", "pair", "ks", "gs", "tps", "stages", "n_tile", "n_ntiles", "tx", "ty", "tz",
+             "smem", "epx", "bcls", "tmem_cols"]
+
+
+def plan_info(g, C_in, C_out, d, df, padding, prec):
+    lib = _lib.load()
+    out = (_lib.C.c_int64 * 16)()
+    _lib.check(lib.cl_conv_plan_info(_lib.int32_array(g), len(g), C_in, C_out, d, df, padding, prec, out))
+    return dict(zip(PLAN_KEYS, list(out)))
+
+
+@pytest.mark.parametrize("prec", [0, 1, 2, 3])
+def test_planner_cfg5_layer(prec):
+    """cfg5's conv (3-D, C=64, 32^3 same): change of basis, halo reuse and the
+    2-SM pair in every mode; int8 keeps one accumulator
+    slot (4 levels x 128 columns = all of TMEM)."""
+    p = plan_info((1, 1, 1), 64, 64, 32, 3, 1, prec)
+    assert p["basis"] == 1 and p["halo"] == 1 and p["pair"] == 1
+    assert (p["tx"], p["ty"], p["tz"]) == (4, 16, 1)  # one 8-row core-matrix group per halo row
+    assert p["smem"] <= 232448 and p["stages"] >= 4 and p["tmem_cols"] == 512
+    assert p["epx"] == 4  # 32-byte pixels as 8-byte TMA elements
+    if prec == 0:
+        assert p["n_tile"] == 128 and p["n_ntiles"] == 2 and p["bcls"] == 1
+    else:
+        assert p["n_tile"] == 256 and p["n_ntiles"] == 1
+
+
+def test_planner_variants():
+    # degenerate signature: the block-triangular basis (cfg4b)
+    assert plan_info((1, -1, 0), 32, 32, 32, 3, 0, 0)["basis"] == 1
+    # quaternion pair + null generator: no basis, 32-byte protocol rows, no halo for tf32
+    p = plan_info((-1, -1, 0), 8, 8, 12, 3, 0, 1)
+    assert p["basis"] == 0 and p["halo"] == 0 and p["epx"] == 0
+    # 3xTF32 pairs only with halo reuse
+    assert plan_info((-1, -1, 0), 8, 8, 12, 3, 0, 3)["pair"] == 0
+    assert plan_info((1, 1, 1), 16, 16, 12, 3, 1, 3)["pair"] == 1
+    # 1-D: no halo (a tile row spans samples)
+    assert plan_info((1,), 16, 16, 64, 3, 0, 0)["halo"] == 0
+    # fp32 K limit (4 s32 levels): Unsupported beyond K = 32000 is checked at create; the planner still plans
+    with pytest.raises(E.ConfigInvalid):
+        plan_info((1, 1), 4, 4, 8, 3, 0, 7)
