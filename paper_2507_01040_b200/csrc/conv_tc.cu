@@ -125,7 +125,7 @@ __device__ __forceinline__ bool decode_tile(const ConvKParams& p, long long t, i
 // basis of the (1,1,1) family: each lane's blades use own rows {0,0,3,3} and
 // partner rows {2,2,1,1} (compile-time picks, 2 shuffles per channel); 0 = any.
 template <int NB, int PREC, bool PAIR, int BCLS = 0>
-__global__ void __launch_bounds__(kConvThreads, 1)
+__global__ void __launch_bounds__(conv_threads(PREC), 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap bmap,
                    const __grid_constant__ ConvKParams p) {
   constexpr bool kSplit = (PREC == kPrec3xTf32);
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   constexpr bool kAOwn = kSplit;
   // epilogue warp groups: warps 4-7, plus warps 8-11 when they are not the
   // 3xTF32 splitter (each group drains half of the accumulator columns)
-  constexpr int kEpiGroups = kSplit ? 1 : 2;
+  constexpr int kEpiGroups = kSplit ? 1 : (kInt8 ? 4 : 2);
   // A row-group bytes: packed 16-byte groups for bf16 / int8 digits / 1-D,
   // otherwise one protocol multivector (16 B in 2-D, 32 B in 3-D)
   constexpr int RB = (PREC == kPrecBf16 || kInt8 || NB == 2) ? 16 : NB * 4;
@@ -487,10 +487,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       if (++acc == slots) { acc = 0; acc_phase ^= 1; }
     }
-  } else if (warp >= 4 && (warp < 8 || !kSplit)) {
+  } else if (warp >= 4 && warp < 4 + 4 * kEpiGroups) {
     // ===================== epilogue =====================
     const int ew = warp & 3;  // TMEM lane quarter this warp may access
-    const int eg = (warp >> 2) - 1;
+    const int eg = (warp - 4) >> 2;
     const int c_half = ((p.n_tile / kEpiGroups + 15) / 16) * 16;
     const int c_beg = eg * c_half, c_end = min(p.n_tile, c_beg + c_half);
     const int row = ew * 32 + lane;
@@ -556,23 +556,24 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         // Phase 1 drains TMEM into registers (level combine, change-of-basis
         // inverse, bias, activation gate) and releases the slot; phase 2 adds
         // the residual and stores while the next tile's MMAs run.
-        constexpr int kHold = 64;  // columns per thread: N_TILE <= 128 over 2 warp groups
+        constexpr int kHold = 32;           // columns per thread: N_TILE <= 128 over 4 warp groups
+        constexpr int CH = (NB == 8 && BCLS == 0) ? 8 : 4;  // columns per chunk: whole channels (BCLS 1 implies the basis: 4)
         float hv[kHold];
 #pragma unroll
-        for (int ci = 0; ci < kHold / 16; ++ci) {
-          const int c0 = c_beg + ci * 16;
+        for (int ci = 0; ci < kHold / CH; ++ci) {
+          const int c0 = c_beg + ci * CH;
           const int n0 = nt * p.n_tile + c0;
           if (c0 < c_end && n0 < p.N && !(p.dbg_skip & 4)) {
-            long long sv[16];  // exact: S = L0 2^24 + L1 2^16 + L2 2^8 + L3 (|S| < 2^53 for K <= 32000)
+            long long sv[CH];  // exact: S = L0 2^24 + L1 2^16 + L2 2^8 + L3 (|S| < 2^53 for K <= 32000)
             {
-              uint32_t l0[16], l1[16], l2[16], l3[16];
-              tmem_ld16(taddr + (uint32_t)c0, l0);
-              tmem_ld16(taddr + (uint32_t)(p.n_tile + c0), l1);
-              tmem_ld16(taddr + (uint32_t)(2 * p.n_tile + c0), l2);
-              tmem_ld16(taddr + (uint32_t)(3 * p.n_tile + c0), l3);
+              uint32_t l0[CH], l1[CH], l2[CH], l3[CH];
+              tmem_ldn<CH>(taddr + (uint32_t)c0, l0);
+              tmem_ldn<CH>(taddr + (uint32_t)(p.n_tile + c0), l1);
+              tmem_ldn<CH>(taddr + (uint32_t)(2 * p.n_tile + c0), l2);
+              tmem_ldn<CH>(taddr + (uint32_t)(3 * p.n_tile + c0), l3);
               tmem_ld_wait();
 #pragma unroll
-              for (int c = 0; c < 16; ++c)
+              for (int c = 0; c < CH; ++c)
                 sv[c] = ((long long)(int)l0[c] << 24) + ((long long)(int)l1[c] << 16) +
                         ((long long)(int)l2[c] << 8) + (long long)(int)l3[c];
             }
@@ -581,9 +582,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 // lane (column bcol) produces blades bcol*W + j: x = (s_o own[o_j] + s_p partner[p_j]) / 2,
                 // combined exactly in int64 (one weight scale per channel), rounded once
                 constexpr int W = NB / 2;
-                float part[16 / W];  // gate pre-activations, finished for all channels together (ILP)
+                float part[CH / W];  // gate pre-activations, finished for all channels together (ILP)
 #pragma unroll
-                for (int cc = 0; cc < 16 / W; ++cc) {
+                for (int cc = 0; cc < CH / W; ++cc) {
                   const int co = n0 / W + cc;
                   const int cq = min(co, p.C_out - 1);
                   long long own[W], oth[W];
@@ -634,28 +635,28 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     if (p.act_mode >= 0) part[cc] = fmaf(v[j], aw[j], part[cc]);
                   }
 #pragma unroll
-                  for (int j = 0; j < W; ++j) hv[ci * 16 + cc * W + j] = v[j];
+                  for (int j = 0; j < W; ++j) hv[ci * CH + cc * W + j] = v[j];
                 }
                 if (p.act_mode >= 0) {  // the chunk's gates: other lane's partial sums, sigmoid, scale
                   const float inv_K = 1.f / p.act_K;
-                  float sg[16 / W];
+                  float sg[CH / W];
 #pragma unroll
-                  for (int cc = 0; cc < 16 / W; ++cc) sg[cc] = part[cc] + __shfl_xor_sync(0xffffffffu, part[cc], 1);
+                  for (int cc = 0; cc < CH / W; ++cc) sg[cc] = part[cc] + __shfl_xor_sync(0xffffffffu, part[cc], 1);
 #pragma unroll
-                  for (int cc = 0; cc < 16 / W; ++cc) {
+                  for (int cc = 0; cc < CH / W; ++cc) {
                     const int cq = min(n0 / W + cc, p.C_out - 1);
                     if (p.act_mode == 0) sg[cc] += __ldg(p.act_b + cq);
                     else if (p.act_mode == 2) sg[cc] = sg[cc] * inv_K;
                     // fast exp / reciprocal: ~1e-7 relative on the gate, far inside the block's 1e-4 bound
                     const float gte = __frcp_rn(1.f + __expf(-sg[cc]));
 #pragma unroll
-                    for (int j = 0; j < W; ++j) hv[ci * 16 + cc * W + j] *= gte;
+                    for (int j = 0; j < W; ++j) hv[ci * CH + cc * W + j] *= gte;
                   }
                 }
               }
             } else {
 #pragma unroll
-              for (int cc = 0; cc < 16 / NB; ++cc) {
+              for (int cc = 0; cc < CH / NB; ++cc) {
                 const int co = n0 / NB + cc;
                 const int cq = min(co, p.C_out - 1);
                 float v[NB];
@@ -671,7 +672,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                   for (int j = 0; j < NB; ++j) v[j] *= gte;
                 }
 #pragma unroll
-                for (int j = 0; j < NB; ++j) hv[ci * 16 + cc * NB + j] = v[j];
+                for (int j = 0; j < NB; ++j) hv[ci * CH + cc * NB + j] = v[j];
               }
             }
           }
@@ -685,23 +686,23 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (++acc == slots) { acc = 0; acc_phase ^= 1; }
         if (!valid || (p.dbg_skip & 4)) continue;
 #pragma unroll
-        for (int ci = 0; ci < kHold / 16; ++ci) {
-          const int c0 = c_beg + ci * 16;
+        for (int ci = 0; ci < kHold / CH; ++ci) {
+          const int c0 = c_beg + ci * CH;
           const int n0 = nt * p.n_tile + c0;
           if (c0 < c_end && n0 < p.N) {
             // W blades of one channel per store: the lane's half (change of basis) or all N_B
             constexpr int W = (NB >= 4) ? NB / 2 : NB;
             const int wv = p.bs.on ? W : NB;
 #pragma unroll
-            for (int cc = 0; cc < 16 / W; ++cc) {
-              if (cc * wv >= 16) break;
+            for (int cc = 0; cc < CH / W; ++cc) {
+              if (cc * wv >= CH) break;
               const int co = n0 / wv + cc;
               if (co >= p.C_out) break;
               const long long off = p.bs.on ? (long long)bcol * W : 0;
               if (p.bs.on) {
                 float h[W];
 #pragma unroll
-                for (int j = 0; j < W; ++j) h[j] = hv[ci * 16 + cc * W + j];
+                for (int j = 0; j < W; ++j) h[j] = hv[ci * CH + cc * W + j];
                 if (p.resid) {
                   const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB + off;
                   if constexpr (W == 2) {
@@ -718,10 +719,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                   else *reinterpret_cast<float4*>(yp) = make_float4(h[0], h[1 % W], h[2 % W], h[3 % W]);
                 }
               } else {
-                if (cc >= 16 / NB) break;
+                if (cc >= CH / NB) break;
                 float v[NB];
 #pragma unroll
-                for (int j = 0; j < NB; ++j) v[j] = hv[ci * 16 + cc * NB + j];
+                for (int j = 0; j < NB; ++j) v[j] = hv[ci * CH + cc * NB + j];
                 if (p.resid) {
                   const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB;
                   if constexpr (NB == 2) {
@@ -966,7 +967,7 @@ static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kConvThreads);
+  cfg.blockDim = dim3(conv_threads(PREC));
   cfg.dynamicSmemBytes = plan.smem_bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -69,6 +69,8 @@ __device__ __forceinline__ double basis_entry(const Sig& sg, const Basis& bs, co
 }
 #endif
 constexpr int kConvThreads = 384;    // 12 warps, see conv_tc.cu
+// the int8 mode runs 20 warps: four epilogue warp groups drain its single accumulator slot
+constexpr int conv_threads(int prec) { return prec == 0 ? 640 : kConvThreads; }
 constexpr int kMaxSmem = 232448;     // 227 KB opt-in dynamic shared memory per CTA
 
 // Tiling plan of one conv layer, fixed at create time (conv.py:101-140 fixes
