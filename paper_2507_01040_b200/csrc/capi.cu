@@ -569,16 +569,20 @@ struct Epi {
 // (the (1,1,1) family), else 0 (runtime picks). Mirrors the kernel's tables.
 static int basis_class(const Basis& bs, int nb) {
   if (!bs.on || nb != 8 || bs.w != 4 || g_no_bcls) return 0;
-  static const int O[4] = {0, 0, 3, 3}, P[4] = {2, 2, 1, 1};
+  // class 1: own rows {0,0,3,3}, partner rows {2,2,1,1} in both lanes ((1,1,1) family)
+  // class 2: lane 0 own {0,1,1,0} / partner {1,0,0,1}, lane 1 mirrored (3 - row): (1,-1,0) family
+  static const int O1[4] = {0, 0, 3, 3}, P1[4] = {2, 2, 1, 1}, Q2[4] = {0, 1, 1, 0}, P2[4] = {1, 0, 0, 1};
+  bool c1 = true, c2 = true;
   for (int c = 0; c < 2; ++c)
     for (int j = 0; j < 4; ++j) {
       const int t = c * 4 + j;
       const int a0 = bs.inv[t][0], a1 = bs.inv[t][1];
       const bool first_own = (a0 / 4) == c;
       const int o = (first_own ? a0 : a1) % 4, pr = (first_own ? a1 : a0) % 4;
-      if (o != O[j] || pr != P[j]) return 0;
+      c1 = c1 && o == O1[j] && pr == P1[j];
+      c2 = c2 && o == (c ? 3 - Q2[j] : Q2[j]) && pr == (c ? 3 - P2[j] : P2[j]);
     }
-  return 1;
+  return c1 ? 1 : (c2 ? 2 : 0);
 }
 
 // 8-byte elements per pixel of the A tensor map's merged (pixel, row) inner

@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(conv_threads(PREC), 1)
         // inverse, bias, activation gate) and releases the slot; phase 2 adds
         // the residual and stores while the next tile's MMAs run.
         constexpr int kHold = 32;           // columns per thread: N_TILE <= 128 over 4 warp groups
-        constexpr int CH = (NB == 8 && BCLS == 0) ? 8 : 4;  // columns per chunk: whole channels (BCLS 1 implies the basis: 4)
+        constexpr int CH = (NB == 8 && BCLS == 0) ? 8 : 4;  // columns per chunk: whole channels (BCLS > 0 implies the basis: 4)
         float hv[kHold];
 #pragma unroll
         for (int ci = 0; ci < kHold / CH; ++ci) {
@@ -588,8 +588,20 @@ __global__ void __launch_bounds__(conv_threads(PREC), 1)
                   const int co = n0 / W + cc;
                   const int cq = min(co, p.C_out - 1);
                   long long own[W], oth[W];
+                  long long recvA = 0, recvB = 0;
+                  if constexpr (BCLS == 2 && W == 4) {
+                    // degenerate (1,-1,0) family: lane 0 sends rows 2, 3, lane 1 rows 0, 1
+#pragma unroll
+                    for (int r = 0; r < W; ++r) { own[r] = sv[cc * W + r]; oth[r] = 0; }
+                    const long long sA = bcol ? own[0] : own[2], sB = bcol ? own[1] : own[3];
+                    recvA = ((long long)__shfl_xor_sync(0xffffffffu, (int)(sA >> 32), 1) << 32) |
+                            (long long)(unsigned)__shfl_xor_sync(0xffffffffu, (int)(sA & 0xffffffffll), 1);
+                    recvB = ((long long)__shfl_xor_sync(0xffffffffu, (int)(sB >> 32), 1) << 32) |
+                            (long long)(unsigned)__shfl_xor_sync(0xffffffffu, (int)(sB & 0xffffffffll), 1);
+                  }
 #pragma unroll
                   for (int r = 0; r < W; ++r) {
+                    if constexpr (BCLS == 2) break;
                     own[r] = sv[cc * W + r];
                     oth[r] = 0;
                     // BCLS 1: the partner only needs rows 1 and 2
@@ -626,6 +638,10 @@ __global__ void __launch_bounds__(conv_threads(PREC), 1)
                     if constexpr (BCLS == 1 && W == 4) {
                       a = own[(j >> 1) * 3];        // rows 0, 0, 3, 3
                       bq = oth[2 - (j >> 1)];       // rows 2, 2, 1, 1
+                    } else if constexpr (BCLS == 2 && W == 4) {
+                      constexpr int kQ[4] = {0, 1, 1, 0};
+                      a = bcol ? own[3 - kQ[j]] : own[kQ[j]];                 // rows 0,1,1,0 / 3,2,2,3
+                      bq = (((j == 0) || (j == 3)) != (bcol != 0)) ? recvB : recvA;
                     } else {
                       a = pick_w<W>(own, inv_o[j]);
                       bq = pick_w<W>(oth, inv_p[j]);
@@ -989,8 +1005,10 @@ static cudaError_t launch_nb(const ConvPlan& plan, const CUtensorMap& tmap, cons
   if (p.pair) {
     switch (plan.prec) {
       case kPrecFp32:
-        if constexpr (NB == 8)
+        if constexpr (NB == 8) {
           if (p.bcls == 1) return launch_t<NB, kPrecFp32, true, 1>(plan, tmap, bmap, p, grid, s);
+          if (p.bcls == 2) return launch_t<NB, kPrecFp32, true, 2>(plan, tmap, bmap, p, grid, s);
+        }
         return launch_t<NB, kPrecFp32, true>(plan, tmap, bmap, p, grid, s);
       case kPrecTf32: return launch_t<NB, kPrecTf32, true>(plan, tmap, bmap, p, grid, s);
       case kPrecBf16: return launch_t<NB, kPrecBf16, true>(plan, tmap, bmap, p, grid, s);

@@ -229,8 +229,9 @@ def test_planner_cfg5_layer(prec):
 
 
 def test_planner_variants():
-    # degenerate signature: the block-triangular basis (cfg4b)
-    assert plan_info((1, -1, 0), 32, 32, 32, 3, 0, 0)["basis"] == 1
+    # degenerate signature: the block-triangular basis (cfg4b), epilogue pattern class 2
+    p = plan_info((1, -1, 0), 32, 32, 32, 3, 0, 0)
+    assert p["basis"] == 1 and p["bcls"] == 2
     # quaternion pair + null generator: no basis, 32-byte protocol rows, no halo for tf32
     p = plan_info((-1, -1, 0), 8, 8, 12, 3, 0, 1)
     assert p["basis"] == 0 and p["halo"] == 0 and p["epx"] == 0
