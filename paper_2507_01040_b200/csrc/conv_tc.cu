@@ -125,7 +125,7 @@ __device__ __forceinline__ bool decode_tile(const ConvKParams& p, long long t, i
 // basis of the (1,1,1) family: each lane's blades use own rows {0,0,3,3} and
 // partner rows {2,2,1,1} (compile-time picks, 2 shuffles per channel); 0 = any.
 template <int NB, int PREC, bool PAIR, int BCLS = 0>
-__global__ void __launch_bounds__(conv_threads(PREC), 1)
+__global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap bmap,
                    const __grid_constant__ ConvKParams p) {
   constexpr bool kSplit = (PREC == kPrec3xTf32);
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(conv_threads(PREC), 1)
   constexpr bool kAOwn = kSplit;
   // epilogue warp groups: warps 4-7, plus warps 8-11 when they are not the
   // 3xTF32 splitter (each group drains half of the accumulator columns)
-  constexpr int kEpiGroups = kSplit ? 1 : (kInt8 ? 4 : 2);
+  constexpr int kEpiGroups = kSplit ? 1 : (conv_threads(PREC, NB) == 640 ? 4 : 2);
   // A row-group bytes: packed 16-byte groups for bf16 / int8 digits / 1-D,
   // otherwise one protocol multivector (16 B in 2-D, 32 B in 3-D)
   constexpr int RB = (PREC == kPrecBf16 || kInt8 || NB == 2) ? 16 : NB * 4;
@@ -983,7 +983,7 @@ static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(conv_threads(PREC));
+  cfg.blockDim = dim3(conv_threads(PREC, NB));
   cfg.dynamicSmemBytes = plan.smem_bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

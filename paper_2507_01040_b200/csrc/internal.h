@@ -69,8 +69,10 @@ __device__ __forceinline__ double basis_entry(const Sig& sg, const Basis& bs, co
 }
 #endif
 constexpr int kConvThreads = 384;    // 12 warps, see conv_tc.cu
-// the int8 mode runs 20 warps: four epilogue warp groups drain its single accumulator slot
-constexpr int conv_threads(int prec) { return prec == 0 ? 640 : kConvThreads; }
+// 20 warps (four epilogue warp groups) for the int8 mode (one accumulator slot to drain) and the
+// 2-D / 1-D fp32-accumulator modes (measured faster); 12 warps (two groups) for 3-D bf16 / tf32
+// (their 3-D epilogue spills at 96 registers) and 3xTF32 (warps 8-11 split A)
+constexpr int conv_threads(int prec, int nb) { return (prec == 0 || (prec != 3 && nb <= 4)) ? 640 : kConvThreads; }
 constexpr int kMaxSmem = 232448;     // 227 KB opt-in dynamic shared memory per CTA
 
 // Tiling plan of one conv layer, fixed at create time (conv.py:101-140 fixes
