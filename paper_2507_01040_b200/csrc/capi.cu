@@ -29,6 +29,7 @@ static bool g_no_halo_i8 = getenv("CL_NO_HALO_I8") != nullptr;  // A/B: halo off
 static bool g_no_tma_merge = getenv("CL_NO_TMA_MERGE") != nullptr;  // A/B: one TMA line per pixel
 static int g_force_tps = getenv("CL_TPS") ? atoi(getenv("CL_TPS")) : 0;  // A/B: taps per stage (halo)
 static bool g_no_bcls = getenv("CL_NO_BCLS") != nullptr;  // A/B: generic basis-inverse picks
+static bool g_no_fused_amax = getenv("CL_NO_FUSED_AMAX") != nullptr;  // A/B: separate absmax pass over y1
 static int g_force_ks = getenv("CL_KS") ? atoi(getenv("CL_KS")) : 0;  // A/B: force the K steps per stage
 static std::atomic<uint64_t> g_launches{0};
 
@@ -562,6 +563,8 @@ struct Epi {
   int res_side = 0, res_crop = 0;
   __nv_bfloat16* y_bf16 = nullptr;  // write bf16 A-ready output for a following bf16 conv
   int ybf_groups = 0;
+  unsigned* amax_out = nullptr;      // int8 mode: per-sample max |y| of this conv's output (atomicMax)
+  const unsigned* amax_in = nullptr; // int8 mode: per-sample max |x| already known (skip the absmax pass)
 };
 
 // Pattern class of the change-of-basis inverse for the int8 epilogue: 1 when
@@ -681,8 +684,10 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
     a_scale = reinterpret_cast<float*>(digits + bytes + (size_t)B * 4);
     const long long per_sample = (long long)h->C_in * P_in * h->nb;
     if (prep) {
-      CL_CUDA(launch_sample_absmax(x, B, per_sample, amax, s), "absmax");
-      CL_CUDA(launch_slice_input(x, amax, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G, pl.bs, s), "slice_input");
+      if (!epi.amax_in) CL_CUDA(launch_sample_absmax(x, B, per_sample, amax, s), "absmax");
+      CL_CUDA(launch_slice_input(x, epi.amax_in ? epi.amax_in : amax, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G,
+                                 pl.bs, s),
+              "slice_input");
     }
     src = digits;
   } else if (pl.packed) {
@@ -765,6 +770,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.act_w = epi.act ? epi.act->w : nullptr;
   p.act_b = epi.act ? epi.act->b : nullptr;
   p.act_K = epi.act ? (float)epi.act->K : 1.f;
+  p.amax_out = epi.amax_out;
   int grid = (int)std::min<long long>(p.num_tiles, (long long)num_sms());
   grid -= grid % p.cs;
   CUtensorMap bmap = map;  // unused unless paired
@@ -1107,7 +1113,9 @@ static size_t block_mid_bytes(const cl_block* h, long long B) {
 }
 static size_t block_ws_bytes(const cl_block* h, long long B) {
   const bool bf = bf16_handoff(h);
-  return block_mid_bytes(h, B) + std::max(conv_ws_bytes(h->c1, B, false), conv_ws_bytes(h->c2, B, bf));
+  // + the per-sample max |y1| conv1's epilogue accumulates for conv2's digit slicing (int8 mode)
+  return block_mid_bytes(h, B) + align_up((size_t)B * 4, 256) +
+         std::max(conv_ws_bytes(h->c1, B, false), conv_ws_bytes(h->c2, B, bf));
 }
 
 static int block_run(const cl_block* h, const float* x, float* y, long long B, void* ws, cudaStream_t s) {
@@ -1116,7 +1124,8 @@ static int block_run(const cl_block* h, const float* x, float* y, long long B, v
   if (B == 0) return CL_OK;
   const size_t mid_bytes = block_mid_bytes(h, B);
   void* mid = ws;
-  void* cws = reinterpret_cast<char*>(ws) + mid_bytes;
+  unsigned* amax_mid = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + mid_bytes);
+  void* cws = reinterpret_cast<char*>(ws) + mid_bytes + align_up((size_t)B * 4, 256);
   Epi e1;
   e1.act = h->act;
   Epi e2;
@@ -1134,6 +1143,12 @@ static int block_run(const cl_block* h, const float* x, float* y, long long B, v
     e1.ybf_groups = c2->plan.G;
     if (int rc = conv_run(c1, x, nullptr, nullptr, B, e1, cws, s)) return rc;
     return conv_run(c2, nullptr, (const __nv_bfloat16*)mid, y, B, e2, cws, s);
+  }
+  if (c2->prec == kPrecFp32 && c1->prec == kPrecFp32 && !g_no_fused_amax) {
+    // conv1's epilogue takes conv2's per-sample max |y1|: no separate absmax pass over y1
+    CL_CUDA(cudaMemsetAsync(amax_mid, 0, (size_t)B * 4, s), "amax memset");
+    e1.amax_out = amax_mid;
+    e2.amax_in = amax_mid;
   }
   if (int rc = conv_run(c1, x, nullptr, (float*)mid, B, e1, cws, s)) return rc;
   return conv_run(c2, (const float*)mid, nullptr, y, B, e2, cws, s);

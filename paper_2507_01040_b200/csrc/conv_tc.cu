@@ -700,7 +700,8 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           atomicAdd(p.dbg_acc + 1, 1ull);
         }
         if (++acc == slots) { acc = 0; acc_phase ^= 1; }
-        if (!valid || (p.dbg_skip & 4)) continue;
+        float ymax = 0.f;  // max |stored value| of this thread (fused absmax for the next conv)
+        if (valid && !(p.dbg_skip & 4))
 #pragma unroll
         for (int ci = 0; ci < kHold / CH; ++ci) {
           const int c0 = c_beg + ci * CH;
@@ -734,6 +735,8 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                   if constexpr (W == 2) *reinterpret_cast<float2*>(yp) = make_float2(h[0], h[1 % W]);
                   else *reinterpret_cast<float4*>(yp) = make_float4(h[0], h[1 % W], h[2 % W], h[3 % W]);
                 }
+#pragma unroll
+                for (int j = 0; j < W; ++j) ymax = fmaxf(ymax, fabsf(h[j]));
               } else {
                 if (cc >= CH / NB) break;
                 float v[NB];
@@ -762,8 +765,19 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                       reinterpret_cast<float4*>(yp)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                   }
                 }
+#pragma unroll
+                for (int j = 0; j < NB; ++j) ymax = fmaxf(ymax, fabsf(v[j]));
               }
             }
+          }
+        }
+        if (p.amax_out) {
+          if (p.k == 1) {  // 1-D: rows of one tile belong to different samples
+            if (valid) atomicMax(p.amax_out + b, __float_as_uint(ymax));
+          } else {  // one sample per tile: reduce over the warp first
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ymax = fmaxf(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
+            if (lane == 0 && real) atomicMax(p.amax_out + b, __float_as_uint(ymax));
           }
         }
         continue;

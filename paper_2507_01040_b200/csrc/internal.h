@@ -152,6 +152,7 @@ struct ConvKParams {
   const float* act_w;         // (C_out, NB) blade-keyed weights / 0-1 mask
   const float* act_b;         // (C_out) Linear bias
   float act_K;                // K as float (Mean divisor)
+  unsigned* amax_out;         // int8 epilogue: per-sample atomicMax of |stored value| (float bits), or null
 };
 
 struct ActParams {

@@ -1,5 +1,6 @@
 """GPU parity of the kernel variants the planner can switch off (1-SM MMA,
-per-tap A loads, per-pixel TMA lines, one tap per B stage). The switches are
+per-tap A loads, per-pixel TMA lines, one tap per B stage, generic basis
+inverse, separate absmax pass, generic digit slicing). The switches are
 read once when the library loads, so each variant runs in a fresh process;
 the default variant is covered by test_gpu_parity.py. Same tolerances."""
 
@@ -30,7 +31,21 @@ for prec in ("fp32", "3xtf32", "tf32", "bf16"):
     for g, B, ci, co, d, df, padding in cases:
         x, f, b, layer, pad = make_conv(rng, g, B, ci, co, d, df, prec, padding)
         y = run_dev(M.conv_forward, x, layer)
-        assert_conv_close(y, O.conv_ref(x, f, b, g, d, df, pad), prec)
+        assert_conv_close(y, O.conv_ref(x, f, b, g, d, df, pad), prec,
+                          K=ci * (1 << len(g)) * df ** len(g))
+# a block (conv -> activation -> conv + residual) in the exact mode
+g, B, C, d = (1, 1, 1), 2, 4, 6
+nb = 8
+x = rng.standard_normal((B, C, d ** 3, nb)).astype(np.float32)
+fan = C * nb * 27
+f1 = rng.uniform(-1, 1, (nb, C, C, 27)).astype(np.float32) / np.float32(np.sqrt(fan))
+f2 = rng.uniform(-1, 1, (nb, C, C, 27)).astype(np.float32) / np.float32(np.sqrt(fan))
+b1 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
+b2 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
+blk = M.make_basic_block(M.Signature(g), B, C, C, C, d, f1, b1, 2, f2, b2, padding="same", residual=True)
+y = M.block_forward(torch.from_numpy(x).cuda(), blk).cpu().numpy()
+ref = O.block_ref(x, g, d, f1, b1, 2, tuple(range(nb)), None, None, f2, b2, padding="same", residual=True)
+assert O.max_rel_error(y, ref) <= 1e-4, O.max_rel_error(y, ref)
 print("ok")
 """
 
@@ -43,7 +58,8 @@ def _run(env_extra):
 
 
 @pytest.mark.parametrize("flags", [{"CL_NO_PAIR": "1"}, {"CL_NO_HALO": "1"}, {"CL_NO_TMA_MERGE": "1"},
-                                   {"CL_TPS": "1"}, {"CL_BASIS_2D": "1"}, {"CL_NO_BASIS": "1"}],
+                                   {"CL_TPS": "1"}, {"CL_BASIS_2D": "1"}, {"CL_NO_BASIS": "1"},
+                                   {"CL_NO_BCLS": "1", "CL_NO_FUSED_AMAX": "1", "CL_NO_SLICE_FIXED": "1"}],
                          ids=lambda f: ",".join(f))
 def test_variant_parity(flags):
     if not torch.cuda.is_available():
