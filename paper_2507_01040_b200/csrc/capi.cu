@@ -823,7 +823,9 @@ static int host_chunked(HostPipe& hp, long long B, size_t in_per, size_t out_per
     chunk = std::max<long long>(1, (long long)(target / std::max<size_t>(in_per, 1)));
     // at least ~8 chunks when the batch allows: the first H2D and the last D2H
     // are not overlapped, so their share shrinks with the chunk count
-    chunk = std::min<long long>(chunk, std::max<long long>(1, (B + 7) / 8));
+    // (but no chunk under ~64 MB: small transfers are launch-overhead bound)
+    const long long min_chunk = std::max<long long>(1, (long long)(((size_t)64 << 20) / std::max<size_t>(in_per, 1)));
+    chunk = std::min<long long>(chunk, std::max<long long>(min_chunk, (B + 7) / 8));
   }
   chunk = std::min(chunk, B);
   for (int i = 0; i < kPipe; ++i)
