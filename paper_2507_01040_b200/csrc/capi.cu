@@ -790,17 +790,20 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   }
   static unsigned long long* dbg_acc = nullptr;  // CL_DBG_CLK: per-launch epilogue / MMA-wait cycle report
   if (getenv("CL_DBG_CLK")) {
-    if (!dbg_acc) cudaMalloc(&dbg_acc, 4 * sizeof(unsigned long long));
-    cudaMemsetAsync(dbg_acc, 0, 4 * sizeof(unsigned long long), s);
+    if (!dbg_acc) cudaMalloc(&dbg_acc, 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(dbg_acc, 0, 8 * sizeof(unsigned long long), s);
     p.dbg_acc = dbg_acc;
   }
   cudaError_t e = launch_conv(pl, map, bmap, p, grid, s);
   if (p.dbg_acc && e == cudaSuccess) {
-    unsigned long long h[4];
+    unsigned long long h[8];
     cudaMemcpyAsync(h, dbg_acc, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    fprintf(stderr, "[CL_DBG_CLK] epilogue phase-1 %.0f cyc/tile (%llu tiles); MMA tempty wait %.0f cyc/tile\n",
-            h[1] ? (double)h[0] / h[1] : 0.0, h[1], h[3] ? (double)h[2] / h[3] : 0.0);
+    fprintf(stderr,
+            "[CL_DBG_CLK] epilogue phase-1 %.0f cyc/tile (%llu tiles); MMA waits per tile: accumulator %.0f, "
+            "halo %.0f cyc\n",
+            h[1] ? (double)h[0] / h[1] : 0.0, h[1], h[3] ? (double)h[2] / h[3] : 0.0,
+            h[3] ? (double)h[4] / h[3] : 0.0);
   }
   if (e != cudaSuccess) return cuda_fail(e, "conv_tc launch");
   return CL_OK;

@@ -312,8 +312,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       const uint32_t d_tmem = tmem_base + (uint32_t)acc * slot_cols;
       if (p.halo) {
         for (int gsi = 0; gsi < p.n_gs; ++gsi) {
+          const long long dbg_h0 = p.dbg_acc ? clock64() : 0;
           if (kSplit) mbar_wait(&hlo[hsl], hphase);
           else mbar_wait(&hfull[hsl], hphase);
+          if (p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 4, (unsigned long long)(clock64() - dbg_h0));
           tc_fence_after();
           const uint32_t hA4 = (smem_u32(smem + (size_t)hsl * p.halo_slot) & 0x3FFFFu) >> 4;
           // tap (qx, qy, qz) -> halo offset in 16-byte rows, stepped without divisions
