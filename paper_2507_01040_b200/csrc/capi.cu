@@ -23,7 +23,19 @@ static thread_local std::string g_last_error;
 static thread_local bool g_time_kernel_only = false;  // cl_conv_time_kernel: skip operand preparation
 static bool g_no_pair = getenv("CL_NO_PAIR") != nullptr || getenv("CL_NO_CLUSTER") != nullptr;  // A/B: 1-SM MMA
 static bool g_no_basis = getenv("CL_NO_BASIS") != nullptr;      // A/B: disable the change of basis
-static bool g_basis_2d = getenv("CL_BASIS_2D") != nullptr;      // A/B: enable it for 2-D layers
+static bool g_basis_2d = getenv("CL_BASIS_2D") != nullptr;      // A/B: enable it for 2-D layers (all modes)
+static bool g_no_basis_2d = getenv("CL_NO_BASIS_2D") != nullptr;  // A/B: disable it for 2-D layers
+
+// The change of basis for a layer of spatial rank sk: always in 3-D; in 2-D
+// for the fp32 (int8) and 3xTF32 modes, where it measured faster (cfg3 block
+// 4.25 -> 3.16 ms / 3.97 -> 3.05 ms); the bf16 / tf32 2-D epilogues measured
+// slower with it (and bf16 loses the block's bf16 hand-off).
+static bool use_basis(int sk, int k, int precision) {
+  if (g_no_basis || sk != k) return false;
+  if (sk == 3) return true;
+  if (sk != 2 || g_no_basis_2d) return false;
+  return g_basis_2d || precision == CL_PREC_FP32 || precision == CL_PREC_3XTF32;
+}
 static bool g_no_halo = getenv("CL_NO_HALO") != nullptr;        // A/B: disable halo reuse of the A tile
 static bool g_no_halo_i8 = getenv("CL_NO_HALO_I8") != nullptr;  // A/B: halo off for the int8 mode only
 static bool g_no_tma_merge = getenv("CL_NO_TMA_MERGE") != nullptr;  // A/B: one TMA line per pixel
@@ -451,10 +463,9 @@ static int conv_create_impl(const int32_t* g, int k, int sk, int C_in, int C_out
     return fail(CL_ERR_UNSUPPORTED, "Unsupported", "fp32 mode supports K = d_filter^k * C_in * N_B <= 32000");
   }
   Basis bs{};
-  // M2(C) change of basis for 3-D layers (measured 2.0x on cfg5);
-  // the 2-D M2(R) basis is available (CL_BASIS_2D=1) but measured slower on
-  // cfg1/cfg3, whose per-tile MMA work is too small to hide its epilogue
-  if (sk == k && !g_no_basis && (sk == 3 || (sk == 2 && g_basis_2d))) find_basis(h->g, k, &bs);
+  // M2(C) change of basis for 3-D layers (measured 2.0x on cfg5),
+  // M2(R) for 2-D layers in the fp32 / 3xTF32 modes (see use_basis)
+  if (use_basis(sk, k, precision)) find_basis(h->g, k, &bs);
   if (!plan_conv(sk, h->nb, precision, C_in, C_out, d_out, d_filter, bs, h->plan)) {
     delete h;
     return fail(CL_ERR_UNSUPPORTED, "Unsupported", "no shared-memory plan fits this layer");
@@ -909,7 +920,7 @@ int cl_conv_plan_info(const int32_t* g, int k, int C_in, int C_out, int d_image,
   int gi[3] = {0, 0, 0};
   for (int i = 0; i < k; ++i) gi[i] = g[i];
   Basis bs{};
-  if (!g_no_basis && (k == 3 || (k == 2 && g_basis_2d))) find_basis(gi, k, &bs);
+  if (use_basis(k, k, precision)) find_basis(gi, k, &bs);
   ConvPlan pl;
   if (!plan_conv(k, 1 << k, precision, C_in, C_out, d_out, d_filter, bs, pl))
     return fail(CL_ERR_UNSUPPORTED, "Unsupported", "no shared-memory plan fits this layer");
