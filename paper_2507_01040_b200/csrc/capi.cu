@@ -735,8 +735,6 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.cs = pl.pair ? 2 : 1;
   p.num_tiles = ((p.num_m_tiles + p.cs - 1) / p.cs) * p.cs * p.n_ntiles;
   p.dbg_skip = getenv("CL_DBG_SKIP") ? atoi(getenv("CL_DBG_SKIP")) : 0;
-  p.sleep_prod = getenv("CL_SLEEP_PROD") ? (uint32_t)atoi(getenv("CL_SLEEP_PROD")) : 0u;
-  p.sleep_epi = getenv("CL_SLEEP_EPI") ? (uint32_t)atoi(getenv("CL_SLEEP_EPI")) : 0u;
   p.d_filter = h->d_filter;
   p.n_gs = pl.n_gs;
   p.gs = pl.gs;

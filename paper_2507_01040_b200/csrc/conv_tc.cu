@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           // one halo box per channel group, then the B stage of every tap
           for (int gsi = 0; gsi < p.n_gs; ++gsi) {
             const int g0 = gsi * p.gs;
-            mbar_wait_sleep(&hempty[hsl], hphase ^ 1, p.sleep_prod);
+            mbar_wait(&hempty[hsl], hphase ^ 1);
             uint8_t* hA = smem + (size_t)hsl * p.halo_slot;
             if (kAOwn) mbar_arrive_expect_tx(&hfull[hsl], p.halo_bytes * (uint32_t)p.n_tma_a);
             else if (arm) mbar_arrive_expect_tx(&hfull[hsl], (PAIR ? 2u : 1u) * p.halo_bytes * (uint32_t)p.n_tma_a);
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
             if (++hsl == HS) { hsl = 0; hphase ^= 1; }
             for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
               const int nq = min(p.tps, nQ - q0);
-              mbar_wait_sleep(&empty[stage], phase ^ 1, p.sleep_prod);
+              mbar_wait(&empty[stage], phase ^ 1);
               if (arm) mbar_arrive_expect_tx(&full[stage], tx_bytes * (uint32_t)nq);
               for (int i = 0; i < nq; ++i) load_b(nt, (q0 + i) * p.n_gs + gsi, (uint32_t)i * b_cta);
               if (++stage == S) { stage = 0; phase ^= 1; }
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           int qx, qy, qz;
           if (p.k == 3) { qz = q / (df * df); qy = (q / df) % df; qx = q % df; }
           else { qz = 0; qy = q / df; qx = q % df; }
-          mbar_wait_sleep(&empty[stage], phase ^ 1, p.sleep_prod);
+          mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = ring + (size_t)stage * p.stage_bytes;
           if (arm) mbar_arrive_expect_tx(&full[stage], tx_bytes);
           for (int d = 0; d < p.n_tma_a; ++d) {
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       }
       double a_sc = 0.0;
       if constexpr (kInt8) if (valid) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
-      mbar_wait_sleep(&tfull[acc], acc_phase, p.sleep_epi);
+      mbar_wait_sleep(&tfull[acc], acc_phase, 64);  // off the critical path: poll gently
       tc_fence_after();
       const long long dbg_t0 = p.dbg_acc ? clock64() : 0;
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)acc * slot_cols;

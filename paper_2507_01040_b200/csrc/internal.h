@@ -135,7 +135,6 @@ struct ConvKParams {
   uint32_t halo_bytes, halo_slot, ring_off;
   Basis bs;                   // change of basis: rows = (pixel, column), epilogue inverse transform
   long long num_m_tiles;      // real pixel tiles (tiles beyond are cluster padding)
-  uint32_t sleep_prod, sleep_epi;  // back-off (ns) of the producer / epilogue barrier polls
   int dbg_skip;
   unsigned long long* dbg_acc;  // timing instrumentation (CL_DBG_CLK): cycle counters, else null               // timing experiments only: bit 0 skips A loads, bit 1 skips B loads (garbage results)
   const uint8_t* b_img;
