@@ -288,6 +288,28 @@ __device__ __forceinline__ void mma_commit_cg2_g(uint32_t issue, uint64_t* bar) 
       : "memory");
 }
 
+// Split-descriptor variants: the 64-bit descriptors travel as (lo, hi) 32-bit
+// halves and are joined inside the asm, so the per-MMA address arithmetic is
+// 32-bit and stays on the uniform datapath (the high halves are loop constants).
+#define CL_MMA_SPLIT(NAME, KIND, GROUP)                                                                    \
+  __device__ __forceinline__ void NAME(uint32_t issue, uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi,     \
+                                       uint32_t b_lo, uint32_t b_hi, uint32_t idesc, uint32_t accumulate) { \
+    asm volatile(                                                                                         \
+        "{\n\t.reg .pred p, q;\n\t.reg .b64 da, db;\n\t"                                                  \
+        "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"                                                 \
+        "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\t"                                                 \
+        "@q tcgen05.mma.cta_group::" GROUP ".kind::" KIND " [%0], da, db, %5, p;\n}" ::"r"(d_tmem),        \
+        "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate), "r"(issue)                \
+        : "memory");                                                                                      \
+  }
+CL_MMA_SPLIT(mma_tf32_s, "tf32", "1")
+CL_MMA_SPLIT(mma_bf16_s, "f16", "1")
+CL_MMA_SPLIT(mma_i8_s, "i8", "1")
+CL_MMA_SPLIT(mma_tf32_cg2_s, "tf32", "2")
+CL_MMA_SPLIT(mma_bf16_cg2_s, "f16", "2")
+CL_MMA_SPLIT(mma_i8_cg2_s, "i8", "2")
+#undef CL_MMA_SPLIT
+
 // Commit the pair's MMAs to the barrier at the same offset in both CTAs.
 __device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
   asm volatile(

@@ -62,6 +62,20 @@ __device__ __forceinline__ void mma_mode_g(uint32_t issue, uint32_t d, uint64_t 
     if constexpr (PAIR) mma_tf32_cg2_g(issue, d, a, b, idesc, acc); else mma_tf32_g(issue, d, a, b, idesc, acc);
   }
 }
+template <int PREC, bool PAIR>
+__device__ __forceinline__ void mma_mode_s(uint32_t issue, uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo,
+                                           uint32_t bhi, uint32_t idesc, uint32_t acc) {
+  if constexpr (PREC == kPrecFp32) {
+    if constexpr (PAIR) mma_i8_cg2_s(issue, d, alo, ahi, blo, bhi, idesc, acc);
+    else mma_i8_s(issue, d, alo, ahi, blo, bhi, idesc, acc);
+  } else if constexpr (PREC == kPrecBf16) {
+    if constexpr (PAIR) mma_bf16_cg2_s(issue, d, alo, ahi, blo, bhi, idesc, acc);
+    else mma_bf16_s(issue, d, alo, ahi, blo, bhi, idesc, acc);
+  } else {
+    if constexpr (PAIR) mma_tf32_cg2_s(issue, d, alo, ahi, blo, bhi, idesc, acc);
+    else mma_tf32_s(issue, d, alo, ahi, blo, bhi, idesc, acc);
+  }
+}
 template <bool PAIR>
 __device__ __forceinline__ void commit_g(uint32_t issue, uint64_t* bar) {
   if constexpr (PAIR) mma_commit_cg2_g(issue, bar); else mma_commit_g(issue, bar);
@@ -379,13 +393,16 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               const uint32_t sB4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
               {
                 // converged issue (every lane computes the warp-uniform descriptors,
-                // one lane's guard is set): the descriptors stay in uniform registers
-                uint64_t a_tap = h_tmpl + (uint64_t)(hA4 + tap4);
-                uint64_t b_cur = b_tmpl + (uint64_t)sB4;
+                // one lane's guard is set); descriptors as 32-bit low halves + constant
+                // high halves, so the per-MMA arithmetic is 32-bit uniform adds
+                const uint32_t a_hi = (uint32_t)(h_tmpl >> 32), b_hi = (uint32_t)(b_tmpl >> 32);
+                uint32_t a_tap = (uint32_t)h_tmpl + hA4 + tap4;
+                uint32_t b_cur = (uint32_t)b_tmpl + sB4;
+                const uint32_t a_ks = (uint32_t)a_kstep, b_ks = b_ks4, a_img = h_img4, b_img = b_img4;
                 uint32_t accf = (gsi == 0 && q0 == 0) ? 0u : 1u;
                 int x = qx, y = qy;
                 for (int i = 0; i < nq; ++i) {
-                  uint64_t a0 = a_tap, b0 = b_cur;
+                  uint32_t a0 = a_tap, b0 = b_cur;
                   for (int s = 0; s < p.ks; ++s) {
                     if constexpr (kInt8) {
 #pragma unroll
@@ -394,20 +411,20 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
 #pragma unroll
                         for (int ii = i0; ii <= L && ii < kDigitsA; ++ii) {
                           const int j = L - ii;
-                          mma_mode_g<PREC, PAIR>(issuer, d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(ii * h_img4),
-                                                 b0 + (uint64_t)(j * b_img4), idesc, ii == i0 ? accf : 1u);
+                          mma_mode_s<PREC, PAIR>(issuer, d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint32_t)ii * a_img,
+                                                 a_hi, b0 + (uint32_t)j * b_img, b_hi, idesc, ii == i0 ? accf : 1u);
                         }
                       }
                     } else if constexpr (kSplit) {
-                      mma_mode_g<kPrecTf32, PAIR>(issuer, d_tmem, a0 + h_img4, b0, idesc, accf);  // A_lo * B_hi
-                      mma_mode_g<kPrecTf32, PAIR>(issuer, d_tmem, a0, b0 + b_img4, idesc, 1u);   // A_hi * B_lo
-                      mma_mode_g<kPrecTf32, PAIR>(issuer, d_tmem, a0, b0, idesc, 1u);            // A_hi * B_hi
+                      mma_mode_s<kPrecTf32, PAIR>(issuer, d_tmem, a0 + a_img, a_hi, b0, b_hi, idesc, accf);  // A_lo * B_hi
+                      mma_mode_s<kPrecTf32, PAIR>(issuer, d_tmem, a0, a_hi, b0 + b_img, b_hi, idesc, 1u);   // A_hi * B_lo
+                      mma_mode_s<kPrecTf32, PAIR>(issuer, d_tmem, a0, a_hi, b0, b_hi, idesc, 1u);           // A_hi * B_hi
                     } else {
-                      mma_mode_g<PREC, PAIR>(issuer, d_tmem, a0, b0, idesc, accf);
+                      mma_mode_s<PREC, PAIR>(issuer, d_tmem, a0, a_hi, b0, b_hi, idesc, accf);
                     }
                     accf = 1u;
-                    a0 += a_kstep;
-                    b0 += b_ks4;
+                    a0 += a_ks;
+                    b0 += b_ks;
                   }
                   b_cur += b_cta4;
                   a_tap += h_dx;
