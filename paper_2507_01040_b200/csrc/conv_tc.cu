@@ -341,9 +341,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               tc_fence_after();
               const uint32_t sB4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
               if (elect_one()) {
+                const uint32_t a_hi = (uint32_t)(h_tmpl >> 32), b_hi = (uint32_t)(b_tmpl >> 32);
+                uint32_t a0 = (uint32_t)h_tmpl + hA4 + tap4, b0 = (uint32_t)b_tmpl + sB4;
                 for (int s = 0; s < p.ks; ++s) {
-                  const uint64_t a0 = h_tmpl + (uint64_t)(hA4 + tap4 + (uint32_t)s * 2u * h_plane4);
-                  const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)s * b_ks4);
                   const uint32_t first = (gsi == 0 && q == 0 && s == 0) ? 1u : 0u;
                   if constexpr (kInt8) {
   #pragma unroll
@@ -352,19 +352,19 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   #pragma unroll
                       for (int i = i0; i <= L && i < kDigitsA; ++i) {
                         const int j = L - i;
-                        mma_mode<PREC, PAIR>(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * h_img4),
-                                             b0 + (uint64_t)(j * b_img4), idesc, (first && i == i0) ? 0u : 1u);
+                        mma_mode_s<PREC, PAIR>(1u, d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint32_t)i * h_img4, a_hi,
+                                               b0 + (uint32_t)j * b_img4, b_hi, idesc, (first && i == i0) ? 0u : 1u);
                       }
                     }
                   } else if constexpr (kSplit) {
-                    mma_mode<kPrecTf32, PAIR>(d_tmem, a0 + h_img4, b0, idesc, first ? 0u : 1u);  // A_lo * B_hi
-                    mma_mode<kPrecTf32, PAIR>(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
-                    mma_mode<kPrecTf32, PAIR>(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
-                  } else if constexpr (PREC == kPrecTf32) {
-                    mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
-                  } else if constexpr (PREC == kPrecBf16) {
-                    mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+                    mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0 + h_img4, a_hi, b0, b_hi, idesc, first ? 0u : 1u);
+                    mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0, a_hi, b0 + b_img4, b_hi, idesc, 1u);
+                    mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, 1u);
+                  } else {
+                    mma_mode_s<PREC, PAIR>(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, first ? 0u : 1u);
                   }
+                  a0 += (uint32_t)a_kstep;
+                  b0 += b_ks4;
                 }
                 if constexpr (PAIR) {
                   mma_commit_cg2(&empty[stage]);
