@@ -74,6 +74,12 @@ def mode_peak(precision, peaks, sustained=True):
     return val, basis + (" sustained" if sustained else " burst")
 
 
+# Nominal dense tensor-core peaks of a B200 at its 1965 MHz boost clock (NVIDIA's
+# figures without 2:4 sparsity), per mode in algorithmic-equivalent TFLOP/s before
+# the change-of-basis factor: bf16 2250, tf32 1125, int8 4500 TOPS / 10, tf32 / 3.
+NOMINAL_MODE_PEAK = {"bf16": 2250.0, "tf32": 1125.0, "3xtf32": 375.0, "fp32": 450.0}
+
+
 def ncu_traffic(spec, prec, batch):
     """roofline.traffic: DRAM bytes of one conv launch from a committed ncu --set full capture
     (profiles/ncu_traffic.json), when one exists for this config / precision / batch."""
@@ -465,6 +471,7 @@ def run_ours(args):
                          "frac_of_burst": achieved / peak_burst,
                          "executed_tflops": achieved * gemm_ratio, "executed_peak": exec_peak,
                          "executed_frac": achieved * gemm_ratio / exec_peak,
+                         "executed_frac_of_nominal": achieved * gemm_ratio / NOMINAL_MODE_PEAK[prec],
                          "kernel_share_of_step": conv_share},
             "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": cpu,
             "clocks": clk.summary(),
