@@ -343,7 +343,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               if (elect_one()) {
                 const uint32_t a_hi = (uint32_t)(h_tmpl >> 32), b_hi = (uint32_t)(b_tmpl >> 32);
                 uint32_t a0 = (uint32_t)h_tmpl + hA4 + tap4, b0 = (uint32_t)b_tmpl + sB4;
-                for (int s = 0; s < p.ks; ++s) {
+                #pragma unroll
+                for (int s = 0; s < 8; ++s) {  // ks <= 8, unrolled: constant per-step offsets
+                  if (s >= p.ks) break;
                   const uint32_t first = (gsi == 0 && q == 0 && s == 0) ? 1u : 0u;
                   if constexpr (kInt8) {
   #pragma unroll
@@ -403,7 +405,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 int x = qx, y = qy;
                 for (int i = 0; i < nq; ++i) {
                   uint32_t a0 = a_tap, b0 = b_cur;
-                  for (int s = 0; s < p.ks; ++s) {
+                  #pragma unroll
+                  for (int s = 0; s < 8; ++s) {  // ks <= 8, unrolled: constant per-step offsets
+                    if (s >= p.ks) break;
                     if constexpr (kInt8) {
 #pragma unroll
                       for (int L = 0; L < kLevels; ++L) {
