@@ -403,7 +403,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 const uint32_t a_ks = (uint32_t)a_kstep, b_ks = b_ks4, a_img = h_img4, b_img = b_img4;
                 uint32_t accf = (gsi == 0 && q0 == 0) ? 0u : 1u;
                 int x = qx, y = qy;
-                for (int i = 0; i < nq; ++i) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {  // taps of this stage (tps <= 4)
+                  if (i >= nq) break;
                   uint32_t a0 = a_tap, b0 = b_cur;
                   #pragma unroll
                   for (int s = 0; s < 8; ++s) {  // ks <= 8, unrolled: constant per-step offsets
