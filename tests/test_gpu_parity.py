@@ -357,3 +357,30 @@ def test_linear_shapes(g, B, ci, co):
     assert_conv_close(y, O.linear_ref(x, w, b, g), "fp32")
     yh = M.linear_forward(x, layer)  # host path
     np.testing.assert_array_equal(yh, y)
+
+
+# ---- seeded shape fuzz over all signatures, precisions, paddings ----------------
+
+def _fuzz_cases(n=48, seed=2507):
+    rng = np.random.default_rng(seed)
+    sigs = O.all_signatures(3)
+    out = []
+    for _ in range(n):
+        g = sigs[rng.integers(len(sigs))]
+        k = len(g)
+        df = int(rng.integers(1, 5 if k == 3 else 6))
+        padding = "same" if (df % 2 == 1 and rng.random() < 0.5) else "valid"
+        d = int(rng.integers(df, {1: 70, 2: 20, 3: 9}[k]))
+        out.append((g, int(rng.integers(1, 4)), int(rng.integers(1, 12)), int(rng.integers(1, 12)), d, df, padding,
+                    ["fp32", "3xtf32", "tf32", "bf16"][int(rng.integers(4))]))
+    return out
+
+
+@pytest.mark.parametrize("n,case", list(enumerate(_fuzz_cases())),
+                         ids=lambda c: f"{c[0]}-B{c[1]}-{c[2]}x{c[3]}-d{c[4]}-f{c[5]}-{c[6]}-{c[7]}" if isinstance(c, tuple) else str(c))
+def test_conv_fuzz(n, case):
+    g, B, ci, co, d, df, padding, prec = case
+    rng = np.random.default_rng(1000 + n)  # deterministic per case
+    x, f, b, layer, pad = make_conv(rng, g, B, ci, co, d, df, prec, padding)
+    y = run_dev(M.conv_forward, x, layer)
+    assert_conv_close(y, O.conv_ref(x, f, b, g, d, df, pad), prec, K=ci * (1 << len(g)) * df ** len(g))
