@@ -384,3 +384,40 @@ def test_conv_fuzz(n, case):
     x, f, b, layer, pad = make_conv(rng, g, B, ci, co, d, df, prec, padding)
     y = run_dev(M.conv_forward, x, layer)
     assert_conv_close(y, O.conv_ref(x, f, b, g, d, df, pad), prec, K=ci * (1 << len(g)) * df ** len(g))
+
+
+def _block_fuzz_cases(n=16, seed=107):
+    rng = np.random.default_rng(seed)
+    sigs = [g for g in O.all_signatures(3) if len(g) >= 2]
+    out = []
+    for _ in range(n):
+        g = sigs[rng.integers(len(sigs))]
+        out.append((g, int(rng.integers(0, 3)), ["same", "valid"][int(rng.integers(2))], bool(rng.integers(2)),
+                    int(rng.integers(1, 4)), int(rng.integers(2, 10)),
+                    ["fp32", "3xtf32", "tf32", "bf16"][int(rng.integers(4))]))
+    return out
+
+
+@pytest.mark.parametrize("n,case", list(enumerate(_block_fuzz_cases())),
+                         ids=lambda c: "-".join(str(v) for v in c) if isinstance(c, tuple) else str(c))
+def test_block_fuzz(n, case):
+    """Blocks over random signatures (incl. degenerate and change-of-basis ones),
+    activation modes, padding, residual on/off and all four precisions."""
+    g, mode, padding, residual, B, C, prec = case  # valid + residual: the input is cropped to the output window
+    rng = np.random.default_rng(2000 + n)
+    k = len(g)
+    nb = 1 << k
+    d = {2: 11, 3: 7}[k]
+    fan = C * nb * 3 ** k
+    f1 = rng.uniform(-1, 1, (nb, C, C, 3 ** k)).astype(np.float32) / np.float32(np.sqrt(fan))
+    f2 = rng.uniform(-1, 1, (nb, C, C, 3 ** k)).astype(np.float32) / np.float32(np.sqrt(fan))
+    b1 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
+    b2 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
+    aw = rng.uniform(-0.5, 0.5, (C, nb)).astype(np.float32) if mode == 0 else None
+    ab = (rng.standard_normal(C) * 0.1).astype(np.float32) if mode == 0 else None
+    x = rng.standard_normal((B, C, d ** k, nb)).astype(np.float32)
+    blk = M.make_basic_block(M.Signature(g), B, C, C, C, d, f1, b1, mode, f2, b2, act_weight=aw, act_bias=ab,
+                             padding=padding, residual=residual, precision=prec)
+    y = run_dev(M.block_forward, x, blk)
+    ref = O.block_ref(x, g, d, f1, b1, mode, tuple(range(nb)), aw, ab, f2, b2, padding=padding, residual=residual)
+    assert_conv_close(y, ref, prec, K=C * nb * 3 ** k)
