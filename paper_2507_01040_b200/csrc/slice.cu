@@ -62,7 +62,7 @@ cudaError_t launch_sample_absmax(const float* x, long long B, long long per_samp
 // differences of blade pairs (2m, 2m+1): x' = (u0, -u3, v2, v1, u2, -u1, v0, v3)
 // with u_m = X_2m + X_2m+1, v_m = X_2m - X_2m+1 (8 adds instead of 64 multiply-adds).
 template <int NB, bool BASIS, bool FIXED = false>
-__global__ void __launch_bounds__(256) slice_input_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(256, FIXED ? 3 : 1) slice_input_kernel(const float* __restrict__ x,
                                                           const unsigned* __restrict__ amax,
                                                           int8_t* __restrict__ out, float* __restrict__ scale,
                                                           long long B, int C, long long P, int G, Basis bs) {
