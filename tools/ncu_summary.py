@@ -1,6 +1,6 @@
 """Summarise .ncu-rep captures into the JSON kept under profiles/.
 
-    python tools/ncu_summary.py out.json name=gpurun_out/x.ncu-rep [name2=...]
+    python tools/ncu_summary.py out.json name=gpurun_out/x.ncu-rep [name2=gpurun_out/ncu/y.raw.csv ...]
 """
 import csv
 import io
@@ -12,6 +12,10 @@ KEYS = [
     "gpu__time_duration.sum",
     "dram__bytes_read.sum",
     "dram__bytes_write.sum",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "dram__bytes.sum.per_second",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
     "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -28,7 +32,10 @@ KEYS = [
 
 
 def summarise(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # a `--page raw --csv` export made on the GPU box (tools/prof_all.sh)
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     head, units, vals = rows[0], rows[1], rows[2]
     res = {"kernel": vals[head.index("Kernel Name")]}
