@@ -5,11 +5,12 @@ basic-block inference: a drop-in for the layer API of the reference
 
 from .activation import (ActivationConfig, AggMode, activation_flops, activation_forward,
                          make_activation_config)
-from .algebra import (Signature, all_valid_signatures, blade_product, product_table,
-                      schedule_flop_count, schedule_terms, validate_signature)
+from .algebra import (BladeProductTable, Signature, all_valid_signatures, blade_product, cayley_tensor,
+                      product_table, schedule_flop_count, schedule_terms, validate_signature)
 from .block import BasicBlock, block_forward, make_basic_block
 from .conv import ConvLayer, build_expanded_kernel, conv_flops, conv_forward, make_conv_layer
-from .layout import Dims, LayoutTag, read_tensor, write_tensor
+from .layout import Dims, LayoutTag, gather_index_table, read_tensor, spatial_coords, write_tensor
+from .specialize import FmaTerm, OpSchedule, build_schedule, schedule_for
 from .linear import LinearLayer, linear_flops, linear_forward, make_linear_layer
 from . import errors
 

@@ -55,9 +55,23 @@ def blade_product(i_mask: int, j_mask: int, sig: Signature) -> tuple[int, int]:
     return t.value, c.value
 
 
+@dataclass(frozen=True, eq=False)
+class BladeProductTable:
+    """Dense N_B x N_B blade product table (algebra.py:100-111): target[i, j] =
+    i xor j, coeff[i, j] in {-1, 0, +1}; read-only arrays. Also unpacks as
+    `target, coeff = table`."""
+
+    sig: Signature
+    target: np.ndarray
+    coeff: np.ndarray
+
+    def __iter__(self):
+        return iter((self.target, self.coeff))
+
+
 @lru_cache(maxsize=None)
-def product_table(sig: Signature) -> tuple[np.ndarray, np.ndarray]:
-    """(target, coeff) int64 tables (algebra.py:116-129)."""
+def product_table(sig: Signature) -> BladeProductTable:
+    """Cached blade product table from the C-ABI's integer code (algebra.py:114-129)."""
     nb = sig.n_blades
     tgt = np.empty((nb, nb), np.int64)
     cof = np.empty((nb, nb), np.int64)
@@ -66,7 +80,20 @@ def product_table(sig: Signature) -> tuple[np.ndarray, np.ndarray]:
             tgt[i, j], cof[i, j] = blade_product(i, j, sig)
     tgt.flags.writeable = False
     cof.flags.writeable = False
-    return tgt, cof
+    return BladeProductTable(sig, tgt, cof)
+
+
+@lru_cache(maxsize=None)
+def cayley_tensor(sig: Signature) -> np.ndarray:
+    """Structure tensor C[i, j, t] = coeff of blade t in e_I e_J (algebra.py:132-145);
+    fp64, read-only. The device builds the expanded filter from the same table."""
+    table = product_table(sig)
+    nb = sig.n_blades
+    cay = np.zeros((nb, nb, nb), dtype=np.float64)
+    ii, jj = np.meshgrid(np.arange(nb), np.arange(nb), indexing="ij")
+    cay[ii, jj, table.target] = table.coeff
+    cay.flags.writeable = False
+    return cay
 
 
 def schedule_terms(sig: Signature) -> int:
@@ -77,9 +104,13 @@ def schedule_terms(sig: Signature) -> int:
     return int(n)
 
 
-def schedule_flop_count(sig: Signature) -> int:
-    """FLOPs of one geometric product (specialize.py:72-74)."""
-    return 2 * schedule_terms(sig)
+def schedule_flop_count(sig_or_schedule) -> int:
+    """FLOPs of one geometric product (specialize.py:72-74). Takes the
+    reference's OpSchedule (`specialize.schedule_for(sig)`) or a Signature."""
+    terms = getattr(sig_or_schedule, "terms", None)
+    if terms is not None:
+        return 2 * len(terms)
+    return 2 * schedule_terms(sig_or_schedule)
 
 
 def all_valid_signatures(k_max: int = 3) -> list[Signature]:

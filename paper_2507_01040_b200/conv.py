@@ -44,6 +44,23 @@ class ConvLayer:
     _handles: dict = field(default_factory=dict, repr=False)
 
     @property
+    def L(self) -> int:
+        """Reference CPU packing width W*U (conv.py:95-97); unused by the B200 path."""
+        return self.W * self.U
+
+    @property
+    def schedule(self):
+        """The signature's FMA schedule (conv.py:131: schedule_for(sig))."""
+        from .specialize import schedule_for
+        return schedule_for(self.sig)
+
+    @property
+    def in_index(self) -> np.ndarray:
+        """Valid-conv gather table (conv.py:136, layout.py:137-146), built on demand."""
+        from .layout import gather_index_table
+        return gather_index_table(self.dims)
+
+    @property
     def pad(self) -> int:
         return (self.dims.d_filter - 1) // 2 if self.padding == "same" else 0
 
@@ -165,11 +182,13 @@ def build_expanded_kernel(layer: ConvLayer):
 
 
 def conv_flops(dims: Dims, sig_or_layer, padding: str = "valid") -> int:
-    """B * C_out * d_out^k * (C_in * Q * 2*terms + N_B) (conv.py:384-387)."""
-    sig = sig_or_layer.sig if isinstance(sig_or_layer, ConvLayer) else getattr(sig_or_layer, "sig", sig_or_layer)
+    """B * C_out * d_out^k * (C_in * Q * 2*terms + N_B) (conv.py:384-387). The
+    second argument is the reference's OpSchedule (`layer.schedule`), a
+    Signature, or a ConvLayer (whose padding then applies)."""
     if isinstance(sig_or_layer, ConvLayer):
         padding = sig_or_layer.padding
+        sig_or_layer = sig_or_layer.sig
     pad = (dims.d_filter - 1) // 2 if padding == "same" else 0
     d_out = dims.d_image + 2 * pad - dims.d_filter + 1
-    per_position = dims.C_in * dims.filter_positions * schedule_flop_count(sig)
+    per_position = dims.C_in * dims.filter_positions * schedule_flop_count(sig_or_layer)
     return dims.B * dims.C_out * d_out ** dims.k * (per_position + dims.n_blades)

@@ -243,3 +243,47 @@ def test_planner_variants():
     # fp32 K limit (4 s32 levels): Unsupported beyond K = 32000 is checked at create; the planner still plans
     with pytest.raises(E.ConfigInvalid):
         plan_info((1, 1), 4, 4, 8, 3, 0, 7)
+
+
+# ---- reference-API host helpers ----------------
+
+def test_schedule_for_matches_reference_golden(golden):
+    """specialize.schedule_for (specialize.py:49-69) term by term, all 36 signatures."""
+    for s in golden["sig_list"]:
+        g = tuple(int(v) for v in str(s).split("_"))
+        sch = M.schedule_for(M.Signature(g))
+        got = np.array([[t.out_blade, t.a_blade, t.b_blade, int(t.negate)] for t in sch.terms], np.int64)
+        np.testing.assert_array_equal(got, golden[f"sched_{s}"])
+        assert M.schedule_flop_count(sch) == M.schedule_flop_count(M.Signature(g)) == 2 * len(sch)
+
+
+def test_product_table_object_and_cayley():
+    sig = M.Signature((1, -1, 0))
+    t = M.product_table(sig)
+    assert isinstance(t, M.BladeProductTable) and t.sig == sig
+    tgt, cof = t  # tuple unpacking still works
+    assert tgt is t.target and cof is t.coeff and not t.coeff.flags.writeable
+    np.testing.assert_array_equal(M.cayley_tensor(sig), O.cayley(sig.g))
+
+
+def test_gather_index_table_golden(golden):
+    for n in range(10):
+        B, ci, co, di, df, k = (int(v) for v in golden[f"conv{n}_dims"])
+        dims = M.Dims(B, ci, co, di, df, k)
+        np.testing.assert_array_equal(M.gather_index_table(dims), golden[f"conv{n}_in_index"])
+    # 2-D, d_image 4, 3x3 filter: output (0,0) reads rows 0..2 of a 4-wide image
+    t = M.gather_index_table(M.Dims(1, 1, 1, 4, 3, 2))
+    assert t.shape == (4, 9) and list(t[0]) == [0, 1, 2, 4, 5, 6, 8, 9, 10]
+
+
+def test_conv_layer_reference_fields():
+    rng = np.random.default_rng(3)
+    dims = M.Dims(2, 3, 4, 6, 3, 2)
+    f = rng.standard_normal(dims.filters_shape()).astype(np.float32)
+    b = rng.standard_normal(dims.bias_shape()).astype(np.float32)
+    layer = M.make_conv_layer(dims, M.Signature((0, 1)), f, b, W=4, U=2)
+    assert layer.L == 8 and len(layer.schedule) == 12
+    np.testing.assert_array_equal(layer.in_index, O.gather_index_table(6, 3, 2))
+    # the reference call shape conv_flops(dims, layer.schedule) (conv.py:384-387)
+    assert M.conv_flops(dims, layer.schedule) == M.conv_flops(dims, layer) == \
+        O.conv_flops(2, 3, 4, 4, 3, (0, 1))
