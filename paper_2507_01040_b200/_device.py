@@ -2,6 +2,7 @@
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 
 import numpy as np
@@ -46,14 +47,36 @@ def is_cpu_tensor(x) -> bool:
     return isinstance(x, torch.Tensor) and not x.is_cuda
 
 
+_cuda_checked = False
+
+
 def current_device() -> int:
-    torch = _lib.require_cuda()
-    return torch.cuda.current_device()
+    global _cuda_checked
+    if not _cuda_checked:
+        _lib.require_cuda()  # fail loudly without a GPU (no CPU fallback)
+        _cuda_checked = True
+    return torch_mod().cuda.current_device()
 
 
 def stream_ptr(device=None) -> int:
+    """cudaStream_t of torch's current stream (the raw query: a few hundred ns
+    instead of building a Stream object per call)."""
     torch = torch_mod()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return raw(torch.cuda.current_device() if device is None else torch.device(device).index)
     return torch.cuda.current_stream(device).cuda_stream
+
+
+_NULL_CTX = contextlib.nullcontext()
+
+
+def on_device(device):
+    """torch.cuda.device(device), or a no-op when it is already current."""
+    torch = torch_mod()
+    if device.index is None or device.index == torch.cuda.current_device():
+        return _NULL_CTX
+    return torch.cuda.device(device)
 
 
 def to_device_f32(arr, device=None):

@@ -116,7 +116,7 @@ def activation_forward(x, cfg: ActivationConfig, variant: str = "b200", out=None
     lib = _lib.load()
     if _device.is_cuda_tensor(x):
         torch = _device.torch_mod()
-        with torch.cuda.device(x.device):
+        with _device.on_device(x.device):
             xc = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
             y = _out(out, tuple(xc.shape), x.device)
             _lib.check(lib.cl_act_forward(C.c_void_p(cfg.handle(C_)), C.c_void_p(xc.data_ptr()),

@@ -90,7 +90,7 @@ def block_forward(x, blk: BasicBlock, chunk: int = 0, out=None):
     B = blk.B
     if _device.is_cuda_tensor(x):
         torch = _device.torch_mod()
-        with torch.cuda.device(x.device):
+        with _device.on_device(x.device):
             xc = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
             y = _out(out, blk.output_shape(), x.device)
             _lib.check(lib.cl_block_forward(C.c_void_p(blk.handle()), C.c_void_p(xc.data_ptr()),

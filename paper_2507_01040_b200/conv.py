@@ -148,7 +148,7 @@ def conv_forward(x, layer: ConvLayer, variant: str = "b200", out=None):
     B = layer.dims.B
     if _device.is_cuda_tensor(x):
         torch = _device.torch_mod()
-        with torch.cuda.device(x.device):
+        with _device.on_device(x.device):
             xc = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
             y = _out(out, layer.output_shape(B), x.device)
             _lib.check(lib.cl_conv_forward(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),

@@ -47,6 +47,52 @@ static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
+namespace {
+struct KernKey {
+  const void* k;
+  int dev;
+  long long a;
+  bool operator==(const KernKey& o) const { return k == o.k && dev == o.dev && a == o.a; }
+};
+std::mutex g_kern_m;
+std::vector<std::pair<KernKey, int>> g_kern_cache;  // a handful of entries: linear scan
+}  // namespace
+
+int resident_blocks_per_sm(const void* kern, int threads, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const KernKey key{kern, dev, ((long long)threads << 32) | (long long)smem};
+  {
+    std::lock_guard<std::mutex> lk(g_kern_m);
+    for (auto& e : g_kern_cache)
+      if (e.first == key) return e.second;
+  }
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem);
+  if (n < 1) n = 1;
+  std::lock_guard<std::mutex> lk(g_kern_m);
+  g_kern_cache.push_back({key, n});
+  return n;
+}
+
+cudaError_t ensure_smem_optin(const void* kern, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const KernKey key{kern, dev, -1};
+  {
+    std::lock_guard<std::mutex> lk(g_kern_m);
+    for (auto& e : g_kern_cache)
+      if (e.first == key && e.second >= bytes) return cudaSuccess;
+  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_kern_m);
+  for (auto& en : g_kern_cache)
+    if (en.first == key) { en.second = std::max(en.second, bytes); return cudaSuccess; }
+  g_kern_cache.push_back({key, bytes});
+  return cudaSuccess;
+}
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -342,6 +388,8 @@ struct cl_conv {
   uint8_t* img = nullptr;    // tensor-core operand images
   float* w_scale = nullptr;  // kPrecFp32: per-column digit scales
   ConvPlan plan;
+  uint64_t uid = 0;        // unique per handle (keys the per-thread input-map cache)
+  alignas(64) CUtensorMap bmap;  // 2-SM pair: the filter images as 512-byte rows (encoded once at create)
   mutable WsCache ws;
   mutable HostPipe host;
 };
@@ -490,6 +538,27 @@ static int conv_create_impl(const int32_t* g, int k, int sk, int C_in, int C_out
       (e = cudaStreamSynchronize(s)) != cudaSuccess) {
     cl_conv_destroy(h);
     return cuda_fail(e, "cl_conv_create");
+  }
+  static std::atomic<uint64_t> next_uid{1};
+  h->uid = next_uid.fetch_add(1);
+  if (h->plan.pair) {
+    // the filter images as 512-byte rows; each CTA of a pair loads its half
+    // of a stage as one (64 x 8 B, half / 512) box
+    const ConvPlan& pl = h->plan;
+    auto enc = get_encode();
+    const cuuint64_t total = (cuuint64_t)pl.n_ntiles * pl.k_iters * pl.b_bytes;
+    cuuint64_t bd[2] = {64, total / 512};
+    cuuint64_t bst[1] = {512};
+    cuuint32_t bbox[2] = {64, (cuuint32_t)(pl.b_bytes / 2 / 512)};
+    cuuint32_t bes[2] = {1, 1};
+    CUresult r = enc ? enc(&h->bmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, h->img, bd, bst, bbox, bes,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
+                     : CUDA_ERROR_NOT_SUPPORTED;
+    if (r != CUDA_SUCCESS) {
+      cl_conv_destroy(h);
+      return fail(CL_ERR_CUDA, "CudaError", "filter tensor map: " + std::to_string((int)r));
+    }
   }
   *out = h;
   return CL_OK;
@@ -709,8 +778,30 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
       src = ws;
     }
   }
-  CUtensorMap map;
-  if (int st = encode_input_map(h, src, B, &map)) return st;
+  // per-thread cache of the last input maps (a layer is usually called with the
+  // same workspace / input buffers; encoding costs host microseconds)
+  struct MapEnt {
+    uint64_t uid;
+    const void* src;
+    long long B;
+    alignas(64) CUtensorMap map;
+  };
+  static thread_local MapEnt mcache[4] = {};
+  static thread_local int mnext = 0;
+  const CUtensorMap* mp = nullptr;
+  for (auto& me : mcache)
+    if (me.uid == h->uid && me.src == src && me.B == B) { mp = &me.map; break; }
+  if (!mp) {
+    MapEnt& me = mcache[mnext];
+    mnext = (mnext + 1) & 3;
+    me.uid = 0;
+    if (int st = encode_input_map(h, src, B, &me.map)) return st;
+    me.uid = h->uid;
+    me.src = src;
+    me.B = B;
+    mp = &me.map;
+  }
+  const CUtensorMap& map = *mp;
   ConvKParams p{};
   p.B = (int)B;
   p.k = h->sk;
@@ -734,7 +825,8 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.pair = pl.pair;
   p.cs = pl.pair ? 2 : 1;
   p.num_tiles = ((p.num_m_tiles + p.cs - 1) / p.cs) * p.cs * p.n_ntiles;
-  p.dbg_skip = getenv("CL_DBG_SKIP") ? atoi(getenv("CL_DBG_SKIP")) : 0;
+  static const int dbg_skip = getenv("CL_DBG_SKIP") ? atoi(getenv("CL_DBG_SKIP")) : 0;
+  p.dbg_skip = dbg_skip;
   p.d_filter = h->d_filter;
   p.n_gs = pl.n_gs;
   p.gs = pl.gs;
@@ -782,23 +874,10 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.amax_out = epi.amax_out;
   int grid = (int)std::min<long long>(p.num_tiles, (long long)num_sms());
   grid -= grid % p.cs;
-  CUtensorMap bmap = map;  // unused unless paired
-  if (pl.pair) {
-    // the filter images as 512-byte rows; each CTA of a pair loads its half
-    // of a stage as one (64 x 8 B, half / 512) box
-    auto enc = get_encode();
-    const cuuint64_t total = (cuuint64_t)pl.n_ntiles * pl.k_iters * pl.b_bytes;
-    cuuint64_t bd[2] = {64, total / 512};
-    cuuint64_t bst[1] = {512};
-    cuuint32_t bbox[2] = {64, (cuuint32_t)(pl.b_bytes / 2 / 512)};
-    cuuint32_t bes[2] = {1, 1};
-    CUresult r = enc(&bmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint8_t*>(h->img), bd, bst, bbox, bes,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(CL_ERR_CUDA, "CudaError", "filter tensor map: " + std::to_string((int)r));
-  }
+  const CUtensorMap& bmap = pl.pair ? h->bmap : map;  // unused unless paired
   static unsigned long long* dbg_acc = nullptr;  // CL_DBG_CLK: per-launch epilogue / MMA-wait cycle report
-  if (getenv("CL_DBG_CLK")) {
+  static const bool dbg_clk = getenv("CL_DBG_CLK") != nullptr;
+  if (dbg_clk) {
     if (!dbg_acc) cudaMalloc(&dbg_acc, 8 * sizeof(unsigned long long));
     cudaMemsetAsync(dbg_acc, 0, 8 * sizeof(unsigned long long), s);
     p.dbg_acc = dbg_acc;

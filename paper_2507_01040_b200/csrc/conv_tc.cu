@@ -1017,8 +1017,7 @@ template <int NB, int PREC, bool PAIR, int BCLS = 0>
 static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const CUtensorMap& bmap,
                             const ConvKParams& p, int grid, cudaStream_t s) {
   auto kfn = conv_tc_kernel<NB, PREC, PAIR, BCLS>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)plan.smem_bytes);
+  cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(kfn), (int)plan.smem_bytes);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
@@ -1164,11 +1163,10 @@ template <int NB, int ESIZE, bool BASIS>
 static void launch_pack_t(const float* x, void* out, long long B, int C, long long P, int G, const Basis& bs,
                           cudaStream_t s) {
   auto kern = pack_rows_kernel<NB, ESIZE, BASIS>;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+  const int per_sm = resident_blocks_per_sm(reinterpret_cast<const void*>(kern), 256, 0);
   const long long total = B * G * P;
   long long blocks = (total + 255) / 256;
-  const long long cap = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
+  const long long cap = (long long)num_sms() * per_sm;
   if (blocks > cap) blocks = cap;
   kern<<<(unsigned)blocks, 256, 0, s>>>(x, reinterpret_cast<uint4*>(out), B, C, P, G, bs);
 }

@@ -187,5 +187,10 @@ cudaError_t launch_weight_colscale(const int* g, const ConvPlan& pl, const float
 
 int num_sms();
 void count_launch(int n = 1);
+// Host-side launch helpers, cached per (kernel, device): resident blocks per SM
+// of a kernel (the occupancy calculator costs microseconds per call) and the
+// dynamic shared-memory opt-in (cudaFuncSetAttribute once, not per launch).
+int resident_blocks_per_sm(const void* kern, int threads, size_t smem);
+cudaError_t ensure_smem_optin(const void* kern, int bytes);
 
 }  // namespace cl

@@ -156,17 +156,17 @@ cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* dig
   if (total == 0) return cudaSuccess;
   // one wave: blocks per SM from the occupancy calculator (the basis variants are register-heavy)
   auto grid = [&](auto kern) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+    const int per_sm = resident_blocks_per_sm(reinterpret_cast<const void*>(kern), 256, 0);
     long long blocks = (total + 255) / 256;
-    const long long cap = (long long)num_sms() * (per_sm > 0 ? per_sm : 1);
+    const long long cap = (long long)num_sms() * per_sm;
     return (unsigned)(blocks > cap ? cap : blocks);
   };
   if (bs.on) {
     static const int8_t kFixed[8][8] = {{1, 1, 0, 0, 0, 0, 0, 0},  {0, 0, 0, 0, 0, 0, -1, -1}, {0, 0, 0, 0, 1, -1, 0, 0},
                                         {0, 0, 1, -1, 0, 0, 0, 0}, {0, 0, 0, 0, 1, 1, 0, 0},   {0, 0, -1, -1, 0, 0, 0, 0},
                                         {1, -1, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0, 1, -1}};
-    bool fixed = nb == 8 && getenv("CL_NO_SLICE_FIXED") == nullptr;
+    static const bool no_fixed = getenv("CL_NO_SLICE_FIXED") != nullptr;
+    bool fixed = nb == 8 && !no_fixed;
     for (int a = 0; a < 8 && fixed; ++a)
       for (int I = 0; I < 8 && fixed; ++I) fixed = bs.T[a * 8 + I] == kFixed[a][I];
     if (nb == 4) slice_input_kernel<4, true><<<grid(slice_input_kernel<4, true>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);

@@ -78,7 +78,7 @@ def linear_forward(x, layer: LinearLayer, variant: str = "b200", out=None):
     lib = _lib.load()
     if _device.is_cuda_tensor(x):
         torch = _device.torch_mod()
-        with torch.cuda.device(x.device):
+        with _device.on_device(x.device):
             xc = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
             y = _out(out, shape, x.device)
             _lib.check(lib.cl_linear_forward(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
