@@ -35,6 +35,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Clifford conv TFLOP/s & % roofline; block samples/s at 1/2/4/8 B200"
+ACT_METRIC = "multivector activation HBM GB/s (cfg2)"
 
 
 def load_peaks():
@@ -201,31 +202,68 @@ def max_over_ranks(v, world):
     return float(t.item())
 
 
-def cpu_block_sample(spec, precision_unused=None, n_samples=1):
-    """Time the oracle port (reference algorithm, fp64 BLAS) on n samples of a block config."""
+def _sample_input(spec, x, n_samples):
+    if x is not None:
+        return np.ascontiguousarray(x, dtype=np.float32)
+    return np.random.default_rng(0).standard_normal((n_samples, spec.C, spec.P, spec.nb)).astype(np.float32)
+
+
+def cpu_block_sample(spec, x=None, n_samples=1):
+    """The oracle port (reference algorithm, fp64 BLAS) on n samples of a block
+    config: (seconds, output). x: those samples of the GPU run's own input."""
     import oracle as O
     from paper_2507_01040_b200 import workloads as W
     f1, b1 = W.conv_params(spec, 1)
     f2, b2 = W.conv_params(spec, 2)
     aw, ab = W.act_params(spec)
-    rng = np.random.default_rng(0)
-    x = rng.standard_normal((n_samples, spec.C, spec.P, spec.nb)).astype(np.float32)
+    x = _sample_input(spec, x, n_samples)
     t0 = time.perf_counter()
-    O.block_ref(x, spec.g, spec.d, f1, b1, spec.mode, tuple(range(spec.nb)), aw, ab, f2, b2,
-                padding=spec.padding, residual=True)
-    return time.perf_counter() - t0
+    ref = O.block_ref(x, spec.g, spec.d, f1, b1, spec.mode, tuple(range(spec.nb)), aw, ab, f2, b2,
+                      padding=spec.padding, residual=True)
+    return time.perf_counter() - t0, ref
 
 
-def cpu_conv_sample(spec, n_samples=1):
+def cpu_conv_sample(spec, x=None, n_samples=1):
     import oracle as O
     from paper_2507_01040_b200 import workloads as W
     f, b = W.conv_params(spec, 1)
-    rng = np.random.default_rng(0)
-    x = rng.standard_normal((n_samples, spec.C, spec.P, spec.nb)).astype(np.float32)
-    pad = 1 if spec.padding == "same" else 0
+    x = _sample_input(spec, x, n_samples)
+    pad = (spec.d_filter - 1) // 2 if spec.padding == "same" else 0
     t0 = time.perf_counter()
-    O.conv_ref(x, f, b, spec.g, spec.d, spec.d_filter, pad)
-    return time.perf_counter() - t0
+    ref = O.conv_ref(x, f, b, spec.g, spec.d, spec.d_filter, pad)
+    return time.perf_counter() - t0, ref
+
+
+def cpu_act_sample(spec, x=None, n_samples=1, mode=None):
+    import oracle as O
+    from paper_2507_01040_b200 import workloads as W
+    mode = spec.mode if mode is None else mode
+    wgt, bias = W.act_params(spec)
+    x = _sample_input(spec, x, n_samples)
+    t0 = time.perf_counter()
+    ref = O.activation_ref(x, mode, tuple(range(spec.nb)), wgt if mode == 0 else None, bias if mode == 0 else None)
+    return time.perf_counter() - t0, ref
+
+
+def cpu_sample_fn(spec):
+    return {"block": cpu_block_sample, "conv": cpu_conv_sample, "activation": cpu_act_sample}[spec.kind]
+
+
+def verify(y, ref, prec):
+    """The parity gate of tests/ on the bench's own output:
+    raises VerificationFailed like the reference's verify-before-time (bench.py:360-377)."""
+    import oracle as O
+    from paper_2507_01040_b200.errors import VerificationFailed
+    if prec == "act":
+        err, tol, metric = O.max_abs_error(y, ref), 1e-5, "max_abs_error"
+    elif prec == "fp32":
+        err, tol, metric = O.max_rel_error(y, ref), 1e-4, "max_rel_error(floor=1e-2)"
+    else:
+        tol = {"3xtf32": 5e-5, "tf32": 2e-2, "bf16": 2e-2}[prec]
+        err, metric = O.max_rel_error(y, ref, floor=float(np.abs(ref).max())), "max_rel_error(floor=max|ref|)"
+    if not err <= tol:
+        raise VerificationFailed(f"bench output vs oracle: {metric} {err:.3e} > {tol:.0e}")
+    return {"metric": metric, "error": float(err), "tol": tol}
 
 
 def run_reference(args):
@@ -237,22 +275,28 @@ def run_reference(args):
     from paper_2507_01040_b200 import workloads as W
     spec = W.CONFIGS[args.config]
     cores = os.cpu_count()
+    fn = cpu_sample_fn(spec)
+    n = 8 if spec.kind == "activation" else 1  # samples per step: a bounded share of the workload
     for _ in range(args.warmup):
-        (cpu_block_sample if spec.kind == "block" else cpu_conv_sample)(spec, n_samples=1) if args.warmup_cpu else None
+        fn(spec, n_samples=n) if args.warmup_cpu else None
     times = []
     for _ in range(args.steps):
-        times.append((cpu_block_sample if spec.kind == "block" else cpu_conv_sample)(spec, n_samples=1))
+        times.append(fn(spec, n_samples=n)[0])
     t = float(np.mean(times))
-    value = 1.0 / t
+    if spec.kind == "activation":  # same metric / unit as the activation arm: GB/s of read + write
+        metric, unit, value = ACT_METRIC, "GB/s", 2 * n * spec.C * spec.P * spec.nb * 4 / t / 1e9
+    else:
+        metric, unit, value = METRIC, "samples/s", n / t
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+        "impl": "reference", "metric": metric, "value": value, "unit": unit,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (oracle)",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 (oracle)" if spec.kind == "activation" else "f64 (oracle)",
         "data": "synthetic (seeded, BASELINE.json distributions)",
-        "config": {"workload": spec.name, "global_batch": spec.B, "sample_per_step": 1},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port",
-                         "sample": f"1 sample of {spec.name} per step, oracle/oracle.py (numpy fp64, multithreaded BLAS)"},
-        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": spec.name, "global_batch": spec.B, "sample_per_step": n},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port",
+                         "sample": f"{n} sample(s) of {spec.name} per step, oracle/oracle.py (numpy, multithreaded BLAS)"},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -309,20 +353,31 @@ def run_activation(args, spec, world, rank, local, dev, peaks, peak_kind, lib):
         te = max_over_ranks((time.perf_counter() - t0) / max(1, args.e2e_steps), world)
         e2e = {"value": nbytes * world / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": x.numel() * 4 * world,
                "d2h_bytes_per_step": x.numel() * 4 * world}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n = 8  # bounded sample: 8 of the 64 samples
+        t_cpu, ref = cpu_act_sample(spec, x[:n].cpu().numpy(), mode=mode)
+        M.activation_forward(x, M.make_activation_config(M.Signature(spec.g), mode, tuple(range(spec.nb)),
+                                                         wgt if mode == 0 else None, bias if mode == 0 else None),
+                             out=y)
+        cpu = {"value": 2 * n * spec.C * spec.P * spec.nb * 4 / t_cpu / 1e9, "unit": "GB/s", "cores": os.cpu_count(),
+               "kind": "port", "sample": f"{n} of {spec.B} samples, oracle/oracle.py activation_ref (numpy fp32)",
+               "verified": verify(y[:n].cpu().numpy(), ref, "act")}
     if rank == 0:
         peak = peaks["hbm_gbs"]
         line = {
-            "metric": "multivector activation HBM GB/s (cfg2)", "value": gbs, "unit": "GB/s", "n_gpus": world,
+            "metric": ACT_METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world,
             "steps": reps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded, BASELINE.json distributions)",
             "config": {"workload": spec.name, "global_batch": spec.B, "mode": mode,
                        "l2": "inputs larger than L2 (%.2f GB)" % (x.numel() * 4 / 1e9)},
             "roofline": {"bound": "hbm", "achieved": gbs / world, "peak": peak, "unit": "GB/s",
-                         "frac": gbs / world / peak, "frac_of_8TBs": gbs / world / 8000.0, "traffic": None,
+                         "frac": gbs / world / peak, "frac_of_8TBs": gbs / world / 8000.0,
+                         "traffic": ncu_traffic(spec, f"act{mode}", nloc),
                          "kernel": "act_kernel", "peak_basis": f"{peak_kind} hbm_gbs copy bandwidth"},
             "modes": {str(m): {"ms": v[0] * 1e3, "GB/s": nbytes * world / v[0] / 1e9} for m, v in res.items()},
-            "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": None, "clocks": clocks,
+            "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": cpu, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     return 0
@@ -463,9 +518,12 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        t_cpu = (cpu_block_sample if spec.kind == "block" else cpu_conv_sample)(spec, n_samples=1)
+        # the oracle on sample 0 of this run's own input: the CPU baseline's timing,
+        # and the check of the timed output (y holds the last timed step's result)
+        t_cpu, ref = cpu_sample_fn(spec)(spec, x[:1].cpu().numpy())
         cpu = {"value": 1.0 / t_cpu, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"1 sample of {spec.name}, oracle/oracle.py (numpy fp64 einsum/BLAS)"}
+               "sample": f"sample 0 of {spec.name}, oracle/oracle.py (numpy fp64 einsum/BLAS)",
+               "verified": verify(y[:1].cpu().numpy(), ref, prec)}
 
     if rank == 0:
         line = {

@@ -13,11 +13,25 @@
 //    SWIZZLE_NONE UMMA core matrices [image][k-step][2 x 16 B chunks][n_tile
 //    rows][16 B], images = {hi, lo} for 3xTF32, {tf32}, {bf16} or the four
 //    four int8 digits of the fp32-accurate mode (per-column power-of-two scale).
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
 namespace cl {
 
+Sig make_sig(const int* g, int k) {
+  Sig sg{{0, 0, 0}, k};
+  for (int i = 0; i < k; ++i) sg.g[i] = g[i];
+  static const int flip = [] {
+    const char* e = getenv("CL_DBG_FLIP_COEFF");
+    int i = 0, j = 0;
+    return (e && sscanf(e, "%d,%d", &i, &j) == 2 && i >= 0 && i < 8 && j >= 0 && j < 8) ? 1 + i * 8 + j : 0;
+  }();
+  sg.flip = flip;
+  return sg;
+}
 
 __global__ void expand_ref_kernel(Sig sg, const float* __restrict__ f, int C_in, int C_out, int Q,
                                   float* __restrict__ out) {
@@ -100,8 +114,7 @@ static unsigned grid_for(long long total) {
 
 cudaError_t launch_expand_ref(const int* g, int k, const float* f, int C_in, int C_out, int Q,
                               float* out, cudaStream_t s) {
-  Sig sg{{0, 0, 0}, k};
-  for (int i = 0; i < k; ++i) sg.g[i] = g[i];
+  const Sig sg = make_sig(g, k);
   const int nb = 1 << k;
   const long long total = (long long)C_out * nb * C_in * nb * Q;
   expand_ref_kernel<<<grid_for(total), 256, 0, s>>>(sg, f, C_in, C_out, Q, out);
@@ -111,8 +124,7 @@ cudaError_t launch_expand_ref(const int* g, int k, const float* f, int C_in, int
 
 cudaError_t launch_expand_images(const int* g, const ConvPlan& pl, const float* f, int C_in,
                                  int C_out, const float* w_scale, uint8_t* img, cudaStream_t s) {
-  Sig sg{{0, 0, 0}, pl.ka};
-  for (int i = 0; i < pl.ka; ++i) sg.g[i] = g[i];
+  const Sig sg = make_sig(g, pl.ka);
   const long long total =
       (long long)pl.n_ntiles * pl.k_iters * (pl.ks * 32 / pl.esize) * pl.n_tile;
   expand_img_kernel<<<grid_for(total), 256, 0, s>>>(sg, f, C_in, C_out, pl, w_scale, img);

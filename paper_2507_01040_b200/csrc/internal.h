@@ -38,14 +38,21 @@ bool find_basis(const int* g, int k, Basis* bs);
 struct Sig {
   int g[3];
   int k;
+  // fault injection (the reference's parity_report schedule_transform,
+  // bench.py:566-576): 1 + i*8 + j negates the product-table coefficient of
+  // (e_i, e_j) in kernel construction; 0 = off. Set only by CL_DBG_FLIP_COEFF="i,j".
+  int flip = 0;
 };
+// Sig of a signature g (k values) with the CL_DBG_FLIP_COEFF fault applied.
+Sig make_sig(const int* g, int k);
 
 #if defined(__CUDACC__)
 // W[(co,t),(ci,j),q] = coeff(t^j, j) f[t^j, ci, co, q]  (conv.py:188-202)
 __device__ __forceinline__ float expanded_entry(const Sig& sg, const float* __restrict__ f, int nb, int C_in,
                                                 int C_out, int Q, int co, int t, int ci, int j, int q) {
   const int i = t ^ j;
-  const int c = blade_coeff(i, j, sg.g, sg.k);
+  int c = blade_coeff(i, j, sg.g, sg.k);
+  if (sg.flip == 1 + i * 8 + j) c = -c;
   if (c == 0) return 0.f;
   const float v = __ldg(f + (((long long)i * C_in + ci) * C_out + co) * Q + q);
   return c > 0 ? v : -v;

@@ -221,8 +221,7 @@ __global__ void weight_colscale_kernel(Sig sg, const float* __restrict__ f, int 
 cudaError_t launch_weight_colscale(const int* g, const ConvPlan& pl, const float* f, int C_in, int C_out,
                                    float* w_scale, cudaStream_t s) {
   const int N_pad = pl.n_ntiles * pl.n_tile;
-  Sig sg{{0, 0, 0}, pl.ka};
-  for (int i = 0; i < pl.ka; ++i) sg.g[i] = g[i];
+  const Sig sg = make_sig(g, pl.ka);
   weight_colscale_kernel<<<N_pad, 256, 0, s>>>(sg, f, C_in, C_out, pl.Q, pl.bs, w_scale);
   count_launch();
   return cudaGetLastError();

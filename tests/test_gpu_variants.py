@@ -65,3 +65,46 @@ def test_variant_parity(flags):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     _run(flags)
+
+
+FAULT_SNIPPET = r"""
+import sys
+import numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import torch
+import oracle as O
+from test_gpu_parity import make_conv, run_dev
+import paper_2507_01040_b200 as M
+torch.cuda.set_device(0)
+rng = np.random.default_rng(3)
+i, j = 1, 2  # CL_DBG_FLIP_COEFF: coeff(e1, e2) negated in kernel construction
+for g in [(1, 1), (1, 1, 1)]:
+    x, f, b, layer, pad = make_conv(rng, g, 2, 3, 4, 6, 3, "fp32", "same")
+    W = M.build_expanded_kernel(layer).cpu().numpy()
+    ref_W = O.expanded_kernel(f, g)
+    nb = 1 << len(g)
+    bad = np.zeros(ref_W.shape, bool)
+    for t in range(nb):
+        if t ^ j == i:  # W[(co, t), (ci, j), q] reads coeff(t ^ j, j)
+            bad[t::nb, j::nb, :] = True
+    assert np.array_equal(W[~bad], ref_W[~bad]) and np.array_equal(W[bad], -ref_W[bad]), "flip not where expected"
+    for prec in ("fp32", "bf16"):
+        x, f, b, layer, pad = make_conv(rng, g, 2, 3, 4, 6, 3, prec, "same")
+        y = run_dev(M.conv_forward, x, layer)
+        ref = O.conv_ref(x, f, b, g, 6, 3, pad)
+        e = O.max_rel_error(y, ref, floor=float(np.abs(ref).max()))
+        assert e > 2e-2, (g, prec, e)  # the parity bound of every mode catches the fault
+print("detected")
+"""
+
+
+def test_fault_injection_is_detected():
+    """Fault injection (the reference's parity_report schedule_transform, bench.py:566-576 /
+    tests/test_bench.py:202-210): one negated product-table coefficient in the device's
+    kernel construction must show up exactly in the expanded filter and break conv parity."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    env = dict(os.environ, CL_DBG_FLIP_COEFF="1,2")
+    code = FAULT_SNIPPET.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("detected"), r.stdout[-2000:] + r.stderr[-4000:]
