@@ -61,8 +61,11 @@ cudaError_t launch_sample_absmax(const float* x, long long B, long long per_samp
 // FIXED: the (1,1,1) M2(C) basis found by find_basis, whose rows are sums /
 // differences of blade pairs (2m, 2m+1): x' = (u0, -u3, v2, v1, u2, -u1, v0, v3)
 // with u_m = X_2m + X_2m+1, v_m = X_2m - X_2m+1 (8 adds instead of 64 multiply-adds).
+#ifndef CL_SLICE_MINB
+#define CL_SLICE_MINB 3  // resident blocks per SM of the fixed-form kernel (A/B builds: -DCL_SLICE_MINB=n)
+#endif
 template <int NB, bool BASIS, bool FIXED = false>
-__global__ void __launch_bounds__(256, FIXED ? 3 : 1) slice_input_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(256, FIXED ? CL_SLICE_MINB : 1) slice_input_kernel(const float* __restrict__ x,
                                                           const unsigned* __restrict__ amax,
                                                           int8_t* __restrict__ out, float* __restrict__ scale,
                                                           long long B, int C, long long P, int G, Basis bs) {
