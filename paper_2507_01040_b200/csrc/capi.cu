@@ -889,9 +889,9 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
     cudaStreamSynchronize(s);
     fprintf(stderr,
             "[CL_DBG_CLK] epilogue phase-1 %.0f cyc/tile (%llu tiles); MMA waits per tile: accumulator %.0f, "
-            "halo %.0f cyc\n",
+            "halo %.0f, operand stages %.0f cyc\n",
             h[1] ? (double)h[0] / h[1] : 0.0, h[1], h[3] ? (double)h[2] / h[3] : 0.0,
-            h[3] ? (double)h[4] / h[3] : 0.0);
+            h[3] ? (double)h[4] / h[3] : 0.0, h[3] ? (double)h[5] / h[3] : 0.0);
   }
   if (e != cudaSuccess) return cuda_fail(e, "conv_tc launch");
   return CL_OK;

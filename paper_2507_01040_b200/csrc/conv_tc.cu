@@ -337,7 +337,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           int qx = 0, qy = 0;
           if (p.tps == 1) {  // one tap per stage (kept separate: the multi-tap loop's codegen costs 20% here)
             for (int q = 0; q < nQ; ++q) {
+              const long long dbg_s0 = p.dbg_acc ? clock64() : 0;
               mbar_wait(&full[stage], phase);
+              if (p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
               tc_fence_after();
               const uint32_t sB4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
               if (elect_one()) {
@@ -390,7 +392,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           } else {
             for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
               const int nq = min(p.tps, nQ - q0);
+              const long long dbg_s0 = p.dbg_acc ? clock64() : 0;
               mbar_wait(&full[stage], phase);
+              if (p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
               tc_fence_after();
               const uint32_t sB4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
               {
@@ -463,8 +467,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         continue;
       }
       for (int kit = 0; kit < p.k_iters; ++kit) {
+        const long long dbg_s0 = p.dbg_acc ? clock64() : 0;
         if (kSplit) mbar_wait(&lo_ready[stage], phase);
         else mbar_wait(&full[stage], phase);
+        if (p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
         tc_fence_after();
         // (cluster launches return cluster-window shared addresses: keep the
         // CTA-local 18 bits so nothing carries past the 14-bit start field)
@@ -955,6 +961,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       }
       tc_fence_before();
       if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
+      if (p.dbg_acc && threadIdx.x == 128) {  // timing instrumentation: epilogue cycles per tile
+        atomicAdd(p.dbg_acc, (unsigned long long)(clock64() - dbg_t0));
+        atomicAdd(p.dbg_acc + 1, 1ull);
+      }
       if (++acc == slots) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 8) {
