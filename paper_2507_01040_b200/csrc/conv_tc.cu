@@ -250,8 +250,12 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
             for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
               const int nq = min(p.tps, nQ - q0);
               mbar_wait(&empty[stage], phase ^ 1);
-              if (arm) mbar_arrive_expect_tx(&full[stage], tx_bytes * (uint32_t)nq);
-              for (int i = 0; i < nq; ++i) load_b(nt, (q0 + i) * p.n_gs + gsi, (uint32_t)i * b_cta);
+              if (p.dbg_skip & 1) {  // timing experiment: no B loads (results garbage)
+                if (arm) mbar_arrive(&full[stage]);
+              } else {
+                if (arm) mbar_arrive_expect_tx(&full[stage], tx_bytes * (uint32_t)nq);
+                for (int i = 0; i < nq; ++i) load_b(nt, (q0 + i) * p.n_gs + gsi, (uint32_t)i * b_cta);
+              }
               if (++stage == S) { stage = 0; phase ^= 1; }
             }
           }

@@ -1,0 +1,7 @@
+# B-operand bandwidth experiment: conv time with and without the B stage loads (CL_DBG_SKIP=1, results garbage)
+for cfg in "5 bf16 64" "5 tf32 64" "4 bf16 16" "5 fp32 64"; do
+  set -- $cfg
+  for v in "" "CL_DBG_SKIP=1"; do
+    echo "== cfg$1 $2 B=$3 $v"; env $v timeout 300 python tools/time_vs_ncu.py $2 $3 $1 2>&1 | tail -1
+  done
+done
