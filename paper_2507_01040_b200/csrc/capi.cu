@@ -359,6 +359,90 @@ struct WsCache {
   }
 };
 
+// CUDA-graph replay of small forwards (launch-bound layers such as BASELINE
+// cfg1): the second call with the same (stream, x, y, B, workspace) captures
+// the launch sequence (absmax / slice / pack / conv ...) on a private stream
+// and later calls replay it with one cudaGraphLaunch on the caller's stream.
+// Large forwards, calls on a stream that is itself being captured and the
+// CL_DBG_CLK instrumentation run directly. CL_NO_GRAPH=1 disables it (A/B).
+static bool g_no_graph = getenv("CL_NO_GRAPH") != nullptr;
+constexpr long long kGraphMaxElems = 8ll << 20;  // input elements below which a forward is launch-bound
+struct GraphCache {
+  std::mutex m;
+  cudaStream_t cap = nullptr;
+  struct Ent {
+    cudaStream_t s;
+    const void* x;
+    const void* y;
+    long long B;
+    const void* ws;
+    int seen;                  // calls seen with this key (captured on the second)
+    cudaGraphExec_t exec;
+    int launches;              // kernels in the graph (for cl_launch_count)
+  };
+  std::vector<Ent> v;
+  ~GraphCache() {
+    for (auto& e : v)
+      if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (cap) cudaStreamDestroy(cap);
+  }
+  // Runs fn(stream) directly, or through the cached graph of this key.
+  template <class F>
+  int run(cudaStream_t s, const void* x, const void* y, long long B, const void* ws, F&& fn) {
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cst) != cudaSuccess || cst != cudaStreamCaptureStatusNone) return fn(s);
+    std::lock_guard<std::mutex> lk(m);
+    Ent* e = nullptr;
+    for (auto& it : v)
+      if (it.s == s && it.x == x && it.y == y && it.B == B && it.ws == ws) { e = &it; break; }
+    if (!e) {
+      if (v.size() >= 8) {  // evict the oldest key (its replays are stream-ordered before ours)
+        if (v.front().exec) {
+          cudaStreamSynchronize(v.front().s);
+          cudaGraphExecDestroy(v.front().exec);
+        }
+        v.erase(v.begin());
+      }
+      v.push_back({s, x, y, B, ws, 0, nullptr, 0});
+      e = &v.back();
+    }
+    if (e->exec) {
+      cudaError_t er = cudaGraphLaunch(e->exec, s);
+      if (er != cudaSuccess) return cuda_fail(er, "graph launch");
+      count_launch(e->launches);
+      return CL_OK;
+    }
+    if (++e->seen < 2) return fn(s);  // first call: direct (sets up attributes, workspaces, maps)
+    if (!cap) CL_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "graph stream");
+    const uint64_t l0 = g_launches.load();
+    CL_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "graph capture");
+    const int rc = fn(cap);
+    cudaGraph_t g = nullptr;
+    cudaError_t er = cudaStreamEndCapture(cap, &g);
+    const int n = (int)(g_launches.load() - l0);
+    g_launches.fetch_sub((uint64_t)n);  // nothing ran during capture
+    if (rc != CL_OK || er != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      e->seen = -1000000;  // this key stays on the direct path
+      return fn(s);
+    }
+    er = cudaGraphInstantiate(&e->exec, g, 0);
+    cudaGraphDestroy(g);
+    if (er != cudaSuccess) {
+      e->exec = nullptr;
+      e->seen = -1000000;
+      cudaGetLastError();
+      return fn(s);
+    }
+    e->launches = n;
+    er = cudaGraphLaunch(e->exec, s);
+    if (er != cudaSuccess) return cuda_fail(er, "graph launch");
+    count_launch(n);
+    return CL_OK;
+  }
+};
+
 // Host-buffer pipeline state of one handle: kPipe streams and their staging
 // buffers + workspaces, reused across calls (host calls on one handle are
 // serialised by the mutex; they are synchronous anyway).
@@ -392,6 +476,7 @@ struct cl_conv {
   alignas(64) CUtensorMap bmap;  // 2-SM pair: the filter images as 512-byte rows (encoded once at create)
   mutable WsCache ws;
   mutable HostPipe host;
+  mutable GraphCache graphs;
 };
 
 struct cl_act {
@@ -410,6 +495,7 @@ struct cl_block {
   int res_crop;
   mutable WsCache ws;
   mutable HostPipe host;
+  mutable GraphCache graphs;
 };
 
 extern "C" {
@@ -1019,12 +1105,20 @@ int cl_conv_forward_ws(const cl_conv* h, const float* x, float* y, int64_t B, vo
   return conv_run(h, x, nullptr, y, B, Epi{}, ws, (cudaStream_t)stream);
 }
 
+static bool graph_ok(long long elems) {
+  static const bool dbg_clk = getenv("CL_DBG_CLK") != nullptr;
+  return !g_no_graph && !dbg_clk && !g_time_kernel_only && elems > 0 && elems <= kGraphMaxElems;
+}
+
 int cl_conv_forward(const cl_conv* h, const float* x, float* y, int64_t B, void* stream) {
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null conv handle");
   if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
   void* ws = nullptr;
-  if (int rc = h->ws.get((cudaStream_t)stream, conv_ws_bytes(h, B, false), &ws)) return rc;
-  return conv_run(h, x, nullptr, y, B, Epi{}, ws, (cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int rc = h->ws.get(s, conv_ws_bytes(h, B, false), &ws)) return rc;
+  if (graph_ok(B * (long long)h->C_in * ipow(h->d_image, h->sk) * h->nb))
+    return h->graphs.run(s, x, y, B, ws, [&](cudaStream_t cs) { return conv_run(h, x, nullptr, y, B, Epi{}, ws, cs); });
+  return conv_run(h, x, nullptr, y, B, Epi{}, ws, s);
 }
 
 int cl_conv_time_kernel(const cl_conv* h, const float* x, float* y, int64_t B, int reps, void* stream,
@@ -1264,8 +1358,11 @@ int cl_block_forward(const cl_block* h, const float* x, float* y, int64_t B, voi
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null block handle");
   if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
   void* ws = nullptr;
-  if (int rc = h->ws.get((cudaStream_t)stream, block_ws_bytes(h, B), &ws)) return rc;
-  return block_run(h, x, y, B, ws, (cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int rc = h->ws.get(s, block_ws_bytes(h, B), &ws)) return rc;
+  if (graph_ok(B * (long long)h->c1->C_in * ipow(h->c1->d_image, h->c1->sk) * h->c1->nb))
+    return h->graphs.run(s, x, y, B, ws, [&](cudaStream_t cs) { return block_run(h, x, y, B, ws, cs); });
+  return block_run(h, x, y, B, ws, s);
 }
 
 int cl_block_forward_host(const cl_block* h, const float* xh, float* yh, int64_t B, int64_t chunk, void* stream) {
