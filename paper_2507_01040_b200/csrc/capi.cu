@@ -822,6 +822,8 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
   return CL_OK;
 }
 
+constexpr long long kSmallPrepElems = 8ll << 20;  // fp32-mode inputs up to this many elements: fused prep
+
 // Workspace bytes of one conv launch: int8 digit planes + per-sample
 // amax/scale (fp32 mode) or the packed bf16 input (bf16 mode).
 static size_t conv_ws_bytes(const cl_conv* h, long long B, bool prepacked) {
@@ -850,10 +852,16 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
     a_scale = reinterpret_cast<float*>(digits + bytes + (size_t)B * 4);
     const long long per_sample = (long long)h->C_in * P_in * h->nb;
     if (prep) {
-      if (!epi.amax_in) CL_CUDA(launch_sample_absmax(x, B, per_sample, amax, s), "absmax");
-      CL_CUDA(launch_slice_input(x, epi.amax_in ? epi.amax_in : amax, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G,
-                                 pl.bs, s),
-              "slice_input");
+      static const bool no_fused_prep = getenv("CL_NO_FUSED_PREP") != nullptr;  // A/B
+      if (!epi.amax_in && !no_fused_prep && B * per_sample <= kSmallPrepElems) {
+        // launch-bound layer: absmax + slice in one cluster launch
+        CL_CUDA(launch_absmax_slice(x, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G, pl.bs, s), "absmax_slice");
+      } else {
+        if (!epi.amax_in) CL_CUDA(launch_sample_absmax(x, B, per_sample, amax, s), "absmax");
+        CL_CUDA(launch_slice_input(x, epi.amax_in ? epi.amax_in : amax, digits, a_scale, h->nb, B, h->C_in, P_in,
+                                   pl.G, pl.bs, s),
+                "slice_input");
+      }
     }
     src = digits;
   } else if (pl.packed) {

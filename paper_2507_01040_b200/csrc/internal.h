@@ -187,6 +187,9 @@ cudaError_t launch_act(int nb, const ActParams& p, cudaStream_t s);
 // kPrecFp32 operand preparation (slice.cu)
 cudaError_t launch_sample_absmax(const float* x, long long B, long long per_sample, unsigned* amax,
                                  cudaStream_t s);
+// small layers: per-sample absmax + slicing in one cluster launch (no amax buffer)
+cudaError_t launch_absmax_slice(const float* x, int8_t* digits, float* scale, int nb, long long B, int C, long long P,
+                                int G, const Basis& bs, cudaStream_t s);
 cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* digits, float* scale,
                                int nb, long long B, int C, long long P, int G, const Basis& bs, cudaStream_t s);
 cudaError_t launch_weight_colscale(const int* g, const ConvPlan& pl, const float* f, int C_in, int C_out,

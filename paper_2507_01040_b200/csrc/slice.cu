@@ -61,6 +61,98 @@ cudaError_t launch_sample_absmax(const float* x, long long B, long long per_samp
 // FIXED: the (1,1,1) M2(C) basis found by find_basis, whose rows are sums /
 // differences of blade pairs (2m, 2m+1): x' = (u0, -u3, v2, v1, u2, -u1, v0, v3)
 // with u_m = X_2m + X_2m+1, v_m = X_2m - X_2m+1 (8 adds instead of 64 multiply-adds).
+// One (b, g, p) item: the 16 K-elements of group g at pixel p of sample b ->
+// 4 digit planes, with the sample's absmax `amx` (see slice_input_kernel).
+template <int NB, bool BASIS, bool FIXED>
+__device__ __forceinline__ void slice_item(const float* __restrict__ x, float amx, int8_t* __restrict__ out,
+                                           float* __restrict__ scale, long long b, int g, long long pp, int C,
+                                           long long P, long long total, long long i, const Basis& bs) {
+  constexpr int W = BASIS ? NB / 2 : NB;
+  constexpr int NCOL = BASIS ? 2 : 1;
+  constexpr int CPG = 16 / W;  // channels per group
+  const float sc = pow2_scale_for(BASIS ? 2.f * amx : amx);  // |x'| <= 2 max|x|
+  if (g == 0 && pp == 0) scale[b] = sc;
+  const float mult = 2147483648.f / sc;  // 2^31 / s, exact power of two
+  uint32_t word[NCOL][4][4];  // [col][digit plane][4 bytes x 4 words]
+#pragma unroll
+  for (int cl = 0; cl < CPG; ++cl) {
+    const int c = g * CPG + cl;
+    int X[NB];
+    if (c < C) {
+      const float* src = x + ((b * C + c) * P + pp) * NB;
+      float v[NB];
+      if constexpr (NB == 2) {
+        const float2 q = __ldg(reinterpret_cast<const float2*>(src));
+        v[0] = q.x; v[1] = q.y;
+      } else {
+#pragma unroll
+        for (int h = 0; h < NB / 4; ++h) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(src) + h);
+          v[4 * h] = q.x; v[4 * h + 1] = q.y; v[4 * h + 2] = q.z; v[4 * h + 3] = q.w;
+        }
+      }
+#pragma unroll
+      for (int I = 0; I < NB; ++I) X[I] = __float2int_rn(v[I] * mult);
+    } else {
+#pragma unroll
+      for (int I = 0; I < NB; ++I) X[I] = 0;
+    }
+#pragma unroll
+    for (int col = 0; col < NCOL; ++col) {
+#pragma unroll
+      for (int r = 0; r < W; ++r) {
+        int Xs;
+        if constexpr (FIXED) {
+          const int a = col * W + r;
+          const int m = (a == 0 || a == 6) ? 0 : (a == 3 || a == 5) ? 1 : (a == 2 || a == 4) ? 2 : 3;
+          const bool use_u = (a == 0 || a == 1 || a == 4 || a == 5);
+          const int val = use_u ? X[2 * m] + X[2 * m + 1] : X[2 * m] - X[2 * m + 1];
+          Xs = (a == 1 || a == 5) ? -val : val;
+        } else if constexpr (BASIS) {
+          Xs = 0;
+#pragma unroll
+          for (int I = 0; I < NB; ++I) Xs += (int)bs.T[(col * W + r) * 8 + I] * X[I];
+        } else {
+          Xs = X[r];
+        }
+        // balanced base-256 digits, least significant first
+        const int e = cl * W + r;  // byte position inside the 16-byte row
+        const int shift = (e & 3) * 8;
+#pragma unroll
+        for (int k = 3; k >= 0; --k) {
+          int d;
+          if (k > 0) {
+            d = (int)(int8_t)(Xs & 0xFF);
+            Xs = (Xs - d) >> 8;
+          } else {
+            d = Xs;
+          }
+          uint32_t& wd = word[col][k][e >> 2];
+          const uint32_t byte = (uint32_t)(uint8_t)d << shift;
+          wd = (shift == 0) ? byte : (wd | byte);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int col = 0; col < NCOL; ++col)
+      reinterpret_cast<uint4*>(out)[((long long)k * total + i) * NCOL + col] =
+          make_uint4(word[col][k][0], word[col][k][1], word[col][k][2], word[col][k][3]);
+}
+
+// One thread per (b, g, p): the 16 K-elements of group g at pixel p -> 4
+// digit planes (digit, b, g, p, [ncol x] 16 B). Without a change of basis a
+// group is 16/NB channels x NB blades; with one (BASIS) each pixel yields 2
+// rows, row c holding 16/W channels x the W = NB/2 transformed components
+// x'[c*W + r] = sum_I T[c*W + r][I] x[I].
+// Integer-exact: X_I = rint(x_I 2^31 / s) (power-of-two scaling, one rounding),
+// X' = sum_I T X_I in int32 (|X'| < 2^31 since s >= 2 max|x| 1.016), and the
+// balanced base-256 digits are the two's-complement bytes of X'.
+// FIXED: the (1,1,1) M2(C) basis found by find_basis, whose rows are sums /
+// differences of blade pairs (2m, 2m+1): x' = (u0, -u3, v2, v1, u2, -u1, v0, v3)
+// with u_m = X_2m + X_2m+1, v_m = X_2m - X_2m+1 (8 adds instead of 64 multiply-adds).
 #ifndef CL_SLICE_MINB
 #define CL_SLICE_MINB 3  // resident blocks per SM of the fixed-form kernel (A/B builds: -DCL_SLICE_MINB=n)
 #endif
@@ -69,9 +161,6 @@ __global__ void __launch_bounds__(256, FIXED ? CL_SLICE_MINB : 1) slice_input_ke
                                                           const unsigned* __restrict__ amax,
                                                           int8_t* __restrict__ out, float* __restrict__ scale,
                                                           long long B, int C, long long P, int G, Basis bs) {
-  constexpr int W = BASIS ? NB / 2 : NB;
-  constexpr int NCOL = BASIS ? 2 : 1;
-  constexpr int CPG = 16 / W;  // channels per group
   const long long total = B * G * P;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -79,78 +168,100 @@ __global__ void __launch_bounds__(256, FIXED ? CL_SLICE_MINB : 1) slice_input_ke
     const long long bg = i / P;
     const int g = (int)(bg % G);
     const long long b = bg / G;
-    const float amx = __uint_as_float(__ldg(amax + b));
-    const float sc = pow2_scale_for(BASIS ? 2.f * amx : amx);  // |x'| <= 2 max|x|
-    if (g == 0 && pp == 0) scale[b] = sc;
-    const float mult = 2147483648.f / sc;  // 2^31 / s, exact power of two
-    uint32_t word[NCOL][4][4];  // [col][digit plane][4 bytes x 4 words]
-#pragma unroll
-    for (int cl = 0; cl < CPG; ++cl) {
-      const int c = g * CPG + cl;
-      int X[NB];
-      if (c < C) {
-        const float* src = x + ((b * C + c) * P + pp) * NB;
-        float v[NB];
-        if constexpr (NB == 2) {
-          const float2 q = __ldg(reinterpret_cast<const float2*>(src));
-          v[0] = q.x; v[1] = q.y;
-        } else {
-#pragma unroll
-          for (int h = 0; h < NB / 4; ++h) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(src) + h);
-            v[4 * h] = q.x; v[4 * h + 1] = q.y; v[4 * h + 2] = q.z; v[4 * h + 3] = q.w;
-          }
-        }
-#pragma unroll
-        for (int I = 0; I < NB; ++I) X[I] = __float2int_rn(v[I] * mult);
-      } else {
-#pragma unroll
-        for (int I = 0; I < NB; ++I) X[I] = 0;
-      }
-#pragma unroll
-      for (int col = 0; col < NCOL; ++col) {
-#pragma unroll
-        for (int r = 0; r < W; ++r) {
-          int Xs;
-          if constexpr (FIXED) {
-            const int a = col * W + r;
-            const int m = (a == 0 || a == 6) ? 0 : (a == 3 || a == 5) ? 1 : (a == 2 || a == 4) ? 2 : 3;
-            const bool use_u = (a == 0 || a == 1 || a == 4 || a == 5);
-            const int val = use_u ? X[2 * m] + X[2 * m + 1] : X[2 * m] - X[2 * m + 1];
-            Xs = (a == 1 || a == 5) ? -val : val;
-          } else if constexpr (BASIS) {
-            Xs = 0;
-#pragma unroll
-            for (int I = 0; I < NB; ++I) Xs += (int)bs.T[(col * W + r) * 8 + I] * X[I];
-          } else {
-            Xs = X[r];
-          }
-          // balanced base-256 digits, least significant first
-          const int e = cl * W + r;  // byte position inside the 16-byte row
-          const int shift = (e & 3) * 8;
-#pragma unroll
-          for (int k = 3; k >= 0; --k) {
-            int d;
-            if (k > 0) {
-              d = (int)(int8_t)(Xs & 0xFF);
-              Xs = (Xs - d) >> 8;
-            } else {
-              d = Xs;
-            }
-            uint32_t& wd = word[col][k][e >> 2];
-            const uint32_t byte = (uint32_t)(uint8_t)d << shift;
-            wd = (shift == 0) ? byte : (wd | byte);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int col = 0; col < NCOL; ++col)
-        reinterpret_cast<uint4*>(out)[((long long)k * total + i) * NCOL + col] =
-            make_uint4(word[col][k][0], word[col][k][1], word[col][k][2], word[col][k][3]);
+    slice_item<NB, BASIS, FIXED>(x, __uint_as_float(__ldg(amax + b)), out, scale, b, g, pp, C, P, total, i, bs);
   }
+}
+
+// Small layers (launch-bound): absmax and slicing in ONE launch. A cluster of
+// kSliceCluster CTAs per sample: each CTA takes the max over its share of the
+// sample, the cluster combines the shares through distributed shared memory,
+// then each CTA slices its share of the sample's (g, p) items. Replaces the
+// memset + absmax + slice launches of the general path (which need a grid-wide
+// max first).
+constexpr int kSliceCluster = 8;
+template <int NB, bool BASIS, bool FIXED = false>
+__global__ void __launch_bounds__(256) absmax_slice_kernel(const float* __restrict__ x, int8_t* __restrict__ out,
+                                                           float* __restrict__ scale, long long B, int C, long long P,
+                                                           int G, Basis bs) {
+  __shared__ float red[8];
+  __shared__ float cmax;
+  const int rank = (int)cluster_ctarank();
+  const long long b = blockIdx.x / kSliceCluster;
+  const long long per_sample = (long long)C * P * NB;
+  const float* xs = x + b * per_sample;
+  float m = 0.f;
+  const long long n0 = per_sample * rank / kSliceCluster, n1 = per_sample * (rank + 1) / kSliceCluster;
+  for (long long i = n0 + threadIdx.x; i < n1; i += blockDim.x) m = fmaxf(m, fabsf(__ldg(xs + i)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float v = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmaxf(v, red[w]);
+    cmax = v;
+  }
+  cluster_sync();  // every CTA's share is in its cmax
+  if (threadIdx.x == 0) {
+    float v = 0.f;
+    for (int r = 0; r < kSliceCluster; ++r) v = fmaxf(v, ld_shared_cluster_f32(&cmax, r));
+    red[0] = v;
+  }
+  cluster_sync();  // peers done reading cmax (no CTA exits while it is read)
+  __syncthreads();
+  const float amx = red[0];
+  const long long total = B * G * P;
+  const long long items = (long long)G * P;
+  const long long i0 = items * rank / kSliceCluster, i1 = items * (rank + 1) / kSliceCluster;
+  for (long long it = i0 + threadIdx.x; it < i1; it += blockDim.x) {
+    const int g = (int)(it / P);
+    const long long pp = it - (long long)g * P;
+    const long long i = (b * G + g) * P + pp;
+    slice_item<NB, BASIS, FIXED>(x, amx, out, scale, b, g, pp, C, P, total, i, bs);
+  }
+}
+
+template <int NB, bool BASIS, bool FIXED>
+static cudaError_t launch_fused_t(const float* x, int8_t* digits, float* scale, long long B, int C, long long P, int G,
+                                  const Basis& bs, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(B * kSliceCluster));
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kSliceCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, absmax_slice_kernel<NB, BASIS, FIXED>, x, digits, scale, B, C, P, G, bs);
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+static bool fixed_111_basis(int nb, const Basis& bs) {
+  static const int8_t kFixed[8][8] = {{1, 1, 0, 0, 0, 0, 0, 0},  {0, 0, 0, 0, 0, 0, -1, -1}, {0, 0, 0, 0, 1, -1, 0, 0},
+                                      {0, 0, 1, -1, 0, 0, 0, 0}, {0, 0, 0, 0, 1, 1, 0, 0},   {0, 0, -1, -1, 0, 0, 0, 0},
+                                      {1, -1, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0, 1, -1}};
+  static const bool no_fixed = getenv("CL_NO_SLICE_FIXED") != nullptr;
+  bool fixed = nb == 8 && bs.on && !no_fixed;
+  for (int a = 0; a < 8 && fixed; ++a)
+    for (int I = 0; I < 8 && fixed; ++I) fixed = bs.T[a * 8 + I] == kFixed[a][I];
+  return fixed;
+}
+
+cudaError_t launch_absmax_slice(const float* x, int8_t* digits, float* scale, int nb, long long B, int C, long long P,
+                                int G, const Basis& bs, cudaStream_t s) {
+  if (B * G * P == 0) return cudaSuccess;
+  if (bs.on) {
+    if (nb == 4) return launch_fused_t<4, true, false>(x, digits, scale, B, C, P, G, bs, s);
+    if (fixed_111_basis(nb, bs)) return launch_fused_t<8, true, true>(x, digits, scale, B, C, P, G, bs, s);
+    return launch_fused_t<8, true, false>(x, digits, scale, B, C, P, G, bs, s);
+  }
+  if (nb == 2) return launch_fused_t<2, false, false>(x, digits, scale, B, C, P, G, bs, s);
+  if (nb == 4) return launch_fused_t<4, false, false>(x, digits, scale, B, C, P, G, bs, s);
+  return launch_fused_t<8, false, false>(x, digits, scale, B, C, P, G, bs, s);
 }
 
 cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* digits, float* scale, int nb,
@@ -165,13 +276,7 @@ cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* dig
     return (unsigned)(blocks > cap ? cap : blocks);
   };
   if (bs.on) {
-    static const int8_t kFixed[8][8] = {{1, 1, 0, 0, 0, 0, 0, 0},  {0, 0, 0, 0, 0, 0, -1, -1}, {0, 0, 0, 0, 1, -1, 0, 0},
-                                        {0, 0, 1, -1, 0, 0, 0, 0}, {0, 0, 0, 0, 1, 1, 0, 0},   {0, 0, -1, -1, 0, 0, 0, 0},
-                                        {1, -1, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0, 1, -1}};
-    static const bool no_fixed = getenv("CL_NO_SLICE_FIXED") != nullptr;
-    bool fixed = nb == 8 && !no_fixed;
-    for (int a = 0; a < 8 && fixed; ++a)
-      for (int I = 0; I < 8 && fixed; ++I) fixed = bs.T[a * 8 + I] == kFixed[a][I];
+    const bool fixed = fixed_111_basis(nb, bs);
     if (nb == 4) slice_input_kernel<4, true><<<grid(slice_input_kernel<4, true>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
     else if (fixed) slice_input_kernel<8, true, true><<<grid(slice_input_kernel<8, true, true>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
     else slice_input_kernel<8, true><<<grid(slice_input_kernel<8, true>), 256, 0, s>>>(x, amax, digits, scale, B, C, P, G, bs);
