@@ -467,6 +467,22 @@ def run_ours(args):
         torch.cuda.synchronize()
         gather = {"payload": "per-sample fp64 checksums (all_gather)", "samples": int(allcs.numel()),
                   "ms": max_over_ranks((time.perf_counter() - t0) * 1e3, world)}
+        if not _gloo():
+            # the outputs themselves to rank 0 (NCCL send/recv over NVLink), checked against the checksums
+            try:
+                barrier(world)
+                t0 = time.perf_counter()
+                yall = D.gather_outputs(y, spec.B, rank, world)
+                torch.cuda.synchronize()
+                t_g = max_over_ranks((time.perf_counter() - t0) * 1e3, world)
+                if rank == 0:
+                    ok = bool(torch.allclose(D.sample_checksums(yall), allcs, rtol=1e-12, atol=0.0))
+                    gather["outputs"] = {"bytes": int(yall.numel() * 4), "ms": t_g,
+                                         "GB/s": yall.numel() * 4 * (world - 1) / world / t_g / 1e6,
+                                         "checksums_match": ok}
+                del yall
+            except Exception as e:  # reported, not fatal: the timed step does not depend on it
+                gather["outputs"] = {"error": f"{type(e).__name__}: {e}"[:200]}
 
     # ---- dominant kernel: the tensor-core conv launch alone, CUDA events on its stream ----
     import ctypes

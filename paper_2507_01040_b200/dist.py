@@ -1,6 +1,7 @@
 """Batch-sharded data parallelism: contiguous sample slices
 per rank, NCCL (or gloo on CPU) broadcast of the compact parameters from
-rank 0, all-gather of per-sample checksums. No collective on the data path."""
+rank 0, all-gather of per-sample checksums and a gather of the outputs to
+rank 0. No collective on the data path (samples are independent)."""
 
 from __future__ import annotations
 
@@ -33,3 +34,22 @@ def gather_checksums(local, B_total: int, rank: int, world: int):
     parts = [torch.zeros_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf)
     return torch.cat([p[: hi - lo] for p, (lo, hi) in zip(parts, sizes)])
+
+
+def gather_outputs(y_local, B_total: int, rank: int, world: int, dst: int = 0):
+    """Gather the sharded (B_total, ...) output to rank `dst` (NCCL point-to-point
+    over NVLink: every rank sends its contiguous slice). Returns the full tensor on
+    `dst`, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    if rank != dst:
+        dist.send(y_local.contiguous(), dst=dst)
+        return None
+    out = torch.empty((B_total,) + tuple(y_local.shape[1:]), dtype=y_local.dtype, device=y_local.device)
+    for r in range(world):
+        lo, hi = shard(B_total, r, world)
+        if r == dst:
+            out[lo:hi].copy_(y_local)
+        else:
+            dist.recv(out[lo:hi], src=r)
+    return out

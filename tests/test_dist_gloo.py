@@ -1,5 +1,5 @@
 """World-size-2 gloo test of the multi-GPU host logic on CPU: sharding,
-parameter broadcast from rank 0 and checksum gather. The per-shard compute is
+parameter broadcast from rank 0, checksum all-gather and output gather. The per-shard compute is
 the CPU oracle (the product kernels need a GPU); what is under test is that
 the sharded job reproduces the single-process result exactly."""
 
@@ -45,9 +45,13 @@ def _worker(rank, world, port, q):
         y = O.conv_ref(xr[lo:hi], f.numpy(), b.numpy(), g, d, 3, 1)
         cs = D.sample_checksums(torch.from_numpy(y))
         allcs = D.gather_checksums(cs, B, rank, world)
+        yall = D.gather_outputs(torch.from_numpy(y), B, rank, world)
         if rank == 0:
             full = O.conv_ref(xr, f.numpy(), b.numpy(), g, d, 3, 1)
+            assert np.array_equal(yall.numpy(), full)  # the gathered outputs, bit for bit
             q.put((allcs.numpy(), D.sample_checksums(torch.from_numpy(full)).numpy()))
+        else:
+            assert yall is None
     finally:
         dist.destroy_process_group()
 
