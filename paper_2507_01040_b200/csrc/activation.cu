@@ -12,11 +12,13 @@
 // as activation.py:385-390 does for its specialised path), so the inner loop
 // is branch-free for any K <= N_B and any C.
 //
-// One thread per multivector: 16 B (2-D) or 32 B (3-D) of contiguous,
-// 16-byte-aligned data -> 128-bit streaming loads/stores; 4 multivectors in
-// flight per thread; grid sized to a multiple of the SM count.
+// One thread per multivector: 8 B (1-D), 16 B (2-D) or 32 B (3-D) of
+// contiguous, aligned data -> 64/128-bit streaming loads/stores; 4 (8 in 1-D)
+// multivectors in flight per thread; one contiguous chunk per block.
 #include "common.cuh"
 #include "internal.h"
+
+#include <type_traits>
 
 namespace cl {
 
@@ -33,61 +35,53 @@ __device__ __forceinline__ void st_stream(float4* p, float4 v) {
                : "memory");
 }
 
-// 1-D (N_B = 2): 8-byte multivectors, 8 in flight per thread.
-template <int MODE>
-__global__ void __launch_bounds__(256) act_kernel_nb2(ActParams p) {
-  constexpr int U = 8;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const float2* __restrict__ x = reinterpret_cast<const float2*>(p.x);
-  float2* __restrict__ y = reinterpret_cast<float2*>(p.y);
-  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < p.n_mv; base += stride * U) {
-    float2 v[U];
+// Exact unsigned division of n < 2^31 (host-side magic numbers, launch_act).
+__device__ __forceinline__ unsigned udiv(unsigned n, unsigned mag, unsigned sh) {
+  return (unsigned)(((unsigned long long)n * mag) >> sh);
+}
+
+// Each block gates one contiguous chunk of 256*U multivectors (no grid-stride
+// loop, many waves): a block streams 16-32 KB of consecutive HBM, which kept
+// DRAM pages open better than a grid-stride loop over a one-wave grid
+// (tools/probe/act_variants.cu at cfg2: 6.2 vs 5.3-5.5 TB/s median). The
+// channel of element i is ((i / P) % C); the block's first index is split
+// once in 64 bits, the rest is 32-bit magic-number division.
+template <int NB, int MODE, int U>
+__global__ void __launch_bounds__(256) act_kernel(ActParams p) {
+  using VT = typename std::conditional<NB == 2, float2, float4>::type;
+  constexpr int V = NB == 2 ? 1 : NB / 4;  // vectors per multivector
+  const long long base0 = (long long)blockIdx.x * (256 * U);
+  const long long bc0 = base0 / p.P;                 // (b, c) plane of the chunk start
+  const unsigned r0 = (unsigned)(base0 - bc0 * p.P);  // offset inside that plane (< P < 2^31)
+  const unsigned c0 = (unsigned)(bc0 % p.C);
+  const VT* __restrict__ x = reinterpret_cast<const VT*>(p.x);
+  VT* __restrict__ y = reinterpret_cast<VT*>(p.y);
+  VT v[U][V];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = base + u * stride;
-      if (i < p.n_mv) v[u] = __ldcs(x + i);
-    }
+  for (int u = 0; u < U; ++u) {
+    const long long i = base0 + u * 256 + threadIdx.x;
+    if (i < p.n_mv) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = base + u * stride;
-      if (i < p.n_mv) {
-        const int c = (int)((i / p.P) % p.C);
-        float s = fmaf(v[u].x, __ldg(p.w + 2 * c), 0.f);
-        s = fmaf(v[u].y, __ldg(p.w + 2 * c + 1), s);
-        if (MODE == 0) s += __ldg(p.b + c);
-        if (MODE == 2) s = s / p.Kf;
-        const float gte = 1.f / (1.f + expf(-s));
-        __stcs(y + i, make_float2(v[u].x * gte, v[u].y * gte));
+      for (int h = 0; h < V; ++h) {
+        if constexpr (NB == 2) v[u][h] = __ldcs(x + i);
+        else v[u][h] = ld_stream(x + i * V + h);
       }
     }
   }
-}
-
-template <int NB, int MODE>
-__global__ void __launch_bounds__(256) act_kernel(ActParams p) {
-  constexpr int V = NB / 4;  // float4 per multivector
-  constexpr int U = 4;       // multivectors in flight per thread
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const float4* __restrict__ x = reinterpret_cast<const float4*>(p.x);
-  float4* __restrict__ y = reinterpret_cast<float4*>(p.y);
-  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < p.n_mv;
-       base += stride * U) {
-    float4 v[U][V];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = base + u * stride;
-      if (i < p.n_mv) {
-#pragma unroll
-        for (int h = 0; h < V; ++h) v[u][h] = ld_stream(x + i * V + h);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = base + u * stride;
-      if (i < p.n_mv) {
-        const int c = (int)((i / p.P) % p.C);
-        const float* w = p.w + c * NB;
-        float s = 0.f;
+  for (int u = 0; u < U; ++u) {
+    const long long i = base0 + u * 256 + threadIdx.x;
+    if (i < p.n_mv) {
+      // planes crossed since the chunk start (r0 + 256U < 2^31: P < 2^30)
+      const unsigned k = udiv(r0 + (unsigned)(u * 256) + threadIdx.x, p.magP, p.shP);
+      const unsigned ck = c0 + k;
+      const unsigned c = ck - udiv(ck, p.magC, p.shC) * (unsigned)p.C;
+      const float* w = p.w + c * NB;
+      float s = 0.f;
+      if constexpr (NB == 2) {
+        s = fmaf(v[u][0].x, __ldg(w + 0), s);
+        s = fmaf(v[u][0].y, __ldg(w + 1), s);
+      } else {
 #pragma unroll
         for (int h = 0; h < V; ++h) {
           s = fmaf(v[u][h].x, __ldg(w + 4 * h + 0), s);
@@ -95,12 +89,17 @@ __global__ void __launch_bounds__(256) act_kernel(ActParams p) {
           s = fmaf(v[u][h].z, __ldg(w + 4 * h + 2), s);
           s = fmaf(v[u][h].w, __ldg(w + 4 * h + 3), s);
         }
-        if (MODE == 0) s += __ldg(p.b + c);
-        if (MODE == 2) s = s / p.Kf;
-        const float gte = 1.f / (1.f + expf(-s));
+      }
+      if (MODE == 0) s += __ldg(p.b + c);
+      if (MODE == 2) s = s / p.Kf;
+      const float gte = 1.f / (1.f + expf(-s));
 #pragma unroll
-        for (int h = 0; h < V; ++h) {
-          float4 o = v[u][h];
+      for (int h = 0; h < V; ++h) {
+        VT o = v[u][h];
+        if constexpr (NB == 2) {
+          o.x *= gte; o.y *= gte;
+          __stcs(y + i, o);
+        } else {
           o.x *= gte; o.y *= gte; o.z *= gte; o.w *= gte;
           st_stream(y + i * V + h, o);
         }
@@ -109,36 +108,12 @@ __global__ void __launch_bounds__(256) act_kernel(ActParams p) {
   }
 }
 
-// Grid = exactly the resident capacity (one wave, no tail): blocks per SM
-// from the occupancy calculator x SM count, capped by the work.
 template <int NB, int MODE>
 static cudaError_t launch_mode(const ActParams& p, cudaStream_t s) {
-  static int per_sm = [] {
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, act_kernel<NB, MODE>, 256, 0);
-    return n > 0 ? n : 1;
-  }();
-  long long blocks = (p.n_mv + 256LL * 4 - 1) / (256LL * 4);
-  const long long cap = (long long)num_sms() * per_sm;
-  if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  act_kernel<NB, MODE><<<(unsigned)blocks, 256, 0, s>>>(p);
-  count_launch();
-  return cudaGetLastError();
-}
-
-template <int MODE>
-static cudaError_t launch_nb2_mode(const ActParams& p, cudaStream_t s) {
-  static int per_sm = [] {
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, act_kernel_nb2<MODE>, 256, 0);
-    return n > 0 ? n : 1;
-  }();
-  long long blocks = (p.n_mv + 256LL * 8 - 1) / (256LL * 8);
-  const long long cap = (long long)num_sms() * per_sm;
-  if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  act_kernel_nb2<MODE><<<(unsigned)blocks, 256, 0, s>>>(p);
+  constexpr int U = NB == 2 ? 8 : 4;
+  const long long blocks = (p.n_mv + 256LL * U - 1) / (256LL * U);
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  act_kernel<NB, MODE, U><<<(unsigned)blocks, 256, 0, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }
@@ -152,13 +127,26 @@ static cudaError_t launch_nb(const ActParams& p, cudaStream_t s) {
   }
 }
 
-cudaError_t launch_act(int nb, const ActParams& p, cudaStream_t s) {
-  if (p.n_mv == 0) return cudaSuccess;
+// n < 2^31: with sh = 31 + ceil(log2 d) and mag = ceil(2^sh / d) < 2^32,
+// (n * mag) >> sh == n / d exactly, because n * (mag * d - 2^sh) < 2^sh.
+static void magic_div(unsigned d, unsigned* mag, unsigned* sh) {
+  unsigned l = 0;
+  while ((1ull << l) < d) ++l;
+  *sh = 31 + l;
+  *mag = (unsigned)(((1ull << *sh) + d - 1) / d);
+}
+
+cudaError_t launch_act(int nb, const ActParams& p0, cudaStream_t s) {
+  if (p0.n_mv == 0) return cudaSuccess;
+  if (p0.P < 1 || p0.P >= (1LL << 30) || p0.C < 1 || p0.C >= (1 << 30)) return cudaErrorInvalidValue;
+  ActParams p = p0;
+  magic_div((unsigned)p.P, &p.magP, &p.shP);
+  magic_div((unsigned)p.C, &p.magC, &p.shC);
   if (nb == 2) {
     switch (p.mode) {
-      case 0: return launch_nb2_mode<0>(p, s);
-      case 1: return launch_nb2_mode<1>(p, s);
-      default: return launch_nb2_mode<2>(p, s);
+      case 0: return launch_mode<2, 0>(p, s);
+      case 1: return launch_mode<2, 1>(p, s);
+      default: return launch_mode<2, 2>(p, s);
     }
   }
   return nb == 4 ? launch_nb<4>(p, s) : launch_nb<8>(p, s);

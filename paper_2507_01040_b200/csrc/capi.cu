@@ -1227,6 +1227,7 @@ int cl_act_create(const int32_t* g, int k, int mode, const int32_t* ki, int K, i
 int cl_act_forward(const cl_act* h, const float* x, float* y, int64_t B, int64_t P, void* stream) {
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null activation handle");
   if (B < 0 || P < 1) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "B >= 0 and P >= 1 required");
+  if (P >= (1LL << 30)) return fail(CL_ERR_UNSUPPORTED, "Unsupported", "activation needs P < 2^30 positions per channel");
   if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) != 0)
     return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "activation buffers must be 16-byte aligned");
   ActParams p{};

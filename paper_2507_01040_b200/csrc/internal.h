@@ -171,6 +171,9 @@ struct ActParams {
   const float* w;     // (C, NB)
   const float* b;     // (C)
   float Kf;
+  // exact unsigned division of n < 2^31 by P and by C: q = (n * mag) >> sh
+  // (filled by launch_act)
+  unsigned magP, shP, magC, shC;
 };
 
 // launchers (conv_tc.cu / expand.cu / activation.cu)

@@ -239,7 +239,7 @@ def test_activation_spatial_golden(golden):
 
 @pytest.mark.parametrize("k", [1, 2, 3])
 @pytest.mark.parametrize("mode", [0, 1, 2])
-@pytest.mark.parametrize("C,P,B", [(1, 1, 1), (13, 7, 3), (64, 1000, 2), (3, 4097, 1)])
+@pytest.mark.parametrize("C,P,B", [(1, 1, 1), (13, 7, 3), (64, 1000, 2), (3, 4097, 1), (5, 3, 300), (7, 1, 1500)])
 def test_activation_shapes(k, mode, C, P, B):
     nb = 1 << k
     rng = np.random.default_rng(k * 100 + mode)
