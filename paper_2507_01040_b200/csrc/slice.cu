@@ -16,7 +16,11 @@
 
 namespace cl {
 
-__global__ void absmax_kernel(const float* __restrict__ x, long long per_sample, unsigned* __restrict__ amax) {
+// Per-sample max |x|. Block (j, b) reduces the j-th contiguous chunk of
+// kAbsmaxU float4 per thread of sample b (many waves, one atomic per block).
+constexpr int kAbsmaxU = 8;
+__global__ void __launch_bounds__(256) absmax_kernel(const float* __restrict__ x, long long per_sample,
+                                                     unsigned* __restrict__ amax) {
   const int b = blockIdx.y;
   const float* xs = x + (long long)b * per_sample;
   float m = 0.f;
@@ -25,25 +29,37 @@ __global__ void absmax_kernel(const float* __restrict__ x, long long per_sample,
   if (head > per_sample) head = per_sample;
   const long long n4 = (per_sample - head) / 4;
   const float4* x4 = reinterpret_cast<const float4*>(xs + head);
-  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
-  for (long long i = tid; i < n4; i += nth) {
-    const float4 v = __ldg(x4 + i);
-    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  const long long base = (long long)blockIdx.x * (256 * kAbsmaxU) + threadIdx.x;
+  float4 v[kAbsmaxU];
+#pragma unroll
+  for (int u = 0; u < kAbsmaxU; ++u)
+    v[u] = base + u * 256 < n4 ? __ldcs(x4 + base + u * 256) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int u = 0; u < kAbsmaxU; ++u)
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+  if (blockIdx.x == 0) {
+    if (threadIdx.x < head) m = fmaxf(m, fabsf(xs[threadIdx.x]));
+    for (long long i = head + n4 * 4 + threadIdx.x; i < per_sample; i += blockDim.x) m = fmaxf(m, fabsf(xs[i]));
   }
-  if (tid < head) m = fmaxf(m, fabsf(xs[tid]));
-  for (long long i = head + n4 * 4 + tid; i < per_sample; i += nth) m = fmaxf(m, fabsf(xs[i]));
+  __shared__ float red[8];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(amax + b, __float_as_uint(m));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
+    atomicMax(amax + b, __float_as_uint(m));
+  }
 }
 
 cudaError_t launch_sample_absmax(const float* x, long long B, long long per_sample, unsigned* amax,
                                  cudaStream_t s) {
   if (B == 0) return cudaSuccess;
+  if (B > 65535) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(unsigned) * B, s);
   if (e != cudaSuccess) return e;
-  long long want = (per_sample / 4 + 255) / 256;
-  long long per = std::max<long long>(1, std::min<long long>(want, ((long long)num_sms() * 8 + B - 1) / B));
+  const long long per = std::max<long long>(1, (per_sample / 4 + 256 * kAbsmaxU - 1) / (256 * kAbsmaxU));
   dim3 grid((unsigned)per, (unsigned)B);
   absmax_kernel<<<grid, 256, 0, s>>>(x, per_sample, amax);
   count_launch();
@@ -63,6 +79,14 @@ cudaError_t launch_sample_absmax(const float* x, long long B, long long per_samp
 // with u_m = X_2m + X_2m+1, v_m = X_2m - X_2m+1 (8 adds instead of 64 multiply-adds).
 // One (b, g, p) item: the 16 K-elements of group g at pixel p of sample b ->
 // 4 digit planes, with the sample's absmax `amx` (see slice_input_kernel).
+// Balanced base-256 digits of X (|X| < 2^31 - 2^23): X = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3
+// with d0..d2 in [-128, 127]. Y = X + 0x808080 has the unsigned bytes d_k + 128
+// (k < 3) and top byte d3, so the two's-complement digit bytes are the bytes
+// of Y ^ 0x808080 -- the same digits as peeling d = sext(X & 255), X = (X - d) >> 8.
+__device__ __forceinline__ uint32_t digits_of(int X) {
+  return ((uint32_t)X + 0x808080u) ^ 0x808080u;
+}
+
 template <int NB, bool BASIS, bool FIXED>
 __device__ __forceinline__ void slice_item(const float* __restrict__ x, float amx, int8_t* __restrict__ out,
                                            float* __restrict__ scale, long long b, int g, long long pp, int C,
@@ -73,7 +97,9 @@ __device__ __forceinline__ void slice_item(const float* __restrict__ x, float am
   const float sc = pow2_scale_for(BASIS ? 2.f * amx : amx);  // |x'| <= 2 max|x|
   if (g == 0 && pp == 0) scale[b] = sc;
   const float mult = 2147483648.f / sc;  // 2^31 / s, exact power of two
-  uint32_t word[NCOL][4][4];  // [col][digit plane][4 bytes x 4 words]
+  // Z[col][e]: the 4 balanced base-256 digits of element e of the 16-byte row,
+  // as the bytes of one word (see digits_of)
+  uint32_t Z[NCOL][16];
 #pragma unroll
   for (int cl = 0; cl < CPG; ++cl) {
     const int c = g * CPG + cl;
@@ -115,31 +141,31 @@ __device__ __forceinline__ void slice_item(const float* __restrict__ x, float am
         } else {
           Xs = X[r];
         }
-        // balanced base-256 digits, least significant first
-        const int e = cl * W + r;  // byte position inside the 16-byte row
-        const int shift = (e & 3) * 8;
-#pragma unroll
-        for (int k = 3; k >= 0; --k) {
-          int d;
-          if (k > 0) {
-            d = (int)(int8_t)(Xs & 0xFF);
-            Xs = (Xs - d) >> 8;
-          } else {
-            d = Xs;
-          }
-          uint32_t& wd = word[col][k][e >> 2];
-          const uint32_t byte = (uint32_t)(uint8_t)d << shift;
-          wd = (shift == 0) ? byte : (wd | byte);
-        }
+        Z[col][cl * W + r] = digits_of(Xs);
       }
     }
   }
+  // digit plane k holds digit 3-k (plane 0 = most significant): a 4x4 byte
+  // transpose of every 4 consecutive elements, 8 byte permutes per 4 words
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int col = 0; col < NCOL; ++col) {
+    uint32_t word[4][4];  // [digit plane][word]
 #pragma unroll
-    for (int col = 0; col < NCOL; ++col)
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t t0 = __byte_perm(Z[col][4 * j], Z[col][4 * j + 1], 0x5140);  // b0 b0' b1 b1'
+      const uint32_t t1 = __byte_perm(Z[col][4 * j], Z[col][4 * j + 1], 0x7362);  // b2 b2' b3 b3'
+      const uint32_t t2 = __byte_perm(Z[col][4 * j + 2], Z[col][4 * j + 3], 0x5140);
+      const uint32_t t3 = __byte_perm(Z[col][4 * j + 2], Z[col][4 * j + 3], 0x7362);
+      word[3][j] = __byte_perm(t0, t2, 0x5410);  // digit 0 (least significant)
+      word[2][j] = __byte_perm(t0, t2, 0x7632);
+      word[1][j] = __byte_perm(t1, t3, 0x5410);
+      word[0][j] = __byte_perm(t1, t3, 0x7632);  // digit 3
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
       reinterpret_cast<uint4*>(out)[((long long)k * total + i) * NCOL + col] =
-          make_uint4(word[col][k][0], word[col][k][1], word[col][k][2], word[col][k][3]);
+          make_uint4(word[k][0], word[k][1], word[k][2], word[k][3]);
+  }
 }
 
 // One thread per (b, g, p): the 16 K-elements of group g at pixel p -> 4
@@ -164,10 +190,19 @@ __global__ void __launch_bounds__(256, FIXED ? CL_SLICE_MINB : 1) slice_input_ke
   const long long total = B * G * P;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    const long long pp = i % P;
-    const long long bg = i / P;
-    const int g = (int)(bg % G);
-    const long long b = bg / G;
+    long long pp, b;
+    int g;
+    if (total <= 0xffffffffLL) {  // 32-bit division (uniform branch)
+      const unsigned bg = (unsigned)i / (unsigned)P;
+      pp = (unsigned)i - bg * (unsigned)P;
+      b = bg / (unsigned)G;
+      g = (int)(bg - (unsigned)b * (unsigned)G);
+    } else {
+      pp = i % P;
+      const long long bg = i / P;
+      g = (int)(bg % G);
+      b = bg / G;
+    }
     slice_item<NB, BASIS, FIXED>(x, __uint_as_float(__ldg(amax + b)), out, scale, b, g, pp, C, P, total, i, bs);
   }
 }
@@ -268,7 +303,10 @@ cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* dig
                                long long B, int C, long long P, int G, const Basis& bs, cudaStream_t s) {
   const long long total = B * G * P;
   if (total == 0) return cudaSuccess;
-  // one wave: blocks per SM from the occupancy calculator (the basis variants are register-heavy)
+  // One wave: blocks per SM from the occupancy calculator (the basis variants
+  // are register-heavy). Unlike the activation, a many-wave grid (one item per
+  // thread) measured slower here: 8.2 vs 7.0 ms per cfg5 tensor (each block
+  // streams 4 input channels and 4 digit planes at once).
   auto grid = [&](auto kern) {
     const int per_sm = resident_blocks_per_sm(reinterpret_cast<const void*>(kern), 256, 0);
     long long blocks = (total + 255) / 256;

@@ -24,6 +24,7 @@ for job in ${JOBS:-act bf16 tf32 x3 cfg4 cfg3 cfg1}; do
     cfg4) run conv_cfg4_fp32_B16 conv_tc tools/prof_conv.py --config 4 --B 16 --precision fp32 --reps 1 ;;
     cfg3) run conv_cfg3_bf16_B32 conv_tc tools/prof_conv.py --config 3 --B 32 --precision bf16 --reps 1 ;;
     fp32) run conv_cfg5_fp32_B64 conv_tc tools/prof_conv.py --config 5 --B 64 --precision fp32 --reps 1 ;;
+    slice) run slice_cfg5_fp32_B64 slice_input tools/prof_conv.py --config 5 --B 64 --precision fp32 --reps 1 ;;
     fp32full) run conv_cfg5_fp32_B256 conv_tc tools/prof_conv.py --config 5 --B 256 --precision fp32 --reps 1 ;;
     cfg1) run conv_cfg1_fp32_B8 conv_tc tools/prof_conv.py --config 1 --B 8 --precision fp32 --reps 3 ;;
   esac
