@@ -295,7 +295,9 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
   if (best < 0) return false;
   pl = bestp;
   pl.tmem_cols = (uint32_t)std::max(32, pow2_at_least(pl.levels * pl.n_tile * pl.acc_slots));
-  pl.smem_bytes = (size_t)pl.ring_off + (size_t)pl.stages * pl.stage_bytes + 1024 + 512;
+  // + 1024 alignment slack + the barrier area (3 x 8 stage barriers, 10 accumulator / halo
+  // barriers, the TMEM slot, the 8-deep tile ring: 472 B; within the 2048 B reserve above)
+  pl.smem_bytes = (size_t)pl.ring_off + (size_t)pl.stages * pl.stage_bytes + 1024 + 768;
   return pl.tmem_cols <= 512;
 }
 
@@ -825,14 +827,20 @@ static int encode_input_map(const cl_conv* h, const void* xsrc, long long B, CUt
 constexpr long long kSmallPrepElems = 8ll << 20;  // fp32-mode inputs up to this many elements: fused prep
 
 // Workspace bytes of one conv launch: int8 digit planes + per-sample
-// amax/scale (fp32 mode) or the packed bf16 input (bf16 mode).
-static size_t conv_ws_bytes(const cl_conv* h, long long B, bool prepacked) {
+// amax/scale (fp32 mode) or the packed bf16 input (bf16 mode), then
+// kSchedBytes for the dynamic tile scheduler's work counter.
+constexpr size_t kSchedBytes = 256;
+static size_t conv_ws_operand_bytes(const cl_conv* h, long long B, bool prepacked) {
   const ConvPlan& pl = h->plan;
   const size_t P_in = (size_t)ipow(h->d_image, h->sk) * (pl.bs.on ? pl.bs.ncol : 1);  // rows per sample
   if (pl.prec == kPrecFp32) return align_up((size_t)kDigitsA * B * pl.G * P_in * 16, 256) + align_up((size_t)B * 8, 256);
   if (pl.packed && !prepacked) return align_up((size_t)B * pl.G * P_in * 16, 256);
   return 0;
 }
+static size_t conv_ws_bytes(const cl_conv* h, long long B, bool prepacked) {
+  return conv_ws_operand_bytes(h, B, prepacked) + kSchedBytes;
+}
+static bool g_static_tiles = getenv("CL_STATIC_TILES") != nullptr;  // A/B: static round-robin tile order
 
 // Run one conv on device buffers. `xbf` (optional) is an already packed bf16
 // A-ready input (bf16 layers); otherwise x is sliced / packed here into `ws`
@@ -968,6 +976,15 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.amax_out = epi.amax_out;
   int grid = (int)std::min<long long>(p.num_tiles, (long long)num_sms());
   grid -= grid % p.cs;
+  // Dynamic tile order for long launches, where the static order's drift
+  // matters: cfg5 B=256 block +2.3 % (fp32) / +3.7 % (bf16) sustained, DRAM
+  // reads of a conv 58.6 -> 17.3 GB. Short launches keep the static order:
+  // the ring hand-off cost ~3 % at cfg4 B=16 bf16 (52 tiles per CTA).
+  if (!g_static_tiles && p.num_tiles >= 128LL * grid) {
+    p.tile_ctr = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) +
+                                                       conv_ws_operand_bytes(h, B, xbf != nullptr));
+    CL_CUDA(cudaMemsetAsync(p.tile_ctr, 0, sizeof(unsigned long long), s), "tile counter reset");
+  }
   const CUtensorMap& bmap = pl.pair ? h->bmap : map;  // unused unless paired
   static unsigned long long* dbg_acc = nullptr;  // CL_DBG_CLK: per-launch epilogue / MMA-wait cycle report
   static const bool dbg_clk = getenv("CL_DBG_CLK") != nullptr;
@@ -983,9 +1000,9 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
     cudaStreamSynchronize(s);
     fprintf(stderr,
             "[CL_DBG_CLK] epilogue phase-1 %.0f cyc/tile (%llu tiles); MMA waits per tile: accumulator %.0f, "
-            "halo %.0f, operand stages %.0f cyc\n",
+            "halo %.0f, operand stages %.0f cyc; CTA finish spread %.1f us\n",
             h[1] ? (double)h[0] / h[1] : 0.0, h[1], h[3] ? (double)h[2] / h[3] : 0.0,
-            h[3] ? (double)h[4] / h[3] : 0.0, h[3] ? (double)h[5] / h[3] : 0.0);
+            h[3] ? (double)h[4] / h[3] : 0.0, h[3] ? (double)h[5] / h[3] : 0.0, (double)(h[6] - ~h[7]) * 1e-3);
   }
   if (e != cudaSuccess) return cuda_fail(e, "conv_tc launch");
   return CL_OK;

@@ -73,6 +73,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait with cluster-scope acquire: for data a peer CTA wrote into this CTA's
+// shared memory before its release-cluster arrive on `bar`.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Store a 64-bit value into CTA `rank`'s copy of a shared variable, then
+// arrive (release, cluster scope) on that CTA's copy of `bar`.
+__device__ __forceinline__ void st_remote_arrive(long long* var, long long v, uint64_t* bar, uint32_t rank) {
+  uint32_t rv, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rv) : "r"(smem_u32(var)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(rv), "l"(v) : "memory");
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+}
+
 // Wait with back-off for warps that are off the critical path (the epilogue
 // waiting for an accumulator, the producer waiting for a free slot): a tight
 // try_wait spin from many warps floods the MIO queue that tcgen05.mma issue

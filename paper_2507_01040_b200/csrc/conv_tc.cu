@@ -169,6 +169,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   uint64_t* hempty = hfull + 2;   //               consumed by the last tap's MMAs
   uint64_t* hlo = hempty + 2;     //               3xTF32 split done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hlo + 2);
+  constexpr int kSchedR = 8;       // tile-scheduler ring depth (> tiles the producer may lead the epilogue by)
+  uint64_t* sfull = hlo + 3;       // ring slot published
+  uint64_t* sempty = sfull + kSchedR;  // ring slot read by every consumer warp (on the leader)
+  long long* sids = reinterpret_cast<long long*>(sempty + kSchedR);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -186,6 +190,13 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       mbar_init(&hfull[a], 1);
       mbar_init(&hempty[a], 1);
       mbar_init(&hlo[a], 128 * (PAIR ? 2 : 1));
+    }
+    // consumers of the tile ring: the MMA warp, the peer's producer, every
+    // epilogue / splitter warp of both CTAs (all arrive on the leader's copy)
+    const uint32_t n_sched = 1u + (PAIR ? 1u : 0u) + (uint32_t)(4 * kEpiGroups + (kSplit ? 4 : 0)) * (PAIR ? 2u : 1u);
+    for (int r = 0; r < kSchedR; ++r) {
+      mbar_init(&sfull[r], 1);
+      mbar_init(&sempty[r], n_sched);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmap);
@@ -208,6 +219,61 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   const int slots = p.acc_slots;
   const uint32_t slot_cols = (uint32_t)(p.levels * p.n_tile);
 
+  // ---- tile scheduler ----
+  // Cluster tile c covers the CTA tiles c*cs + rank (decode_tile). Static
+  // order (p.tile_ctr null): c = cluster + it * clusters. Dynamic: the first
+  // tile is the cluster's own, later ones come from an atomic counter that
+  // the (leader's) producer bumps; it publishes each c through a kSchedR-deep
+  // ring in shared memory (the peer's copy written over DSMEM), and every
+  // consumer warp reads the same sequence. Keeps the CTAs' in-flight tiles a
+  // compact window (halo neighbours meet in L2) and leaves no drift tail.
+  const long long n_ct = num_tiles / cs, n_cl = (long long)gridDim.x / cs, c_first = (long long)blockIdx.x / cs;
+  const bool dyn = p.tile_ctr != nullptr;
+  auto sched_read = [&](int it, bool one_lane) -> long long {
+    if (!dyn || it == 0) {  // the first tile is the cluster's own in both orders
+      const long long c = c_first + (long long)it * n_cl;
+      return c < n_ct ? c : -1;
+    }
+    const int slot = (it - 1) & (kSchedR - 1);  // ring entry j = it - 1 holds tile it
+    const uint32_t ph = (uint32_t)((it - 1) / kSchedR) & 1u;
+    if (PAIR && crank != 0) mbar_wait_cluster(&sfull[slot], ph);
+    else mbar_wait(&sfull[slot], ph);
+    const long long c = *reinterpret_cast<volatile long long*>(&sids[slot]);
+    if (!one_lane) __syncwarp();
+    if (one_lane || lane == 0) {  // CTA-scope arrive on the leader (a cluster release would
+      if (PAIR && crank != 0) mbar_arrive_leader(&sempty[slot]);  // stall the MMA warp)
+      else mbar_arrive(&sempty[slot]);
+    }
+    return c;
+  };
+  // The leader's producer publishes tile it+1 early in tile it (after the
+  // tile's first A load, so the release / DSMEM store never delays it; the
+  // peer's producer finds the id ready), and bumps the counter one tile
+  // earlier still (the atomic's round trip overlaps a tile).
+  unsigned long long ahead = 0;  // counter value requested during the previous tile
+  long long c_next = -1;         // published id of the next tile
+  auto sched_cur = [&](int it) -> long long {  // the (leader's) producer
+    if (!dyn || it == 0) {
+      const long long c = c_first + (long long)it * n_cl;
+      return c < n_ct ? c : -1;
+    }
+    return c_next;
+  };
+  auto sched_pub = [&](int it) {  // once per tile it >= 0 of the leader's producer
+    if (!dyn) return;
+    if (it == 0) ahead = atomicAdd(p.tile_ctr, 1ull);
+    long long n = n_cl + (long long)ahead;
+    if (n >= n_ct) n = -1;
+    else ahead = atomicAdd(p.tile_ctr, 1ull);
+    const int slot = it & (kSchedR - 1);  // ring entry j = it holds tile it + 1
+    const uint32_t ph = (uint32_t)(it / kSchedR) & 1u;
+    mbar_wait(&sempty[slot], ph ^ 1u);
+    sids[slot] = n;
+    if constexpr (PAIR) st_remote_arrive(&sids[slot], n, &sfull[slot], 1);
+    mbar_arrive(&sfull[slot]);
+    c_next = n;
+  };
+
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
@@ -227,7 +293,12 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         if constexpr (PAIR) tma_load_2d_cg2(sB, &bmap, &full[stage], 0, (int)((off + (size_t)crank * b_cta) >> 9));
         else bulk_load(sB, p.b_img + off, p.b_bytes, &full[stage]);
       };
-      for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int it = 0;; ++it) {
+        const bool leader = !PAIR || crank == 0;
+        const long long c = leader ? sched_cur(it) : sched_read(it, true);
+        if (c < 0) break;
+        bool published = !leader;  // the leader publishes the next tile once per tile
+        const long long t = c * cs;
         int nt, tx, ty, tz, b;
         decode_tile(p, t, crank, nt, tx, ty, tz, b);
         const int x0 = tx * p.tx - p.pad, y0 = ty * p.ty - p.pad, z0 = tz * p.tz - p.pad;
@@ -247,6 +318,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 load_a_box<PAIR && !kAOwn>(p, hA + (size_t)d * p.a_bytes, &tmap, &hfull[hsl], x0, y0, g0, bb);
             }
             if (++hsl == HS) { hsl = 0; hphase ^= 1; }
+            if (!published) { sched_pub(it); published = true; }
             for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
               const int nq = min(p.tps, nQ - q0);
               mbar_wait(&empty[stage], phase ^ 1);
@@ -259,6 +331,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               if (++stage == S) { stage = 0; phase ^= 1; }
             }
           }
+          if (!published) sched_pub(it);
           continue;
         }
         for (int kit = 0; kit < p.k_iters; ++kit) {
@@ -280,7 +353,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           }
           load_b(nt, kit);
           if (++stage == S) { stage = 0; phase ^= 1; }
+          if (!published) { sched_pub(it); published = true; }
         }
+        if (!published) sched_pub(it);
       }
     }
   } else if (warp == 1 && (!PAIR || crank == 0)) {
@@ -319,7 +394,8 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
     const uint32_t h_dx = (uint32_t)ncol;                                  // next tap along x
     const uint32_t h_wrap_x = (uint32_t)((p.hx - df) * ncol);              // x wrapped: next halo row
     const uint32_t h_wrap_y = (uint32_t)((p.hy - df) * p.hx * ncol);       // y wrapped: next halo plane
-    for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int it = 0;; ++it) {
+      if (sched_read(it, false) < 0) break;
       const long long dbg_w0 = p.dbg_acc ? clock64() : 0;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
@@ -561,7 +637,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                                        : (p.k == 2 ? (long long)p.res_side * p.res_side : (long long)p.res_side);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int it = 0;; ++it) {
+      const long long c = sched_read(it, false);
+      if (c < 0) break;
+      const long long t = c * cs;
       int nt, tx, ty, tz, b;
       const bool real = decode_tile(p, t, crank, nt, tx, ty, tz, b);
       const int ox = tx * p.tx + lx, oy = ty * p.ty + ly, oz = tz * p.tz + lz;
@@ -997,7 +1076,8 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       uint32_t phase = 0;
       int hsl = 0;
       uint32_t hphase = 0;
-      for (long long t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int it = 0;; ++it) {
+        if (sched_read(it, false) < 0) break;
         if (p.halo) {
           for (int gsi = 0; gsi < p.n_gs; ++gsi) {
             mbar_wait(&hfull[hsl], hphase);
@@ -1020,6 +1100,12 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   tc_fence_before();
   __syncthreads();
   if (cs > 1) cluster_sync();  // no CTA leaves while its pair may still touch its smem / TMEM
+  if (p.dbg_acc && threadIdx.x == 0) {  // timing instrumentation: spread of the CTAs' finish times
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    atomicMax(p.dbg_acc + 6, t_end);
+    atomicMax(p.dbg_acc + 7, ~t_end);
+  }
   if (warp == 2) {
     tc_fence_after();
     if constexpr (PAIR) tmem_dealloc_cg2(tmem_base, p.tmem_cols);

@@ -159,6 +159,7 @@ struct ConvKParams {
   const float* act_b;         // (C_out) Linear bias
   float act_K;                // K as float (Mean divisor)
   unsigned* amax_out;         // int8 epilogue: per-sample atomicMax of |stored value| (float bits), or null
+  unsigned long long* tile_ctr;  // dynamic tile scheduler: zeroed work counter (cluster tiles), or null = static order
 };
 
 struct ActParams {

@@ -115,3 +115,35 @@ def test_cfg5_shape_other_modes(prec, tol):
     e = O.max_rel_error(y, r, floor=float(np.abs(r).max()))
     print(f"cfg5 {prec} normwise max_rel_error {e:.3e}")
     assert e <= tol
+
+
+def _plan(g, C, d, prec):
+    from paper_2507_01040_b200 import _lib
+    lib = _lib.load()
+    out = (_lib.C.c_int64 * 16)()
+    _lib.check(lib.cl_conv_plan_info(_lib.int32_array(g), len(g), C, C, d, 3, 1, M.conv.PRECISIONS[prec], out))
+    return list(out)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16", "tf32", "3xtf32"])
+def test_cfg5_dynamic_tile_order_bit_exact(prec):
+    """Long launches (>= 128 tiles per CTA, capi.cu) take their tiles from an
+    atomic counter (conv_tc.cu tile ring); short ones keep the static order.
+    A batch just past the threshold must equal the same samples run as
+    2-sample blocks (static order) bit for bit: every output tile is computed
+    the same way whichever CTA takes it."""
+    spec = W.CONFIGS[5]
+    pl = _plan(spec.g, spec.C, spec.d, prec)
+    n_ntiles, tx, ty, tz = pl[8], pl[9], pl[10], pl[11]
+    m_tiles = -(-spec.d // tx) * -(-spec.d // ty) * -(-spec.d // tz)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    B = -(-128 * sms // (m_tiles * n_ntiles)) + 1
+    blk, _ = _block(spec, B, prec)
+    x = W.make_input(spec, 0, B)
+    y = M.block_forward(x, blk)
+    blk2, _ = _block(spec, 2, prec)
+    for i in (0, B // 2 - 1, B - 2):
+        y2 = M.block_forward(x[i:i + 2].contiguous(), blk2)
+        assert torch.equal(y2, y[i:i + 2]), f"{prec} B={B} samples {i}..{i + 1}"
+    del x, y
+    torch.cuda.empty_cache()
