@@ -116,7 +116,9 @@ int cl_conv_out_side(const cl_conv* h, int* d_out);
 /* x_dev (B, C_in, d_image^k, N_B) -> y_dev (B, C_out, d_out^k, N_B) */
 int cl_conv_forward(const cl_conv* h, const float* x_dev, float* y_dev, int64_t B, void* stream);
 /* explicit-workspace variant: ws (device) of >= cl_conv_workspace_bytes(h, B) bytes
- * (int8 digit planes of the input in fp32 mode, packed bf16 input in bf16 mode).
+ * (int8 digit planes of the input in fp32 mode, packed bf16 input in bf16 mode,
+ * then 256 bytes for the tile scheduler's work counter; contents need not be
+ * initialised, and concurrent calls need distinct workspaces).
  * cl_conv_forward uses a per-(handle, stream) cached workspace instead. */
 size_t cl_conv_workspace_bytes(const cl_conv* h, int64_t B);
 int cl_conv_forward_ws(const cl_conv* h, const float* x_dev, float* y_dev, int64_t B, void* ws,
