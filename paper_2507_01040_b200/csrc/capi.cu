@@ -841,6 +841,7 @@ static size_t conv_ws_bytes(const cl_conv* h, long long B, bool prepacked) {
   return conv_ws_operand_bytes(h, B, prepacked) + kSchedBytes;
 }
 static bool g_static_tiles = getenv("CL_STATIC_TILES") != nullptr;  // A/B: static round-robin tile order
+static bool g_dyn_tiles = getenv("CL_DYN_TILES") != nullptr;  // tests: dynamic order for every launch
 
 // Run one conv on device buffers. `xbf` (optional) is an already packed bf16
 // A-ready input (bf16 layers); otherwise x is sliced / packed here into `ws`
@@ -980,7 +981,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   // matters: cfg5 B=256 block +2.3 % (fp32) / +3.7 % (bf16) sustained, DRAM
   // reads of a conv 58.6 -> 17.3 GB. Short launches keep the static order:
   // the ring hand-off cost ~3 % at cfg4 B=16 bf16 (52 tiles per CTA).
-  if (!g_static_tiles && p.num_tiles >= 128LL * grid) {
+  if (!g_static_tiles && (g_dyn_tiles || p.num_tiles >= 128LL * grid)) {
     p.tile_ctr = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) +
                                                        conv_ws_operand_bytes(h, B, xbf != nullptr));
     CL_CUDA(cudaMemsetAsync(p.tile_ctr, 0, sizeof(unsigned long long), s), "tile counter reset");

@@ -1,7 +1,9 @@
 """GPU parity of the kernel variants the planner can switch off (1-SM MMA,
 per-tap A loads, per-pixel TMA lines, one tap per B stage, generic basis
 inverse, separate absmax pass, generic digit slicing, the small-layer fused
-absmax + slice launch and graph replay). The switches are
+absmax + slice launch and graph replay) and the dynamic tile order forced on
+every launch (CL_DYN_TILES: 1-D / 2-D / 3-D, paired and 1-SM, the 3xTF32
+splitter). The switches are
 read once when the library loads, so each variant runs in a fresh process;
 the default variant is covered by test_gpu_parity.py. Same tolerances."""
 
@@ -61,7 +63,8 @@ def _run(env_extra):
 @pytest.mark.parametrize("flags", [{"CL_NO_PAIR": "1"}, {"CL_NO_HALO": "1"}, {"CL_NO_TMA_MERGE": "1"},
                                    {"CL_TPS": "1"}, {"CL_BASIS_2D": "1"}, {"CL_NO_BASIS": "1"}, {"CL_NO_BASIS_2D": "1"},
                                    {"CL_NO_BCLS": "1", "CL_NO_FUSED_AMAX": "1", "CL_NO_SLICE_FIXED": "1"},
-                                   {"CL_NO_FUSED_PREP": "1", "CL_NO_GRAPH": "1"}],
+                                   {"CL_NO_FUSED_PREP": "1", "CL_NO_GRAPH": "1"},
+                                   {"CL_DYN_TILES": "1"}, {"CL_DYN_TILES": "1", "CL_NO_PAIR": "1"}],
                          ids=lambda f: ",".join(f))
 def test_variant_parity(flags):
     if not torch.cuda.is_available():
