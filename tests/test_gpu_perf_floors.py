@@ -1,0 +1,72 @@
+"""Performance floors at the north-star targets (BASELINE.json), in the spirit
+of the reference's relative-speedup acceptance floors (tests/test_acceptance.py:256-299):
+the standalone activation reaches >= 70 % of 8 TB/s, and the 3-D conv (cfg4,
+fp32-accurate mode) >= 60 % of its tensor-core roofline. Median of event-timed
+launches after warm-up; the measured values sit well above the floors
+(6.5 TB/s, 1.0 of roofline)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2507_01040_b200 as M  # noqa: E402
+from paper_2507_01040_b200 import workloads as W  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _median_ms(fn, reps=20, warm=5, inner=1):
+    """Median over `reps` event-timed groups of `inner` back-to-back calls, per call."""
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(inner):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / inner)
+    return float(np.median(ts))
+
+
+def test_activation_hbm_floor():
+    spec = W.CONFIGS[2]
+    wgt, bias = W.act_params(spec)
+    cfg = M.make_activation_config(M.Signature(spec.g), spec.mode, tuple(range(spec.nb)), wgt, bias)
+    x = W.make_input(spec, 0, spec.B)
+    y = torch.empty_like(x)
+    ms = _median_ms(lambda: M.activation_forward(x, cfg, out=y), inner=20)
+    tbs = 2 * x.numel() * 4 / (ms * 1e-3) / 1e12
+    print(f"cfg2 activation {tbs:.2f} TB/s")
+    assert tbs >= 0.70 * 8.0
+
+
+def test_conv3d_tensor_roofline_floor():
+    spec = W.CONFIGS[4]
+    f, b = W.conv_params(spec, 1)
+    layer = M.make_conv_layer(M.Dims(spec.B, spec.C, spec.C, spec.d, spec.d_filter, spec.k), M.Signature(spec.g), f, b,
+                              padding=spec.padding)
+    x = W.make_input(spec, 0, spec.B)
+    y = torch.empty(layer.output_shape(), device="cuda")
+    ms = _median_ms(lambda: M.conv_forward(x, layer, out=y), reps=10, warm=3)
+    tflops = M.conv_flops(layer.dims, layer) / (ms * 1e-3) / 1e12
+    # fp32 mode roofline: measured cuBLAS int8 burst / 10 digit MMAs, x2 under the change of basis
+    peaks = json.load(open(os.path.join(ROOT, "profiles", "r01_mode_peaks.json")))
+    roof = float(peaks["int8_tops"]) / 10 * 2
+    print(f"cfg4 conv {ms:.3f} ms = {tflops:.0f} TFLOP/s = {tflops / roof:.2f} of {roof:.0f}")
+    assert tflops >= 0.60 * roof
