@@ -79,6 +79,8 @@ def mode_peak(precision, peaks, sustained=True):
 # figures without 2:4 sparsity), per mode in algorithmic-equivalent TFLOP/s before
 # the change-of-basis factor: bf16 2250, tf32 1125, int8 4500 TOPS / 10, tf32 / 3.
 NOMINAL_MODE_PEAK = {"bf16": 2250.0, "tf32": 1125.0, "3xtf32": 375.0, "fp32": 450.0}
+# executed GEMM FLOP of a mode -> bf16-dense-equivalent MMA work (see roofline.vs_MEASURED_PEAKS_bf16)
+BF16_EQUIV = {"bf16": 1.0, "tf32": 2.0, "3xtf32": 6.0, "fp32": 5.0}
 
 
 def ncu_traffic(spec, prec, batch):
@@ -582,6 +584,13 @@ def run_ours(args):
                          "executed_tflops": achieved * gemm_ratio, "executed_peak": exec_peak_burst,
                          "executed_frac": achieved * gemm_ratio / exec_peak_burst,
                          "executed_frac_of_nominal": achieved * gemm_ratio / NOMINAL_MODE_PEAK[prec],
+                         # the same kernel against MEASURED_PEAKS.json's own bf16 figure: executed MMA
+                         # work in bf16-dense-equivalent units (an int8 MMA runs at 2x, a tf32 MMA at
+                         # 1/2x the bf16 rate; fp32 mode = 10 int8 MMAs, 3xtf32 = 3 tf32 MMAs)
+                         "vs_MEASURED_PEAKS_bf16": {
+                             "peak": peaks["bf16_tflops"], "peak_kind": peak_kind + " burst",
+                             "achieved_bf16_equiv": achieved * gemm_ratio * BF16_EQUIV[prec],
+                             "frac": achieved * gemm_ratio * BF16_EQUIV[prec] / peaks["bf16_tflops"]},
                          "kernel_share_of_step": conv_share},
             "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": cpu, "output_gather": gather,
             "clocks": clk.summary(),
