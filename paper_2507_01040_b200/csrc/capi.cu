@@ -1022,7 +1022,10 @@ static int host_chunked(HostPipe& hp, long long B, size_t in_per, size_t out_per
   if (B == 0) return CL_OK;
   std::lock_guard<std::mutex> lk(hp.m);
   if (chunk <= 0) {
-    const size_t target = (size_t)512 << 20;  // ~512 MB of input per chunk
+    // ~256 MB of input per chunk: cfg5 block e2e (tools/e2e_chunks.py) measured
+    // best at 2-4 samples (134-268 MB): fp32 656 vs 646 samples/s at 7, bf16
+    // (PCIe-bound) 704 vs 687
+    const size_t target = (size_t)256 << 20;
     chunk = std::max<long long>(1, (long long)(target / std::max<size_t>(in_per, 1)));
     // at least ~8 chunks when the batch allows: the first H2D and the last D2H
     // are not overlapped, so their share shrinks with the chunk count
