@@ -421,7 +421,13 @@ __device__ __forceinline__ void tmem_ld_wait() {
 // (two's-complement bytes of the rounded fixed-point value).
 #if defined(__CUDACC__)
 // power-of-two s with amax * 128/126 <= s: the leading digit stays in [-127, 127]
+// |v| as float bits, for max-reductions as unsigned integers: NaN (> Inf >
+// any finite) sticks, where fmaxf would drop it.
+__device__ __forceinline__ unsigned abs_bits(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+// Power-of-two scale above amax; NaN when amax is not finite, so a sample
+// holding Inf / NaN comes out NaN in the exact mode instead of as digits of garbage.
 __device__ __forceinline__ float pow2_scale_for(float amax) {
+  if (!(amax <= 3.4028235e38f)) return __uint_as_float(0x7fc00000u);
   if (!(amax > 0.f)) return 1.f;
   int e;
   frexpf(amax * 1.016f, &e);

@@ -814,7 +814,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           atomicAdd(p.dbg_acc + 1, 1ull);
         }
         if (++acc == slots) { acc = 0; acc_phase ^= 1; }
-        float ymax = 0.f;  // max |stored value| of this thread (fused absmax for the next conv)
+        unsigned ymax = 0;  // max |stored value| of this thread as float bits, NaN-sticky (fused absmax for the next conv)
         if (valid && !(p.dbg_skip & 4))
 #pragma unroll
         for (int ci = 0; ci < kHold / CH; ++ci) {
@@ -850,7 +850,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                   else *reinterpret_cast<float4*>(yp) = make_float4(h[0], h[1 % W], h[2 % W], h[3 % W]);
                 }
 #pragma unroll
-                for (int j = 0; j < W; ++j) ymax = fmaxf(ymax, fabsf(h[j]));
+                for (int j = 0; j < W; ++j) ymax = max(ymax, abs_bits(h[j]));
               } else {
                 if (cc >= CH / NB) break;
                 float v[NB];
@@ -880,18 +880,18 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                   }
                 }
 #pragma unroll
-                for (int j = 0; j < NB; ++j) ymax = fmaxf(ymax, fabsf(v[j]));
+                for (int j = 0; j < NB; ++j) ymax = max(ymax, abs_bits(v[j]));
               }
             }
           }
         }
         if (p.amax_out) {
           if (p.k == 1) {  // 1-D: rows of one tile belong to different samples
-            if (valid) atomicMax(p.amax_out + b, __float_as_uint(ymax));
+            if (valid) atomicMax(p.amax_out + b, ymax);
           } else {  // one sample per tile: reduce over the warp first
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) ymax = fmaxf(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
-            if (lane == 0 && real) atomicMax(p.amax_out + b, __float_as_uint(ymax));
+            for (int o = 16; o > 0; o >>= 1) ymax = max(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
+            if (lane == 0 && real) atomicMax(p.amax_out + b, ymax);
           }
         }
         continue;

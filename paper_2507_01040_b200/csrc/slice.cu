@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(256) absmax_kernel(const float* __restrict__ x
                                                      unsigned* __restrict__ amax) {
   const int b = blockIdx.y;
   const float* xs = x + (long long)b * per_sample;
-  float m = 0.f;
+  unsigned m = 0;  // max |x| as float bits (NaN-sticky)
   // samples need not start 16-byte aligned (1-D tensors): scalar head, float4 body, scalar tail
   long long head = (long long)((16 - (reinterpret_cast<uintptr_t>(xs) & 15)) & 15) / 4;
   if (head > per_sample) head = per_sample;
@@ -36,20 +36,20 @@ __global__ void __launch_bounds__(256) absmax_kernel(const float* __restrict__ x
     v[u] = base + u * 256 < n4 ? __ldcs(x4 + base + u * 256) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int u = 0; u < kAbsmaxU; ++u)
-    m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+    m = max(m, max(max(abs_bits(v[u].x), abs_bits(v[u].y)), max(abs_bits(v[u].z), abs_bits(v[u].w))));
   if (blockIdx.x == 0) {
-    if (threadIdx.x < head) m = fmaxf(m, fabsf(xs[threadIdx.x]));
-    for (long long i = head + n4 * 4 + threadIdx.x; i < per_sample; i += blockDim.x) m = fmaxf(m, fabsf(xs[i]));
+    if (threadIdx.x < head) m = max(m, abs_bits(xs[threadIdx.x]));
+    for (long long i = head + n4 * 4 + threadIdx.x; i < per_sample; i += blockDim.x) m = max(m, abs_bits(xs[i]));
   }
-  __shared__ float red[8];
+  __shared__ unsigned red[8];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
-    atomicMax(amax + b, __float_as_uint(m));
+    for (int w = 1; w < 8; ++w) m = max(m, red[w]);
+    atomicMax(amax + b, m);
   }
 }
 
@@ -218,33 +218,33 @@ template <int NB, bool BASIS, bool FIXED = false>
 __global__ void __launch_bounds__(256) absmax_slice_kernel(const float* __restrict__ x, int8_t* __restrict__ out,
                                                            float* __restrict__ scale, long long B, int C, long long P,
                                                            int G, Basis bs) {
-  __shared__ float red[8];
+  __shared__ unsigned red[8];  // max |x| as float bits (NaN-sticky)
   __shared__ float cmax;
   const int rank = (int)cluster_ctarank();
   const long long b = blockIdx.x / kSliceCluster;
   const long long per_sample = (long long)C * P * NB;
   const float* xs = x + b * per_sample;
-  float m = 0.f;
+  unsigned m = 0;
   const long long n0 = per_sample * rank / kSliceCluster, n1 = per_sample * (rank + 1) / kSliceCluster;
-  for (long long i = n0 + threadIdx.x; i < n1; i += blockDim.x) m = fmaxf(m, fabsf(__ldg(xs + i)));
+  for (long long i = n0 + threadIdx.x; i < n1; i += blockDim.x) m = max(m, abs_bits(__ldg(xs + i)));
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
-    float v = 0.f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmaxf(v, red[w]);
-    cmax = v;
+    unsigned v = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = max(v, red[w]);
+    cmax = __uint_as_float(v);
   }
   cluster_sync();  // every CTA's share is in its cmax
   if (threadIdx.x == 0) {
-    float v = 0.f;
-    for (int r = 0; r < kSliceCluster; ++r) v = fmaxf(v, ld_shared_cluster_f32(&cmax, r));
+    unsigned v = 0;
+    for (int r = 0; r < kSliceCluster; ++r) v = max(v, __float_as_uint(ld_shared_cluster_f32(&cmax, r)));
     red[0] = v;
   }
   cluster_sync();  // peers done reading cmax (no CTA exits while it is read)
   __syncthreads();
-  const float amx = red[0];
+  const float amx = __uint_as_float(red[0]);
   const long long total = B * G * P;
   const long long items = (long long)G * P;
   const long long i0 = items * rank / kSliceCluster, i1 = items * (rank + 1) / kSliceCluster;
@@ -337,7 +337,7 @@ __global__ void weight_colscale_kernel(Sig sg, const float* __restrict__ f, int 
   const int w = bs.on ? bs.w : nb;
   const int n = blockIdx.x;
   const int co = n / w, t = n % w;
-  float m = 0.f;
+  unsigned m = 0;  // max |entry| as float bits (NaN-sticky: a NaN filter gives a NaN scale)
   // under a change of basis all w columns of a channel share one scale, so the
   // epilogue can combine the two column terms of the inverse as exact integers
   const int t0 = bs.on ? 0 : t, t1 = bs.on ? w : t + 1;
@@ -349,18 +349,18 @@ __global__ void weight_colscale_kernel(Sig sg, const float* __restrict__ f, int 
         const int ci = idx / (Q * w);
         const double e = bs.on ? basis_entry(sg, bs, f, C_in, C_out, Q, co, tt, ci, j, q)
                                : (double)expanded_entry(sg, f, nb, C_in, C_out, Q, co, tt, ci, j, q);
-        m = fmaxf(m, (float)fabs(e));
+        m = max(m, abs_bits((float)e));
       }
   }
-  __shared__ float red[32];
+  __shared__ unsigned red[32];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww) m = fmaxf(m, red[ww]);
+    for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww) m = max(m, red[ww]);
     // float rounding of |e| may round down: one more power of two of headroom is free
-    w_scale[n] = pow2_scale_for(m * 1.0000002f);
+    w_scale[n] = pow2_scale_for(__uint_as_float(m) * 1.0000002f);
   }
 }
 

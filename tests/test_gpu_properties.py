@@ -97,3 +97,51 @@ def test_activation_gate_scale_covariance(mode, alpha):
     s2 = s_of((np.float32(alpha) * x).astype(np.float32))
     ok = np.abs(alpha * s1) < 6
     np.testing.assert_allclose(s2[ok], alpha * s1[ok], rtol=1e-3, atol=1e-4)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "3xtf32", "tf32", "bf16"])
+@pytest.mark.parametrize("g", [(1, 1), (1, 1, 1), (1, -1, 0)])
+def test_conv_non_finite_inputs(prec, g):
+    """A NaN / Inf in a sample's input never turns into finite garbage: every
+    output the fp64 oracle gives as non-finite is non-finite here too (the
+    exact mode's per-sample scale becomes NaN, so that whole sample is NaN),
+    and the other samples are untouched."""
+    import oracle as O
+    k = len(g)
+    nb = 1 << k
+    rng = np.random.default_rng(5)
+    B, C, d, df = 3, 3, 6, 3
+    x = rng.standard_normal((B, C, d ** k, nb)).astype(np.float32)
+    x[1, 0, 7, 1] = np.nan
+    x[2, 2, 3, 0] = np.inf
+    f = rng.uniform(-1, 1, (nb, C, C, df ** k)).astype(np.float32) / np.float32(np.sqrt(C * nb * df ** k))
+    b = (rng.standard_normal((nb, C)) * 0.01).astype(np.float32)
+    y = M.conv_forward(torch.from_numpy(x).cuda(), _conv(g, B, C, C, d, df, f, b, prec)).cpu().numpy()
+    with np.errstate(invalid="ignore"):
+        ref = O.conv_ref(x, f, b, g, d, df, 0)
+    bad = ~np.isfinite(ref)
+    assert bad[1].any() and bad[2].any()
+    assert np.all(~np.isfinite(y[bad])), prec
+    assert np.all(np.isfinite(y[0]))
+    assert O.max_rel_error(y[:1], ref[:1], floor=float(np.abs(ref[0]).max())) <= {"fp32": 1e-6, "3xtf32": 1e-4}.get(prec, 2e-2)
+
+
+def test_block_non_finite_input_exact_mode():
+    """The block's fused absmax of y1 (conv1 epilogue) keeps a NaN too."""
+    import oracle as O
+    rng = np.random.default_rng(9)
+    g, B, C, d, nb = (1, 1, 1), 2, 4, 6, 8
+    fan = C * nb * 27
+    f1 = rng.uniform(-1, 1, (nb, C, C, 27)).astype(np.float32) / np.float32(np.sqrt(fan))
+    f2 = rng.uniform(-1, 1, (nb, C, C, 27)).astype(np.float32) / np.float32(np.sqrt(fan))
+    b1 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
+    b2 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
+    x = rng.standard_normal((B, C, d ** 3, nb)).astype(np.float32)
+    x[1, 1, 100, 3] = np.nan
+    blk = M.make_basic_block(M.Signature(g), B, C, C, C, d, f1, b1, 2, f2, b2, padding="same", residual=True)
+    y = M.block_forward(torch.from_numpy(x).cuda(), blk).cpu().numpy()
+    with np.errstate(invalid="ignore"):
+        ref = O.block_ref(x, g, d, f1, b1, 2, tuple(range(nb)), None, None, f2, b2, padding="same", residual=True)
+    bad = ~np.isfinite(ref)
+    assert bad[1].any() and np.all(~np.isfinite(y[bad]))
+    assert O.max_rel_error(y[:1], ref[:1]) <= 1e-4
