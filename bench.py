@@ -10,13 +10,17 @@ inputs resident in HBM; `value` is samples/s of the whole job.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config 5] [--precision fp32|3xtf32|tf32|bf16]
 
-Under torchrun (N > 1) every rank takes a contiguous slice of the batch;
-NCCL is used only to broadcast the compact weights from rank 0 and to reduce
-the per-rank times (max) -- the data path has no collective.
+With --gpus N > 1 outside torchrun the script re-executes itself under
+torch.distributed.run with N ranks (one per GPU). Every rank takes a
+contiguous slice of the batch; NCCL is used only to broadcast the compact
+weights from rank 0 and to reduce the per-rank times (max) -- the data path
+has no collective.
 
---impl reference times the reference algorithm on the host CPU (the oracle
-port, oracle/oracle.py, multi-threaded BLAS) on a bounded sample of the same
-workload; rank 0 only.
+--impl reference times the reference's own fastest CPU path (the unmodified
+package in baseline/_ref, 'specialized' variants, one pinned process per host
+core; baseline/ref_cpu.py) on a bounded sample of the same workload, rank 0
+only; the oracle port (oracle/oracle.py) stands in only if baseline/_ref is
+missing.
 """
 
 from __future__ import annotations
@@ -166,14 +170,41 @@ class ClockSampler:
                               "200 ms sampling period)"} if getattr(self, "extended", False) else {})}
 
 
+def _free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec this script
+    under torch.distributed.run with one rank per GPU (the form the driver's
+    scaling run may use), so --gpus is never silently ignored."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execvp(cmd[0], cmd)
+
+
 def dist_setup(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a "
+                         f"{world}-rank run as {args.gpus} GPUs")
+    shared = bool(os.environ.get("BENCH_SHARE_GPU"))
+    if world > 1 and not shared and torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPU(s) "
+                         "(BENCH_SHARE_GPU=1 validates the multi-rank path on one GPU, labelled as such)")
+    backend = None
     if world > 1:
         import torch.distributed as dist
-        if os.environ.get("BENCH_SHARE_GPU"):
+        if shared:
             # validation of the multi-rank code path on a 1-GPU box: every rank on
             # cuda:0, gloo for the (host-side) broadcast / max-reduce; no kernel of
             # one rank ever waits on another rank
@@ -183,9 +214,39 @@ def dist_setup(args):
         else:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = dist.get_backend()
+        if dist.get_world_size() != args.gpus:
+            raise SystemExit(f"bench.py: process group has {dist.get_world_size()} ranks, --gpus {args.gpus}")
     else:
         torch.cuda.set_device(0)
+    args.backend = backend
+    args.shared_gpu = shared and world > 1
     return world, rank, local
+
+
+def dist_config(args, world):
+    """The parallelism fields of the JSON line's config."""
+    if world == 1:
+        return {"parallelism": "single GPU", "nranks": 1}
+    if args.shared_gpu:
+        return {"parallelism": f"batch-sharded x{world} ranks SHARING cuda:0 (multi-rank path validation, not a "
+                               f"scaling number)", "nranks": world, "shared_gpu": True, "backend": args.backend}
+    return {"parallelism": f"batch-sharded x{world}, {args.backend.upper()} broadcast of weights only",
+            "nranks": world, "backend": args.backend}
+
+
+def arm_config(spec, args, world, mode=None):
+    """The `config` object of the JSON line -- identical for both arms at the
+    same N (the reference arm reports the workload it is measured on)."""
+    from paper_2507_01040_b200 import workloads as W
+    lo, hi = W.shard(spec.B, 0, world)
+    per_rank_gb = (hi - lo) * spec.C * spec.P * spec.nb * 4 / 1e9
+    if spec.kind == "activation":
+        return {"workload": spec.name, "global_batch": spec.B, "mode": spec.mode if mode is None else mode,
+                **dist_config(args, world), "l2": "inputs larger than L2 (%.2f GB)" % per_rank_gb}
+    return {"workload": spec.name, "global_batch": spec.B, "per_rank_batch": hi - lo,
+            "precision": args.precision, "padding": spec.padding, **dist_config(args, world),
+            "l2": "inputs larger than L2 (%.1f GB per rank)" % per_rank_gb}
 
 
 def _gloo():
@@ -285,36 +346,63 @@ def verify(y, ref, prec):
     return {"metric": metric, "error": float(err), "tol": tol}
 
 
+def reference_cpu(spec, steps, warmup):
+    """The reference's own fastest CPU path (baseline/_ref, one pinned process
+    per host core, baseline/ref_cpu.py); None when it is not installed."""
+    sys.path.insert(0, ROOT)
+    from baseline import ref_cpu
+    why = ref_cpu.unavailable()
+    if why:
+        return None, why
+    return ref_cpu.time_reference(spec, steps=steps, warmup=warmup), None
+
+
 def run_reference(args):
-    """--impl reference: the reference algorithm on host cores (rank 0 only)."""
+    """--impl reference: the reference's own CPU implementation of the path on
+    the host cores (rank 0 only). Its fastest variants ('specialized' conv and
+    activation, composed into the block) from the unmodified package in
+    baseline/_ref; the oracle port (oracle/oracle.py) only if that is absent."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from paper_2507_01040_b200 import workloads as W
     spec = W.CONFIGS[args.config]
-    cores = os.cpu_count()
-    fn = cpu_sample_fn(spec)
-    n = 8 if spec.kind == "activation" else 1  # samples per step: a bounded share of the workload
-    for _ in range(args.warmup):
-        fn(spec, n_samples=n) if args.warmup_cpu else None
-    times = []
-    for _ in range(args.steps):
-        times.append(fn(spec, n_samples=n)[0])
-    t = float(np.mean(times))
-    if spec.kind == "activation":  # same metric / unit as the activation arm: GB/s of read + write
-        metric, unit, value = ACT_METRIC, "GB/s", 2 * n * spec.C * spec.P * spec.nb * 4 / t / 1e9
+    n_gpus = max(world, args.gpus)
+    args.shared_gpu, args.backend = bool(os.environ.get("BENCH_SHARE_GPU")) and n_gpus > 1, \
+        ("gloo" if os.environ.get("BENCH_SHARE_GPU") else "nccl")
+    r, why = reference_cpu(spec, args.steps, args.warmup)
+    if r is not None:
+        if spec.kind == "activation":
+            metric, unit, value = ACT_METRIC, "GB/s", r["gbs"]
+        else:
+            metric, unit, value = METRIC, "samples/s", r["samples_per_s"]
+        cpu = {"value": value, "unit": unit, "cores": r["cores"], "kind": "reference",
+               "sample": r["sample"], "per_sample_s_per_core": r["per_sample_s"], "jit_s_excluded": r["jit_s"],
+               "impl": "baseline/_ref mvkernels (unmodified reference package), variant 'specialized'"}
+        t = r["step_s"]
+        dtype = "f32 (reference numba kernels)"
     else:
-        metric, unit, value = METRIC, "samples/s", n / t
+        # fallback: the oracle port on one sample per step, all host threads (BLAS)
+        cores = os.cpu_count()
+        fn = cpu_sample_fn(spec)
+        n = 8 if spec.kind == "activation" else 1
+        times = [fn(spec, n_samples=n)[0] for _ in range(args.steps)]
+        t = float(np.mean(times))
+        if spec.kind == "activation":
+            metric, unit, value = ACT_METRIC, "GB/s", 2 * n * spec.C * spec.P * spec.nb * 4 / t / 1e9
+        else:
+            metric, unit, value = METRIC, "samples/s", n / t
+        cpu = {"value": value, "unit": unit, "cores": cores, "kind": "port", "unavailable_reference": why,
+               "sample": f"{n} sample(s) of {spec.name} per step, oracle/oracle.py (numpy, multithreaded BLAS)"}
+        dtype = "f64 (oracle)"
     line = {
         "impl": "reference", "metric": metric, "value": value, "unit": unit,
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 (oracle)" if spec.kind == "activation" else "f64 (oracle)",
-        "data": "synthetic (seeded, BASELINE.json distributions)",
-        "config": {"workload": spec.name, "global_batch": spec.B, "sample_per_step": n},
-        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port",
-                         "sample": f"{n} sample(s) of {spec.name} per step, oracle/oracle.py (numpy, multithreaded BLAS)"},
+        "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (seeded, BASELINE.json distributions); CPU only, rank 0, no GPU work",
+        "config": arm_config(spec, args, n_gpus),
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -373,16 +461,20 @@ def run_activation(args, spec, world, rank, local, dev, peaks, peak_kind, lib):
         te = max_over_ranks((time.perf_counter() - t0) / max(1, args.e2e_steps), world)
         e2e = {"value": nbytes * world / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": x.numel() * 4 * world,
                "d2h_bytes_per_step": x.numel() * 4 * world}
-    cpu = None
+    cpu = cpu_port = None
     if rank == 0 and world == 1 and not args.no_cpu:
         n = 8  # bounded sample: 8 of the 64 samples
         t_cpu, ref = cpu_act_sample(spec, x[:n].cpu().numpy(), mode=mode)
         M.activation_forward(x, M.make_activation_config(M.Signature(spec.g), mode, tuple(range(spec.nb)),
                                                          wgt if mode == 0 else None, bias if mode == 0 else None),
                              out=y)
-        cpu = {"value": 2 * n * spec.C * spec.P * spec.nb * 4 / t_cpu / 1e9, "unit": "GB/s", "cores": os.cpu_count(),
-               "kind": "port", "sample": f"{n} of {spec.B} samples, oracle/oracle.py activation_ref (numpy fp32)",
-               "verified": verify(y[:n].cpu().numpy(), ref, "act")}
+        cpu_port = {"value": 2 * n * spec.C * spec.P * spec.nb * 4 / t_cpu / 1e9, "unit": "GB/s",
+                    "cores": os.cpu_count(), "kind": "port",
+                    "sample": f"{n} of {spec.B} samples, oracle/oracle.py activation_ref (numpy fp32)",
+                    "verified": verify(y[:n].cpu().numpy(), ref, "act")}
+        r, why = reference_cpu(spec, steps=2, warmup=0)
+        cpu = ({"value": r["gbs"], "unit": "GB/s", "cores": r["cores"], "kind": "reference", "sample": r["sample"]}
+               if r is not None else dict(cpu_port, unavailable_reference=why))
     if rank == 0:
         peak = peaks["hbm_gbs"]
         line = {
@@ -390,14 +482,14 @@ def run_activation(args, spec, world, rank, local, dev, peaks, peak_kind, lib):
             "steps": reps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded, BASELINE.json distributions)",
-            "config": {"workload": spec.name, "global_batch": spec.B, "mode": mode,
-                       "l2": "inputs larger than L2 (%.2f GB)" % (x.numel() * 4 / 1e9)},
+            "config": arm_config(spec, args, world, mode),
             "roofline": {"bound": "hbm", "achieved": gbs / world, "peak": peak, "unit": "GB/s",
                          "frac": gbs / world / peak, "frac_of_8TBs": gbs / world / 8000.0,
                          "traffic": ncu_traffic(spec, f"act{mode}", nloc),
                          "kernel": "act_kernel", "peak_basis": f"{peak_kind} hbm_gbs copy bandwidth"},
             "modes": {str(m): {"ms": v[0] * 1e3, "GB/s": nbytes * world / v[0] / 1e9} for m, v in res.items()},
-            "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": cpu, "clocks": clocks,
+            "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": cpu, "cpu_baseline_port": cpu_port,
+            "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     return 0
@@ -553,14 +645,18 @@ def run_ours(args):
                "path": "block_forward(pinned host tensor) -> cl_block_forward_host (chunked H2D/compute/D2H over 3 streams)"}
         del xh, yh
 
-    cpu = None
+    cpu = cpu_port = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        # the oracle on sample 0 of this run's own input: the CPU baseline's timing,
-        # and the check of the timed output (y holds the last timed step's result)
+        # the oracle on sample 0 of this run's own input: the check of the timed
+        # output (y holds the last timed step's result), timed as a second baseline
         t_cpu, ref = cpu_sample_fn(spec)(spec, x[:1].cpu().numpy())
-        cpu = {"value": 1.0 / t_cpu, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"sample 0 of {spec.name}, oracle/oracle.py (numpy fp64 einsum/BLAS)",
-               "verified": verify(y[:1].cpu().numpy(), ref, prec)}
+        cpu_port = {"value": 1.0 / t_cpu, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+                    "sample": f"sample 0 of {spec.name}, oracle/oracle.py (numpy fp64 einsum/BLAS)",
+                    "verified": verify(y[:1].cpu().numpy(), ref, prec)}
+        r, why = reference_cpu(spec, steps=2, warmup=0)
+        cpu = ({"value": r["samples_per_s"], "unit": "samples/s", "cores": r["cores"], "kind": "reference",
+                "sample": r["sample"], "per_sample_s_per_core": r["per_sample_s"]}
+               if r is not None else dict(cpu_port, unavailable_reference=why))
 
     if rank == 0:
         line = {
@@ -570,10 +666,7 @@ def run_ours(args):
             "dtype": {"fp32": "f32 (int8-slice exact accumulation)", "3xtf32": "f32 (3xTF32)",
                       "tf32": "tf32", "bf16": "bf16"}[prec],
             "data": "synthetic (seeded, BASELINE.json distributions; inputs generated on device)",
-            "config": {"workload": spec.name, "global_batch": spec.B, "per_rank_batch": nloc,
-                       "precision": prec, "padding": spec.padding,
-                       "parallelism": f"batch-sharded x{world}, NCCL broadcast of weights only",
-                       "l2": "inputs larger than L2 (%.1f GB per rank)" % (x.numel() * 4 / 1e9)},
+            "config": arm_config(spec, args, world),
             "tflops": flops_per_sample * spec.B / t_step / 1e12,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(spec, prec, conv_layer.dims.B),
@@ -592,7 +685,8 @@ def run_ours(args):
                              "achieved_bf16_equiv": achieved * gemm_ratio * BF16_EQUIV[prec],
                              "frac": achieved * gemm_ratio * BF16_EQUIV[prec] / peaks["bf16_tflops"]},
                          "kernel_share_of_step": conv_share},
-            "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": cpu, "output_gather": gather,
+            "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": cpu, "cpu_baseline_port": cpu_port,
+            "output_gather": gather,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -618,6 +712,7 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    self_launch(args)
     return run_ours(args)
 
 

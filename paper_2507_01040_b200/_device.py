@@ -79,6 +79,16 @@ def on_device(device):
     return torch.cuda.device(device)
 
 
+def device_input(x):
+    """A CUDA tensor as the C-ABI takes it: fp32, contiguous, 16-byte aligned
+    (a view with a 4-byte storage offset is copied rather than rejected)."""
+    torch = torch_mod()
+    if x.dtype == torch.float32 and x.is_contiguous() and x.data_ptr() % 16 == 0:
+        return x
+    y = x.float().contiguous()
+    return y if y.data_ptr() % 16 == 0 else y.clone()
+
+
 def to_device_f32(arr, device=None):
     """Contiguous fp32 CUDA copy of a numpy array / tensor."""
     torch = _lib.require_cuda()

@@ -17,7 +17,7 @@ import numpy as np
 from . import _device, _lib
 from .activation import ActivationConfig, AggMode, make_activation_config
 from .algebra import Signature
-from .conv import ConvLayer, _out, conv_flops, make_conv_layer
+from .conv import ConvLayer, _out, _out_np, conv_flops, make_conv_layer
 from .errors import ShapeMismatch
 from .layout import Dims
 
@@ -91,7 +91,7 @@ def block_forward(x, blk: BasicBlock, chunk: int = 0, out=None):
     if _device.is_cuda_tensor(x):
         torch = _device.torch_mod()
         with _device.on_device(x.device):
-            xc = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
+            xc = _device.device_input(x)
             y = _out(out, blk.output_shape(), x.device)
             _lib.check(lib.cl_block_forward(C.c_void_p(blk.handle()), C.c_void_p(xc.data_ptr()),
                                             C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
@@ -104,7 +104,7 @@ def block_forward(x, blk: BasicBlock, chunk: int = 0, out=None):
                                              C.c_void_p(y.data_ptr()), B, chunk, C.c_void_p(_device.stream_ptr())))
         return y
     xa = np.ascontiguousarray(x, dtype=np.float32)
-    y = out if out is not None else np.empty(blk.output_shape(), dtype=np.float32)
+    y = _out_np(out, blk.output_shape())
     _lib.check(lib.cl_block_forward_host(C.c_void_p(blk.handle()), C.c_void_p(xa.ctypes.data),
                                          C.c_void_p(y.ctypes.data), B, chunk, C.c_void_p(_device.stream_ptr())))
     return y

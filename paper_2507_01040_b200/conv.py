@@ -26,9 +26,24 @@ from .layout import Dims
 
 PRECISIONS = {"fp32": 0, "tf32": 1, "bf16": 2, "3xtf32": 3}
 PADDINGS = {"valid": 0, "same": 1}
-# The reference variant names are accepted so existing callers keep working;
-# all of them run the B200 kernel (there is no CPU implementation here).
-VARIANTS = ("b200", "reference", "kernelized", "packed", "specialized")
+VARIANTS = ("b200",)
+# The reference CPU implementations (conv.py:371-381 / activation.py:400-416 /
+# linear.py:97-102) are not provided here: naming one is an error, so a harness
+# that verifies variants against variant="reference" cannot silently compare
+# the B200 path with itself.
+REFERENCE_CPU_VARIANTS = ("reference", "kernelized", "packed", "specialized")
+
+
+def check_variant(variant, kind: str, cpu_variants) -> None:
+    """ValueError for any variant but "b200" (the reference raises ValueError for
+    unknown names, conv.py:381); its own CPU variant names get a message saying
+    they are not implemented by this package."""
+    if variant == "b200":
+        return
+    if variant in cpu_variants:
+        raise ValueError(f"{kind} variant {variant!r} is a CPU implementation of the reference mvkernels "
+                         f"package and is not provided by the B200 path (use 'b200')")
+    raise ValueError(f"unknown {kind} variant {variant!r}")
 
 
 @dataclass(frozen=True, eq=False)
@@ -130,6 +145,20 @@ def _out(out, shape, device, pinned=False):
     return out
 
 
+def _out_np(out, shape):
+    """Validate a caller-provided numpy output array (host path) or allocate one.
+    The C-ABI writes straight into it, so shape, dtype and layout must be exact."""
+    if out is None:
+        return np.empty(shape, dtype=np.float32)
+    if not isinstance(out, np.ndarray):
+        raise ShapeMismatch(f"out must be a numpy array for numpy input, got {type(out).__name__}")
+    if (tuple(out.shape) != tuple(shape) or out.dtype != np.float32 or not out.flags.c_contiguous
+            or not out.flags.writeable):
+        raise ShapeMismatch(f"out has shape {tuple(out.shape)} dtype {out.dtype}, expected writeable "
+                            f"C-contiguous float32 {tuple(shape)}")
+    return out
+
+
 def _check_input(x, layer: ConvLayer):
     shape = tuple(x.shape)
     if shape != layer.dims.input_shape():
@@ -141,15 +170,14 @@ def conv_forward(x, layer: ConvLayer, variant: str = "b200", out=None):
 
     `out` (optional) receives the result (a CUDA tensor for CUDA input, a
     CPU tensor / numpy array for host input)."""
-    if variant not in VARIANTS:
-        raise ValueError(f"unknown conv variant {variant!r}")
+    check_variant(variant, "conv", REFERENCE_CPU_VARIANTS)
     _check_input(x, layer)
     lib = _lib.load()
     B = layer.dims.B
     if _device.is_cuda_tensor(x):
         torch = _device.torch_mod()
         with _device.on_device(x.device):
-            xc = x if (x.dtype == torch.float32 and x.is_contiguous()) else x.float().contiguous()
+            xc = _device.device_input(x)
             y = _out(out, layer.output_shape(B), x.device)
             _lib.check(lib.cl_conv_forward(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
                                            C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
@@ -162,7 +190,7 @@ def conv_forward(x, layer: ConvLayer, variant: str = "b200", out=None):
                                             C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
         return y
     xa = np.ascontiguousarray(x, dtype=np.float32)
-    y = out if out is not None else np.empty(layer.output_shape(B), dtype=np.float32)
+    y = _out_np(out, layer.output_shape(B))
     _lib.check(lib.cl_conv_forward_host(C.c_void_p(layer.handle()), C.c_void_p(xa.ctypes.data),
                                         C.c_void_p(y.ctypes.data), B, C.c_void_p(_device.stream_ptr())))
     return y

@@ -840,6 +840,16 @@ static size_t conv_ws_operand_bytes(const cl_conv* h, long long B, bool prepacke
 static size_t conv_ws_bytes(const cl_conv* h, long long B, bool prepacked) {
   return conv_ws_operand_bytes(h, B, prepacked) + kSchedBytes;
 }
+// The operand-prep and epilogue kernels move whole multivectors with 16-byte
+// (8-byte in 1-D) vector accesses: misaligned buffers are rejected up front
+// rather than faulting (a misaligned-address fault poisons the CUDA context).
+static int check_io_align(const void* x, const void* y, int nb) {
+  const uintptr_t m = nb == 2 ? 7u : 15u;
+  if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & m) != 0)
+    return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch",
+                std::string("input and output buffers must be ") + (nb == 2 ? "8" : "16") + "-byte aligned");
+  return CL_OK;
+}
 static bool g_static_tiles = getenv("CL_STATIC_TILES") != nullptr;  // A/B: static round-robin tile order
 static bool g_dyn_tiles = getenv("CL_DYN_TILES") != nullptr;  // tests: dynamic order for every launch
 
@@ -1131,6 +1141,7 @@ int cl_conv_forward_ws(const cl_conv* h, const float* x, float* y, int64_t B, vo
   if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
   if (ws_bytes < conv_ws_bytes(h, B, false))
     return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "workspace too small");
+  if (int st = check_io_align(x, y, h->nb)) return st;
   return conv_run(h, x, nullptr, y, B, Epi{}, ws, (cudaStream_t)stream);
 }
 
@@ -1142,6 +1153,7 @@ static bool graph_ok(long long elems) {
 int cl_conv_forward(const cl_conv* h, const float* x, float* y, int64_t B, void* stream) {
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null conv handle");
   if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
+  if (int st = check_io_align(x, y, h->nb)) return st;
   void* ws = nullptr;
   cudaStream_t s = (cudaStream_t)stream;
   if (int rc = h->ws.get(s, conv_ws_bytes(h, B, false), &ws)) return rc;
@@ -1381,12 +1393,14 @@ int cl_block_forward_ws(const cl_block* h, const float* x, float* y, int64_t B, 
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null block handle");
   if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
   if (ws_bytes < block_ws_bytes(h, B)) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "workspace too small");
+  if (int st = check_io_align(x, y, h->c1->nb)) return st;
   return block_run(h, x, y, B, ws, (cudaStream_t)stream);
 }
 
 int cl_block_forward(const cl_block* h, const float* x, float* y, int64_t B, void* stream) {
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null block handle");
   if (B < 0) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "batch must be >= 0");
+  if (int st = check_io_align(x, y, h->c1->nb)) return st;
   void* ws = nullptr;
   cudaStream_t s = (cudaStream_t)stream;
   if (int rc = h->ws.get(s, block_ws_bytes(h, B), &ws)) return rc;

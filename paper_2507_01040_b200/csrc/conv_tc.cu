@@ -909,23 +909,28 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         const int n0 = nt * p.n_tile + c0;
         const bool more = c0 + 16 < c_stop && n0 + 16 < p.N;
         if (more) tmem_ld16(taddr + (uint32_t)(c0 + 16), nxt);
-        // the chunk's residual values, loaded up front so their latencies overlap
+        // the chunk's residual values (16 floats: the lane's share of every
+        // channel of the chunk), loaded up front so their latencies overlap.
+        // Channel cc of the chunk occupies floats [cc*wv, cc*wv + wv) of rq:
+        // wv = 4 -> rq[cc]; wv = 2 (2-D under the change of basis, 8 channels
+        // per chunk) -> rq[cc / 2].xy or .zw.
         float4 rq[4];
         const bool use_res = p.resid != nullptr && valid;
-        if (use_res) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) rq[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (use_res && (p.bs.on || NB == 4)) {  // NB = 8 / NB = 2 without a basis: loaded in place below
           const int wv = p.bs.on ? NB / 2 : NB;  // floats of one channel this lane adds
           const int nch = 16 / wv;
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            rq[cc] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (!p.bs.on && NB != 4) break;  // NB = 8: 2 float4 per channel, NB = 2: 8 channels; loaded in place below
+          for (int cc = 0; cc < 8; ++cc) {
             const int co = n0 / wv + cc;
             if (cc < nch && co < p.C_out) {
               const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB + (p.bs.on ? bcol * wv : 0);
               if (wv == 2) {
                 const float2 q2 = __ldg(reinterpret_cast<const float2*>(rp));
-                rq[cc] = make_float4(q2.x, q2.y, 0.f, 0.f);
-              } else {
+                if (cc & 1) { rq[cc >> 1].z = q2.x; rq[cc >> 1].w = q2.y; }
+                else { rq[cc >> 1].x = q2.x; rq[cc >> 1].y = q2.y; }
+              } else if (cc < 4) {
                 rq[cc] = __ldg(reinterpret_cast<const float4*>(rp));
               }
             }
@@ -965,9 +970,14 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               }
               if (valid && co < p.C_out) {
                 if (use_res) {
-                  const float4 q4 = rq[cc % 4];
-                  h[0] += q4.x; h[1 % W] += q4.y;
-                  if constexpr (W == 4) { h[2 % W] += q4.z; h[3 % W] += q4.w; }
+                  if constexpr (W == 4) {
+                    const float4 q4 = rq[cc % 4];
+                    h[0] += q4.x; h[1 % W] += q4.y; h[2 % W] += q4.z; h[3 % W] += q4.w;
+                  } else {  // W == 2: channel cc is rq[cc / 2].xy (even) or .zw (odd)
+                    const float4 q4 = rq[(cc >> 1) % 4];
+                    h[0] += (cc & 1) ? q4.z : q4.x;
+                    h[1 % W] += (cc & 1) ? q4.w : q4.y;
+                  }
                 }
                 if (p.y) {
                   float* yp = p.y + (((long long)b * p.C_out + co) * P_out + pix) * NB + bcol * W;

@@ -19,17 +19,22 @@ namespace cl {
 // Per-sample max |x|. Block (j, b) reduces the j-th contiguous chunk of
 // kAbsmaxU float4 per thread of sample b (many waves, one atomic per block).
 constexpr int kAbsmaxU = 8;
+// The grid is 1-D over (sample, chunk) pairs -- any B (a linear layer can
+// have far more than gridDim.y's 65535 samples); launches of more than 2^31-1
+// blocks are split by the host with `blk0`.
 __global__ void __launch_bounds__(256) absmax_kernel(const float* __restrict__ x, long long per_sample,
-                                                     unsigned* __restrict__ amax) {
-  const int b = blockIdx.y;
-  const float* xs = x + (long long)b * per_sample;
+                                                     long long per, long long blk0, unsigned* __restrict__ amax) {
+  const long long bid = blk0 + (long long)blockIdx.x;
+  const long long b = bid / per;
+  const long long chunk = bid - b * per;
+  const float* xs = x + b * per_sample;
   unsigned m = 0;  // max |x| as float bits (NaN-sticky)
   // samples need not start 16-byte aligned (1-D tensors): scalar head, float4 body, scalar tail
   long long head = (long long)((16 - (reinterpret_cast<uintptr_t>(xs) & 15)) & 15) / 4;
   if (head > per_sample) head = per_sample;
   const long long n4 = (per_sample - head) / 4;
   const float4* x4 = reinterpret_cast<const float4*>(xs + head);
-  const long long base = (long long)blockIdx.x * (256 * kAbsmaxU) + threadIdx.x;
+  const long long base = chunk * (256 * kAbsmaxU) + threadIdx.x;
   float4 v[kAbsmaxU];
 #pragma unroll
   for (int u = 0; u < kAbsmaxU; ++u)
@@ -37,7 +42,7 @@ __global__ void __launch_bounds__(256) absmax_kernel(const float* __restrict__ x
 #pragma unroll
   for (int u = 0; u < kAbsmaxU; ++u)
     m = max(m, max(max(abs_bits(v[u].x), abs_bits(v[u].y)), max(abs_bits(v[u].z), abs_bits(v[u].w))));
-  if (blockIdx.x == 0) {
+  if (chunk == 0) {
     if (threadIdx.x < head) m = max(m, abs_bits(xs[threadIdx.x]));
     for (long long i = head + n4 * 4 + threadIdx.x; i < per_sample; i += blockDim.x) m = max(m, abs_bits(xs[i]));
   }
@@ -56,14 +61,17 @@ __global__ void __launch_bounds__(256) absmax_kernel(const float* __restrict__ x
 cudaError_t launch_sample_absmax(const float* x, long long B, long long per_sample, unsigned* amax,
                                  cudaStream_t s) {
   if (B == 0) return cudaSuccess;
-  if (B > 65535) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(unsigned) * B, s);
   if (e != cudaSuccess) return e;
   const long long per = std::max<long long>(1, (per_sample / 4 + 256 * kAbsmaxU - 1) / (256 * kAbsmaxU));
-  dim3 grid((unsigned)per, (unsigned)B);
-  absmax_kernel<<<grid, 256, 0, s>>>(x, per_sample, amax);
-  count_launch();
-  return cudaGetLastError();
+  const long long total = per * B;
+  for (long long b0 = 0; b0 < total; b0 += 0x7fffffffLL) {
+    const long long n = std::min<long long>(0x7fffffffLL, total - b0);
+    absmax_kernel<<<(unsigned)n, 256, 0, s>>>(x, per_sample, per, b0, amax);
+    count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // One thread per (b, g, p): the 16 K-elements of group g at pixel p -> 4

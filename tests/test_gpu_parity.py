@@ -324,6 +324,29 @@ def test_block_random(g, mode, padding, residual, prec):
     assert np.array_equal(yh, y)
 
 
+@pytest.mark.parametrize("prec", ["fp32", "3xtf32", "tf32", "bf16"])
+@pytest.mark.parametrize("g,C", [((1, 1), 8), ((1, -1), 12), ((1, 1), 16), ((1, 1, 1), 9)])
+def test_block_residual_wide_channels(g, C, prec):
+    """Residual fusion with C_out >= 8: under the 2-D change of basis (3xTF32 /
+    fp32 modes) one 16-column epilogue chunk covers 8 output channels, each
+    with its own residual (advisor finding: channels 4-7 once re-used 0-3's)."""
+    rng = np.random.default_rng(40 + C)
+    k = len(g)
+    nb = 1 << k
+    B, d = 2, {2: 10, 3: 6}[k]
+    fan = C * nb * 3 ** k
+    f1 = rng.uniform(-1, 1, (nb, C, C, 3 ** k)).astype(np.float32) / np.float32(np.sqrt(fan))
+    f2 = rng.uniform(-1, 1, (nb, C, C, 3 ** k)).astype(np.float32) / np.float32(np.sqrt(fan))
+    b1 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
+    b2 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
+    x = (rng.standard_normal((B, C, d ** k, nb)) * (1 + np.arange(C)[None, :, None, None])).astype(np.float32)
+    blk = M.make_basic_block(M.Signature(g), B, C, C, C, d, f1, b1, 2, f2, b2, padding="same", residual=True,
+                             precision=prec)
+    y = run_dev(M.block_forward, x, blk)
+    ref = O.block_ref(x, g, d, f1, b1, 2, tuple(range(nb)), None, None, f2, b2, padding="same", residual=True)
+    assert_conv_close(y, ref, prec, K=C * nb * 3 ** k)
+
+
 def test_launch_counter_moves():
     from paper_2507_01040_b200 import _lib
     n0 = _lib.launch_count()

@@ -68,8 +68,11 @@ def test_conv_activation_block_roundtrip(tmp_path):
                           "dfilter": 3, "filters": paths["f1"], "bias": paths["b1"], "padding": "same"}, h)
     hc = r["handle"]
     out = str(tmp_path / "y.mvtf")
-    r = S.handle_request({"op": "forward", "handle": hc, "input": paths["x"], "output": out, "variant": "packed"}, h)
+    r = S.handle_request({"op": "forward", "handle": hc, "input": paths["x"], "output": out, "variant": "b200"}, h)
     assert r["ok"] and r["shape"] == [B, C, d * d, nb], r
+    # the reference's CPU variant names are not aliases of the B200 path
+    r = S.handle_request({"op": "forward", "handle": hc, "input": paths["x"], "output": out, "variant": "packed"}, h)
+    assert not r["ok"] and "ValueError" in r["error"] and "packed" in r["error"], r
     y = read_tensor(out).data
     assert O.max_rel_error(y, O.conv_ref(x, f1, b1, g, d, 3, 1)) <= 1e-4
     # spatial activation
