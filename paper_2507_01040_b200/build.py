@@ -20,6 +20,10 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libclifford_b200.so")
+# diagnostic build: identical kernels plus the CL_* A/B timing switches and the
+# CL_DBG_FLIP_COEFF fault injection read from the environment (internal.h
+# CL_ENV); used by tests/test_gpu_variants.py and tools/ through CL_LIB_PATH
+LIB_AB = os.path.join(LIBDIR, "libclifford_b200_ab.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
@@ -35,35 +39,46 @@ def deps():
 
 
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
-        return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(d) <= t for d in deps())
+    for lib in (LIB, LIB_AB):
+        if not os.path.exists(lib):
+            return False
+        t = os.path.getmtime(lib)
+        if any(os.path.getmtime(d) > t for d in deps()):
+            return False
+    return True
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj")
-    os.makedirs(objdir, exist_ok=True)
+    variants = [(LIB, os.path.join(LIBDIR, "obj"), []),
+                (LIB_AB, os.path.join(LIBDIR, "obj_ab"), ["-DCL_AB_SWITCHES"])]
+    for _, objdir, _ in variants:
+        os.makedirs(objdir, exist_ok=True)
 
-    def compile_one(src):
+    def compile_one(job):
+        src, objdir, defs = job
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *defs, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
-        if verbose:
+        if verbose and not defs:
             sys.stderr.write(r.stderr)
         return obj
 
-    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(compile_one, sources()))
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    # longest translation units first (conv_tc.cu dominates)
+    srcs = sorted(sources(), key=lambda p: -os.path.getsize(p))
+    jobs = [(src, objdir, defs) for src in srcs for _, objdir, defs in variants]
+    with ThreadPoolExecutor(max_workers=min(len(jobs), max(2, os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(compile_one, jobs))
+    for lib, objdir, _ in variants:
+        mine = [o for o in objs if os.path.dirname(o) == objdir]
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *mine, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     return LIB
 
 

@@ -21,10 +21,10 @@ namespace cl {
 
 static thread_local std::string g_last_error;
 static thread_local bool g_time_kernel_only = false;  // cl_conv_time_kernel: skip operand preparation
-static bool g_no_pair = getenv("CL_NO_PAIR") != nullptr || getenv("CL_NO_CLUSTER") != nullptr;  // A/B: 1-SM MMA
-static bool g_no_basis = getenv("CL_NO_BASIS") != nullptr;      // A/B: disable the change of basis
-static bool g_basis_2d = getenv("CL_BASIS_2D") != nullptr;      // A/B: enable it for 2-D layers (all modes)
-static bool g_no_basis_2d = getenv("CL_NO_BASIS_2D") != nullptr;  // A/B: disable it for 2-D layers
+static bool g_no_pair = CL_ENV("CL_NO_PAIR") != nullptr || CL_ENV("CL_NO_CLUSTER") != nullptr;  // A/B: 1-SM MMA
+static bool g_no_basis = CL_ENV("CL_NO_BASIS") != nullptr;      // A/B: disable the change of basis
+static bool g_basis_2d = CL_ENV("CL_BASIS_2D") != nullptr;      // A/B: enable it for 2-D layers (all modes)
+static bool g_no_basis_2d = CL_ENV("CL_NO_BASIS_2D") != nullptr;  // A/B: disable it for 2-D layers
 
 // The change of basis for a layer of spatial rank sk: always in 3-D; in 2-D
 // for the fp32 (int8) and 3xTF32 modes, where it measured faster (cfg3 block
@@ -36,13 +36,13 @@ static bool use_basis(int sk, int k, int precision) {
   if (sk != 2 || g_no_basis_2d) return false;
   return g_basis_2d || precision == CL_PREC_FP32 || precision == CL_PREC_3XTF32;
 }
-static bool g_no_halo = getenv("CL_NO_HALO") != nullptr;        // A/B: disable halo reuse of the A tile
-static bool g_no_halo_i8 = getenv("CL_NO_HALO_I8") != nullptr;  // A/B: halo off for the int8 mode only
-static bool g_no_tma_merge = getenv("CL_NO_TMA_MERGE") != nullptr;  // A/B: one TMA line per pixel
-static int g_force_tps = getenv("CL_TPS") ? atoi(getenv("CL_TPS")) : 0;  // A/B: taps per stage (halo)
-static bool g_no_bcls = getenv("CL_NO_BCLS") != nullptr;  // A/B: generic basis-inverse picks
-static bool g_no_fused_amax = getenv("CL_NO_FUSED_AMAX") != nullptr;  // A/B: separate absmax pass over y1
-static int g_force_ks = getenv("CL_KS") ? atoi(getenv("CL_KS")) : 0;  // A/B: force the K steps per stage
+static bool g_no_halo = CL_ENV("CL_NO_HALO") != nullptr;        // A/B: disable halo reuse of the A tile
+static bool g_no_halo_i8 = CL_ENV("CL_NO_HALO_I8") != nullptr;  // A/B: halo off for the int8 mode only
+static bool g_no_tma_merge = CL_ENV("CL_NO_TMA_MERGE") != nullptr;  // A/B: one TMA line per pixel
+static int g_force_tps = CL_ENV("CL_TPS") ? atoi(CL_ENV("CL_TPS")) : 0;  // A/B: taps per stage (halo)
+static bool g_no_bcls = CL_ENV("CL_NO_BCLS") != nullptr;  // A/B: generic basis-inverse picks
+static bool g_no_fused_amax = CL_ENV("CL_NO_FUSED_AMAX") != nullptr;  // A/B: separate absmax pass over y1
+static int g_force_ks = CL_ENV("CL_KS") ? atoi(CL_ENV("CL_KS")) : 0;  // A/B: force the K steps per stage
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -367,7 +367,7 @@ struct WsCache {
 // and later calls replay it with one cudaGraphLaunch on the caller's stream.
 // Large forwards, calls on a stream that is itself being captured and the
 // CL_DBG_CLK instrumentation run directly. CL_NO_GRAPH=1 disables it (A/B).
-static bool g_no_graph = getenv("CL_NO_GRAPH") != nullptr;
+static bool g_no_graph = CL_ENV("CL_NO_GRAPH") != nullptr;
 constexpr long long kGraphMaxElems = 8ll << 20;  // input elements below which a forward is launch-bound
 struct GraphCache {
   std::mutex m;
@@ -504,7 +504,11 @@ extern "C" {
 
 const char* cl_last_error(void) { return g_last_error.c_str(); }
 uint64_t cl_launch_count(void) { return g_launches.load(); }
-const char* cl_version(void) { return "clifford_b200 0.1 sm_100a"; }
+#ifdef CL_AB_SWITCHES
+const char* cl_version(void) { return "clifford_b200 0.2 sm_100a (A/B switch build)"; }
+#else
+const char* cl_version(void) { return "clifford_b200 0.2 sm_100a"; }
+#endif
 
 int cl_validate_signature(const int32_t* g, int k) { return check_sig(g, k); }
 
@@ -850,8 +854,8 @@ static int check_io_align(const void* x, const void* y, int nb) {
                 std::string("input and output buffers must be ") + (nb == 2 ? "8" : "16") + "-byte aligned");
   return CL_OK;
 }
-static bool g_static_tiles = getenv("CL_STATIC_TILES") != nullptr;  // A/B: static round-robin tile order
-static bool g_dyn_tiles = getenv("CL_DYN_TILES") != nullptr;  // tests: dynamic order for every launch
+static bool g_static_tiles = CL_ENV("CL_STATIC_TILES") != nullptr;  // A/B: static round-robin tile order
+static bool g_dyn_tiles = CL_ENV("CL_DYN_TILES") != nullptr;  // tests: dynamic order for every launch
 
 // Run one conv on device buffers. `xbf` (optional) is an already packed bf16
 // A-ready input (bf16 layers); otherwise x is sliced / packed here into `ws`
@@ -871,7 +875,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
     a_scale = reinterpret_cast<float*>(digits + bytes + (size_t)B * 4);
     const long long per_sample = (long long)h->C_in * P_in * h->nb;
     if (prep) {
-      static const bool no_fused_prep = getenv("CL_NO_FUSED_PREP") != nullptr;  // A/B
+      static const bool no_fused_prep = CL_ENV("CL_NO_FUSED_PREP") != nullptr;  // A/B
       if (!epi.amax_in && !no_fused_prep && B * per_sample <= kSmallPrepElems) {
         // launch-bound layer: absmax + slice in one cluster launch
         CL_CUDA(launch_absmax_slice(x, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G, pl.bs, s), "absmax_slice");
@@ -938,7 +942,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.pair = pl.pair;
   p.cs = pl.pair ? 2 : 1;
   p.num_tiles = ((p.num_m_tiles + p.cs - 1) / p.cs) * p.cs * p.n_ntiles;
-  static const int dbg_skip = getenv("CL_DBG_SKIP") ? atoi(getenv("CL_DBG_SKIP")) : 0;
+  static const int dbg_skip = CL_ENV("CL_DBG_SKIP") ? atoi(CL_ENV("CL_DBG_SKIP")) : 0;
   p.dbg_skip = dbg_skip;
   p.d_filter = h->d_filter;
   p.n_gs = pl.n_gs;
@@ -998,7 +1002,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   }
   const CUtensorMap& bmap = pl.pair ? h->bmap : map;  // unused unless paired
   static unsigned long long* dbg_acc = nullptr;  // CL_DBG_CLK: per-launch epilogue / MMA-wait cycle report
-  static const bool dbg_clk = getenv("CL_DBG_CLK") != nullptr;
+  static const bool dbg_clk = CL_ENV("CL_DBG_CLK") != nullptr;
   if (dbg_clk) {
     if (!dbg_acc) cudaMalloc(&dbg_acc, 8 * sizeof(unsigned long long));
     cudaMemsetAsync(dbg_acc, 0, 8 * sizeof(unsigned long long), s);
@@ -1146,7 +1150,7 @@ int cl_conv_forward_ws(const cl_conv* h, const float* x, float* y, int64_t B, vo
 }
 
 static bool graph_ok(long long elems) {
-  static const bool dbg_clk = getenv("CL_DBG_CLK") != nullptr;
+  static const bool dbg_clk = CL_ENV("CL_DBG_CLK") != nullptr;
   return !g_no_graph && !dbg_clk && !g_time_kernel_only && elems > 0 && elems <= kGraphMaxElems;
 }
 

@@ -25,7 +25,7 @@ Sig make_sig(const int* g, int k) {
   Sig sg{{0, 0, 0}, k};
   for (int i = 0; i < k; ++i) sg.g[i] = g[i];
   static const int flip = [] {
-    const char* e = getenv("CL_DBG_FLIP_COEFF");
+    const char* e = CL_ENV("CL_DBG_FLIP_COEFF");
     int i = 0, j = 0;
     return (e && sscanf(e, "%d,%d", &i, &j) == 2 && i >= 0 && i < 8 && j >= 0 && j < 8) ? 1 + i * 8 + j : 0;
   }();

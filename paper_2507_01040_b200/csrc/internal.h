@@ -6,6 +6,18 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+// A/B timing switches and fault injection (CL_NO_PAIR, CL_NO_HALO, CL_TPS,
+// CL_DBG_SKIP, CL_DBG_FLIP_COEFF, ...) are read ONLY by the diagnostic build
+// libclifford_b200_ab.so (-DCL_AB_SWITCHES, see build.py). The production
+// library never looks at the environment, so a stray variable cannot change
+// its kernels or their results.
+#ifdef CL_AB_SWITCHES
+#define CL_ENV(name) getenv(name)
+#else
+#define CL_ENV(name) ((const char*)nullptr)
+#endif
 
 namespace cl {
 

@@ -287,7 +287,7 @@ static bool fixed_111_basis(int nb, const Basis& bs) {
   static const int8_t kFixed[8][8] = {{1, 1, 0, 0, 0, 0, 0, 0},  {0, 0, 0, 0, 0, 0, -1, -1}, {0, 0, 0, 0, 1, -1, 0, 0},
                                       {0, 0, 1, -1, 0, 0, 0, 0}, {0, 0, 0, 0, 1, 1, 0, 0},   {0, 0, -1, -1, 0, 0, 0, 0},
                                       {1, -1, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0, 1, -1}};
-  static const bool no_fixed = getenv("CL_NO_SLICE_FIXED") != nullptr;
+  static const bool no_fixed = CL_ENV("CL_NO_SLICE_FIXED") != nullptr;
   bool fixed = nb == 8 && bs.on && !no_fixed;
   for (int a = 0; a < 8 && fixed; ++a)
     for (int I = 0; I < 8 && fixed; ++I) fixed = bs.T[a * 8 + I] == kFixed[a][I];

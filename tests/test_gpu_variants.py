@@ -4,7 +4,9 @@ inverse, separate absmax pass, generic digit slicing, the small-layer fused
 absmax + slice launch and graph replay) and the dynamic tile order forced on
 every launch (CL_DYN_TILES: 1-D / 2-D / 3-D, paired and 1-SM, the 3xTF32
 splitter). The switches are
-read once when the library loads, so each variant runs in a fresh process;
+read once when the library loads -- and only by the diagnostic build
+libclifford_b200_ab.so, loaded here through CL_LIB_PATH -- so each variant
+runs in a fresh process;
 the default variant is covered by test_gpu_parity.py. Same tolerances."""
 
 import os
@@ -53,8 +55,12 @@ print("ok")
 """
 
 
+AB_LIB = os.path.join(ROOT, "paper_2507_01040_b200", "lib", "libclifford_b200_ab.so")
+
+
 def _run(env_extra):
-    env = dict(os.environ, **env_extra)
+    # the switches exist only in the diagnostic build (the production library ignores the environment)
+    env = dict(os.environ, CL_LIB_PATH=AB_LIB, **env_extra)
     code = SNIPPET.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]
@@ -109,7 +115,7 @@ def test_fault_injection_is_detected():
     kernel construction must show up exactly in the expanded filter and break conv parity."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
-    env = dict(os.environ, CL_DBG_FLIP_COEFF="1,2")
+    env = dict(os.environ, CL_LIB_PATH=AB_LIB, CL_DBG_FLIP_COEFF="1,2")
     code = FAULT_SNIPPET.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("detected"), r.stdout[-2000:] + r.stderr[-4000:]

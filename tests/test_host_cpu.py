@@ -356,3 +356,15 @@ def test_reference_patch_applies_to_baseline_ref(tmp_path):
     r = subprocess.run(["patch", "-p1", "--dry-run", "-d", str(tmp_path), "-i",
                         os.path.join(ROOT, "tests", "reference_b200.patch")], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_production_library_ignores_the_environment():
+    """The CL_* A/B timing switches and the fault injection are compiled only
+    into the diagnostic build (libclifford_b200_ab.so); the production library
+    contains no getenv of them (VERDICT r1 weak #9)."""
+    from paper_2507_01040_b200 import build as B
+    prod = open(B.LIB, "rb").read()
+    ab = open(B.LIB_AB, "rb").read()
+    for name in (b"CL_NO_PAIR", b"CL_NO_HALO", b"CL_DBG_SKIP", b"CL_DBG_FLIP_COEFF", b"CL_TPS", b"CL_NO_GRAPH"):
+        assert name not in prod, name
+        assert name in ab, name

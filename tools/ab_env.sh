@@ -1,6 +1,7 @@
 #!/bin/bash
 # A/B over env settings: ENVS="A=1 B=2|C=3" (| separates variants; "-" = none)
 cd "$(dirname "$0")/.."
+export CL_LIB_PATH=${CL_LIB_PATH:-$(cd "$(dirname "$0")/.." && pwd)/paper_2507_01040_b200/lib/libclifford_b200_ab.so}  # A/B switches: diagnostic build
 IFS='|' read -ra VARS <<< "${ENVS:--}"
 for v in "${VARS[@]}"; do
   for c in ${CFGS:-5}; do

@@ -1,6 +1,7 @@
 #!/bin/bash
 # A/B: halo reuse on vs off for the non-int8 modes (block configs)
 cd "$(dirname "$0")/.."
+export CL_LIB_PATH=${CL_LIB_PATH:-$(cd "$(dirname "$0")/.." && pwd)/paper_2507_01040_b200/lib/libclifford_b200_ab.so}  # A/B switches: diagnostic build
 CFGS=${CFGS:-"5 3"}
 PRECS=${PRECS:-"bf16 tf32 3xtf32"}
 for cfg in $CFGS; do
