@@ -409,12 +409,12 @@ def run_reference(args):
     return 0
 
 
-def run_activation(args, spec, world, rank, local, dev, peaks, peak_kind, lib):
+def run_activation(args, spec, world, rank, local, dev, peaks, peak_kind):
     """cfg2: standalone multivector activation, HBM-bound; value = GB/s of
     algorithmic traffic (read + write of the (B, C, P, N_B) tensor)."""
     import torch
     import paper_2507_01040_b200 as M
-    from paper_2507_01040_b200 import workloads as W
+    from paper_2507_01040_b200 import _ops, workloads as W
     lo, hi = W.shard(spec.B, rank, world)
     nloc = hi - lo
     wgt, bias = W.act_params(spec)
@@ -430,7 +430,7 @@ def run_activation(args, spec, world, rank, local, dev, peaks, peak_kind, lib):
             M.activation_forward(x, cfg, out=y)
         torch.cuda.synchronize()
         barrier(world)
-        launches0 = lib.cl_launch_count()
+        launches0 = _ops.launch_count()
         reps = max(args.steps, 20)  # a step is ~0.1 ms: time enough launches
         with ClockSampler(local) as clk:
             e0 = torch.cuda.Event(enable_timing=True)
@@ -442,7 +442,7 @@ def run_activation(args, spec, world, rank, local, dev, peaks, peak_kind, lib):
             torch.cuda.synchronize()
             clk.extend(lambda: M.activation_forward(x, cfg, out=y))
         t = max_over_ranks(e0.elapsed_time(e1) / 1e3 / reps, world)
-        res[mode] = (t, lib.cl_launch_count() - launches0, clk.summary())
+        res[mode] = (t, _ops.launch_count() - launches0, clk.summary())
     mode = spec.mode
     t, launches, clocks = res[mode]
     gbs = nbytes * world / t / 1e9
@@ -498,13 +498,12 @@ def run_activation(args, spec, world, rank, local, dev, peaks, peak_kind, lib):
 def run_ours(args):
     import torch
     import paper_2507_01040_b200 as M
-    from paper_2507_01040_b200 import _lib, workloads as W
+    from paper_2507_01040_b200 import _ops, workloads as W
 
     world, rank, local = dist_setup(args)
     spec = W.CONFIGS[args.config]
     prec = args.precision
     peaks, peak_kind = load_peaks()
-    lib = _lib.load()
     lo, hi = W.shard(spec.B, rank, world)
     nloc = hi - lo
     dev = torch.device("cuda", local)
@@ -538,7 +537,7 @@ def run_ours(args):
         flops_per_sample = M.conv_flops(layer.dims, layer) / nloc
         conv_layer = layer
     else:
-        return run_activation(args, spec, world, rank, local, dev, peaks, peak_kind, lib)
+        return run_activation(args, spec, world, rank, local, dev, peaks, peak_kind)
 
     x = W.make_input(spec, lo, nloc, device=dev)
     y = run(x)
@@ -549,7 +548,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier(world)
 
-    launches0 = lib.cl_launch_count()
+    launches0 = _ops.launch_count()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         barrier(world)
@@ -560,7 +559,7 @@ def run_ours(args):
             y = run(x, out=y)
         ev1.record()
         torch.cuda.synchronize()
-        launches = lib.cl_launch_count() - launches0
+        launches = _ops.launch_count() - launches0
         clk.extend(lambda: run(x, out=y))
         barrier(world)
     t_step = ev0.elapsed_time(ev1) / 1e3 / args.steps
@@ -598,19 +597,12 @@ def run_ours(args):
                 gather["outputs"] = {"error": f"{type(e).__name__}: {e}"[:200]}
 
     # ---- dominant kernel: the tensor-core conv launch alone, CUDA events on its stream ----
-    import ctypes
     xc = x if spec.kind == "conv" else torch.empty(conv_layer.dims.input_shape(), device=dev).normal_()
     yc = torch.empty(conv_layer.output_shape(), device=dev)
-    ms = ctypes.c_float()
-    _lib.check(lib.cl_conv_time_kernel(ctypes.c_void_p(conv_layer.handle()), ctypes.c_void_p(xc.data_ptr()),
-                                       ctypes.c_void_p(yc.data_ptr()), conv_layer.dims.B, max(2, args.steps),
-                                       ctypes.c_void_p(torch.cuda.current_stream().cuda_stream), ctypes.byref(ms)))
-    t_conv = ms.value / 1e3
+    t_conv = _ops.op("conv_time_kernel", conv_layer.handle(), xc, conv_layer.dims.B, max(2, args.steps), yc) / 1e3
     del yc
-    alg_f, exe_f, basis_on = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
-    _lib.check(lib.cl_conv_gemm_flops(ctypes.c_void_p(conv_layer.handle()), conv_layer.dims.B, ctypes.byref(alg_f),
-                                      ctypes.byref(exe_f), ctypes.byref(basis_on)))
-    gemm_ratio = exe_f.value / alg_f.value  # executed tensor-core work per algorithmic FLOP
+    alg_f, exe_f, basis_on = _ops.op("conv_gemm_flops", conv_layer.handle(), conv_layer.dims.B)
+    gemm_ratio = exe_f / alg_f  # executed tensor-core work per algorithmic FLOP
     conv_flops = M.conv_flops(conv_layer.dims, conv_layer)
     achieved = conv_flops / t_conv / 1e12
     exec_peak, _ = mode_peak(prec, peaks, sustained=True)
@@ -672,7 +664,7 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": ncu_traffic(spec, prec, conv_layer.dims.B),
                          "kernel": "conv_tc_kernel (conv2 of the block)",
                          "peak_basis": f"{prec}: {peak_basis}" + (
-                             "; x2 algorithmic/executed (M2(C) change of basis, SURVEY 8f f4)" if basis_on.value else ""),
+                             "; x2 algorithmic/executed (M2(C) change of basis, SURVEY 8f f4)" if basis_on else ""),
                          "frac_of_sustained": achieved / peak_sust,
                          "executed_tflops": achieved * gemm_ratio, "executed_peak": exec_peak_burst,
                          "executed_frac": achieved * gemm_ratio / exec_peak_burst,

@@ -148,6 +148,15 @@ int cl_act_forward(const cl_act* h, const float* x_dev, float* y_dev, int64_t B,
                    void* stream);
 int cl_act_forward_host(const cl_act* h, const float* x_host, float* y_host, int64_t B, int64_t P,
                         void* stream);
+/* pre-sigmoid gate s per (b, c, p) <- activation.gate_preactivation  activation.py:110-117
+ * x_dev (B, C, P, N_B) -> s_dev (B, C, P); kernel blades in kernel_indices order */
+int cl_act_preactivation(const cl_act* h, const float* x_dev, float* s_dev, int64_t B, int64_t P,
+                         void* stream);
+/* kernel blades of every multivector <- activation.gather_vpack  activation.py:99-107
+ * x_dev (B, C, P, N_B) -> v_dev (B, C, P, K) */
+int cl_act_gather(const cl_act* h, const float* x_dev, float* v_dev, int64_t B, int64_t P, void* stream);
+/* K (number of kernel blades) of the handle, or -status */
+int cl_act_kernel_count(const cl_act* h);
 void cl_act_destroy(cl_act* h);
 
 /* ---- (4) basic block: conv1 -> act -> conv2 [+ residual] ---------------- */

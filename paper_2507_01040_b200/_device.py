@@ -3,11 +3,8 @@
 from __future__ import annotations
 
 import contextlib
-import ctypes as C
 
 import numpy as np
-
-from . import _lib
 
 
 class Handle:
@@ -20,10 +17,24 @@ class Handle:
     def __del__(self):
         if self.ptr and self._destroy is not None:
             try:
-                self._destroy(C.c_void_p(self.ptr))
+                self._destroy(self.ptr)
             except Exception:
                 pass
             self.ptr = 0
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        from .errors import ConfigInvalid
+        raise ConfigInvalid("the B200 path needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def host_view(a):
+    """A zero-copy torch view of a C-contiguous float32 numpy array (host path)."""
+    import torch
+    return torch.from_numpy(a)
 
 
 def torch_mod():
@@ -53,7 +64,7 @@ _cuda_checked = False
 def current_device() -> int:
     global _cuda_checked
     if not _cuda_checked:
-        _lib.require_cuda()  # fail loudly without a GPU (no CPU fallback)
+        require_cuda()  # fail loudly without a GPU (no CPU fallback)
         _cuda_checked = True
     return torch_mod().cuda.current_device()
 
@@ -91,7 +102,7 @@ def device_input(x):
 
 def to_device_f32(arr, device=None):
     """Contiguous fp32 CUDA copy of a numpy array / tensor."""
-    torch = _lib.require_cuda()
+    torch = require_cuda()
     if isinstance(arr, torch.Tensor):
         return arr.detach().to(device=device or torch.cuda.current_device(), dtype=torch.float32).contiguous().clone()
     a = np.ascontiguousarray(arr, dtype=np.float32)

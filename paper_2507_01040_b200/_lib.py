@@ -1,8 +1,7 @@
-"""ctypes binding of the C-ABI (include/clifford_b200.h).
-
-This replaces the paper's ctypes bindings with a binding of
-libclifford_b200.so. There is deliberately no CPU fallback: if the library
-or a CUDA device is missing, calls fail loudly.
+"""Plain-ctypes view of the C-ABI (include/clifford_b200.h), for the tests
+that check the boundary itself (every header symbol is exported, raw C
+calls, status codes) -- the package calls the library through its PyTorch
+operator registration instead (_ops.py, torch.ops.clifford_b200.*).
 """
 
 from __future__ import annotations
@@ -22,7 +21,8 @@ EXPORTS = (
     "cl_conv_create", "cl_conv_gemm_flops", "cl_conv_plan_info", "cl_conv_out_side", "cl_conv_forward", "cl_conv_forward_host",
     "cl_conv_workspace_bytes", "cl_conv_time_kernel", "cl_conv_forward_ws", "cl_block_workspace_bytes", "cl_block_forward_ws",
     "cl_conv_destroy", "cl_linear_create", "cl_linear_forward", "cl_linear_forward_host",
-    "cl_linear_destroy", "cl_act_create", "cl_act_forward", "cl_act_forward_host",
+    "cl_linear_destroy", "cl_act_create", "cl_act_forward", "cl_act_forward_host", "cl_act_preactivation", "cl_act_gather",
+    "cl_act_kernel_count",
     "cl_act_destroy", "cl_block_create", "cl_block_forward", "cl_block_forward_host",
     "cl_block_destroy", "cl_last_error", "cl_launch_count", "cl_version",
 )
@@ -69,6 +69,9 @@ def load():
         "cl_act_create": (C.c_int, [I32P, C.c_int, C.c_int, I32P, C.c_int, C.c_int, P, P, P, C.POINTER(P)]),
         "cl_act_forward": (C.c_int, [P, P, P, C.c_int64, C.c_int64, P]),
         "cl_act_forward_host": (C.c_int, [P, P, P, C.c_int64, C.c_int64, P]),
+        "cl_act_preactivation": (C.c_int, [P, P, P, C.c_int64, C.c_int64, P]),
+        "cl_act_gather": (C.c_int, [P, P, P, C.c_int64, C.c_int64, P]),
+        "cl_act_kernel_count": (C.c_int, [P]),
         "cl_act_destroy": (None, [P]),
         "cl_block_create": (C.c_int, [P, P, P, C.c_int, C.POINTER(P)]),
         "cl_block_forward": (C.c_int, [P, P, P, C.c_int64, P]),

@@ -11,13 +11,12 @@ any K <= N_B work (the reference's 'specialized' preconditions do not apply).
 
 from __future__ import annotations
 
-import ctypes as C
 from dataclasses import dataclass, field
 from enum import IntEnum
 
 import numpy as np
 
-from . import _device, _lib
+from . import _device, _ops
 from .algebra import Signature
 from .conv import _out, _out_np, check_variant
 from .errors import IndexOutOfRange, ModeConfigMismatch, ShapeMismatch
@@ -56,19 +55,12 @@ class ActivationConfig:
         key = (_device.current_device(), C_)
         h = self._handles.get(key)
         if h is None:
-            lib = _lib.load()
             w = b = None
             if self.agg_mode == AggMode.LINEAR:
                 w = _device.to_device_f32(self.weight)
                 b = _device.to_device_f32(self.bias)
-            out = C.c_void_p()
-            _lib.check(lib.cl_act_create(
-                _lib.int32_array(self.sig.g), self.sig.k, int(self.agg_mode),
-                _lib.int32_array(self.kernel_indices), self.K, C_,
-                C.c_void_p(w.data_ptr()) if w is not None else None,
-                C.c_void_p(b.data_ptr()) if b is not None else None,
-                C.c_void_p(_device.stream_ptr()), C.byref(out)))
-            h = _device.Handle(out.value, lib.cl_act_destroy)
+            ptr = _ops.op("act_create", list(self.sig.g), int(self.agg_mode), list(self.kernel_indices), C_, w, b)
+            h = _device.Handle(ptr, _ops.destroyer("act_destroy"))
             self._handles[key] = h
         return h.ptr
 
@@ -117,27 +109,72 @@ def activation_forward(x, cfg: ActivationConfig, variant: str = "b200", out=None
     """Gated scaling of every multivector (activation.py:400-416 semantics)."""
     check_variant(variant, "activation", REFERENCE_CPU_VARIANTS)
     B, C_, P = _dims(x, cfg)
-    lib = _lib.load()
     if _device.is_cuda_tensor(x):
-        torch = _device.torch_mod()
         with _device.on_device(x.device):
             xc = _device.device_input(x)
             y = _out(out, tuple(xc.shape), x.device)
-            _lib.check(lib.cl_act_forward(C.c_void_p(cfg.handle(C_)), C.c_void_p(xc.data_ptr()),
-                                          C.c_void_p(y.data_ptr()), B, P, C.c_void_p(_device.stream_ptr())))
+            _ops.op("act_forward", cfg.handle(C_), xc, B, P, y)
         return y
     if _device.is_cpu_tensor(x):
-        torch = _device.torch_mod()
         xc = x.float().contiguous()
         y = _out(out, tuple(xc.shape), None, pinned=xc.is_pinned())
-        _lib.check(lib.cl_act_forward_host(C.c_void_p(cfg.handle(C_)), C.c_void_p(xc.data_ptr()),
-                                           C.c_void_p(y.data_ptr()), B, P, C.c_void_p(_device.stream_ptr())))
+        _ops.op("act_forward_host", cfg.handle(C_), xc, B, P, y)
         return y
     xa = np.ascontiguousarray(x, dtype=np.float32)
     y = _out_np(out, xa.shape)
-    _lib.check(lib.cl_act_forward_host(C.c_void_p(cfg.handle(C_)), C.c_void_p(xa.ctypes.data),
-                                       C.c_void_p(y.ctypes.data), B, P, C.c_void_p(_device.stream_ptr())))
+    _ops.op("act_forward_host", cfg.handle(C_), _device.host_view(xa), B, P, _device.host_view(y))
     return y
+
+
+def sigmoid(s):
+    """Logistic function 1 / (1 + exp(-s)) of activation.py:92-96 (a host
+    helper for property checks, saturating cleanly in both tails; the device
+    gate is fp32 1/(1+expf(-s)), within 1e-6 of it on [-30, 30])."""
+    s = np.asarray(s)
+    with np.errstate(over="ignore"):
+        return 1.0 / (1.0 + np.exp(-s))
+
+
+def _aux(op_name, x, cfg: ActivationConfig, width):
+    """Run a device-side activation helper; numpy / CPU inputs are copied to
+    the current CUDA device and the result back (there is no CPU path)."""
+    B, C_, P = _dims(x, cfg)
+    torch = _device.require_cuda()
+    on_dev = _device.is_cuda_tensor(x)
+    if on_dev:
+        dev = x.device
+        xd = _device.device_input(x)
+    else:
+        dev = torch.device("cuda", _device.current_device())
+        xh = x if _device.is_cpu_tensor(x) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+        xd = xh.to(device=dev, dtype=torch.float32).contiguous()
+    shape = tuple(x.shape[:-1]) + ((width,) if width else ())
+    with _device.on_device(dev):
+        y = torch.empty(shape, device=dev, dtype=torch.float32)
+        _ops.op(op_name, cfg.handle(C_), xd, B, P, y)
+    if on_dev:
+        return y
+    y = y.cpu()
+    return y if _device.is_cpu_tensor(x) else y.numpy()
+
+
+def gather_vpack(x, cfg: ActivationConfig):
+    """The kernel blades of every multivector, in `kernel_indices` order
+    (activation.py:99-107): (B, C, N_B) -> (B, C, K); the spatial form
+    (B, C, P, N_B) -> (B, C, P, K). Computed on the device."""
+    if x.ndim not in (3, 4):
+        raise ShapeMismatch(f"input shape {tuple(x.shape)}, expected (B, C, N_B)")
+    if any(i >= x.shape[-1] for i in cfg.kernel_indices):
+        raise IndexOutOfRange(f"kernel indices {cfg.kernel_indices} outside [0, {x.shape[-1]})")
+    return _aux("act_gather", x, cfg, cfg.K)
+
+
+def gate_preactivation(x, cfg: ActivationConfig):
+    """The pre-sigmoid scalar s per (b, c) (activation.py:110-117): Linear
+    sum_k x[ki[k]] w[c, k] + bias[c], Sum sum_k x[ki[k]], Mean that / K;
+    (B, C, N_B) -> (B, C), spatial (B, C, P, N_B) -> (B, C, P). Computed on
+    the device."""
+    return _aux("act_preactivation", x, cfg, 0)
 
 
 def activation_flops(B: int, C: int, n_blades: int, K: int, mode, sigmoid_cost: int = 30) -> int:

@@ -1,7 +1,8 @@
 """Signatures and blade products (host side of the reference algebra module,
 algebra.py:26-63, :87-99, :116-145). Blade products come from the C-ABI
-(`cl_blade_product`), i.e. the same integer code that builds the device
-kernels; the Python side only validates and shapes the results."""
+(`cl_blade_product`, through torch.ops.clifford_b200), i.e. the same integer
+code that builds the device kernels; the Python side only validates and
+shapes the results."""
 
 from __future__ import annotations
 
@@ -11,8 +12,8 @@ from typing import Iterable
 
 import numpy as np
 
-from . import _lib
-from .errors import InvalidMetricValue, InvalidSignature
+from . import _ops
+from .errors import DimensionMismatch, InvalidMetricValue, InvalidSignature
 
 
 @dataclass(frozen=True)
@@ -47,12 +48,8 @@ def validate_signature(values: Iterable[float]) -> Signature:
 
 def blade_product(i_mask: int, j_mask: int, sig: Signature) -> tuple[int, int]:
     """(target, coeff) of e_I e_J via the C-ABI (algebra.py:87-99)."""
-    lib = _lib.load()
-    t = _lib.C.c_int()
-    c = _lib.C.c_int()
-    _lib.check(lib.cl_blade_product(int(i_mask), int(j_mask), _lib.int32_array(sig.g), sig.k,
-                                    _lib.C.byref(t), _lib.C.byref(c)))
-    return t.value, c.value
+    t, c = _ops.op("blade_product", int(i_mask), int(j_mask), list(sig.g))
+    return int(t), int(c)
 
 
 @dataclass(frozen=True, eq=False)
@@ -96,12 +93,35 @@ def cayley_tensor(sig: Signature) -> np.ndarray:
     return cay
 
 
+def geometric_product(x, y, table: BladeProductTable) -> np.ndarray:
+    """Geometric product of multivector arrays over their last (blade) axis,
+    broadcasting the leading axes (algebra.py:155-173): accumulated in fp64,
+    rounded once to the operands' common dtype; DimensionMismatch if a blade
+    axis is not N_B. Host algebra helper (like the product table): the
+    layers' products run on the device.
+
+    out[..., i ^ j] += coeff[i, j] x[..., i] y[..., j], one blade row at a time."""
+    x = np.asarray(x)
+    y = np.asarray(y)
+    nb = table.sig.n_blades
+    for name, a in (("x", x), ("y", y)):
+        if a.ndim == 0 or a.shape[-1] != nb:
+            raise DimensionMismatch(f"{name} has blade axis {a.shape[-1] if a.ndim else '()'}, expected {nb}")
+    out_dtype = np.result_type(x.dtype, y.dtype)
+    xd = x.astype(np.float64, copy=False)
+    yd = y.astype(np.float64, copy=False)
+    out = np.zeros(np.broadcast_shapes(x.shape, y.shape), np.float64)
+    for i in range(nb):
+        for j in range(nb):
+            c = int(table.coeff[i, j])
+            if c:
+                out[..., int(table.target[i, j])] += c * xd[..., i] * yd[..., j]
+    return out.astype(out_dtype, copy=False)
+
+
 def schedule_terms(sig: Signature) -> int:
     """Number of non-zero FMA terms of the signature schedule (specialize.py:49-63)."""
-    n = _lib.load().cl_schedule_terms(_lib.int32_array(sig.g), sig.k)
-    if n < 0:
-        _lib.check(-n)
-    return int(n)
+    return int(_ops.op("schedule_terms", list(sig.g)))
 
 
 def schedule_flop_count(sig_or_schedule) -> int:

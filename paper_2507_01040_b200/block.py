@@ -9,12 +9,11 @@ the activation runs inside conv1's epilogue and the residual inside conv2's
 
 from __future__ import annotations
 
-import ctypes as C
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _device, _lib
+from . import _device, _ops
 from .activation import ActivationConfig, AggMode, make_activation_config
 from .algebra import Signature
 from .conv import ConvLayer, _out, _out_np, conv_flops, make_conv_layer
@@ -47,12 +46,9 @@ class BasicBlock:
         dev = _device.current_device()
         h = self._handles.get(dev)
         if h is None:
-            lib = _lib.load()
-            out = C.c_void_p()
-            _lib.check(lib.cl_block_create(
-                C.c_void_p(self.conv1.handle()), C.c_void_p(self.act.handle(self.conv1.dims.C_out)),
-                C.c_void_p(self.conv2.handle()), int(self.residual), C.byref(out)))
-            h = _device.Handle(out.value, lib.cl_block_destroy)
+            ptr = _ops.op("block_create", self.conv1.handle(), self.act.handle(self.conv1.dims.C_out),
+                          self.conv2.handle(), bool(self.residual))
+            h = _device.Handle(ptr, _ops.destroyer("block_destroy"))
             self._handles[dev] = h
         return h.ptr
 
@@ -86,25 +82,19 @@ def block_forward(x, blk: BasicBlock, chunk: int = 0, out=None):
     """y = conv2(act(conv1(x))) [+ x] (block.ts:134-148 + residual)."""
     if tuple(x.shape) != blk.input_shape():
         raise ShapeMismatch(f"input shape {tuple(x.shape)}, expected {blk.input_shape()}")
-    lib = _lib.load()
     B = blk.B
     if _device.is_cuda_tensor(x):
-        torch = _device.torch_mod()
         with _device.on_device(x.device):
             xc = _device.device_input(x)
             y = _out(out, blk.output_shape(), x.device)
-            _lib.check(lib.cl_block_forward(C.c_void_p(blk.handle()), C.c_void_p(xc.data_ptr()),
-                                            C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
+            _ops.op("block_forward", blk.handle(), xc, B, y)
         return y
     if _device.is_cpu_tensor(x):
-        torch = _device.torch_mod()
         xc = x.float().contiguous()
         y = _out(out, blk.output_shape(), None, pinned=xc.is_pinned())
-        _lib.check(lib.cl_block_forward_host(C.c_void_p(blk.handle()), C.c_void_p(xc.data_ptr()),
-                                             C.c_void_p(y.data_ptr()), B, chunk, C.c_void_p(_device.stream_ptr())))
+        _ops.op("block_forward_host", blk.handle(), xc, B, chunk, y)
         return y
     xa = np.ascontiguousarray(x, dtype=np.float32)
     y = _out_np(out, blk.output_shape())
-    _lib.check(lib.cl_block_forward_host(C.c_void_p(blk.handle()), C.c_void_p(xa.ctypes.data),
-                                         C.c_void_p(y.ctypes.data), B, chunk, C.c_void_p(_device.stream_ptr())))
+    _ops.op("block_forward_host", blk.handle(), _device.host_view(xa), B, chunk, _device.host_view(y))
     return y

@@ -14,12 +14,11 @@ in and out inside the call, and returns the same kind.
 
 from __future__ import annotations
 
-import ctypes as C
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _device, _lib
+from . import _device, _ops
 from .algebra import Signature, schedule_flop_count
 from .errors import ShapeMismatch
 from .layout import Dims
@@ -92,16 +91,11 @@ class ConvLayer:
         dev = _device.current_device()
         h = self._handles.get(dev)
         if h is None:
-            lib = _lib.load()
             f = _device.to_device_f32(self.filters)
             b = _device.to_device_f32(self.bias)
-            out = C.c_void_p()
-            _lib.check(lib.cl_conv_create(
-                _lib.int32_array(self.sig.g), self.sig.k, self.dims.C_in, self.dims.C_out,
-                self.dims.d_image, self.dims.d_filter, PADDINGS[self.padding],
-                PRECISIONS[self.precision], C.c_void_p(f.data_ptr()), C.c_void_p(b.data_ptr()),
-                C.c_void_p(_device.stream_ptr()), C.byref(out)))
-            h = _device.Handle(out.value, lib.cl_conv_destroy)
+            ptr = _ops.op("conv_create", list(self.sig.g), self.dims.C_in, self.dims.C_out, self.dims.d_image,
+                          self.dims.d_filter, PADDINGS[self.padding], PRECISIONS[self.precision], f, b)
+            h = _device.Handle(ptr, _ops.destroyer("conv_destroy"))
             self._handles[dev] = h
         return h.ptr
 
@@ -172,40 +166,32 @@ def conv_forward(x, layer: ConvLayer, variant: str = "b200", out=None):
     CPU tensor / numpy array for host input)."""
     check_variant(variant, "conv", REFERENCE_CPU_VARIANTS)
     _check_input(x, layer)
-    lib = _lib.load()
     B = layer.dims.B
     if _device.is_cuda_tensor(x):
-        torch = _device.torch_mod()
         with _device.on_device(x.device):
             xc = _device.device_input(x)
             y = _out(out, layer.output_shape(B), x.device)
-            _lib.check(lib.cl_conv_forward(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
-                                           C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
+            _ops.op("conv_forward", layer.handle(), xc, B, y)
         return y
     if _device.is_cpu_tensor(x):
-        torch = _device.torch_mod()
         xc = x.float().contiguous()
         y = _out(out, layer.output_shape(B), None, pinned=xc.is_pinned())
-        _lib.check(lib.cl_conv_forward_host(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
-                                            C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
+        _ops.op("conv_forward_host", layer.handle(), xc, B, y)
         return y
     xa = np.ascontiguousarray(x, dtype=np.float32)
     y = _out_np(out, layer.output_shape(B))
-    _lib.check(lib.cl_conv_forward_host(C.c_void_p(layer.handle()), C.c_void_p(xa.ctypes.data),
-                                        C.c_void_p(y.ctypes.data), B, C.c_void_p(_device.stream_ptr())))
+    _ops.op("conv_forward_host", layer.handle(), _device.host_view(xa), B, _device.host_view(y))
     return y
 
 
 def build_expanded_kernel(layer: ConvLayer):
     """(C_out*N_B, C_in*N_B, Q) real filter built on the device (conv.py:188-202)."""
-    torch = _lib.require_cuda()
+    torch = _device.require_cuda()
     d = layer.dims
     nb = d.n_blades
     f = _device.to_device_f32(layer.filters)
     out = torch.empty((d.C_out * nb, d.C_in * nb, d.filter_positions), device=f.device, dtype=torch.float32)
-    _lib.check(_lib.load().cl_expand_kernel(
-        _lib.int32_array(layer.sig.g), layer.sig.k, C.c_void_p(f.data_ptr()), d.C_in, d.C_out,
-        d.filter_positions, C.c_void_p(out.data_ptr()), C.c_void_p(_device.stream_ptr())))
+    _ops.op("expand_kernel", list(layer.sig.g), f, d.C_in, d.C_out, d.filter_positions, out)
     return out
 
 

@@ -8,9 +8,11 @@
 //   s = sum_k x[ki[k]] / K                    (Mean)
 //   out[j] = x[j] * sigmoid(s)  for every blade j.
 // The kernel-blade subset and the Linear weights are re-keyed once at create
-// time to a dense (C, N_B) blade-ordered table (zero for non-kernel blades,
-// as activation.py:385-390 does for its specialised path), so the inner loop
-// is branch-free for any K <= N_B and any C.
+// time to a dense (C, N_B) blade-ordered table (as activation.py:385-390 does
+// for its specialised path), so the inner loop is branch-free for any K <= N_B
+// and any C. Non-kernel blades are SELECTED out (kmask), not multiplied by a
+// zero weight: the reference never reads them (activation.py:142-162), so an
+// Inf / NaN there must not reach the gate (0 * Inf = NaN).
 //
 // One thread per multivector: 8 B (1-D), 16 B (2-D) or 32 B (3-D) of
 // contiguous, aligned data -> 64/128-bit streaming loads/stores; 4 (8 in 1-D)
@@ -46,7 +48,7 @@ __device__ __forceinline__ unsigned udiv(unsigned n, unsigned mag, unsigned sh) 
 // (tools/probe/act_variants.cu at cfg2: 6.2 vs 5.3-5.5 TB/s median). The
 // channel of element i is ((i / P) % C); the block's first index is split
 // once in 64 bits, the rest is 32-bit magic-number division.
-template <int NB, int MODE, int U>
+template <int NB, int MODE, int U, bool FULL>
 __global__ void __launch_bounds__(256) act_kernel(ActParams p) {
   using VT = typename std::conditional<NB == 2, float2, float4>::type;
   constexpr int V = NB == 2 ? 1 : NB / 4;  // vectors per multivector
@@ -77,17 +79,22 @@ __global__ void __launch_bounds__(256) act_kernel(ActParams p) {
       const unsigned ck = c0 + k;
       const unsigned c = ck - udiv(ck, p.magC, p.shC) * (unsigned)p.C;
       const float* w = p.w + c * NB;
+      // every blade is a kernel blade (FULL), or a select keeps the others out
+      auto acc = [&](float s, float xv, int j) {
+        const float t = fmaf(xv, __ldg(w + j), s);
+        return (FULL || ((p.kmask >> j) & 1u)) ? t : s;
+      };
       float s = 0.f;
       if constexpr (NB == 2) {
-        s = fmaf(v[u][0].x, __ldg(w + 0), s);
-        s = fmaf(v[u][0].y, __ldg(w + 1), s);
+        s = acc(s, v[u][0].x, 0);
+        s = acc(s, v[u][0].y, 1);
       } else {
 #pragma unroll
         for (int h = 0; h < V; ++h) {
-          s = fmaf(v[u][h].x, __ldg(w + 4 * h + 0), s);
-          s = fmaf(v[u][h].y, __ldg(w + 4 * h + 1), s);
-          s = fmaf(v[u][h].z, __ldg(w + 4 * h + 2), s);
-          s = fmaf(v[u][h].w, __ldg(w + 4 * h + 3), s);
+          s = acc(s, v[u][h].x, 4 * h + 0);
+          s = acc(s, v[u][h].y, 4 * h + 1);
+          s = acc(s, v[u][h].z, 4 * h + 2);
+          s = acc(s, v[u][h].w, 4 * h + 3);
         }
       }
       if (MODE == 0) s += __ldg(p.b + c);
@@ -113,7 +120,8 @@ static cudaError_t launch_mode(const ActParams& p, cudaStream_t s) {
   constexpr int U = NB == 2 ? 8 : 4;
   const long long blocks = (p.n_mv + 256LL * U - 1) / (256LL * U);
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
-  act_kernel<NB, MODE, U><<<(unsigned)blocks, 256, 0, s>>>(p);
+  if (p.kmask == (1u << NB) - 1u) act_kernel<NB, MODE, U, true><<<(unsigned)blocks, 256, 0, s>>>(p);
+  else act_kernel<NB, MODE, U, false><<<(unsigned)blocks, 256, 0, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }
@@ -151,5 +159,46 @@ cudaError_t launch_act(int nb, const ActParams& p0, cudaStream_t s) {
   }
   return nb == 4 ? launch_nb<4>(p, s) : launch_nb<8>(p, s);
 }
+
+// gate_preactivation (activation.py:110-117): s per (b, c, p) -- the kernel
+// blades in the caller's order ki[0..K), Linear weights from the re-keyed
+// table, + bias (Linear) or / K (Mean). gather_vpack (activation.py:99-107):
+// the K kernel blades of every multivector, in ki order, (B, C, P, K).
+// Diagnostic / property-check entry points (one thread per multivector).
+template <int NB, bool GATHER>
+__global__ void __launch_bounds__(256) act_aux_kernel(ActParams p) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.n_mv;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float* xv = p.x + i * NB;
+    if constexpr (GATHER) {
+      for (int k = 0; k < p.K; ++k) p.y[i * p.K + k] = xv[p.ki[k]];
+    } else {
+      const int c = (int)((i / p.P) % p.C);
+      float s = 0.f;
+      for (int k = 0; k < p.K; ++k) {
+        const float a = xv[p.ki[k]];
+        s = p.mode == 0 ? fmaf(a, __ldg(p.w + c * NB + p.ki[k]), s) : s + a;
+      }
+      if (p.mode == 0) s += __ldg(p.b + c);
+      else if (p.mode == 2) s = s / p.Kf;
+      p.y[i] = s;
+    }
+  }
+}
+
+template <bool GATHER>
+static cudaError_t launch_aux(int nb, const ActParams& p, cudaStream_t s) {
+  if (p.n_mv == 0) return cudaSuccess;
+  long long blocks = (p.n_mv + 255) / 256;
+  blocks = blocks > 4LL * num_sms() * 8 ? 4LL * num_sms() * 8 : blocks;
+  if (nb == 2) act_aux_kernel<2, GATHER><<<(unsigned)blocks, 256, 0, s>>>(p);
+  else if (nb == 4) act_aux_kernel<4, GATHER><<<(unsigned)blocks, 256, 0, s>>>(p);
+  else act_aux_kernel<8, GATHER><<<(unsigned)blocks, 256, 0, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_act_preact(int nb, const ActParams& p, cudaStream_t s) { return launch_aux<false>(nb, p, s); }
+cudaError_t launch_act_gather(int nb, const ActParams& p, cudaStream_t s) { return launch_aux<true>(nb, p, s); }
 
 }  // namespace cl

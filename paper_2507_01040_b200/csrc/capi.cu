@@ -735,8 +735,10 @@ struct Epi {
   int res_side = 0, res_crop = 0;
   __nv_bfloat16* y_bf16 = nullptr;  // write bf16 A-ready output for a following bf16 conv
   int ybf_groups = 0;
-  unsigned* amax_out = nullptr;      // int8 mode: per-sample max |y| of this conv's output (atomicMax)
-  const unsigned* amax_in = nullptr; // int8 mode: per-sample max |x| already known (skip the absmax pass)
+  unsigned* amax_out = nullptr;      // int8 mode: per-sample max finite |y| of this conv's output (atomicMax)
+  unsigned* nf_out = nullptr;        //            and per-sample "y holds Inf / NaN" flags (atomicOr)
+  const unsigned* amax_in = nullptr; // int8 mode: per-sample max finite |x| already known (skip the absmax pass)
+  const unsigned* nf_in = nullptr;   //            and the matching non-finite flags
 };
 
 // Pattern class of the change-of-basis inverse for the int8 epilogue: 1 when
@@ -837,7 +839,8 @@ constexpr size_t kSchedBytes = 256;
 static size_t conv_ws_operand_bytes(const cl_conv* h, long long B, bool prepacked) {
   const ConvPlan& pl = h->plan;
   const size_t P_in = (size_t)ipow(h->d_image, h->sk) * (pl.bs.on ? pl.bs.ncol : 1);  // rows per sample
-  if (pl.prec == kPrecFp32) return align_up((size_t)kDigitsA * B * pl.G * P_in * 16, 256) + align_up((size_t)B * 8, 256);
+  // digits | amax[B] | non-finite flags[B] | scale[B]
+  if (pl.prec == kPrecFp32) return align_up((size_t)kDigitsA * B * pl.G * P_in * 16, 256) + align_up((size_t)B * 12, 256);
   if (pl.packed && !prepacked) return align_up((size_t)B * pl.G * P_in * 16, 256);
   return 0;
 }
@@ -866,21 +869,24 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   if (B == 0) return CL_OK;
   const long long P_in = (long long)ipow(h->d_image, h->sk);
   float* a_scale = nullptr;
+  const unsigned* nf_in = nullptr;  // int8 mode: per-sample "x holds Inf / NaN"
   const void* src = x;
   const bool prep = !g_time_kernel_only;
   if (pl.prec == kPrecFp32) {
     const size_t bytes = align_up((size_t)kDigitsA * B * pl.G * P_in * (pl.bs.on ? pl.bs.ncol : 1) * 16, 256);
     int8_t* digits = reinterpret_cast<int8_t*>(ws);
     unsigned* amax = reinterpret_cast<unsigned*>(digits + bytes);
-    a_scale = reinterpret_cast<float*>(digits + bytes + (size_t)B * 4);
+    unsigned* nf = amax + B;
+    a_scale = reinterpret_cast<float*>(digits + bytes + (size_t)B * 8);
+    nf_in = epi.amax_in ? epi.nf_in : nf;
     const long long per_sample = (long long)h->C_in * P_in * h->nb;
     if (prep) {
       static const bool no_fused_prep = CL_ENV("CL_NO_FUSED_PREP") != nullptr;  // A/B
       if (!epi.amax_in && !no_fused_prep && B * per_sample <= kSmallPrepElems) {
         // launch-bound layer: absmax + slice in one cluster launch
-        CL_CUDA(launch_absmax_slice(x, digits, a_scale, h->nb, B, h->C_in, P_in, pl.G, pl.bs, s), "absmax_slice");
+        CL_CUDA(launch_absmax_slice(x, digits, a_scale, nf, h->nb, B, h->C_in, P_in, pl.G, pl.bs, s), "absmax_slice");
       } else {
-        if (!epi.amax_in) CL_CUDA(launch_sample_absmax(x, B, per_sample, amax, s), "absmax");
+        if (!epi.amax_in) CL_CUDA(launch_sample_absmax(x, B, per_sample, amax, nf, s), "absmax");
         CL_CUDA(launch_slice_input(x, epi.amax_in ? epi.amax_in : amax, digits, a_scale, h->nb, B, h->C_in, P_in,
                                    pl.G, pl.bs, s),
                 "slice_input");
@@ -988,7 +994,11 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.act_w = epi.act ? epi.act->w : nullptr;
   p.act_b = epi.act ? epi.act->b : nullptr;
   p.act_K = epi.act ? (float)epi.act->K : 1.f;
+  p.act_kmask = 0;
+  if (epi.act)
+    for (int a = 0; a < epi.act->K; ++a) p.act_kmask |= 1u << epi.act->ki[a];
   p.amax_out = epi.amax_out;
+  p.nf_out = epi.nf_out;
   int grid = (int)std::min<long long>(p.num_tiles, (long long)num_sms());
   grid -= grid % p.cs;
   // Dynamic tile order for long launches, where the static order's drift
@@ -1020,6 +1030,26 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
             h[3] ? (double)h[4] / h[3] : 0.0, h[3] ? (double)h[5] / h[3] : 0.0, (double)(h[6] - ~h[7]) * 1e-3);
   }
   if (e != cudaSuccess) return cuda_fail(e, "conv_tc launch");
+  if (pl.prec == kPrecFp32 && prep && y && x) {
+    // non-finite inputs were sliced as 0: NaN over their receptive fields (reference semantics)
+    PoisonParams pp{};
+    pp.x = x;
+    pp.y = y;
+    pp.flags = nf_in;
+    pp.flags_out = epi.nf_out;
+    pp.B = B;
+    pp.P_in = P_in;
+    pp.P_out = (long long)ipow(h->d_out, h->sk);
+    pp.C_in = h->C_in;
+    pp.C_out = h->C_out;
+    pp.nb = h->nb;
+    pp.k = h->sk;
+    pp.d_in = h->d_image;
+    pp.d_out = h->d_out;
+    pp.d_filter = h->d_filter;
+    pp.pad = h->pad;
+    CL_CUDA(launch_poison_nonfinite(pp, s), "poison_nonfinite");
+  }
   return CL_OK;
 }
 
@@ -1208,6 +1238,26 @@ int cl_conv_forward_host(const cl_conv* h, const float* xh, float* yh, int64_t B
 }
 
 // ---- activation -------------------------------------------------------------
+static ActParams act_params(const cl_act* h, const float* x, float* y, long long B, long long P) {
+  ActParams p{};
+  p.x = x;
+  p.y = y;
+  p.n_mv = B * h->C * P;
+  p.P = P;
+  p.C = h->C;
+  p.mode = h->mode;
+  p.w = h->w;
+  p.b = h->b;
+  p.Kf = (float)h->K;
+  p.K = h->K;
+  p.kmask = 0;
+  for (int a = 0; a < 8; ++a) {
+    p.ki[a] = a < h->K ? h->ki[a] : 0;
+    if (a < h->K) p.kmask |= 1u << h->ki[a];
+  }
+  return p;
+}
+
 int cl_act_create(const int32_t* g, int k, int mode, const int32_t* ki, int K, int C,
                   const float* weight, const float* bias, void* stream, cl_act** out) {
   if (!out) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null output handle pointer");
@@ -1267,19 +1317,26 @@ int cl_act_forward(const cl_act* h, const float* x, float* y, int64_t B, int64_t
   if (P >= (1LL << 30)) return fail(CL_ERR_UNSUPPORTED, "Unsupported", "activation needs P < 2^30 positions per channel");
   if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) != 0)
     return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "activation buffers must be 16-byte aligned");
-  ActParams p{};
-  p.x = x;
-  p.y = y;
-  p.n_mv = (long long)B * h->C * P;
-  p.P = P;
-  p.C = h->C;
-  p.mode = h->mode;
-  p.w = h->w;
-  p.b = h->b;
-  p.Kf = (float)h->K;
+  ActParams p = act_params(h, x, y, B, P);
   CL_CUDA(launch_act(h->nb, p, (cudaStream_t)stream), "activation launch");
   return CL_OK;
 }
+
+int cl_act_preactivation(const cl_act* h, const float* x, float* s_out, int64_t B, int64_t P, void* stream) {
+  if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null activation handle");
+  if (B < 0 || P < 1) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "B >= 0 and P >= 1 required");
+  CL_CUDA(launch_act_preact(h->nb, act_params(h, x, s_out, B, P), (cudaStream_t)stream), "preactivation launch");
+  return CL_OK;
+}
+
+int cl_act_gather(const cl_act* h, const float* x, float* v_out, int64_t B, int64_t P, void* stream) {
+  if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null activation handle");
+  if (B < 0 || P < 1) return fail(CL_ERR_SHAPE_MISMATCH, "ShapeMismatch", "B >= 0 and P >= 1 required");
+  CL_CUDA(launch_act_gather(h->nb, act_params(h, x, v_out, B, P), (cudaStream_t)stream), "gather launch");
+  return CL_OK;
+}
+
+int cl_act_kernel_count(const cl_act* h) { return h ? h->K : -CL_ERR_CONFIG_INVALID; }
 
 int cl_act_forward_host(const cl_act* h, const float* xh, float* yh, int64_t B, int64_t P, void* stream) {
   if (!h) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "null activation handle");
@@ -1347,7 +1404,7 @@ static size_t block_mid_bytes(const cl_block* h, long long B) {
 static size_t block_ws_bytes(const cl_block* h, long long B) {
   const bool bf = bf16_handoff(h);
   // + the per-sample max |y1| conv1's epilogue accumulates for conv2's digit slicing (int8 mode)
-  return block_mid_bytes(h, B) + align_up((size_t)B * 4, 256) +
+  return block_mid_bytes(h, B) + align_up((size_t)B * 8, 256) +
          std::max(conv_ws_bytes(h->c1, B, false), conv_ws_bytes(h->c2, B, bf));
 }
 
@@ -1358,7 +1415,8 @@ static int block_run(const cl_block* h, const float* x, float* y, long long B, v
   const size_t mid_bytes = block_mid_bytes(h, B);
   void* mid = ws;
   unsigned* amax_mid = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + mid_bytes);
-  void* cws = reinterpret_cast<char*>(ws) + mid_bytes + align_up((size_t)B * 4, 256);
+  unsigned* nf_mid = amax_mid + B;  // y1 holds Inf / NaN (exact mode)
+  void* cws = reinterpret_cast<char*>(ws) + mid_bytes + align_up((size_t)B * 8, 256);
   Epi e1;
   e1.act = h->act;
   Epi e2;
@@ -1379,9 +1437,11 @@ static int block_run(const cl_block* h, const float* x, float* y, long long B, v
   }
   if (c2->prec == kPrecFp32 && c1->prec == kPrecFp32 && !g_no_fused_amax) {
     // conv1's epilogue takes conv2's per-sample max |y1|: no separate absmax pass over y1
-    CL_CUDA(cudaMemsetAsync(amax_mid, 0, (size_t)B * 4, s), "amax memset");
+    CL_CUDA(cudaMemsetAsync(amax_mid, 0, (size_t)B * 8, s), "amax memset");
     e1.amax_out = amax_mid;
+    e1.nf_out = nf_mid;
     e2.amax_in = amax_mid;
+    e2.nf_in = nf_mid;
   }
   if (int rc = conv_run(c1, x, nullptr, (float*)mid, B, e1, cws, s)) return rc;
   return conv_run(c2, (const float*)mid, nullptr, y, B, e2, cws, s);

@@ -424,6 +424,15 @@ __device__ __forceinline__ void tmem_ld_wait() {
 // |v| as float bits, for max-reductions as unsigned integers: NaN (> Inf >
 // any finite) sticks, where fmaxf would drop it.
 __device__ __forceinline__ unsigned abs_bits(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+// |v| as float bits, 0 for Inf / NaN: the exact mode's scales cover the FINITE
+// values; non-finite inputs are sliced as 0 and their receptive fields are
+// poisoned to NaN afterwards (slice.cu poison_nonfinite_kernel), as the
+// reference's fp64 einsum turns them (0 * Inf = NaN, conv.py:168-176).
+__device__ __forceinline__ unsigned finite_abs_bits(float v) {
+  const unsigned a = __float_as_uint(v) & 0x7fffffffu;
+  return a < 0x7f800000u ? a : 0u;
+}
+__device__ __forceinline__ bool non_finite(float v) { return (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u; }
 // Power-of-two scale above amax; NaN when amax is not finite, so a sample
 // holding Inf / NaN comes out NaN in the exact mode instead of as digits of garbage.
 __device__ __forceinline__ float pow2_scale_for(float amax) {

@@ -28,12 +28,17 @@
 
 namespace cl {
 
+// Gate of one multivector. Non-kernel blades are selected out (kmask), not
+// weighted by zero: the reference never reads them (activation.py:142-162).
 template <int NB>
 __device__ __forceinline__ float act_gate(const float (&v)[NB], int mode, const float* __restrict__ w,
-                                          float bias, float Kf) {
+                                          float bias, float Kf, unsigned kmask) {
   float s = 0.f;
 #pragma unroll
-  for (int j = 0; j < NB; ++j) s = fmaf(v[j], __ldg(w + j), s);
+  for (int j = 0; j < NB; ++j) {
+    const float t = fmaf(v[j], __ldg(w + j), s);
+    s = ((kmask >> j) & 1u) ? t : s;
+  }
   if (mode == 0) s += bias;
   else if (mode == 2) s = s / Kf;
   return 1.f / (1.f + expf(-s));
@@ -762,7 +767,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                     }
                     const long long xs = (inv_os[j] > 0 ? a : -a) + (inv_ps[j] > 0 ? bq : -bq);
                     v[j] = (float)fma((double)xs, sc, (double)bw[j]);
-                    if (p.act_mode >= 0) part[cc] = fmaf(v[j], aw[j], part[cc]);
+                    if (p.act_mode >= 0 && ((p.act_kmask >> (bcol * W + j)) & 1u)) part[cc] = fmaf(v[j], aw[j], part[cc]);
                   }
 #pragma unroll
                   for (int j = 0; j < W; ++j) hv[ci * CH + cc * W + j] = v[j];
@@ -797,7 +802,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 }
                 if (p.act_mode >= 0 && co < p.C_out) {
                   const float gte = act_gate<NB>(v, p.act_mode, p.act_w + co * NB,
-                                                 p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K);
+                                                 p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K, p.act_kmask);
 #pragma unroll
                   for (int j = 0; j < NB; ++j) v[j] *= gte;
                 }
@@ -814,7 +819,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           atomicAdd(p.dbg_acc + 1, 1ull);
         }
         if (++acc == slots) { acc = 0; acc_phase ^= 1; }
-        unsigned ymax = 0;  // max |stored value| of this thread as float bits, NaN-sticky (fused absmax for the next conv)
+        // fused absmax for the next conv: max finite |stored value| (float bits) and a
+        // non-finite marker (NaN-sticky max of |value| bits), see finite_abs_bits
+        unsigned ymax = 0, yany = 0;
         if (valid && !(p.dbg_skip & 4))
 #pragma unroll
         for (int ci = 0; ci < kHold / CH; ++ci) {
@@ -850,7 +857,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                   else *reinterpret_cast<float4*>(yp) = make_float4(h[0], h[1 % W], h[2 % W], h[3 % W]);
                 }
 #pragma unroll
-                for (int j = 0; j < W; ++j) ymax = max(ymax, abs_bits(h[j]));
+                for (int j = 0; j < W; ++j) { ymax = max(ymax, finite_abs_bits(h[j])); yany = max(yany, abs_bits(h[j])); }
               } else {
                 if (cc >= CH / NB) break;
                 float v[NB];
@@ -880,18 +887,27 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                   }
                 }
 #pragma unroll
-                for (int j = 0; j < NB; ++j) ymax = max(ymax, abs_bits(v[j]));
+                for (int j = 0; j < NB; ++j) { ymax = max(ymax, finite_abs_bits(v[j])); yany = max(yany, abs_bits(v[j])); }
               }
             }
           }
         }
         if (p.amax_out) {
           if (p.k == 1) {  // 1-D: rows of one tile belong to different samples
-            if (valid) atomicMax(p.amax_out + b, ymax);
+            if (valid) {
+              atomicMax(p.amax_out + b, ymax);
+              if (yany >= 0x7f800000u) atomicOr(p.nf_out + b, 1u);
+            }
           } else {  // one sample per tile: reduce over the warp first
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) ymax = max(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
-            if (lane == 0 && real) atomicMax(p.amax_out + b, ymax);
+            for (int o = 16; o > 0; o >>= 1) {
+              ymax = max(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
+              yany = max(yany, __shfl_xor_sync(0xffffffffu, yany, o));
+            }
+            if (lane == 0 && real) {
+              atomicMax(p.amax_out + b, ymax);
+              if (yany >= 0x7f800000u) atomicOr(p.nf_out + b, 1u);
+            }
           }
         }
         continue;
@@ -958,7 +974,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 const float a = pick_wf<W>(own, inv_o[j]), bq = pick_wf<W>(oth, inv_p[j]);
                 const int t = bcol * W + j;
                 h[j] = 0.5f * ((inv_os[j] > 0 ? a : -a) + (inv_ps[j] > 0 ? bq : -bq)) + __ldg(p.bias + t * p.C_out + cq);
-                if (p.act_mode >= 0) part = fmaf(h[j], __ldg(p.act_w + cq * NB + t), part);
+                if (p.act_mode >= 0 && ((p.act_kmask >> t) & 1u)) part = fmaf(h[j], __ldg(p.act_w + cq * NB + t), part);
               }
               if (p.act_mode >= 0) {
                 float sg = part + __shfl_xor_sync(0xffffffffu, part, 1);
@@ -998,7 +1014,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
             if (!valid || co >= p.C_out) continue;
             if (p.act_mode >= 0) {
               const float gte = act_gate<NB>(v, p.act_mode, p.act_w + co * NB,
-                                             p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K);
+                                             p.act_mode == 0 ? __ldg(p.act_b + co) : 0.f, p.act_K, p.act_kmask);
 #pragma unroll
               for (int j = 0; j < NB; ++j) v[j] *= gte;
             }

@@ -170,7 +170,9 @@ struct ConvKParams {
   const float* act_w;         // (C_out, NB) blade-keyed weights / 0-1 mask
   const float* act_b;         // (C_out) Linear bias
   float act_K;                // K as float (Mean divisor)
-  unsigned* amax_out;         // int8 epilogue: per-sample atomicMax of |stored value| (float bits), or null
+  unsigned act_kmask;         // kernel blades of the gate (non-kernel blades are selected out, never * 0)
+  unsigned* amax_out;         // int8 epilogue: per-sample atomicMax of finite |stored value| (float bits), or null
+  unsigned* nf_out;           // int8 epilogue: per-sample flag, a stored value is Inf / NaN (with amax_out)
   unsigned long long* tile_ctr;  // dynamic tile scheduler: zeroed work counter (cluster tiles), or null = static order
 };
 
@@ -184,6 +186,9 @@ struct ActParams {
   const float* w;     // (C, NB)
   const float* b;     // (C)
   float Kf;
+  unsigned kmask;     // bit j set: blade j is a kernel blade (only those enter the gate)
+  int K;              // kernel blades, in the caller's order ki[0..K)
+  int ki[8];
   // exact unsigned division of n < 2^31 by P and by C: q = (n * mag) >> sh
   // (filled by launch_act)
   unsigned magP, shP, magC, shC;
@@ -200,12 +205,28 @@ cudaError_t launch_transpose(const float* in, float* out, int rows, int cols, cu
 cudaError_t launch_pack_rows(const float* x, void* out, int nb, int esize, long long B, int C, long long P,
                              int G, const Basis& bs, cudaStream_t s);
 cudaError_t launch_act(int nb, const ActParams& p, cudaStream_t s);
-// kPrecFp32 operand preparation (slice.cu)
-cudaError_t launch_sample_absmax(const float* x, long long B, long long per_sample, unsigned* amax,
+// gate_preactivation (s per multivector, written to p.y as (B, C, P)) and
+// gather_vpack (the K kernel blades in ki order, p.y as (B, C, P, K))
+cudaError_t launch_act_preact(int nb, const ActParams& p, cudaStream_t s);
+cudaError_t launch_act_gather(int nb, const ActParams& p, cudaStream_t s);
+// kPrecFp32 operand preparation (slice.cu): per-sample max over the finite
+// values + a per-sample non-finite flag (zeroed by the launcher)
+cudaError_t launch_sample_absmax(const float* x, long long B, long long per_sample, unsigned* amax, unsigned* flags,
                                  cudaStream_t s);
-// small layers: per-sample absmax + slicing in one cluster launch (no amax buffer)
-cudaError_t launch_absmax_slice(const float* x, int8_t* digits, float* scale, int nb, long long B, int C, long long P,
-                                int G, const Basis& bs, cudaStream_t s);
+// small layers: per-sample absmax + slicing in one cluster launch (no amax
+// buffer; flags[b] is written, not accumulated)
+cudaError_t launch_absmax_slice(const float* x, int8_t* digits, float* scale, unsigned* flags, int nb, long long B,
+                                int C, long long P, int G, const Basis& bs, cudaStream_t s);
+// exact mode: NaN over the receptive fields of non-finite inputs (flagged samples only)
+struct PoisonParams {
+  const float* x;           // conv input (B, C_in, d_in^k, nb)
+  float* y;                 // conv output (B, C_out, d_out^k, nb)
+  const unsigned* flags;    // per-sample: input holds Inf / NaN
+  unsigned* flags_out;      // optional: per-sample flags for the next conv (block)
+  long long B, P_in, P_out;
+  int C_in, C_out, nb, k, d_in, d_out, d_filter, pad;
+};
+cudaError_t launch_poison_nonfinite(const PoisonParams& p, cudaStream_t s);
 cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* digits, float* scale,
                                int nb, long long B, int C, long long P, int G, const Basis& bs, cudaStream_t s);
 cudaError_t launch_weight_colscale(const int* g, const ConvPlan& pl, const float* f, int C_in, int C_out,

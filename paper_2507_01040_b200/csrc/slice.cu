@@ -16,19 +16,27 @@
 
 namespace cl {
 
-// Per-sample max |x|. Block (j, b) reduces the j-th contiguous chunk of
-// kAbsmaxU float4 per thread of sample b (many waves, one atomic per block).
+// Per-sample max |x| over the FINITE values, and a per-sample flag when the
+// sample holds Inf / NaN (those are sliced as 0 and their receptive fields
+// poisoned afterwards, poison_nonfinite_kernel). Block (j, b) reduces the j-th
+// contiguous chunk of kAbsmaxU float4 per thread of sample b (many waves, one
+// atomic per block). The grid is 1-D over (sample, chunk) pairs -- any B (a
+// linear layer can have far more than gridDim.y's 65535 samples); launches of
+// more than 2^31-1 blocks are split by the host with `blk0`.
 constexpr int kAbsmaxU = 8;
-// The grid is 1-D over (sample, chunk) pairs -- any B (a linear layer can
-// have far more than gridDim.y's 65535 samples); launches of more than 2^31-1
-// blocks are split by the host with `blk0`.
 __global__ void __launch_bounds__(256) absmax_kernel(const float* __restrict__ x, long long per_sample,
-                                                     long long per, long long blk0, unsigned* __restrict__ amax) {
+                                                     long long per, long long blk0, unsigned* __restrict__ amax,
+                                                     unsigned* __restrict__ flags) {
   const long long bid = blk0 + (long long)blockIdx.x;
   const long long b = bid / per;
   const long long chunk = bid - b * per;
   const float* xs = x + b * per_sample;
-  unsigned m = 0;  // max |x| as float bits (NaN-sticky)
+  unsigned m = 0;    // max finite |x| as float bits
+  unsigned any = 0;  // max |x| as float bits, NaN-sticky: >= 0x7f800000 iff a value is non-finite
+  auto take = [&](float v) {
+    m = max(m, finite_abs_bits(v));
+    any = max(any, abs_bits(v));
+  };
   // samples need not start 16-byte aligned (1-D tensors): scalar head, float4 body, scalar tail
   long long head = (long long)((16 - (reinterpret_cast<uintptr_t>(xs) & 15)) & 15) / 4;
   if (head > per_sample) head = per_sample;
@@ -40,34 +48,44 @@ __global__ void __launch_bounds__(256) absmax_kernel(const float* __restrict__ x
   for (int u = 0; u < kAbsmaxU; ++u)
     v[u] = base + u * 256 < n4 ? __ldcs(x4 + base + u * 256) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-  for (int u = 0; u < kAbsmaxU; ++u)
-    m = max(m, max(max(abs_bits(v[u].x), abs_bits(v[u].y)), max(abs_bits(v[u].z), abs_bits(v[u].w))));
-  if (chunk == 0) {
-    if (threadIdx.x < head) m = max(m, abs_bits(xs[threadIdx.x]));
-    for (long long i = head + n4 * 4 + threadIdx.x; i < per_sample; i += blockDim.x) m = max(m, abs_bits(xs[i]));
+  for (int u = 0; u < kAbsmaxU; ++u) {
+    take(v[u].x); take(v[u].y); take(v[u].z); take(v[u].w);
   }
-  __shared__ unsigned red[8];
+  if (chunk == 0) {
+    if (threadIdx.x < head) take(xs[threadIdx.x]);
+    for (long long i = head + n4 * 4 + threadIdx.x; i < per_sample; i += blockDim.x) take(xs[i]);
+  }
+  __shared__ unsigned red[8], redn[8];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  for (int o = 16; o > 0; o >>= 1) {
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    any = max(any, __shfl_xor_sync(0xffffffffu, any, o));
+  }
+  if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = m; redn[threadIdx.x >> 5] = any; }
   __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int w = 1; w < 8; ++w) m = max(m, red[w]);
+    for (int w = 1; w < 8; ++w) { m = max(m, red[w]); any = max(any, redn[w]); }
     atomicMax(amax + b, m);
+    if (any >= 0x7f800000u) atomicOr(flags + b, 1u);
   }
 }
 
-cudaError_t launch_sample_absmax(const float* x, long long B, long long per_sample, unsigned* amax,
+cudaError_t launch_sample_absmax(const float* x, long long B, long long per_sample, unsigned* amax, unsigned* flags,
                                  cudaStream_t s) {
   if (B == 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(unsigned) * B, s);
+  cudaError_t e;
+  if (flags == amax + B) {  // adjacent arrays (the conv workspace layout): one memset
+    e = cudaMemsetAsync(amax, 0, sizeof(unsigned) * 2 * B, s);
+  } else if ((e = cudaMemsetAsync(amax, 0, sizeof(unsigned) * B, s)) == cudaSuccess) {
+    e = cudaMemsetAsync(flags, 0, sizeof(unsigned) * B, s);
+  }
   if (e != cudaSuccess) return e;
   const long long per = std::max<long long>(1, (per_sample / 4 + 256 * kAbsmaxU - 1) / (256 * kAbsmaxU));
   const long long total = per * B;
   for (long long b0 = 0; b0 < total; b0 += 0x7fffffffLL) {
     const long long n = std::min<long long>(0x7fffffffLL, total - b0);
-    absmax_kernel<<<(unsigned)n, 256, 0, s>>>(x, per_sample, per, b0, amax);
+    absmax_kernel<<<(unsigned)n, 256, 0, s>>>(x, per_sample, per, b0, amax, flags);
     count_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
@@ -126,7 +144,7 @@ __device__ __forceinline__ void slice_item(const float* __restrict__ x, float am
         }
       }
 #pragma unroll
-      for (int I = 0; I < NB; ++I) X[I] = __float2int_rn(v[I] * mult);
+      for (int I = 0; I < NB; ++I) X[I] = non_finite(v[I]) ? 0 : __float2int_rn(v[I] * mult);  // see finite_abs_bits
     } else {
 #pragma unroll
       for (int I = 0; I < NB; ++I) X[I] = 0;
@@ -224,31 +242,43 @@ __global__ void __launch_bounds__(256, FIXED ? CL_SLICE_MINB : 1) slice_input_ke
 constexpr int kSliceCluster = 8;
 template <int NB, bool BASIS, bool FIXED = false>
 __global__ void __launch_bounds__(256) absmax_slice_kernel(const float* __restrict__ x, int8_t* __restrict__ out,
-                                                           float* __restrict__ scale, long long B, int C, long long P,
-                                                           int G, Basis bs) {
-  __shared__ unsigned red[8];  // max |x| as float bits (NaN-sticky)
-  __shared__ float cmax;
+                                                           float* __restrict__ scale, unsigned* __restrict__ flags,
+                                                           long long B, int C, long long P, int G, Basis bs) {
+  __shared__ unsigned red[8], redn[8];  // max finite |x| / max |x| (NaN-sticky) as float bits
+  __shared__ float cmax, cany;
   const int rank = (int)cluster_ctarank();
   const long long b = blockIdx.x / kSliceCluster;
   const long long per_sample = (long long)C * P * NB;
   const float* xs = x + b * per_sample;
-  unsigned m = 0;
+  unsigned m = 0, any = 0;
   const long long n0 = per_sample * rank / kSliceCluster, n1 = per_sample * (rank + 1) / kSliceCluster;
-  for (long long i = n0 + threadIdx.x; i < n1; i += blockDim.x) m = max(m, abs_bits(__ldg(xs + i)));
+  for (long long i = n0 + threadIdx.x; i < n1; i += blockDim.x) {
+    const float v = __ldg(xs + i);
+    m = max(m, finite_abs_bits(v));
+    any = max(any, abs_bits(v));
+  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  for (int o = 16; o > 0; o >>= 1) {
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    any = max(any, __shfl_xor_sync(0xffffffffu, any, o));
+  }
+  if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = m; redn[threadIdx.x >> 5] = any; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned v = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = max(v, red[w]);
+    unsigned v = 0, vn = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { v = max(v, red[w]); vn = max(vn, redn[w]); }
     cmax = __uint_as_float(v);
+    cany = __uint_as_float(vn);
   }
-  cluster_sync();  // every CTA's share is in its cmax
+  cluster_sync();  // every CTA's share is in its cmax / cany
   if (threadIdx.x == 0) {
-    unsigned v = 0;
-    for (int r = 0; r < kSliceCluster; ++r) v = max(v, __float_as_uint(ld_shared_cluster_f32(&cmax, r)));
+    unsigned v = 0, vn = 0;
+    for (int r = 0; r < kSliceCluster; ++r) {
+      v = max(v, __float_as_uint(ld_shared_cluster_f32(&cmax, r)));
+      vn = max(vn, __float_as_uint(ld_shared_cluster_f32(&cany, r)));
+    }
     red[0] = v;
+    if (rank == 0) flags[b] = vn >= 0x7f800000u ? 1u : 0u;  // written every call: no zeroing launch
   }
   cluster_sync();  // peers done reading cmax (no CTA exits while it is read)
   __syncthreads();
@@ -265,8 +295,8 @@ __global__ void __launch_bounds__(256) absmax_slice_kernel(const float* __restri
 }
 
 template <int NB, bool BASIS, bool FIXED>
-static cudaError_t launch_fused_t(const float* x, int8_t* digits, float* scale, long long B, int C, long long P, int G,
-                                  const Basis& bs, cudaStream_t s) {
+static cudaError_t launch_fused_t(const float* x, int8_t* digits, float* scale, unsigned* flags, long long B, int C,
+                                  long long P, int G, const Basis& bs, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(B * kSliceCluster));
   cfg.blockDim = dim3(256);
@@ -278,7 +308,7 @@ static cudaError_t launch_fused_t(const float* x, int8_t* digits, float* scale, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, absmax_slice_kernel<NB, BASIS, FIXED>, x, digits, scale, B, C, P, G, bs);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, absmax_slice_kernel<NB, BASIS, FIXED>, x, digits, scale, flags, B, C, P, G, bs);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -294,17 +324,17 @@ static bool fixed_111_basis(int nb, const Basis& bs) {
   return fixed;
 }
 
-cudaError_t launch_absmax_slice(const float* x, int8_t* digits, float* scale, int nb, long long B, int C, long long P,
-                                int G, const Basis& bs, cudaStream_t s) {
+cudaError_t launch_absmax_slice(const float* x, int8_t* digits, float* scale, unsigned* flags, int nb, long long B,
+                                int C, long long P, int G, const Basis& bs, cudaStream_t s) {
   if (B * G * P == 0) return cudaSuccess;
   if (bs.on) {
-    if (nb == 4) return launch_fused_t<4, true, false>(x, digits, scale, B, C, P, G, bs, s);
-    if (fixed_111_basis(nb, bs)) return launch_fused_t<8, true, true>(x, digits, scale, B, C, P, G, bs, s);
-    return launch_fused_t<8, true, false>(x, digits, scale, B, C, P, G, bs, s);
+    if (nb == 4) return launch_fused_t<4, true, false>(x, digits, scale, flags, B, C, P, G, bs, s);
+    if (fixed_111_basis(nb, bs)) return launch_fused_t<8, true, true>(x, digits, scale, flags, B, C, P, G, bs, s);
+    return launch_fused_t<8, true, false>(x, digits, scale, flags, B, C, P, G, bs, s);
   }
-  if (nb == 2) return launch_fused_t<2, false, false>(x, digits, scale, B, C, P, G, bs, s);
-  if (nb == 4) return launch_fused_t<4, false, false>(x, digits, scale, B, C, P, G, bs, s);
-  return launch_fused_t<8, false, false>(x, digits, scale, B, C, P, G, bs, s);
+  if (nb == 2) return launch_fused_t<2, false, false>(x, digits, scale, flags, B, C, P, G, bs, s);
+  if (nb == 4) return launch_fused_t<4, false, false>(x, digits, scale, flags, B, C, P, G, bs, s);
+  return launch_fused_t<8, false, false>(x, digits, scale, flags, B, C, P, G, bs, s);
 }
 
 cudaError_t launch_slice_input(const float* x, const unsigned* amax, int8_t* digits, float* scale, int nb,
@@ -377,6 +407,62 @@ cudaError_t launch_weight_colscale(const int* g, const ConvPlan& pl, const float
   const int N_pad = pl.n_ntiles * pl.n_tile;
   const Sig sg = make_sig(g, pl.ka);
   weight_colscale_kernel<<<N_pad, 256, 0, s>>>(sg, f, C_in, C_out, pl.Q, pl.bs, w_scale);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Exact mode, non-finite inputs (after the conv): every output pixel whose
+// receptive field holds an Inf / NaN input becomes NaN in all channels and
+// blades -- what the reference's fp64 einsum gives there (a non-finite input
+// times the Cayley tensor's structural zeros, conv.py:168-176) -- while every
+// other output keeps its exact value (the slice pass encoded the non-finite
+// inputs as 0). Samples without a flag return at once, so the launch is a few
+// microseconds when the input is finite. `flags_out` (optional) marks the
+// samples the next conv of a block must treat the same way.
+__global__ void __launch_bounds__(256) poison_nonfinite_kernel(PoisonParams p) {
+  const long long total = p.B * p.P_out;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / p.P_out;
+    if (!__ldg(p.flags + b)) continue;
+    const long long o = i - b * p.P_out;
+    const int d = p.d_out;
+    const int ox = (int)(o % d), oy = p.k >= 2 ? (int)((o / d) % d) : 0, oz = p.k == 3 ? (int)(o / ((long long)d * d)) : 0;
+    const int qz_n = p.k == 3 ? p.d_filter : 1, qy_n = p.k >= 2 ? p.d_filter : 1;
+    bool hit = false;
+    for (int qz = 0; qz < qz_n && !hit; ++qz) {
+      const int iz = oz + qz - (p.k == 3 ? p.pad : 0);
+      if (iz < 0 || iz >= (p.k == 3 ? p.d_in : 1)) continue;
+      for (int qy = 0; qy < qy_n && !hit; ++qy) {
+        const int iy = oy + qy - (p.k >= 2 ? p.pad : 0);
+        if (iy < 0 || iy >= (p.k >= 2 ? p.d_in : 1)) continue;
+        for (int qx = 0; qx < p.d_filter && !hit; ++qx) {
+          const int ix = ox + qx - p.pad;
+          if (ix < 0 || ix >= p.d_in) continue;
+          const long long pin = ((long long)iz * p.d_in + iy) * p.d_in + ix;
+          for (int c = 0; c < p.C_in && !hit; ++c) {
+            const float* xp = p.x + ((b * p.C_in + c) * p.P_in + pin) * p.nb;
+            for (int j = 0; j < p.nb; ++j) hit = hit || non_finite(xp[j]);
+          }
+        }
+      }
+    }
+    if (!hit) continue;
+    for (int co = 0; co < p.C_out; ++co) {
+      float* yp = p.y + ((b * p.C_out + co) * p.P_out + o) * p.nb;
+      for (int t = 0; t < p.nb; ++t) yp[t] = __uint_as_float(0x7fc00000u);
+    }
+    if (p.flags_out) atomicOr(p.flags_out + b, 1u);
+  }
+}
+
+cudaError_t launch_poison_nonfinite(const PoisonParams& p, cudaStream_t s) {
+  const long long total = p.B * p.P_out;
+  if (total == 0) return cudaSuccess;
+  long long blocks = (total + 255) / 256;
+  const long long cap = 8LL * num_sms();
+  if (blocks > cap) blocks = cap;
+  poison_nonfinite_kernel<<<(unsigned)blocks, 256, 0, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }

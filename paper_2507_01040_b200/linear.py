@@ -9,12 +9,11 @@ the samples, 128 samples per tile), in any of the four precision modes.
 
 from __future__ import annotations
 
-import ctypes as C
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _device, _lib
+from . import _device, _ops
 from .algebra import Signature, schedule_flop_count
 from .conv import PRECISIONS, _out, _out_np, check_variant
 from .errors import ShapeMismatch
@@ -41,15 +40,12 @@ class LinearLayer:
         dev = _device.current_device()
         h = self._handles.get(dev)
         if h is None:
-            lib = _lib.load()
-            out = C.c_void_p()
-            w = np.ascontiguousarray(self.weight)
-            b = np.ascontiguousarray(self.bias)
-            _lib.check(lib.cl_linear_create(
-                _lib.int32_array(self.sig.g), self.sig.k, self.C_in, self.C_out,
-                C.c_void_p(w.ctypes.data), C.c_void_p(b.ctypes.data), PRECISIONS[self.precision],
-                C.c_void_p(_device.stream_ptr()), C.byref(out)))
-            h = _device.Handle(out.value, lib.cl_linear_destroy)
+            torch = _device.torch_mod()
+            w = torch.from_numpy(np.ascontiguousarray(self.weight))
+            b = torch.from_numpy(np.ascontiguousarray(self.bias))
+            ptr = _ops.op("linear_create", list(self.sig.g), self.C_in, self.C_out, w, b,
+                          PRECISIONS[self.precision])
+            h = _device.Handle(ptr, _ops.destroyer("conv_destroy"))
             self._handles[dev] = h
         return h.ptr
 
@@ -79,25 +75,20 @@ def linear_forward(x, layer: LinearLayer, variant: str = "b200", out=None):
         raise ShapeMismatch(f"input shape {tuple(x.shape)}, expected (B, {layer.C_in}, {nb})")
     B = int(x.shape[0])
     shape = (B, layer.C_out, nb)
-    lib = _lib.load()
     if _device.is_cuda_tensor(x):
-        torch = _device.torch_mod()
         with _device.on_device(x.device):
             xc = _device.device_input(x)
             y = _out(out, shape, x.device)
-            _lib.check(lib.cl_linear_forward(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
-                                             C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
+            _ops.op("conv_forward", layer.handle(), xc, B, y)  # cl_linear_forward == cl_conv_forward
         return y
     if _device.is_cpu_tensor(x):
         xc = x.float().contiguous()
         y = _out(out, shape, None, pinned=xc.is_pinned())
-        _lib.check(lib.cl_linear_forward_host(C.c_void_p(layer.handle()), C.c_void_p(xc.data_ptr()),
-                                              C.c_void_p(y.data_ptr()), B, C.c_void_p(_device.stream_ptr())))
+        _ops.op("conv_forward_host", layer.handle(), xc, B, y)
         return y
     xa = np.ascontiguousarray(x, dtype=np.float32)
     y = _out_np(out, shape)
-    _lib.check(lib.cl_linear_forward_host(C.c_void_p(layer.handle()), C.c_void_p(xa.ctypes.data),
-                                          C.c_void_p(y.ctypes.data), B, C.c_void_p(_device.stream_ptr())))
+    _ops.op("conv_forward_host", layer.handle(), _device.host_view(xa), B, _device.host_view(y))
     return y
 
 

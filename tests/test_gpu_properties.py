@@ -9,6 +9,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
+import oracle as O  # noqa: E402
 import paper_2507_01040_b200 as M  # noqa: E402
 
 TOL = {"fp32": (1e-6, 1e-6), "3xtf32": (1e-4, 1e-5), "tf32": (2e-3, 1e-4), "bf16": (2e-2, 1e-3)}
@@ -99,49 +100,131 @@ def test_activation_gate_scale_covariance(mode, alpha):
     np.testing.assert_allclose(s2[ok], alpha * s1[ok], rtol=1e-3, atol=1e-4)
 
 
+def _finite_close(y, ref, prec):
+    """Same finiteness pattern as the oracle (both directions), and the finite
+    entries within the mode's bound."""
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isfinite(y), fin), (int((np.isfinite(y) != fin).sum()), prec)
+    yz, rz = np.where(fin, y, 0), np.where(fin, ref, 0)
+    if prec == "fp32":
+        assert O.max_rel_error(yz, rz) <= 1e-4
+    else:
+        tol = {"3xtf32": 1e-4}.get(prec, 2e-2)
+        assert O.max_rel_error(yz, rz, floor=float(np.abs(rz).max())) <= tol
+
+
 @pytest.mark.parametrize("prec", ["fp32", "3xtf32", "tf32", "bf16"])
-@pytest.mark.parametrize("g", [(1, 1), (1, 1, 1), (1, -1, 0)])
-def test_conv_non_finite_inputs(prec, g):
-    """A NaN / Inf in a sample's input never turns into finite garbage: every
-    output the fp64 oracle gives as non-finite is non-finite here too (the
-    exact mode's per-sample scale becomes NaN, so that whole sample is NaN),
-    and the other samples are untouched."""
-    import oracle as O
+@pytest.mark.parametrize("g,padding", [((1, 1), "valid"), ((1, 1, 1), "same"), ((1, -1, 0), "valid"), ((1,), "same"),
+                                       ((0, 1), "same")])
+def test_conv_non_finite_inputs(prec, g, padding):
+    """A NaN / Inf input turns exactly the outputs the fp64 oracle gives as
+    non-finite into non-finite ones -- the receptive fields of the bad inputs,
+    all channels and blades -- and nothing else: oracle finite <=> B200 finite,
+    finite values within the mode's bound. (The exact mode scales samples by
+    their finite max, slices Inf / NaN as 0 and poisons their receptive fields
+    afterwards; the fp32-accumulator modes propagate them through the MMAs.)"""
     k = len(g)
     nb = 1 << k
     rng = np.random.default_rng(5)
-    B, C, d, df = 3, 3, 6, 3
+    B, C, d, df = 4, 3, {1: 30, 2: 7, 3: 6}[k], 3
     x = rng.standard_normal((B, C, d ** k, nb)).astype(np.float32)
     x[1, 0, 7, 1] = np.nan
     x[2, 2, 3, 0] = np.inf
+    x[3, 1, d ** k - 1, nb - 1] = -np.inf  # a corner: clipped receptive fields
     f = rng.uniform(-1, 1, (nb, C, C, df ** k)).astype(np.float32) / np.float32(np.sqrt(C * nb * df ** k))
     b = (rng.standard_normal((nb, C)) * 0.01).astype(np.float32)
-    y = M.conv_forward(torch.from_numpy(x).cuda(), _conv(g, B, C, C, d, df, f, b, prec)).cpu().numpy()
-    with np.errstate(invalid="ignore"):
-        ref = O.conv_ref(x, f, b, g, d, df, 0)
+    layer = M.make_conv_layer(M.Dims(B, C, C, d, df, k), M.Signature(g), f, b, precision=prec, padding=padding)
+    y = M.conv_forward(torch.from_numpy(x).cuda(), layer).cpu().numpy()
+    pad = 1 if padding == "same" else 0
+    with np.errstate(invalid="ignore", over="ignore"):
+        ref = O.conv_ref(x, f, b, g, d, df, pad)
     bad = ~np.isfinite(ref)
-    assert bad[1].any() and bad[2].any()
-    assert np.all(~np.isfinite(y[bad])), prec
-    assert np.all(np.isfinite(y[0]))
-    assert O.max_rel_error(y[:1], ref[:1], floor=float(np.abs(ref[0]).max())) <= {"fp32": 1e-6, "3xtf32": 1e-4}.get(prec, 2e-2)
+    assert bad[1].any() and bad[2].any() and bad[3].any() and not bad[0].any()
+    assert bad[1].sum() < bad[1].size  # the poisoned set is a receptive field, not the whole sample
+    _finite_close(y, ref, prec)
 
 
-def test_block_non_finite_input_exact_mode():
-    """The block's fused absmax of y1 (conv1 epilogue) keeps a NaN too."""
-    import oracle as O
+@pytest.mark.parametrize("prec", ["fp32", "3xtf32", "bf16"])
+def test_block_non_finite_input(prec):
+    """Block: a NaN input poisons conv1's receptive field, the gate keeps it
+    (NaN), conv2 widens it (the fused absmax of y1 carries a non-finite flag to
+    conv2 in the exact mode), the residual adds it; everything else stays
+    finite and accurate -- the oracle's pattern in both directions."""
     rng = np.random.default_rng(9)
-    g, B, C, d, nb = (1, 1, 1), 2, 4, 6, 8
+    g, B, C, d, nb = (1, 1, 1), 3, 4, 7, 8
     fan = C * nb * 27
     f1 = rng.uniform(-1, 1, (nb, C, C, 27)).astype(np.float32) / np.float32(np.sqrt(fan))
     f2 = rng.uniform(-1, 1, (nb, C, C, 27)).astype(np.float32) / np.float32(np.sqrt(fan))
     b1 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
     b2 = (rng.standard_normal((nb, C)) * 0.1).astype(np.float32)
     x = rng.standard_normal((B, C, d ** 3, nb)).astype(np.float32)
-    x[1, 1, 100, 3] = np.nan
-    blk = M.make_basic_block(M.Signature(g), B, C, C, C, d, f1, b1, 2, f2, b2, padding="same", residual=True)
+    x[1, 1, 0, 3] = np.nan
+    x[2, 0, 171, 5] = np.inf
+    blk = M.make_basic_block(M.Signature(g), B, C, C, C, d, f1, b1, 2, f2, b2, padding="same", residual=True,
+                             precision=prec)
     y = M.block_forward(torch.from_numpy(x).cuda(), blk).cpu().numpy()
-    with np.errstate(invalid="ignore"):
+    with np.errstate(invalid="ignore", over="ignore"):
         ref = O.block_ref(x, g, d, f1, b1, 2, tuple(range(nb)), None, None, f2, b2, padding="same", residual=True)
     bad = ~np.isfinite(ref)
-    assert bad[1].any() and np.all(~np.isfinite(y[bad]))
-    assert O.max_rel_error(y[:1], ref[:1]) <= 1e-4
+    assert bad[1].any() and bad[2].any() and not bad[0].any() and bad[1].sum() < bad[1].size
+    _finite_close(y, ref, prec)
+
+
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_activation_non_kernel_blades_never_reach_the_gate(k, mode):
+    """K < N_B: an Inf / NaN in a NON-kernel blade must not touch the gate --
+    the reference never reads those blades (activation.py:142-162) -- so only
+    that blade itself is non-finite in the output; a non-finite kernel blade
+    poisons the whole multivector as in the reference. (The gate fused into
+    a block's conv1 epilogue uses the same kernel-blade select.)"""
+    nb = 1 << k
+    rng = np.random.default_rng(20 + k * 3 + mode)
+    ki = (1, 0) if k == 2 else (5, 2, 0)
+    C = 5
+    w = rng.uniform(-0.5, 0.5, (C, len(ki))).astype(np.float32) if mode == 0 else None
+    b = (rng.standard_normal(C) * 0.1).astype(np.float32) if mode == 0 else None
+    cfg = M.make_activation_config(M.Signature((1,) * k), mode, ki, w, b)
+    x = rng.standard_normal((3, C, 6, nb)).astype(np.float32)
+    x[0, 1, 2, 3] = np.inf      # non-kernel blade
+    x[1, 2, 0, nb - 1] = np.nan  # non-kernel blade
+    x[2, 0, 4, ki[0]] = np.inf   # kernel blade
+    y = M.activation_forward(torch.from_numpy(x).cuda(), cfg).cpu().numpy()
+    with np.errstate(invalid="ignore", over="ignore"):
+        ref = O.activation_ref(x, mode, ki, w, b)
+    assert np.array_equal(np.isfinite(y), np.isfinite(ref))
+    assert np.isfinite(y[0, 1, 2, :3]).all() and not np.isfinite(y[0, 1, 2, 3])
+    fin = np.isfinite(ref)
+    assert O.max_abs_error(np.where(fin, y, 0), np.where(fin, ref, 0)) <= 1e-5
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_gather_vpack_and_gate_preactivation(k, mode):
+    """Device-backed gather_vpack / gate_preactivation (activation.py:99-117):
+    numpy in -> numpy out, CUDA in -> CUDA out, flat and spatial forms, against
+    the reference's formulas (kernel blades in kernel_indices order)."""
+    nb = 1 << k
+    rng = np.random.default_rng(100 + 7 * k + mode)
+    ki = tuple(int(i) for i in rng.permutation(nb)[: max(1, nb - 1)])
+    C = 6
+    w = rng.uniform(-0.5, 0.5, (C, len(ki))).astype(np.float32) if mode == 0 else None
+    b = (rng.standard_normal(C) * 0.1).astype(np.float32) if mode == 0 else None
+    cfg = M.make_activation_config(M.Signature((1,) * k), mode, ki, w, b)
+    x = rng.standard_normal((4, C, nb)).astype(np.float32)
+    vp = M.gather_vpack(x, cfg)
+    assert isinstance(vp, np.ndarray) and vp.shape == (4, C, len(ki))
+    np.testing.assert_array_equal(vp, x[:, :, list(ki)])
+    s = M.gate_preactivation(x, cfg)
+    want = ((vp * w[None]).sum(axis=2) + b[None]) if mode == 0 else (vp.sum(axis=2) if mode == 1 else vp.mean(axis=2))
+    assert s.shape == (4, C) and np.max(np.abs(s - want)) <= 1e-5
+    xs = rng.standard_normal((2, C, 9, nb)).astype(np.float32)
+    sd = M.gate_preactivation(torch.from_numpy(xs).cuda(), cfg)
+    assert sd.is_cuda and tuple(sd.shape) == (2, C, 9)
+    vps = xs[..., list(ki)]
+    want = ((vps * w[None, :, None]).sum(-1) + b[None, :, None]) if mode == 0 else (
+        vps.sum(-1) if mode == 1 else vps.mean(-1))
+    assert np.max(np.abs(sd.cpu().numpy() - want)) <= 1e-5
+    # the gate the forward applies is sigmoid(preactivation)
+    y = M.activation_forward(x, cfg)
+    np.testing.assert_allclose(y, x * M.sigmoid(s)[..., None].astype(np.float32), rtol=2e-6, atol=2e-6)

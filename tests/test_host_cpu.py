@@ -368,3 +368,51 @@ def test_production_library_ignores_the_environment():
     for name in (b"CL_NO_PAIR", b"CL_NO_HALO", b"CL_DBG_SKIP", b"CL_DBG_FLIP_COEFF", b"CL_TPS", b"CL_NO_GRAPH"):
         assert name not in prod, name
         assert name in ab, name
+
+
+def test_torch_operator_registration():
+    """The C-ABI is registered as PyTorch operators (the package's binding):
+    host-only operators run without a GPU and C-ABI failures come back as the
+    reference's exception classes."""
+    import torch
+    from paper_2507_01040_b200 import _ops
+    o = _ops.ops()
+    assert o is torch.ops.clifford_b200
+    assert torch.ops.clifford_b200.version().startswith("clifford_b200")
+    assert list(_ops.op("blade_product", 2, 1, [1, 1])) == [3, -1]
+    assert _ops.op("schedule_terms", [1, -1, 0]) == 48
+    with pytest.raises(E.InvalidSignature):
+        _ops.op("validate_signature", [0, 0])
+    with pytest.raises(E.InvalidMetricValue):
+        _ops.op("validate_signature", [1, 2])
+    with pytest.raises(E.IndexOutOfRange):
+        _ops.op("blade_product", 9, 1, [1, 1])
+    with pytest.raises(E.ShapeMismatch, match="CUDA tensor"):
+        _ops.op("conv_forward", 0, torch.zeros(4), 1, torch.zeros(4))
+    for name in ("conv_create", "conv_forward", "conv_forward_host", "act_forward", "act_preactivation",
+                 "act_gather", "block_forward", "block_forward_host", "linear_create", "expand_kernel"):
+        assert hasattr(o, name), name
+
+
+def test_geometric_product_and_metrics():
+    """Host helpers re-exported for drop-in callers (algebra.py:155-173,
+    bench.py:74-96), checked against the oracle and known answers."""
+    rng = np.random.default_rng(3)
+    for g in [(1, 1), (1, -1, 0), (-1,), (0, 1, 1)]:
+        sig = M.Signature(g)
+        a = rng.standard_normal((5, sig.n_blades)).astype(np.float32)
+        b = rng.standard_normal((5, sig.n_blades)).astype(np.float32)
+        got = M.geometric_product(a, b, M.product_table(sig))
+        assert got.dtype == np.float32
+        want = np.einsum("...i,ijt,...j->...t", a.astype(np.float64), O.cayley(g), b.astype(np.float64))
+        np.testing.assert_allclose(got, want.astype(np.float32), rtol=1e-6, atol=1e-7)
+    with pytest.raises(E.DimensionMismatch):
+        M.geometric_product(np.zeros(3), np.zeros(4), M.product_table(M.Signature((1, 1))))
+    assert M.max_rel_error(np.array([1.0, 0.0]), np.array([1.0, 0.001])) == pytest.approx(0.001 / 0.011)
+    assert M.max_abs_error(np.zeros(3), np.array([0.0, -2.0, 1.0])) == 2.0
+    assert M.max_rel_error(np.zeros(0), np.zeros(0)) == 0.0
+    with pytest.raises(E.VerificationFailed):
+        M.max_abs_error(np.zeros(2), np.zeros(3))
+    assert float(M.sigmoid(4.0)) == pytest.approx(0.98201379003790844, abs=1e-15)  # tests/test_activation.py:38-40
+    assert float(M.sigmoid(0.0)) == 0.5
+    assert float(M.sigmoid(-1000.0)) == 0.0
