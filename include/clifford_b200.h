@@ -172,6 +172,11 @@ int cl_block_forward_ws(const cl_block* h, const float* x_dev, float* y_dev, int
  * (0 = automatic) with copy/compute overlap */
 int cl_block_forward_host(const cl_block* h, const float* x_host, float* y_host, int64_t B,
                           int64_t chunk, void* stream);
+/* diagnostics: one forward, then `reps` launches of the block's conv2 alone
+ * (its fused residual included, on the operand the forward prepared), timed
+ * with CUDA events on `stream`: the roofline kernel of bench.py */
+int cl_block_time_conv2(const cl_block* h, const float* x_dev, float* y_dev, int64_t B, int reps, void* stream,
+                        float* avg_ms);
 void cl_block_destroy(cl_block* h);
 
 /* ---- diagnostics --------------------------------------------------------- */

@@ -24,7 +24,7 @@ EXPORTS = (
     "cl_linear_destroy", "cl_act_create", "cl_act_forward", "cl_act_forward_host", "cl_act_preactivation", "cl_act_gather",
     "cl_act_kernel_count",
     "cl_act_destroy", "cl_block_create", "cl_block_forward", "cl_block_forward_host",
-    "cl_block_destroy", "cl_last_error", "cl_launch_count", "cl_version",
+    "cl_block_destroy", "cl_block_time_conv2", "cl_last_error", "cl_launch_count", "cl_version",
 )
 
 P = C.c_void_p
@@ -77,6 +77,7 @@ def load():
         "cl_block_forward": (C.c_int, [P, P, P, C.c_int64, P]),
         "cl_block_forward_host": (C.c_int, [P, P, P, C.c_int64, C.c_int64, P]),
         "cl_block_destroy": (None, [P]),
+        "cl_block_time_conv2": (C.c_int, [P, P, P, C.c_int64, C.c_int, P, C.POINTER(C.c_float)]),
         "cl_last_error": (C.c_char_p, []),
         "cl_launch_count": (C.c_uint64, []),
         "cl_version": (C.c_char_p, []),

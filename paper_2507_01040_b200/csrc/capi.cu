@@ -1387,6 +1387,31 @@ int cl_block_create(const cl_conv* c1, const cl_act* act, const cl_conv* c2, int
 }  // extern "C"
 
 namespace cl {
+// CUDA-event timing of `reps` calls of fn on stream s in kernel-only mode
+// (operand preparation and the non-finite pass skipped: the operand of the
+// call before is reused).
+template <class F>
+static int time_launches(int reps, float* avg_ms, cudaStream_t s, F&& fn) {
+  g_time_kernel_only = true;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  int rc = CL_OK;
+  for (int i = 0; i < reps && rc == CL_OK; ++i) rc = fn();
+  cudaEventRecord(e1, s);
+  g_time_kernel_only = false;
+  cudaError_t e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc != CL_OK) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "time_launches");
+  *avg_ms = ms / reps;
+  return CL_OK;
+}
+
 // bf16 blocks hand conv2 its packed operand straight from conv1's epilogue
 // (protocol basis only; with a change of basis conv2 packs conv1's fp32 output)
 static bool bf16_handoff(const cl_block* h) {
@@ -1408,7 +1433,11 @@ static size_t block_ws_bytes(const cl_block* h, long long B) {
          std::max(conv_ws_bytes(h->c1, B, false), conv_ws_bytes(h->c2, B, bf));
 }
 
-static int block_run(const cl_block* h, const float* x, float* y, long long B, void* ws, cudaStream_t s) {
+// time_reps > 0 (diagnostics): after the forward, re-launch the block's conv2
+// (with its fused residual, on the operand the forward just prepared) that
+// many times alone and report its average duration in *avg_ms.
+static int block_run(const cl_block* h, const float* x, float* y, long long B, void* ws, cudaStream_t s,
+                     int time_reps = 0, float* avg_ms = nullptr) {
   const cl_conv* c1 = h->c1;
   const cl_conv* c2 = h->c2;
   if (B == 0) return CL_OK;
@@ -1433,7 +1462,10 @@ static int block_run(const cl_block* h, const float* x, float* y, long long B, v
     e1.y_bf16 = (__nv_bfloat16*)mid;
     e1.ybf_groups = c2->plan.G;
     if (int rc = conv_run(c1, x, nullptr, nullptr, B, e1, cws, s)) return rc;
-    return conv_run(c2, nullptr, (const __nv_bfloat16*)mid, y, B, e2, cws, s);
+    if (int rc = conv_run(c2, nullptr, (const __nv_bfloat16*)mid, y, B, e2, cws, s)) return rc;
+    return time_reps > 0 ? time_launches(time_reps, avg_ms, s, [&] {
+      return conv_run(c2, nullptr, (const __nv_bfloat16*)mid, y, B, e2, cws, s);
+    }) : CL_OK;
   }
   if (c2->prec == kPrecFp32 && c1->prec == kPrecFp32 && !g_no_fused_amax) {
     // conv1's epilogue takes conv2's per-sample max |y1|: no separate absmax pass over y1
@@ -1444,7 +1476,10 @@ static int block_run(const cl_block* h, const float* x, float* y, long long B, v
     e2.nf_in = nf_mid;
   }
   if (int rc = conv_run(c1, x, nullptr, (float*)mid, B, e1, cws, s)) return rc;
-  return conv_run(c2, (const float*)mid, nullptr, y, B, e2, cws, s);
+  if (int rc = conv_run(c2, (const float*)mid, nullptr, y, B, e2, cws, s)) return rc;
+  return time_reps > 0 ? time_launches(time_reps, avg_ms, s, [&] {
+    return conv_run(c2, (const float*)mid, nullptr, y, B, e2, cws, s);
+  }) : CL_OK;
 }
 }  // namespace cl
 
@@ -1483,6 +1518,16 @@ int cl_block_forward_host(const cl_block* h, const float* xh, float* yh, int64_t
       [&](const float* dx, float* dy, long long nb, void* ws, cudaStream_t s) {
         return block_run(h, dx, dy, nb, ws, s);
       });
+}
+
+int cl_block_time_conv2(const cl_block* h, const float* x, float* y, int64_t B, int reps, void* stream,
+                        float* avg_ms) {
+  if (!h || !avg_ms || reps < 1 || B < 1) return fail(CL_ERR_CONFIG_INVALID, "ConfigInvalid", "bad arguments");
+  if (int st = check_io_align(x, y, h->c1->nb)) return st;
+  void* ws = nullptr;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int rc = h->ws.get(s, block_ws_bytes(h, B), &ws)) return rc;
+  return block_run(h, x, y, B, ws, s, reps, avg_ms);
 }
 
 void cl_block_destroy(cl_block* h) { delete h; }

@@ -51,6 +51,7 @@ struct Api {
   int (*block_forward)(const void*, const float*, float*, int64_t, void*);
   int (*block_forward_host)(const void*, const float*, float*, int64_t, int64_t, void*);
   void (*block_destroy)(void*);
+  int (*block_time_conv2)(const void*, const float*, float*, int64_t, int, void*, float*);
   const char* (*last_error)();
   uint64_t (*launch_count)();
   const char* (*version)();
@@ -116,6 +117,7 @@ std::string load_library(std::string path) {
   bind(h, a.block_forward, "cl_block_forward", miss);
   bind(h, a.block_forward_host, "cl_block_forward_host", miss);
   bind(h, a.block_destroy, "cl_block_destroy", miss);
+  bind(h, a.block_time_conv2, "cl_block_time_conv2", miss);
   bind(h, a.last_error, "cl_last_error", miss);
   bind(h, a.launch_count, "cl_launch_count", miss);
   bind(h, a.version, "cl_version", miss);
@@ -352,6 +354,15 @@ void block_forward_host(int64_t h, const at::Tensor& x, int64_t B, int64_t chunk
   check(api().block_forward_host(H(h), fptr(x), fptr_mut(y), B, chunk, current_stream()));
 }
 
+double block_time_conv2(int64_t h, const at::Tensor& x, int64_t B, int64_t reps, const at::Tensor& y) {
+  dev_f32(x, "input");
+  dev_f32(y, "out");
+  c10::cuda::CUDAGuard guard(x.device());
+  float ms = 0.f;
+  check(api().block_time_conv2(H(h), fptr(x), fptr_mut(y), B, (int)reps, stream_of(x), &ms));
+  return ms;
+}
+
 int64_t launch_count() { return (int64_t)api().launch_count(); }
 std::string version() { return api().version(); }
 
@@ -392,4 +403,5 @@ TORCH_LIBRARY(clifford_b200, m) {
   m.def("block_destroy(int h) -> ()", &block_destroy);
   m.def("block_forward(int h, Tensor x, int B, Tensor(a!) y) -> ()", &block_forward);
   m.def("block_forward_host(int h, Tensor x, int B, int chunk, Tensor(a!) y) -> ()", &block_forward_host);
+  m.def("block_time_conv2(int h, Tensor x, int B, int reps, Tensor(a!) y) -> float", &block_time_conv2);
 }

@@ -41,8 +41,8 @@ class LinearLayer:
         h = self._handles.get(dev)
         if h is None:
             torch = _device.torch_mod()
-            w = torch.from_numpy(np.ascontiguousarray(self.weight))
-            b = torch.from_numpy(np.ascontiguousarray(self.bias))
+            w = torch.from_numpy(np.array(self.weight, dtype=np.float32))
+            b = torch.from_numpy(np.array(self.bias, dtype=np.float32))
             ptr = _ops.op("linear_create", list(self.sig.g), self.C_in, self.C_out, w, b,
                           PRECISIONS[self.precision])
             h = _device.Handle(ptr, _ops.destroyer("conv_destroy"))
