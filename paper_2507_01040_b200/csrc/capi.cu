@@ -294,6 +294,15 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
   }
   if (best < 0) return false;
   pl = bestp;
+  // accumulation groups: one per tile unless the exact mode's reduction
+  // exceeds kMaxKGroup, then `drain` stages per group (see ConvPlan)
+  pl.stages_per_tile = pl.halo ? pl.n_gs * ((pl.Q + pl.tps - 1) / pl.tps) : pl.k_iters;
+  pl.drain = pl.stages_per_tile;
+  if (i8) {
+    const long long k_stage = (long long)pl.ks * 32 * (pl.halo ? pl.tps : 1);  // int8 K elements per stage
+    if (k_stage * pl.stages_per_tile > kMaxKGroup) pl.drain = (int)std::max<long long>(1, kMaxKGroup / k_stage);
+  }
+  pl.n_groups = (pl.stages_per_tile + pl.drain - 1) / pl.drain;
   pl.tmem_cols = (uint32_t)std::max(32, pow2_at_least(pl.levels * pl.n_tile * pl.acc_slots));
   // + 1024 alignment slack + the barrier area (3 x 8 stage barriers, 10 accumulator / halo
   // barriers, the TMEM slot, the 8-deep tile ring: 472 B; within the 2048 B reserve above)
@@ -598,10 +607,6 @@ static int conv_create_impl(const int32_t* g, int k, int sk, int C_in, int C_out
   h->pad = pad;
   h->d_out = d_out;
   h->prec = precision;
-  if (precision == CL_PREC_FP32 && (long long)ipow(d_filter, sk) * C_in * (1 << k) > 32000) {
-    delete h;  // s32 level accumulators: 4 pairs x 128 x 128 x K must stay below 2^31
-    return fail(CL_ERR_UNSUPPORTED, "Unsupported", "fp32 mode supports K = d_filter^k * C_in * N_B <= 32000");
-  }
   Basis bs{};
   // M2(C) change of basis for 3-D layers (measured 2.0x on cfg5),
   // M2(R) for 2-D layers in the fp32 / 3xTF32 modes (see use_basis)
@@ -844,8 +849,14 @@ static size_t conv_ws_operand_bytes(const cl_conv* h, long long B, bool prepacke
   if (pl.packed && !prepacked) return align_up((size_t)B * pl.G * P_in * 16, 256);
   return 0;
 }
+// exact mode with several accumulation groups: int64 partial sums per
+// (CTA, TMEM row, tile column), reused tile after tile by the same thread
+static size_t conv_ws_group_bytes(const cl_conv* h) {
+  const ConvPlan& pl = h->plan;
+  return pl.n_groups > 1 ? align_up((size_t)num_sms() * kTileM * pl.n_tile * 8, 256) : 0;
+}
 static size_t conv_ws_bytes(const cl_conv* h, long long B, bool prepacked) {
-  return conv_ws_operand_bytes(h, B, prepacked) + kSchedBytes;
+  return conv_ws_operand_bytes(h, B, prepacked) + kSchedBytes + conv_ws_group_bytes(h);
 }
 // The operand-prep and epilogue kernels move whole multivectors with 16-byte
 // (8-byte in 1-D) vector accesses: misaligned buffers are rejected up front
@@ -978,6 +989,11 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.n_tma_a = pl.n_tma_a;
   p.levels = pl.levels;
   p.acc_slots = pl.acc_slots;
+  p.drain = pl.drain;
+  p.n_groups = pl.n_groups;
+  p.grp_scratch = pl.n_groups > 1 ? reinterpret_cast<long long*>(static_cast<char*>(ws) +
+                                                                 conv_ws_operand_bytes(h, B, xbf != nullptr) + kSchedBytes)
+                                  : nullptr;
   p.a_scale = a_scale;
   p.w_scale = h->w_scale;
   p.bs = pl.bs;

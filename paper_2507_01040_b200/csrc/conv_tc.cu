@@ -140,10 +140,47 @@ __device__ __forceinline__ bool decode_tile(const ConvKParams& p, long long t, i
   return real;
 }
 
+// Exact mode with several accumulation groups per tile (reductions longer
+// than kMaxKGroup): drain the first n_groups - 1 groups of this thread's TMEM
+// row into its int64 partial sums, S = L0 2^24 + L1 2^16 + L2 2^8 + L3 per
+// column (each group's s32 levels are exact, so the sum is exact); the last
+// group is combined with them in the epilogue's phase 1. Only the GROUPS
+// instantiation of the kernel contains it (the extra loop would cost the
+// common epilogue registers).
+template <bool PAIR>
+__device__ __forceinline__ void drain_groups(const ConvKParams& p, uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base,
+                                          int ew, int row, int c_beg, int c_end, uint32_t slot_cols, int slots,
+                                          int& acc, uint32_t& acc_phase) {
+  long long* scr = p.grp_scratch + ((long long)blockIdx.x * kTileM + row) * p.n_tile;
+  for (int grp = 0; grp + 1 < p.n_groups; ++grp) {
+    mbar_wait_sleep(&tfull[acc], acc_phase, 64);
+    tc_fence_after();
+    const uint32_t ta = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)acc * slot_cols;
+    for (int c0 = c_beg; c0 < c_end; c0 += 4) {
+      uint32_t l0[4], l1[4], l2[4], l3[4];
+      tmem_ldn<4>(ta + (uint32_t)c0, l0);
+      tmem_ldn<4>(ta + (uint32_t)(p.n_tile + c0), l1);
+      tmem_ldn<4>(ta + (uint32_t)(2 * p.n_tile + c0), l2);
+      tmem_ldn<4>(ta + (uint32_t)(3 * p.n_tile + c0), l3);
+      tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        long long sv = ((long long)(int)l0[c] << 24) + ((long long)(int)l1[c] << 16) +
+                       ((long long)(int)l2[c] << 8) + (long long)(int)l3[c];
+        if (grp > 0) sv += scr[c0 + c];
+        scr[c0 + c] = sv;
+      }
+    }
+    tc_fence_before();
+    if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
+    if (++acc == slots) { acc = 0; acc_phase ^= 1; }
+  }
+}
+
 // BCLS: change-of-basis pattern class of the int8 epilogue. 1 = the M2(C)
 // basis of the (1,1,1) family: each lane's blades use own rows {0,0,3,3} and
 // partner rows {2,2,1,1} (compile-time picks, 2 shuffles per channel); 0 = any.
-template <int NB, int PREC, bool PAIR, int BCLS = 0>
+template <int NB, int PREC, bool PAIR, int BCLS = 0, bool GROUPS = false>
 __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap bmap,
                    const __grid_constant__ ConvKParams p) {
@@ -399,8 +436,14 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
     const uint32_t h_dx = (uint32_t)ncol;                                  // next tap along x
     const uint32_t h_wrap_x = (uint32_t)((p.hx - df) * ncol);              // x wrapped: next halo row
     const uint32_t h_wrap_y = (uint32_t)((p.hy - df) * p.hx * ncol);       // y wrapped: next halo plane
-    for (int it = 0;; ++it) {
-      if (sched_read(it, false) < 0) break;
+    // Accumulation groups: `p.drain` consecutive pipeline stages accumulate
+    // into one TMEM slot (the first MMA of a group overwrites it); the last
+    // stage of a group commits it to the epilogue, the next group waits for a
+    // free slot. One group per tile except in the exact mode's long
+    // reductions (ConvPlan::drain).
+    uint32_t d_tmem = 0;
+    int sg = 0;  // stage index inside the current group
+    auto group_begin = [&]() {
       const long long dbg_w0 = p.dbg_acc ? clock64() : 0;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
@@ -408,7 +451,21 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         atomicAdd(p.dbg_acc + 2, (unsigned long long)(clock64() - dbg_w0));
         atomicAdd(p.dbg_acc + 3, 1ull);
       }
-      const uint32_t d_tmem = tmem_base + (uint32_t)acc * slot_cols;
+      d_tmem = tmem_base + (uint32_t)acc * slot_cols;
+    };
+    // after a stage (warp-uniform): close the group when it ended, open the next one
+    auto stage_done = [&](bool gend, bool tile_last) {
+      if (gend) {
+        if (++acc == slots) { acc = 0; acc_phase ^= 1; }
+        sg = 0;
+        if (!tile_last) group_begin();
+      } else {
+        ++sg;
+      }
+    };
+    for (int it = 0;; ++it) {
+      if (sched_read(it, false) < 0) break;
+      group_begin();
       if (p.halo) {
         for (int gsi = 0; gsi < p.n_gs; ++gsi) {
           const long long dbg_h0 = p.dbg_acc ? clock64() : 0;
@@ -433,7 +490,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 #pragma unroll
                 for (int s = 0; s < 8; ++s) {  // ks <= 8, unrolled: constant per-step offsets
                   if (s >= p.ks) break;
-                  const uint32_t first = (gsi == 0 && q == 0 && s == 0) ? 1u : 0u;
+                  const uint32_t first = (sg == 0 && s == 0) ? 1u : 0u;
                   if constexpr (kInt8) {
   #pragma unroll
                     for (int L = 0; L < kLevels; ++L) {
@@ -455,18 +512,23 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                   a0 += (uint32_t)a_kstep;
                   b0 += b_ks4;
                 }
+                const bool tile_last = q == nQ - 1 && gsi == p.n_gs - 1;
                 if constexpr (PAIR) {
                   mma_commit_cg2(&empty[stage]);
                   if (q == nQ - 1) mma_commit_cg2(&hempty[hsl]);  // halo reusable once the last tap retires
-                  if (q == nQ - 1 && gsi == p.n_gs - 1) mma_commit_cg2(&tfull[acc]);
+                  if (sg == p.drain - 1 || tile_last) mma_commit_cg2(&tfull[acc]);
                 } else {
                   mma_commit(&empty[stage]);
                   if (q == nQ - 1) mma_commit(&hempty[hsl]);
-                  if (q == nQ - 1 && gsi == p.n_gs - 1) mma_commit(&tfull[acc]);
+                  if (sg == p.drain - 1 || tile_last) mma_commit(&tfull[acc]);
                 }
               }
               __syncwarp();
               if (++stage == S) { stage = 0; phase ^= 1; }
+              {
+                const bool tile_last = q == nQ - 1 && gsi == p.n_gs - 1;
+                stage_done(sg == p.drain - 1 || tile_last, tile_last);
+              }
               tap4 += h_dx;
               if (++qx == df) {
                 qx = 0;
@@ -490,7 +552,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 uint32_t a_tap = (uint32_t)h_tmpl + hA4 + tap4;
                 uint32_t b_cur = (uint32_t)b_tmpl + sB4;
                 const uint32_t a_ks = (uint32_t)a_kstep, b_ks = b_ks4, a_img = h_img4, b_img = b_img4;
-                uint32_t accf = (gsi == 0 && q0 == 0) ? 0u : 1u;
+                uint32_t accf = (sg == 0) ? 0u : 1u;
                 int x = qx, y = qy;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {  // taps of this stage (tps <= 4)
@@ -532,10 +594,14 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 const bool last = q0 + nq == nQ;
                 commit_g<PAIR>(issuer, &empty[stage]);
                 if (last) commit_g<PAIR>(issuer, &hempty[hsl]);  // halo reusable once the last tap retires
-                if (last && gsi == p.n_gs - 1) commit_g<PAIR>(issuer, &tfull[acc]);
+                if (sg == p.drain - 1 || (last && gsi == p.n_gs - 1)) commit_g<PAIR>(issuer, &tfull[acc]);
               }
               __syncwarp();
               if (++stage == S) { stage = 0; phase ^= 1; }
+              {
+                const bool tile_last = q0 + nq == nQ && gsi == p.n_gs - 1;
+                stage_done(sg == p.drain - 1 || tile_last, tile_last);
+              }
               for (int i = 0; i < nq; ++i) {  // advance the warp-uniform tap state
                 tap4 += h_dx;
                 if (++qx == df) {
@@ -548,7 +614,6 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           }
           if (++hsl == HS) { hsl = 0; hphase ^= 1; }
         }
-        if (++acc == slots) { acc = 0; acc_phase ^= 1; }
         continue;
       }
       for (int kit = 0; kit < p.k_iters; ++kit) {
@@ -565,7 +630,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           for (int s = 0; s < p.ks; ++s) {
             const uint64_t a0 = a_tmpl + (uint64_t)(sA4 + (uint32_t)s * 256u);
             const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)s * b_ks4);
-            const uint32_t first = (kit == 0 && s == 0) ? 1u : 0u;
+            const uint32_t first = (sg == 0 && s == 0) ? 1u : 0u;
             if constexpr (kInt8) {
               // D_L += A_i * B_j over digit pairs with i + j = L <= 3 (Ozaki levels,
               // 4 digits each): 10 MMAs per K step
@@ -590,18 +655,19 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
             }
           }
           // smem slot free (in both CTAs of a pair) once these MMAs retire
+          const bool gend = sg == p.drain - 1 || kit == p.k_iters - 1;
           if constexpr (PAIR) {
             mma_commit_cg2(&empty[stage]);
-            if (kit == p.k_iters - 1) mma_commit_cg2(&tfull[acc]);  // accumulator ready for the epilogues
+            if (gend) mma_commit_cg2(&tfull[acc]);  // accumulator (group) ready for the epilogues
           } else {
             mma_commit(&empty[stage]);
-            if (kit == p.k_iters - 1) mma_commit(&tfull[acc]);
+            if (gend) mma_commit(&tfull[acc]);
           }
         }
         __syncwarp();
         if (++stage == S) { stage = 0; phase ^= 1; }
+        stage_done(sg == p.drain - 1 || kit == p.k_iters - 1, kit == p.k_iters - 1);
       }
-      if (++acc == slots) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4 && warp < 4 + 4 * kEpiGroups) {
     // ===================== epilogue =====================
@@ -665,6 +731,8 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       }
       double a_sc = 0.0;
       if constexpr (kInt8) if (valid) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
+      if constexpr (kInt8 && GROUPS)  // exact mode, several accumulation groups per tile
+        drain_groups<PAIR>(p, tfull, tempty, tmem_base, ew, row, c_beg, c_end, slot_cols, slots, acc, acc_phase);
       mbar_wait_sleep(&tfull[acc], acc_phase, 64);  // off the critical path: poll gently
       tc_fence_after();
       const long long dbg_t0 = p.dbg_acc ? clock64() : 0;
@@ -695,6 +763,11 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               for (int c = 0; c < CH; ++c)
                 sv[c] = ((long long)(int)l0[c] << 24) + ((long long)(int)l1[c] << 16) +
                         ((long long)(int)l2[c] << 8) + (long long)(int)l3[c];
+              if constexpr (GROUPS) {  // the earlier accumulation groups of this tile (exact int64 sum)
+                const long long* scr = p.grp_scratch + ((long long)blockIdx.x * kTileM + row) * p.n_tile + c0;
+#pragma unroll
+                for (int c = 0; c < CH; ++c) sv[c] += scr[c];
+              }
             }
             if (p.bs.on) {
               if constexpr (NB >= 4) {
@@ -1139,10 +1212,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   }
 }
 
-template <int NB, int PREC, bool PAIR, int BCLS = 0>
+template <int NB, int PREC, bool PAIR, int BCLS = 0, bool GROUPS = false>
 static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const CUtensorMap& bmap,
                             const ConvKParams& p, int grid, cudaStream_t s) {
-  auto kfn = conv_tc_kernel<NB, PREC, PAIR, BCLS>;
+  auto kfn = conv_tc_kernel<NB, PREC, PAIR, BCLS, GROUPS>;
   cudaError_t e = ensure_smem_optin(reinterpret_cast<const void*>(kfn), (int)plan.smem_bytes);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1166,6 +1239,10 @@ static cudaError_t launch_t(const ConvPlan& plan, const CUtensorMap& tmap, const
 template <int NB>
 static cudaError_t launch_nb(const ConvPlan& plan, const CUtensorMap& tmap, const CUtensorMap& bmap,
                              const ConvKParams& p, int grid, cudaStream_t s) {
+  if (plan.prec == kPrecFp32 && p.n_groups > 1) {  // long exact-mode reductions (generic basis picks)
+    if (p.pair) return launch_t<NB, kPrecFp32, true, 0, true>(plan, tmap, bmap, p, grid, s);
+    return launch_t<NB, kPrecFp32, false, 0, true>(plan, tmap, bmap, p, grid, s);
+  }
   if (p.pair) {
     switch (plan.prec) {
       case kPrecFp32:

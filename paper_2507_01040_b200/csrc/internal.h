@@ -32,6 +32,10 @@ constexpr int kDigitsW = 4;  // int8 digits per filter value (31 bits, per-colum
 constexpr int kLevels = 4;   // digit-pair levels kept: i + j <= 3 (0-based)
 
 constexpr int kTileM = 128;          // GEMM rows per tile (= TMEM lanes)
+// exact mode: reduction length of one accumulation group. Level L sums
+// (L + 1) <= 4 digit-pair products of |d_i w_j| <= 2^14 per K element, so
+// |L| <= 4 * 2^14 * K < 2^31 for K <= 32000 (s32 TMEM accumulators).
+constexpr int kMaxKGroup = 32000;
 
 // Change of basis (basis.cu): x' = T x splits the conv into ncol independent
 // GEMMs sharing a w x w filter; T rows = (column, component), entries +-1/0,
@@ -122,6 +126,11 @@ struct ConvPlan {
   int n_tma_a;          // A tensor loads per stage (4 for int8 digits, else 1)
   int levels;           // TMEM accumulators per tile (4 digit levels for kPrecFp32)
   int acc_slots;        // accumulator buffers (2 = epilogue overlaps next tile's MMA)
+  // accumulation groups (exact mode, long reductions): the s32 level
+  // accumulators are drained every `drain` pipeline stages -- each group's
+  // reduction length stays <= kMaxKGroup -- and the groups are combined
+  // exactly in int64 by the epilogue; drain = stages per tile (one group) otherwise
+  int drain, n_groups, stages_per_tile;
   int stages;
   uint32_t tmem_cols;
   size_t smem_bytes;
@@ -145,6 +154,8 @@ struct ConvKParams {
   int d_filter, n_gs, gs, G, merged_bc, k_iters, ks;
   uint32_t a_bytes, b_bytes, b_img_bytes, stage_bytes, tmem_cols;
   int stages, n_a, n_tma_a, levels, acc_slots;
+  int drain, n_groups;        // accumulation group = `drain` pipeline stages; n_groups per tile (see ConvPlan)
+  long long* grp_scratch;     // n_groups > 1: per-(CTA, row, column) int64 partial sums of the exact mode
   int cs;                     // cluster size: 2 for a 2-SM (cta_group::2) pair, else 1
   int pair;                   // 2-SM MMA: M = 256 over the pair, B columns split between the two CTAs
   int halo, hx, hy, hz, hs;   // halo mode (see ConvPlan)

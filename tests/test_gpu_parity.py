@@ -484,3 +484,47 @@ def test_graph_replay_small_forwards():
     assert np.array_equal(res[1], res[0]) and np.array_equal(res[2], res[0])
     ref = O.block_ref(xb, g, d, f1, b1, 1, tuple(range(nb)), None, None, f2, b2, padding="same", residual=True)
     assert O.max_rel_error(res[2], ref) <= 1e-4
+
+
+# ---- exact-mode limits lifted: long reductions (K > 32000) and huge batches ----
+
+@pytest.mark.parametrize("g,B,ci,co,d,df,padding", [
+    ((1, 1, 1), 1, 512, 4, 4, 3, "valid"),   # 3-D, C_in = 512: K = 27 * 512 * 4 (basis) = 55296 -> 2 groups
+    ((1, 1, 1), 2, 320, 9, 5, 3, "same"),    # K = 34560 -> 2 groups, several N / M tiles
+    ((1, -1), 1, 1900, 3, 5, 3, "same"),     # 2-D halo path: K = 9 * 1900 * 2 = 34200
+    ((1, 0, -1), 1, 200, 5, 4, 3, "valid"),  # degenerate signature: K = 27 * 200 * 4 or 8 > 32000
+])
+def test_exact_mode_long_reductions(g, B, ci, co, d, df, padding):
+    """The exact mode's s32 level accumulators hold reductions up to K = 32000;
+    longer ones are split into accumulation groups drained into exact int64
+    partial sums (ConvPlan::drain) instead of being rejected."""
+    rng = np.random.default_rng(ci)
+    x, f, b, layer, pad = make_conv(rng, g, B, ci, co, d, df, "fp32", padding)
+    y = run_dev(M.conv_forward, x, layer)
+    e = O.max_rel_error(y, O.conv_ref(x, f, b, g, d, df, pad))
+    assert e <= 1e-4, e
+    # the same digits summed in one s32 group would overflow in the worst case only; a
+    # reduction of exactly-representable integers checks the int64 combine bit-exactly
+    xi = np.round(x * 4).astype(np.float32)
+    fi = np.round(f * 1024).astype(np.float32)
+    li = M.make_conv_layer(M.Dims(B, ci, co, d, df, len(g)), M.Signature(g), fi, np.zeros_like(b), padding=padding)
+    yi = run_dev(M.conv_forward, xi, li)
+    ri = O.conv_ref(xi, fi, np.zeros_like(b), g, d, df, pad)
+    assert np.array_equal(yi, ri)
+
+
+def test_linear_huge_batch_and_long_reduction():
+    """linear_forward on B = 100000 samples (the per-sample absmax grid is 1-D,
+    no 65535-sample limit) and a C_in whose reduction exceeds 32000."""
+    rng = np.random.default_rng(8)
+    g, nb = (1, 1, 1), 8
+    for B, ci, co in [(100_000, 16, 8), (300, 4100, 5)]:
+        w = (rng.standard_normal((nb, co, ci)) / np.sqrt(ci * nb)).astype(np.float32)
+        b = (rng.standard_normal((nb, co)) * 0.1).astype(np.float32)
+        x = rng.standard_normal((B, ci, nb)).astype(np.float32)
+        layer = M.make_linear_layer(M.Signature(g), w, b)
+        y = run_dev(M.linear_forward, x, layer)
+        idx = np.r_[0:50, B - 50:B]
+        assert O.max_rel_error(y[idx], O.linear_ref(x[idx], w, b, g)) <= 1e-4
+        yh = M.linear_forward(x, layer)  # host path
+        np.testing.assert_array_equal(yh, y)

@@ -7,7 +7,7 @@ NCU="ncu --set full --clock-control none --import-source on -c 1"
 run() {  # name kernel-regex driver-args...
   local name=$1 kre=$2; shift 2
   timeout 300 python "$@" > gpurun_out/ncu/$name.plain.log 2>&1 && \
-    timeout 900 $NCU -k regex:$kre -f -o /tmp/ncu_$name python "$@" > gpurun_out/ncu/$name.ncu.log 2>&1
+    timeout 1200 $NCU ${NCU_EXTRA:-} -k regex:$kre -f -o /tmp/ncu_$name python "$@" > gpurun_out/ncu/$name.ncu.log 2>&1
   echo "$name rc=$?" >> gpurun_out/ncu/status.txt
   # the .ncu-rep stays on the box (gpurun_out is capped at 64 MiB): bring back the raw
   # metrics and the details page (KEEP_REP=1 also copies the report)
@@ -27,5 +27,10 @@ for job in ${JOBS:-act bf16 tf32 x3 cfg4 cfg3 cfg1}; do
     slice) run slice_cfg5_fp32_B64 slice_input tools/prof_conv.py --config 5 --B 64 --precision fp32 --reps 1 ;;
     fp32full) run conv_cfg5_fp32_B256 conv_tc tools/prof_conv.py --config 5 --B 256 --precision fp32 --reps 1 ;;
     cfg1) run conv_cfg1_fp32_B8 conv_tc tools/prof_conv.py --config 1 --B 8 --precision fp32 --reps 3 ;;
+    # the block's conv2 (fused residual): skip conv1, capture the second conv_tc launch
+    blk2) NCU_EXTRA="--launch-skip 1" run block_cfg5_fp32_B64_conv2 conv_tc tools/prof_block.py --config 5 --B 64 --precision fp32 ;;
+    blk2full) NCU_EXTRA="--launch-skip 1" run block_cfg5_fp32_B256_conv2 conv_tc tools/prof_block.py --config 5 --B 256 --precision fp32 ;;
+    cfg4bf16) run conv_cfg4_bf16_B16 conv_tc tools/prof_conv.py --config 4 --B 16 --precision bf16 --reps 1 ;;
+    cfg4tf32) run conv_cfg4_tf32_B16 conv_tc tools/prof_conv.py --config 4 --B 16 --precision tf32 --reps 1 ;;
   esac
 done
