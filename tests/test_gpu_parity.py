@@ -528,3 +528,24 @@ def test_linear_huge_batch_and_long_reduction():
         assert O.max_rel_error(y[idx], O.linear_ref(x[idx], w, b, g)) <= 1e-4
         yh = M.linear_forward(x, layer)  # host path
         np.testing.assert_array_equal(yh, y)
+
+
+def test_misaligned_buffers_are_copied_or_rejected():
+    """A contiguous CUDA view with a 4-byte storage offset is realigned (copied)
+    by the Python shim; a misaligned `out` is rejected with ShapeMismatch by the
+    C-ABI instead of faulting (a misaligned-address fault poisons the context)."""
+    rng = np.random.default_rng(12)
+    x, f, b, layer, pad = make_conv(rng, (1, 1), 2, 3, 3, 7, 3, "fp32")
+    flat = torch.zeros(x.size + 1, device="cuda")
+    flat[1:] = torch.from_numpy(x.ravel()).cuda()
+    xv = flat[1:].view(x.shape)
+    assert xv.data_ptr() % 16 != 0 and xv.is_contiguous()
+    y = M.conv_forward(xv, layer).cpu().numpy()
+    assert O.max_rel_error(y, O.conv_ref(x, f, b, (1, 1), 7, 3, pad)) <= 1e-4
+    out_flat = torch.zeros(int(np.prod(layer.output_shape())) + 1, device="cuda")
+    with pytest.raises(M.errors.ShapeMismatch, match="aligned"):
+        M.conv_forward(torch.from_numpy(x).cuda(), layer, out=out_flat[1:].view(layer.output_shape()))
+    for prec in ("bf16", "tf32"):
+        lp = M.make_conv_layer(M.Dims(2, 3, 3, 7, 3, 2), M.Signature((1, 1)), f, b, precision=prec)
+        assert_conv_close(M.conv_forward(xv, lp).cpu().numpy(), O.conv_ref(x, f, b, (1, 1), 7, 3, pad), prec)
+    torch.cuda.synchronize()  # the context is healthy

@@ -1,0 +1,7 @@
+export CL_LIB_PATH=$PWD/paper_2507_01040_b200/lib/libclifford_b200_ab.so
+for v in "-" "CL_KS=8" "CL_KS=2" "CL_TPS=2" "CL_TPS=4" "CL_KS=8 CL_TPS=2" "CL_NO_HALO=1" "CL_NO_HALO=1 CL_KS=8" "CL_NO_HALO=1 CL_KS=4" "CL_NO_PAIR=1" "CL_NO_BASIS=1" "CL_DBG_SKIP=4" "CL_DBG_SKIP=1" "CL_DBG_SKIP=2" "CL_STATIC_TILES=1"; do
+  for p in bf16 tf32; do env $([ "$v" = "-" ] || echo $v) timeout 300 python tools/conv_kernel_time.py $p 16 4 2>&1 | tail -1; done
+done
+for v in "-" "CL_KS=4" "CL_TPS=1" "CL_TPS=2" "CL_NO_HALO=1"; do
+  env $([ "$v" = "-" ] || echo $v) timeout 300 python tools/conv_kernel_time.py bf16 32 5 2>&1 | tail -1
+done

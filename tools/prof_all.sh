@@ -13,6 +13,7 @@ run() {  # name kernel-regex driver-args...
   # metrics and the details page (KEEP_REP=1 also copies the report)
   ncu -i /tmp/ncu_$name.ncu-rep --page raw --csv > gpurun_out/ncu/$name.raw.csv 2>/dev/null
   ncu -i /tmp/ncu_$name.ncu-rep --page details --csv > gpurun_out/ncu/$name.details.csv 2>/dev/null
+  [ -n "$SOURCE" ] && ncu -i /tmp/ncu_$name.ncu-rep --page source --csv --print-source sass > gpurun_out/ncu/$name.sass.csv 2>/dev/null
   [ -n "$KEEP_REP" ] && cp /tmp/ncu_$name.ncu-rep gpurun_out/ncu/
 }
 for job in ${JOBS:-act bf16 tf32 x3 cfg4 cfg3 cfg1}; do
