@@ -28,6 +28,16 @@
 
 namespace cl {
 
+// Timing instrumentation (CL_DBG_CLK cycle counters, CL_DBG_SKIP work
+// skipping) exists only in the diagnostic build; the production kernels
+// compile it out.
+#ifdef CL_AB_SWITCHES
+constexpr bool kDbg = true;
+#else
+constexpr bool kDbg = false;
+#endif
+__device__ __forceinline__ int dbg_skip(const ConvKParams& p) { return kDbg ? p.dbg_skip : 0; }
+
 // Gate of one multivector. Non-kernel blades are selected out (kmask), not
 // weighted by zero: the reference never reads them (activation.py:142-162).
 template <int NB>
@@ -364,7 +374,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
             for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
               const int nq = min(p.tps, nQ - q0);
               mbar_wait(&empty[stage], phase ^ 1);
-              if (p.dbg_skip & 1) {  // timing experiment: no B loads (results garbage)
+              if (dbg_skip(p) & 1) {  // timing experiment: no B loads (results garbage)
                 if (arm) mbar_arrive(&full[stage]);
               } else {
                 if (arm) mbar_arrive_expect_tx(&full[stage], tx_bytes * (uint32_t)nq);
@@ -444,10 +454,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
     uint32_t d_tmem = 0;
     int sg = 0;  // stage index inside the current group
     auto group_begin = [&]() {
-      const long long dbg_w0 = p.dbg_acc ? clock64() : 0;
+      const long long dbg_w0 = (kDbg && p.dbg_acc) ? clock64() : 0;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      if (p.dbg_acc && lane == 0) {  // timing instrumentation: MMA warp's wait for the accumulator
+      if (kDbg && p.dbg_acc && lane == 0) {  // timing instrumentation: MMA warp's wait for the accumulator
         atomicAdd(p.dbg_acc + 2, (unsigned long long)(clock64() - dbg_w0));
         atomicAdd(p.dbg_acc + 3, 1ull);
       }
@@ -468,10 +478,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       group_begin();
       if (p.halo) {
         for (int gsi = 0; gsi < p.n_gs; ++gsi) {
-          const long long dbg_h0 = p.dbg_acc ? clock64() : 0;
+          const long long dbg_h0 = (kDbg && p.dbg_acc) ? clock64() : 0;
           if (kSplit) mbar_wait(&hlo[hsl], hphase);
           else mbar_wait(&hfull[hsl], hphase);
-          if (p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 4, (unsigned long long)(clock64() - dbg_h0));
+          if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 4, (unsigned long long)(clock64() - dbg_h0));
           tc_fence_after();
           const uint32_t hA4 = (smem_u32(smem + (size_t)hsl * p.halo_slot) & 0x3FFFFu) >> 4;
           // tap (qx, qy, qz) -> halo offset in 16-byte rows, stepped without divisions
@@ -479,9 +489,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           int qx = 0, qy = 0;
           if (p.tps == 1) {  // one tap per stage (kept separate: the multi-tap loop's codegen costs 20% here)
             for (int q = 0; q < nQ; ++q) {
-              const long long dbg_s0 = p.dbg_acc ? clock64() : 0;
+              const long long dbg_s0 = (kDbg && p.dbg_acc) ? clock64() : 0;
               mbar_wait(&full[stage], phase);
-              if (p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
+              if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
               tc_fence_after();
               const uint32_t sB4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
               if (elect_one()) {
@@ -539,9 +549,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           } else {
             for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
               const int nq = min(p.tps, nQ - q0);
-              const long long dbg_s0 = p.dbg_acc ? clock64() : 0;
+              const long long dbg_s0 = (kDbg && p.dbg_acc) ? clock64() : 0;
               mbar_wait(&full[stage], phase);
-              if (p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
+              if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
               tc_fence_after();
               const uint32_t sB4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
               {
@@ -617,19 +627,24 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         continue;
       }
       for (int kit = 0; kit < p.k_iters; ++kit) {
-        const long long dbg_s0 = p.dbg_acc ? clock64() : 0;
+        const long long dbg_s0 = (kDbg && p.dbg_acc) ? clock64() : 0;
         if (kSplit) mbar_wait(&lo_ready[stage], phase);
         else mbar_wait(&full[stage], phase);
-        if (p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
+        if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
         tc_fence_after();
         // (cluster launches return cluster-window shared addresses: keep the
         // CTA-local 18 bits so nothing carries past the 14-bit start field)
         const uint32_t sA4 = (smem_u32(ring + (size_t)stage * p.stage_bytes) & 0x3FFFFu) >> 4;
         const uint32_t sB4 = sA4 + a_tot4;
         if (elect_one()) {
-          for (int s = 0; s < p.ks; ++s) {
-            const uint64_t a0 = a_tmpl + (uint64_t)(sA4 + (uint32_t)s * 256u);
-            const uint64_t b0 = b_tmpl + (uint64_t)(sB4 + (uint32_t)s * b_ks4);
+          // descriptors as 32-bit low halves + constant high halves (the
+          // per-MMA arithmetic is a 32-bit add on the uniform datapath), the
+          // K steps unrolled with a uniform early exit
+          const uint32_t a_hi = (uint32_t)(a_tmpl >> 32), b_hi = (uint32_t)(b_tmpl >> 32);
+          uint32_t a0 = (uint32_t)a_tmpl + sA4, b0 = (uint32_t)b_tmpl + sB4;
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {  // ks <= 8
+            if (s >= p.ks) break;
             const uint32_t first = (sg == 0 && s == 0) ? 1u : 0u;
             if constexpr (kInt8) {
               // D_L += A_i * B_j over digit pairs with i + j = L <= 3 (Ozaki levels,
@@ -640,19 +655,19 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
 #pragma unroll
                 for (int i = i0; i <= L && i < kDigitsA; ++i) {
                   const int j = L - i;
-                  mma_mode<PREC, PAIR>(d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint64_t)(i * a_img4),
-                                       b0 + (uint64_t)(j * b_img4), idesc, (first && i == i0) ? 0u : 1u);
+                  mma_mode_s<PREC, PAIR>(1u, d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint32_t)i * a_img4, a_hi,
+                                         b0 + (uint32_t)j * b_img4, b_hi, idesc, (first && i == i0) ? 0u : 1u);
                 }
               }
             } else if constexpr (kSplit) {
-              mma_tf32(d_tmem, a0 + a_img4, b0, idesc, first ? 0u : 1u);  // A_lo * B_hi
-              mma_tf32(d_tmem, a0, b0 + b_img4, idesc, 1u);              // A_hi * B_lo
-              mma_tf32(d_tmem, a0, b0, idesc, 1u);                       // A_hi * B_hi
-            } else if constexpr (PREC == kPrecTf32) {
-              mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+              mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0 + a_img4, a_hi, b0, b_hi, idesc, first ? 0u : 1u);  // A_lo * B_hi
+              mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0, a_hi, b0 + b_img4, b_hi, idesc, 1u);              // A_hi * B_lo
+              mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, 1u);                       // A_hi * B_hi
             } else {
-              mma_mode<PREC, PAIR>(d_tmem, a0, b0, idesc, first ? 0u : 1u);
+              mma_mode_s<PREC, PAIR>(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, first ? 0u : 1u);
             }
+            a0 += 256u;
+            b0 += b_ks4;
           }
           // smem slot free (in both CTAs of a pair) once these MMAs retire
           const bool gend = sg == p.drain - 1 || kit == p.k_iters - 1;
@@ -735,7 +750,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         drain_groups<PAIR>(p, tfull, tempty, tmem_base, ew, row, c_beg, c_end, slot_cols, slots, acc, acc_phase);
       mbar_wait_sleep(&tfull[acc], acc_phase, 64);  // off the critical path: poll gently
       tc_fence_after();
-      const long long dbg_t0 = p.dbg_acc ? clock64() : 0;
+      const long long dbg_t0 = (kDbg && p.dbg_acc) ? clock64() : 0;
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)acc * slot_cols;
       if constexpr (kInt8) {
         // Two-phase epilogue: this mode has ONE accumulator slot (4 exact
@@ -750,7 +765,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         for (int ci = 0; ci < kHold / CH; ++ci) {
           const int c0 = c_beg + ci * CH;
           const int n0 = nt * p.n_tile + c0;
-          if (c0 < c_end && n0 < p.N && !(p.dbg_skip & 4)) {
+          if (c0 < c_end && n0 < p.N && !(dbg_skip(p) & 4)) {
             long long sv[CH];  // exact: S = L0 2^24 + L1 2^16 + L2 2^8 + L3 (|S| < 2^53 for K <= 32000)
             {
               uint32_t l0[CH], l1[CH], l2[CH], l3[CH];
@@ -887,7 +902,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         }
         tc_fence_before();
         if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
-        if (p.dbg_acc && threadIdx.x == 128) {  // timing instrumentation: phase-1 cycles per tile
+        if (kDbg && p.dbg_acc && threadIdx.x == 128) {  // timing instrumentation: phase-1 cycles per tile
           atomicAdd(p.dbg_acc, (unsigned long long)(clock64() - dbg_t0));
           atomicAdd(p.dbg_acc + 1, 1ull);
         }
@@ -895,7 +910,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         // fused absmax for the next conv: max finite |stored value| (float bits) and a
         // non-finite marker (NaN-sticky max of |value| bits), see finite_abs_bits
         unsigned ymax = 0, yany = 0;
-        if (valid && !(p.dbg_skip & 4))
+        if (valid && !(dbg_skip(p) & 4))
 #pragma unroll
         for (int ci = 0; ci < kHold / CH; ++ci) {
           const int c0 = c_beg + ci * CH;
@@ -987,7 +1002,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       }
       // fp32-accumulator modes (tf32 / 3xTF32 / bf16): fp32 math, the next
       // chunk's TMEM load in flight while this one is processed
-      const int c_stop = (p.dbg_skip & 4) ? c_beg : c_end;
+      const int c_stop = (dbg_skip(p) & 4) ? c_beg : c_end;
       uint32_t cur[16], nxt[16];
       bool have = c_beg < c_stop && nt * p.n_tile + c_beg < p.N;
       if (have) {
@@ -1143,7 +1158,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       }
       tc_fence_before();
       if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
-      if (p.dbg_acc && threadIdx.x == 128) {  // timing instrumentation: epilogue cycles per tile
+      if (kDbg && p.dbg_acc && threadIdx.x == 128) {  // timing instrumentation: epilogue cycles per tile
         atomicAdd(p.dbg_acc, (unsigned long long)(clock64() - dbg_t0));
         atomicAdd(p.dbg_acc + 1, 1ull);
       }
@@ -1199,7 +1214,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   tc_fence_before();
   __syncthreads();
   if (cs > 1) cluster_sync();  // no CTA leaves while its pair may still touch its smem / TMEM
-  if (p.dbg_acc && threadIdx.x == 0) {  // timing instrumentation: spread of the CTAs' finish times
+  if (kDbg && p.dbg_acc && threadIdx.x == 0) {  // timing instrumentation: spread of the CTAs' finish times
     unsigned long long t_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
     atomicMax(p.dbg_acc + 6, t_end);
