@@ -316,15 +316,6 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
 static bool plan_conv(int k, int nb, int prec, int C_in, int C_out, int d_out, int d_filter, const Basis& bs,
                       ConvPlan& pl) {
   if (plan_conv_impl(k, nb, prec, C_in, C_out, d_out, d_filter, bs, true, pl) && (!pl.halo || pl.stages >= 4)) {
-    // bf16 / tf32: a halo plan with fewer than 8 MMAs per pipeline stage is
-    // MMA-issue bound (the per-stage barrier / descriptor work of the MMA warp
-    // exceeds 4 MMAs of tensor time: cfg4 bf16 tensor pipe 42 %); per-tap A
-    // loads with 8 K-steps per stage measured faster (cfg4 bf16 1.078 ->
-    // 0.997 ms, tf32 2.023 -> 1.835 ms)
-    if (pl.halo && (prec == kPrecBf16 || prec == kPrecTf32) && pl.ks * pl.tps < 8 && !g_no_halo) {
-      ConvPlan alt;
-      if (plan_conv_impl(k, nb, prec, C_in, C_out, d_out, d_filter, bs, false, alt) && alt.ks >= 8) pl = alt;
-    }
     return true;
   }
   return plan_conv_impl(k, nb, prec, C_in, C_out, d_out, d_filter, bs, false, pl);

@@ -339,6 +339,371 @@ CL_MMA_SPLIT(mma_bf16_cg2_s, "f16", "2")
 CL_MMA_SPLIT(mma_i8_cg2_s, "i8", "2")
 #undef CL_MMA_SPLIT
 
+// KS consecutive K steps of one pipeline stage in ONE asm block (tf32 / f16
+// kinds): the 64-bit descriptors are joined once and advanced by 64-bit adds
+// inside the block (straight-line), so per MMA the issue path is an add pair
+// plus the MMA. Per-MMA asm calls cost ~16 SASS instructions each
+// (R2UR.BROADCAST of every operand, VOTEU, UMOV), which left N = 128 stages
+// MMA-issue bound (cfg4 bf16: tensor pipe 42 %). `issue` guards the MMAs
+// (warp-converged issue); `acc0` is the first MMA's accumulate flag; the
+// strides are in 16-byte descriptor units. (Generated: one body per KS.)
+// One K step of the exact (int8) mode in ONE asm block: the 10 digit-pair
+// MMAs D_L += A_i * B_j (i + j = L <= 3, 4 digits each; conv_tc.cu Ozaki
+// levels), the 4 A-plane / 4 B-image descriptors and the 4 level columns
+// formed once. acc0 = accumulate flag of each level's first MMA.
+__device__ __forceinline__ void mma_i8_kstep(uint32_t issue, uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                        uint32_t b_hi, uint32_t idesc, uint32_t acc0, uint32_t a_img, uint32_t b_img,
+                                        uint32_t level_cols) {
+  asm volatile(
+        "{\n\t.reg .pred p, q, t;\n\t.reg .b64 a0, a1, a2, a3, b0, b1, b2, b3, sa, sb;\n\t.reg .b32 d1, d2, d3;\n\t"
+        "mov.b64 a0, {%1, %2};\n\tmov.b64 b0, {%3, %4};\n\t"
+        "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+        "add.s64 a1, a0, sa;\n\tadd.s64 a2, a1, sa;\n\tadd.s64 a3, a2, sa;\n\t"
+        "add.s64 b1, b0, sb;\n\tadd.s64 b2, b1, sb;\n\tadd.s64 b3, b2, sb;\n\t"
+        "add.u32 d1, %0, %10;\n\tadd.u32 d2, d1, %10;\n\tadd.u32 d3, d2, %10;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::i8 [%0], a0, b0, %5, p;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::i8 [d1], a0, b1, %5, p;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::i8 [d1], a1, b0, %5, t;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::i8 [d2], a0, b2, %5, p;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::i8 [d2], a1, b1, %5, t;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::i8 [d2], a2, b0, %5, t;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::i8 [d3], a0, b3, %5, p;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::i8 [d3], a1, b2, %5, t;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::i8 [d3], a2, b1, %5, t;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::i8 [d3], a3, b0, %5, t;\n\t"
+        "}"
+        ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_img),
+        "r"(b_img), "r"(level_cols)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_cg2_kstep(uint32_t issue, uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                        uint32_t b_hi, uint32_t idesc, uint32_t acc0, uint32_t a_img, uint32_t b_img,
+                                        uint32_t level_cols) {
+  asm volatile(
+        "{\n\t.reg .pred p, q, t;\n\t.reg .b64 a0, a1, a2, a3, b0, b1, b2, b3, sa, sb;\n\t.reg .b32 d1, d2, d3;\n\t"
+        "mov.b64 a0, {%1, %2};\n\tmov.b64 b0, {%3, %4};\n\t"
+        "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+        "add.s64 a1, a0, sa;\n\tadd.s64 a2, a1, sa;\n\tadd.s64 a3, a2, sa;\n\t"
+        "add.s64 b1, b0, sb;\n\tadd.s64 b2, b1, sb;\n\tadd.s64 b3, b2, sb;\n\t"
+        "add.u32 d1, %0, %10;\n\tadd.u32 d2, d1, %10;\n\tadd.u32 d3, d2, %10;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+        "@q tcgen05.mma.cta_group::2.kind::i8 [%0], a0, b0, %5, p;\n\t"
+        "@q tcgen05.mma.cta_group::2.kind::i8 [d1], a0, b1, %5, p;\n\t"
+        "@q tcgen05.mma.cta_group::2.kind::i8 [d1], a1, b0, %5, t;\n\t"
+        "@q tcgen05.mma.cta_group::2.kind::i8 [d2], a0, b2, %5, p;\n\t"
+        "@q tcgen05.mma.cta_group::2.kind::i8 [d2], a1, b1, %5, t;\n\t"
+        "@q tcgen05.mma.cta_group::2.kind::i8 [d2], a2, b0, %5, t;\n\t"
+        "@q tcgen05.mma.cta_group::2.kind::i8 [d3], a0, b3, %5, p;\n\t"
+        "@q tcgen05.mma.cta_group::2.kind::i8 [d3], a1, b2, %5, t;\n\t"
+        "@q tcgen05.mma.cta_group::2.kind::i8 [d3], a2, b1, %5, t;\n\t"
+        "@q tcgen05.mma.cta_group::2.kind::i8 [d3], a3, b0, %5, t;\n\t"
+        "}"
+        ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_img),
+        "r"(b_img), "r"(level_cols)
+      : "memory");
+}
+template <int KS>
+__device__ __forceinline__ void mma_tf32_ks(uint32_t issue, uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                         uint32_t b_hi, uint32_t idesc, uint32_t acc0, uint32_t a_step, uint32_t b_step) {
+  static_assert(KS == 1 || KS == 2 || KS == 4 || KS == 8, "K steps per stage");
+  if constexpr (KS == 1) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 2) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 4) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 8) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+}
+template <int KS>
+__device__ __forceinline__ void mma_bf16_ks(uint32_t issue, uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                         uint32_t b_hi, uint32_t idesc, uint32_t acc0, uint32_t a_step, uint32_t b_step) {
+  static_assert(KS == 1 || KS == 2 || KS == 4 || KS == 8, "K steps per stage");
+  if constexpr (KS == 1) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 2) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 4) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 8) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+}
+template <int KS>
+__device__ __forceinline__ void mma_tf32_cg2_ks(uint32_t issue, uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                         uint32_t b_hi, uint32_t idesc, uint32_t acc0, uint32_t a_step, uint32_t b_step) {
+  static_assert(KS == 1 || KS == 2 || KS == 4 || KS == 8, "K steps per stage");
+  if constexpr (KS == 1) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, p;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 2) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 4) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 8) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+}
+template <int KS>
+__device__ __forceinline__ void mma_bf16_cg2_ks(uint32_t issue, uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                         uint32_t b_hi, uint32_t idesc, uint32_t acc0, uint32_t a_step, uint32_t b_step) {
+  static_assert(KS == 1 || KS == 2 || KS == 4 || KS == 8, "K steps per stage");
+  if constexpr (KS == 1) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, p;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 2) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 4) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+  else if constexpr (KS == 8) {
+    asm volatile(
+          "{\n\t.reg .pred p, q, t;\n\t.reg .b64 da, db, sa, sb;\n\t"
+          "mov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+          "cvt.u64.u32 sa, %8;\n\tcvt.u64.u32 sb, %9;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %7, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, p;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, t;\n\t"
+          "add.s64 da, da, sa;\n\tadd.s64 db, db, sb;\n\t"
+          "@q tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, t;\n\t"
+          "}"
+          ::"r"(d_tmem), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(issue), "r"(a_step),
+          "r"(b_step)
+        : "memory");
+  }
+}
+
 // Commit the pair's MMAs to the barrier at the same offset in both CTAs.
 __device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
   asm volatile(

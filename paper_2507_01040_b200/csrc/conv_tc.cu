@@ -95,6 +95,30 @@ template <bool PAIR>
 __device__ __forceinline__ void commit_g(uint32_t issue, uint64_t* bar) {
   if constexpr (PAIR) mma_commit_cg2_g(issue, bar); else mma_commit_g(issue, bar);
 }
+// The ks K steps of one stage (tf32 / bf16 modes) in one asm block (common.cuh
+// mma_*_ks): strides in 16-byte descriptor units, acc0 = first MMA's accumulate.
+template <int PREC, bool PAIR, int KS>
+__device__ __forceinline__ void mma_stage_t(uint32_t issue, uint32_t d, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                            uint32_t b_hi, uint32_t idesc, uint32_t acc0, uint32_t a_st, uint32_t b_st) {
+  if constexpr (PREC == kPrecBf16) {
+    if constexpr (PAIR) mma_bf16_cg2_ks<KS>(issue, d, a_lo, a_hi, b_lo, b_hi, idesc, acc0, a_st, b_st);
+    else mma_bf16_ks<KS>(issue, d, a_lo, a_hi, b_lo, b_hi, idesc, acc0, a_st, b_st);
+  } else {
+    if constexpr (PAIR) mma_tf32_cg2_ks<KS>(issue, d, a_lo, a_hi, b_lo, b_hi, idesc, acc0, a_st, b_st);
+    else mma_tf32_ks<KS>(issue, d, a_lo, a_hi, b_lo, b_hi, idesc, acc0, a_st, b_st);
+  }
+}
+template <int PREC, bool PAIR>
+__device__ __forceinline__ void mma_stage(int ks, uint32_t issue, uint32_t d, uint32_t a_lo, uint32_t a_hi,
+                                          uint32_t b_lo, uint32_t b_hi, uint32_t idesc, uint32_t acc0, uint32_t a_st,
+                                          uint32_t b_st) {
+  switch (ks) {
+    case 1: mma_stage_t<PREC, PAIR, 1>(issue, d, a_lo, a_hi, b_lo, b_hi, idesc, acc0, a_st, b_st); break;
+    case 2: mma_stage_t<PREC, PAIR, 2>(issue, d, a_lo, a_hi, b_lo, b_hi, idesc, acc0, a_st, b_st); break;
+    case 4: mma_stage_t<PREC, PAIR, 4>(issue, d, a_lo, a_hi, b_lo, b_hi, idesc, acc0, a_st, b_st); break;
+    default: mma_stage_t<PREC, PAIR, 8>(issue, d, a_lo, a_hi, b_lo, b_hi, idesc, acc0, a_st, b_st); break;
+  }
+}
 
 // A-operand TMA box at (x, c1, c2, c3). With a merged (pixel x row-bytes)
 // inner dimension of 8-byte elements (p.epx per pixel; one TMA line per tile
@@ -497,21 +521,20 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               if (elect_one()) {
                 const uint32_t a_hi = (uint32_t)(h_tmpl >> 32), b_hi = (uint32_t)(b_tmpl >> 32);
                 uint32_t a0 = (uint32_t)h_tmpl + hA4 + tap4, b0 = (uint32_t)b_tmpl + sB4;
+                if constexpr (!kInt8 && !kSplit)
+                  mma_stage<PREC, PAIR>(p.ks, 1u, d_tmem, a0, a_hi, b0, b_hi, idesc, sg == 0 ? 0u : 1u,
+                                        (uint32_t)a_kstep, b_ks4);
                 #pragma unroll
                 for (int s = 0; s < 8; ++s) {  // ks <= 8, unrolled: constant per-step offsets
-                  if (s >= p.ks) break;
+                  if (kInt8 || kSplit ? s >= p.ks : true) break;
                   const uint32_t first = (sg == 0 && s == 0) ? 1u : 0u;
-                  if constexpr (kInt8) {
-  #pragma unroll
-                    for (int L = 0; L < kLevels; ++L) {
-                      const int i0 = L > kDigitsW - 1 ? L - (kDigitsW - 1) : 0;
-  #pragma unroll
-                      for (int i = i0; i <= L && i < kDigitsA; ++i) {
-                        const int j = L - i;
-                        mma_mode_s<PREC, PAIR>(1u, d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint32_t)i * h_img4, a_hi,
-                                               b0 + (uint32_t)j * b_img4, b_hi, idesc, (first && i == i0) ? 0u : 1u);
-                      }
-                    }
+                  if constexpr (kInt8) {  // the K step's 10 digit-pair MMAs in one asm block
+                    if constexpr (PAIR)
+                      mma_i8_cg2_kstep(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, first ? 0u : 1u, h_img4, b_img4,
+                                       (uint32_t)p.n_tile);
+                    else
+                      mma_i8_kstep(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, first ? 0u : 1u, h_img4, b_img4,
+                                   (uint32_t)p.n_tile);
                   } else if constexpr (kSplit) {
                     mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0 + h_img4, a_hi, b0, b_hi, idesc, first ? 0u : 1u);
                     mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0, a_hi, b0 + b_img4, b_hi, idesc, 1u);
@@ -547,6 +570,8 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               }
             }
           } else {
+            // several taps per stage: converged per-MMA issue (measured faster here
+            // than one lane issuing mma_stage blocks: cfg5 bf16 5.38 vs 5.88 ms at B = 32)
             for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
               const int nq = min(p.tps, nQ - q0);
               const long long dbg_s0 = (kDbg && p.dbg_acc) ? clock64() : 0;
@@ -642,23 +667,21 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           // K steps unrolled with a uniform early exit
           const uint32_t a_hi = (uint32_t)(a_tmpl >> 32), b_hi = (uint32_t)(b_tmpl >> 32);
           uint32_t a0 = (uint32_t)a_tmpl + sA4, b0 = (uint32_t)b_tmpl + sB4;
+          if constexpr (!kInt8 && !kSplit)
+            mma_stage<PREC, PAIR>(p.ks, 1u, d_tmem, a0, a_hi, b0, b_hi, idesc, sg == 0 ? 0u : 1u, 256u, b_ks4);
 #pragma unroll
           for (int s = 0; s < 8; ++s) {  // ks <= 8
-            if (s >= p.ks) break;
+            if (kInt8 || kSplit ? s >= p.ks : true) break;
             const uint32_t first = (sg == 0 && s == 0) ? 1u : 0u;
             if constexpr (kInt8) {
               // D_L += A_i * B_j over digit pairs with i + j = L <= 3 (Ozaki levels,
-              // 4 digits each): 10 MMAs per K step
-#pragma unroll
-              for (int L = 0; L < kLevels; ++L) {
-                const int i0 = L > kDigitsW - 1 ? L - (kDigitsW - 1) : 0;
-#pragma unroll
-                for (int i = i0; i <= L && i < kDigitsA; ++i) {
-                  const int j = L - i;
-                  mma_mode_s<PREC, PAIR>(1u, d_tmem + (uint32_t)(L * p.n_tile), a0 + (uint32_t)i * a_img4, a_hi,
-                                         b0 + (uint32_t)j * b_img4, b_hi, idesc, (first && i == i0) ? 0u : 1u);
-                }
-              }
+              // 4 digits each): 10 MMAs per K step, one asm block
+              if constexpr (PAIR)
+                mma_i8_cg2_kstep(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, first ? 0u : 1u, a_img4, b_img4,
+                                 (uint32_t)p.n_tile);
+              else
+                mma_i8_kstep(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, first ? 0u : 1u, a_img4, b_img4,
+                             (uint32_t)p.n_tile);
             } else if constexpr (kSplit) {
               mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0 + a_img4, a_hi, b0, b_hi, idesc, first ? 0u : 1u);  // A_lo * B_hi
               mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0, a_hi, b0 + b_img4, b_hi, idesc, 1u);              // A_hi * B_lo
