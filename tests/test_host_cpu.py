@@ -134,9 +134,21 @@ def test_mvtf_roundtrip(tmp_path, golden):
     tf = M.read_tensor(p)
     np.testing.assert_array_equal(tf.data, golden["mvtf_arr"])
     assert tf.tag == M.LayoutTag.CONV_INPUT and tf.k == 2
-    p.write_bytes(b"XXXX" + p.read_bytes()[4:])
+    good = p.read_bytes()
+    # malformed files (tests/test_layout.py:133-165 of the reference): bad magic,
+    # truncated header, unknown version / dtype code, short or long payload
+    import struct
+    bad = [b"XXXX" + good[4:], good[:10], good[:4] + struct.pack("<I", 2) + good[8:],
+           good[:8] + struct.pack("<I", 7) + good[12:], good[:-4], good + b"\0\0\0\0"]
+    for raw in bad:
+        p.write_bytes(raw)
+        with pytest.raises(E.ShapeMismatch):
+            M.read_tensor(p)
+    # float64 payloads are representable (and rejected by the server, not here)
+    M.write_tensor(p, np.zeros((2, 3)), M.LayoutTag.GENERIC, 0)
+    assert M.read_tensor(p).data.dtype == np.float64
     with pytest.raises(E.ShapeMismatch):
-        M.read_tensor(p)
+        M.write_tensor(p, np.zeros(3, np.int32))
 
 
 def test_no_oracle_in_product():
