@@ -1031,20 +1031,22 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   static unsigned long long* dbg_acc = nullptr;  // CL_DBG_CLK: per-launch epilogue / MMA-wait cycle report
   static const bool dbg_clk = CL_ENV("CL_DBG_CLK") != nullptr;
   if (dbg_clk) {
-    if (!dbg_acc) cudaMalloc(&dbg_acc, 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(dbg_acc, 0, 8 * sizeof(unsigned long long), s);
+    if (!dbg_acc) cudaMalloc(&dbg_acc, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(dbg_acc, 0, 16 * sizeof(unsigned long long), s);
     p.dbg_acc = dbg_acc;
   }
   cudaError_t e = launch_conv(pl, map, bmap, p, grid, s);
   if (p.dbg_acc && e == cudaSuccess) {
-    unsigned long long h[8];
+    unsigned long long h[16];
     cudaMemcpyAsync(h, dbg_acc, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
+    const double mt = h[3] ? (double)h[3] : 1.0;
     fprintf(stderr,
-            "[CL_DBG_CLK] epilogue phase-1 %.0f cyc/tile (%llu tiles); MMA waits per tile: accumulator %.0f, "
-            "halo %.0f, operand stages %.0f cyc; CTA finish spread %.1f us\n",
-            h[1] ? (double)h[0] / h[1] : 0.0, h[1], h[3] ? (double)h[2] / h[3] : 0.0,
-            h[3] ? (double)h[4] / h[3] : 0.0, h[3] ? (double)h[5] / h[3] : 0.0, (double)(h[6] - ~h[7]) * 1e-3);
+            "[CL_DBG_CLK] epilogue phase-1 %.0f cyc/tile (%llu tiles); MMA warp per tile: %.0f cyc, waits: accumulator "
+            "%.0f, halo %.0f, operand stages %.0f; producer per tile: empty-stage waits %.0f, halo-slot waits %.0f; "
+            "CTA finish spread %.1f us\n",
+            h[1] ? (double)h[0] / h[1] : 0.0, h[1], h[8] / mt, h[2] / mt, h[4] / mt, h[5] / mt,
+            h[9] / (2.0 * mt), h[10] / (2.0 * mt), (double)(h[6] - ~h[7]) * 1e-3);
   }
   if (e != cudaSuccess) return cuda_fail(e, "conv_tc launch");
   if (pl.prec == kPrecFp32 && prep && y && x) {

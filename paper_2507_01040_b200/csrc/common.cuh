@@ -704,6 +704,70 @@ __device__ __forceinline__ void mma_bf16_cg2_ks(uint32_t issue, uint32_t d_tmem,
   }
 }
 
+// KS MMAs of one stage issued by the whole (converged) warp: elect.sync inside
+// the asm picks the issuing lane, so ptxas emits bare UTC*MMA instructions on
+// uniform registers (no per-lane guard, no R2UR.BROADCAST / VOTEU). The
+// descriptor low halves advance by 32-bit adds (start-address field; the
+// high halves are loop constants). KIND: 1 = f16 (bf16), 2 = tf32. acc0 =
+// accumulate flag of the first MMA. Must be called by all 32 lanes; the
+// matching commit is commit_e (elect.sync picks the same lowest lane).
+#define CL_MMA_E_HEAD                                                                                    \
+  "{\n\t.reg .pred e, p;\n\t.reg .b32 al, bl;\n\t.reg .b64 da, db;\n\t"                                  \
+  "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %6, 0;\n\t"                                              \
+  "mov.b32 al, %1;\n\tmov.b32 bl, %3;\n\tmov.b64 da, {al, %2};\n\tmov.b64 db, {bl, %4};\n\t"
+#define CL_MMA_E_NEXT "add.u32 al, al, %7;\n\tadd.u32 bl, bl, %8;\n\tmov.b64 da, {al, %2};\n\tmov.b64 db, {bl, %4};\n\t"
+#define CL_MMA_E_ARGS                                                                                    \
+  ::"r"(d), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(a_step), "r"(b_step) \
+      : "memory"
+template <int KIND, int CG, int KS>
+__device__ __forceinline__ void mma_stage_e(uint32_t d, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
+                                            uint32_t idesc, uint32_t acc0, uint32_t a_step, uint32_t b_step) {
+  static_assert(KIND == 1 || KIND == 2, "f16 / tf32 kinds");
+  static_assert(CG == 1 || CG == 2, "cta_group");
+  static_assert(KS == 1 || KS == 2 || KS == 4 || KS == 8, "K steps per stage");
+  // (asm strings must be literals: one body per (KIND, CG, KS))
+  if constexpr (CG == 2 && KIND == 1) {
+    if constexpr (KS == 1) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, p;\n}" CL_MMA_E_ARGS);
+    else if constexpr (KS == 2) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+    else if constexpr (KS == 4) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+    else asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+  } else if constexpr (CG == 2 && KIND == 2) {
+    if constexpr (KS == 1) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, p;\n}" CL_MMA_E_ARGS);
+    else if constexpr (KS == 2) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+    else if constexpr (KS == 4) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+    else asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+  } else if constexpr (CG == 1 && KIND == 1) {
+    if constexpr (KS == 1) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n}" CL_MMA_E_ARGS);
+    else if constexpr (KS == 2) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+    else if constexpr (KS == 4) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+    else asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+  } else {
+    if constexpr (KS == 1) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n}" CL_MMA_E_ARGS);
+    else if constexpr (KS == 2) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+    else if constexpr (KS == 4) asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+    else asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
+  }
+}
+#undef CL_MMA_E_HEAD
+#undef CL_MMA_E_NEXT
+#undef CL_MMA_E_ARGS
+// Commit (whole converged warp; elect.sync picks the lane that issued the MMAs).
+template <int CG>
+__device__ __forceinline__ void commit_e(uint64_t* bar) {
+  if constexpr (CG == 2)
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
 // Commit the pair's MMAs to the barrier at the same offset in both CTAs.
 __device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
   asm volatile(

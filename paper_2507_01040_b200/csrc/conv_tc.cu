@@ -23,6 +23,8 @@
 //
 // 3xTF32: D += A_lo*B_hi + A_hi*B_lo + A_hi*B_hi with hi = fp32 with the 13
 // low mantissa bits cleared (exactly representable in tf32) and lo = x - hi.
+#include <type_traits>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -250,7 +252,11 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   uint64_t* sempty = sfull + kSchedR;  // ring slot read by every consumer warp (on the leader)
   long long* sids = reinterpret_cast<long long*>(sempty + kSchedR);
 
-  const int warp = threadIdx.x >> 5;
+  // warp index through a shuffle: ptxas then knows it is warp-uniform, so the
+  // role branches below are uniform and each role's loop values can live on
+  // the uniform datapath (with threadIdx.x >> 5 the MMA issue loop ran on
+  // vector registers and R2UR'd every descriptor)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
 
   const int cs = p.cs;
@@ -286,7 +292,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   __syncthreads();
   if (cs > 1) cluster_sync();  // the pair's barriers and TMEM exist before any cross-CTA traffic
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform (see `warp`)
   const int crank = cs > 1 ? (int)cluster_ctarank() : 0;
 
   const long long num_tiles = p.num_tiles;
@@ -382,7 +388,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           // one halo box per channel group, then the B stage of every tap
           for (int gsi = 0; gsi < p.n_gs; ++gsi) {
             const int g0 = gsi * p.gs;
+            const long long dbg_e0 = (kDbg && p.dbg_acc) ? clock64() : 0;
             mbar_wait(&hempty[hsl], hphase ^ 1);
+            if (kDbg && p.dbg_acc) atomicAdd(p.dbg_acc + 10, (unsigned long long)(clock64() - dbg_e0));
             uint8_t* hA = smem + (size_t)hsl * p.halo_slot;
             if (kAOwn) mbar_arrive_expect_tx(&hfull[hsl], p.halo_bytes * (uint32_t)p.n_tma_a);
             else if (arm) mbar_arrive_expect_tx(&hfull[hsl], (PAIR ? 2u : 1u) * p.halo_bytes * (uint32_t)p.n_tma_a);
@@ -397,7 +405,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
             if (!published) { sched_pub(it); published = true; }
             for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
               const int nq = min(p.tps, nQ - q0);
+              const long long dbg_e1 = (kDbg && p.dbg_acc) ? clock64() : 0;
               mbar_wait(&empty[stage], phase ^ 1);
+              if (kDbg && p.dbg_acc) atomicAdd(p.dbg_acc + 9, (unsigned long long)(clock64() - dbg_e1));
               if (dbg_skip(p) & 1) {  // timing experiment: no B loads (results garbage)
                 if (arm) mbar_arrive(&full[stage]);
               } else {
@@ -498,8 +508,115 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       }
     };
     for (int it = 0;; ++it) {
-      if (sched_read(it, false) < 0) break;
+      // the exit test on a warp-uniform copy of the tile id (REDUX writes a
+      // uniform register): a branch on the raw shared-memory load made ptxas
+      // treat the whole issue loop as divergent, moving every descriptor,
+      // stage and phase value to vector registers (R2UR before each MMA)
+      if (__reduce_min_sync(0xffffffffu, sched_read(it, false) < 0 ? -1 : 0) < 0) break;
       group_begin();
+      if constexpr (!kInt8 && !kSplit) {
+        if (p.halo) {
+          // bf16 / tf32 halo mode: lean warp-converged issue. Every lane runs
+          // the loop on warp-uniform values, `issuer` guards the tcgen05
+          // instructions (no per-stage elect / divergence), one accumulation
+          // group per tile. The per-stage MMA-warp cost bounded the N = 128
+          // stages of these modes (cfg4 bf16: ~110 SASS instructions, ~650
+          // cycles per 4-MMA stage of 256 tensor cycles; tensor pipe 44 %).
+          const uint32_t a_hi = (uint32_t)(h_tmpl >> 32), b_hi = (uint32_t)(b_tmpl >> 32);
+          const uint32_t stg4 = p.stage_bytes >> 4, hslot4 = p.halo_slot >> 4;
+          const uint32_t h_base = (uint32_t)h_tmpl + ((smem_u32(smem) & 0x3FFFFu) >> 4);
+          const uint32_t b_base = (uint32_t)b_tmpl + ((smem_u32(ring) & 0x3FFFFu) >> 4);
+          const uint32_t a_ks = (uint32_t)a_kstep;
+          uint32_t accf = 0;
+          const long long dbg_t0 = (kDbg && p.dbg_acc) ? clock64() : 0;
+          // one tap per stage: compile-time K steps, elect inside the asm, the
+          // halo-slot / accumulator commits after the stage loop (a commit
+          // covers every earlier MMA of the issuing thread)
+          auto taps1 = [&](auto ks_c) {
+            constexpr int KS = decltype(ks_c)::value;
+            constexpr int KIND = PREC == kPrecBf16 ? 1 : 2;
+            const uint32_t b_end = b_base + (uint32_t)S * stg4;
+            uint32_t b_cur = b_base + (uint32_t)stage * stg4;
+            for (int gsi = 0; gsi < p.n_gs; ++gsi) {
+              const long long dbg_h0 = (kDbg && p.dbg_acc) ? clock64() : 0;
+              mbar_wait(&hfull[hsl], hphase);
+              if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 4, (unsigned long long)(clock64() - dbg_h0));
+              tc_fence_after();
+              uint32_t a_cur = h_base + (uint32_t)hsl * hslot4;
+              int qx = 0, qy = 0;
+              for (int q = 0; q < nQ; ++q) {
+                const long long dbg_s0 = (kDbg && p.dbg_acc) ? clock64() : 0;
+                mbar_wait(&full[stage], phase);
+                if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
+                tc_fence_after();
+                mma_stage_e<KIND, PAIR ? 2 : 1, KS>(d_tmem, a_cur, a_hi, b_cur, b_hi, idesc, accf, a_ks, b_ks4);
+                accf = 1u;
+                commit_e<PAIR ? 2 : 1>(&empty[stage]);
+                b_cur += stg4;
+                if (++stage == S) { stage = 0; phase ^= 1; b_cur = b_base; }
+                a_cur += h_dx;
+                if (++qx == df) {
+                  qx = 0;
+                  a_cur += h_wrap_x;
+                  if (++qy == df) { qy = 0; a_cur += h_wrap_y; }
+                }
+              }
+              commit_e<PAIR ? 2 : 1>(&hempty[hsl]);  // halo reusable once its last tap retires
+              if (++hsl == HS) { hsl = 0; hphase ^= 1; }
+            }
+            commit_e<PAIR ? 2 : 1>(&tfull[acc]);
+            (void)b_end;
+          };
+          if (p.tps == 1) {
+            switch (p.ks) {
+              case 1: taps1(std::integral_constant<int, 1>{}); break;
+              case 2: taps1(std::integral_constant<int, 2>{}); break;
+              case 4: taps1(std::integral_constant<int, 4>{}); break;
+              default: taps1(std::integral_constant<int, 8>{}); break;
+            }
+            if (++acc == slots) { acc = 0; acc_phase ^= 1; }
+            if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 8, (unsigned long long)(clock64() - dbg_t0));
+            continue;
+          }
+          for (int gsi = 0; gsi < p.n_gs; ++gsi) {
+            const long long dbg_h0 = (kDbg && p.dbg_acc) ? clock64() : 0;
+            mbar_wait(&hfull[hsl], hphase);
+            if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 4, (unsigned long long)(clock64() - dbg_h0));
+            tc_fence_after();
+            const uint32_t hA = h_base + (uint32_t)hsl * hslot4;
+            uint32_t tap4 = 0;
+            int qx = 0, qy = 0;
+            for (int q0 = 0; q0 < nQ; q0 += p.tps) {
+              const int nq = min(p.tps, nQ - q0);
+              const long long dbg_s0 = (kDbg && p.dbg_acc) ? clock64() : 0;
+              mbar_wait(&full[stage], phase);
+              if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
+              tc_fence_after();
+              uint32_t b0 = b_base + (uint32_t)stage * stg4;
+              for (int i = 0; i < nq; ++i) {
+                mma_stage<PREC, PAIR>(p.ks, issuer, d_tmem, hA + tap4, a_hi, b0, b_hi, idesc, accf, a_ks, b_ks4);
+                accf = 1u;
+                b0 += b_cta4;
+                tap4 += h_dx;
+                if (++qx == df) {
+                  qx = 0;
+                  tap4 += h_wrap_x;
+                  if (++qy == df) { qy = 0; tap4 += h_wrap_y; }
+                }
+              }
+              const bool last = q0 + nq == nQ;
+              commit_g<PAIR>(issuer, &empty[stage]);
+              if (last) commit_g<PAIR>(issuer, &hempty[hsl]);  // halo reusable once the last tap retires
+              if (last && gsi == p.n_gs - 1) commit_g<PAIR>(issuer, &tfull[acc]);
+              if (++stage == S) { stage = 0; phase ^= 1; }
+            }
+            if (++hsl == HS) { hsl = 0; hphase ^= 1; }
+          }
+          if (++acc == slots) { acc = 0; acc_phase ^= 1; }
+          if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 8, (unsigned long long)(clock64() - dbg_t0));
+          continue;
+        }
+      }
       if (p.halo) {
         for (int gsi = 0; gsi < p.n_gs; ++gsi) {
           const long long dbg_h0 = (kDbg && p.dbg_acc) ? clock64() : 0;
@@ -1304,9 +1421,13 @@ static cudaError_t launch_nb(const ConvPlan& plan, const CUtensorMap& tmap, cons
 
 cudaError_t launch_conv(const ConvPlan& plan, const CUtensorMap& tmap, const CUtensorMap& bmap,
                         const ConvKParams& p, int grid, cudaStream_t s) {
+#ifdef CL_PROBE_ONE  // SASS experiments only (nvcc -cubin -DCL_PROBE_ONE=<prec>): one instantiation
+  return launch_t<8, CL_PROBE_ONE, true>(plan, tmap, bmap, p, grid, s);
+#else
   if (plan.nb == 2) return launch_nb<2>(plan, tmap, bmap, p, grid, s);
   if (plan.nb == 4) return launch_nb<4>(plan, tmap, bmap, p, grid, s);
   return launch_nb<8>(plan, tmap, bmap, p, grid, s);
+#endif
 }
 
 // fp32 protocol (B, C, P, NB) -> packed 16-byte row groups (B, G, P, [ncol x] 16 B):
