@@ -216,7 +216,7 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
     pl.hx = tx + d_filter - 1;
     pl.hy = ty + d_filter - 1;
     pl.hz = k == 3 ? d_filter : 1;
-    pl.hs = 2;
+    pl.hs = 2;  // halo slots (the kernel has barriers for up to 4; a third measured no gain for 3xTF32)
   }
   pl.tx = tx;
   pl.ty = ty;
@@ -229,8 +229,11 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
   pl.n_a = i8 ? kDigitsA : pl.n_img;
   pl.n_tma_a = i8 ? kDigitsA : 1;
   pl.levels = i8 ? kLevels : 1;
-  pl.acc_slots = i8 ? 1 : 2;
-  const int max_tile = i8 ? 128 : 256;  // levels x n_tile x slots <= 512 TMEM columns
+  // 3xTF32 drains its accumulator every kX3GroupK reduction elements into
+  // fp32 registers (accumulation groups): 4 rotating 128-column slots
+  const bool x3 = prec == kPrec3xTf32;
+  pl.acc_slots = i8 ? 1 : (x3 ? 4 : 2);
+  const int max_tile = (i8 || x3) ? 128 : 256;  // levels x n_tile x slots <= 512 TMEM columns
   pl.N = C_out * wk;
   pl.n_ntiles = (pl.N + max_tile - 1) / max_tile;
   const int per = (pl.N + pl.n_ntiles - 1) / pl.n_ntiles;
@@ -284,11 +287,21 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
       // (fewer barrier round trips per MMA; bf16 / tf32 stages are short)
       for (int tps : {4, 2}) {
         if (g_force_tps && tps != g_force_tps) continue;
+        if (x3 && ks * tps * 8 > kX3GroupK) continue;  // a stage must not span a 3xTF32 drain
         const int st = (int)((kMaxSmem - 2048 - c.ring_off) / (c.stage_bytes * tps));
         if (st >= (g_force_tps ? 2 : 4)) { c.tps = tps; c.stage_bytes *= tps; break; }
       }
     }
     c.stages = std::min(8, (int)((kMaxSmem - 2048 - c.ring_off) / c.stage_bytes));
+    if (x3 && pl.halo && k == 3) {
+      // 3-D 3xTF32: the most K steps per stage (fewer, longer B stages;
+      // smaller halos), then the deepest ring; measured cfg5 33.1 vs 35.3 ms
+      // (B = 32) for ks 1 x 4 taps against ks 2 x 1 tap. (2-D keeps the
+      // largest ks: cfg3 ks 4 x 1 tap 1.49 ms, 2 x 4 taps 1.70, 1 x 4 2.02.)
+      const int score = c.stages >= 4 ? 100 * c.ks * c.tps + c.stages : c.stages;
+      if (c.stages >= 2 && score > best) { bestp = c; best = score; }
+      continue;
+    }
     if (c.stages >= 4 || (i8 && c.stages >= 3)) { bestp = c; best = 4; break; }
     if (c.stages >= 2 && best < c.stages) { bestp = c; best = c.stages; }
   }
@@ -301,6 +314,9 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
   if (i8) {
     const long long k_stage = (long long)pl.ks * 32 * (pl.halo ? pl.tps : 1);  // int8 K elements per stage
     if (k_stage * pl.stages_per_tile > kMaxKGroup) pl.drain = (int)std::max<long long>(1, kMaxKGroup / k_stage);
+  } else if (x3) {
+    const int k_stage = pl.ks * 8 * (pl.halo ? pl.tps : 1);  // tf32 K elements per stage
+    pl.drain = std::max(1, kX3GroupK / k_stage);
   }
   pl.n_groups = (pl.stages_per_tile + pl.drain - 1) / pl.drain;
   pl.tmem_cols = (uint32_t)std::max(32, pow2_at_least(pl.levels * pl.n_tile * pl.acc_slots));
@@ -854,7 +870,7 @@ static size_t conv_ws_operand_bytes(const cl_conv* h, long long B, bool prepacke
 // (CTA, TMEM row, tile column), reused tile after tile by the same thread
 static size_t conv_ws_group_bytes(const cl_conv* h) {
   const ConvPlan& pl = h->plan;
-  return pl.n_groups > 1 ? align_up((size_t)num_sms() * kTileM * pl.n_tile * 8, 256) : 0;
+  return (pl.prec == kPrecFp32 && pl.n_groups > 1) ? align_up((size_t)num_sms() * kTileM * pl.n_tile * 8, 256) : 0;
 }
 static size_t conv_ws_bytes(const cl_conv* h, long long B, bool prepacked) {
   return conv_ws_operand_bytes(h, B, prepacked) + kSchedBytes + conv_ws_group_bytes(h);
@@ -992,7 +1008,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.acc_slots = pl.acc_slots;
   p.drain = pl.drain;
   p.n_groups = pl.n_groups;
-  p.grp_scratch = pl.n_groups > 1 ? reinterpret_cast<long long*>(static_cast<char*>(ws) +
+  p.grp_scratch = (pl.prec == kPrecFp32 && pl.n_groups > 1) ? reinterpret_cast<long long*>(static_cast<char*>(ws) +
                                                                  conv_ws_operand_bytes(h, B, xbf != nullptr) + kSchedBytes)
                                   : nullptr;
   p.a_scale = a_scale;

@@ -748,6 +748,49 @@ __device__ __forceinline__ void mma_stage_e(uint32_t d, uint32_t a_lo, uint32_t 
     else asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
   }
 }
+// 3xTF32: KS K steps of 3 tf32 MMAs each, D += A_lo*B_hi + A_hi*B_lo + A_hi*B_hi
+// (the lo images sit a_img / b_img 16-byte units after the hi ones); same
+// issue conventions as mma_stage_e. acc0 applies to the first MMA only.
+#define CL_X3_HEAD                                                                                       \
+  "{\n\t.reg .pred e, p;\n\t.reg .b32 al, bl, t;\n\t.reg .b64 da, db, dl;\n\t"                           \
+  "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %6, 0;\n\tmov.b32 al, %1;\n\tmov.b32 bl, %3;\n\t"
+#define CL_X3_STEP(CGS, ACC)                                                                             \
+  "add.u32 t, al, %9;\n\tmov.b64 dl, {t, %2};\n\tmov.b64 db, {bl, %4};\n\t"                                \
+  "@e tcgen05.mma.cta_group::" CGS ".kind::tf32 [%0], dl, db, %5, " ACC ";\n\t"                             \
+  "add.u32 t, bl, %10;\n\tmov.b64 da, {al, %2};\n\tmov.b64 dl, {t, %4};\n\t"                               \
+  "@e tcgen05.mma.cta_group::" CGS ".kind::tf32 [%0], da, dl, %5, 1;\n\t"                                   \
+  "@e tcgen05.mma.cta_group::" CGS ".kind::tf32 [%0], da, db, %5, 1;\n\t"                                   \
+  "add.u32 al, al, %7;\n\tadd.u32 bl, bl, %8;\n\t"
+#define CL_X3_ARGS                                                                                        \
+  ::"r"(d), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(a_step), "r"(b_step), \
+      "r"(a_img), "r"(b_img)                                                                               \
+      : "memory"
+template <int CG, int KS>
+__device__ __forceinline__ void mma_stage_x3_e(uint32_t d, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
+                                               uint32_t idesc, uint32_t acc0, uint32_t a_step, uint32_t b_step,
+                                               uint32_t a_img, uint32_t b_img) {
+  static_assert(KS == 1 || KS == 2 || KS == 4 || KS == 8, "K steps per stage");
+  if constexpr (CG == 2) {
+    if constexpr (KS == 1) asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p") "}" CL_X3_ARGS);
+    else if constexpr (KS == 2) asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p") CL_X3_STEP("2", "1") "}" CL_X3_ARGS);
+    else if constexpr (KS == 4)
+      asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") "}" CL_X3_ARGS);
+    else
+      asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1")
+                       CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") "}" CL_X3_ARGS);
+  } else {
+    if constexpr (KS == 1) asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p") "}" CL_X3_ARGS);
+    else if constexpr (KS == 2) asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p") CL_X3_STEP("1", "1") "}" CL_X3_ARGS);
+    else if constexpr (KS == 4)
+      asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") "}" CL_X3_ARGS);
+    else
+      asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1")
+                       CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") "}" CL_X3_ARGS);
+  }
+}
+#undef CL_X3_HEAD
+#undef CL_X3_STEP
+#undef CL_X3_ARGS
 #undef CL_MMA_E_HEAD
 #undef CL_MMA_E_NEXT
 #undef CL_MMA_E_ARGS
@@ -795,6 +838,22 @@ __device__ __forceinline__ void mma_commit_multicast(uint64_t* bar, uint16_t cta
 // tcgen05.wait::ld that also ties the loaded registers to the wait, so the
 // compiler cannot move their uses above it (for loads left in flight while
 // other work runs).
+// fp32 bits rounded to the nearest tf32 (ties away; cvt.rna.tf32.f32)
+__device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t u) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(__uint_as_float(u)));
+  return r;
+}
+// 16 columns of this thread's TMEM lane (32x32b shape, like tmem_ld16)
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld_wait_dep16(uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;"
                : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),

@@ -19,7 +19,8 @@
 //   warps 4-7   epilogue: tcgen05.ld -> bias [-> activation] [-> residual]
 //               -> coalesced stores in the protocol layout (thread = pixel
 //               row, holds all N_B blades of each output channel)
-//   warps 8-11  3xTF32 splitter: A -> (A_hi, A_lo) in shared memory
+//   warps 12-15 3xTF32 splitter: A -> (A_hi, A_lo) in shared memory (the
+//               3xTF32 kernel has 512 threads: epilogue warps 4-11)
 //
 // 3xTF32: D += A_lo*B_hi + A_hi*B_lo + A_hi*B_hi with hi = fp32 with the 13
 // low mantissa bits cleared (exactly representable in tf32) and lo = x - hi.
@@ -213,6 +214,52 @@ __device__ __forceinline__ void drain_groups(const ConvKParams& p, uint64_t* tfu
   }
 }
 
+// 3xTF32 accumulation groups: the MMA warp rotates `slots` TMEM slots, one
+// group of kX3GroupK reduction elements each. This thread drains the first
+// n_groups - 1 groups of its row (columns [c_beg, c_end), <= 64) into fp32
+// registers with round-to-nearest adds, then adds the sums into the last
+// group's slot in TMEM (tcgen05.st) and returns with that slot full, so the
+// regular epilogue reads the complete accumulator. (The tensor core's fp32
+// accumulation truncates; over K = 13824 its error reached 7e-3 under the
+// reference metric, profiles/r02_3xtf32_drain_study.txt.)
+template <bool PAIR>
+__device__ __forceinline__ void x3_drain_groups(const ConvKParams& p, uint64_t* tfull, uint64_t* tempty,
+                                                uint32_t tmem_base, int ew, int c_beg, int c_end, uint32_t slot_cols,
+                                                int slots, int& acc, uint32_t& acc_phase) {
+  float sm[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) sm[i] = 0.f;
+  const uint32_t lane_base = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)c_beg;
+  for (int grp = 0; grp < p.n_groups; ++grp) {
+    mbar_wait_sleep(&tfull[acc], acc_phase, 20);
+    tc_fence_after();
+    const uint32_t ta = lane_base + (uint32_t)acc * slot_cols;
+    const bool last = grp + 1 == p.n_groups;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (c_beg + 16 * j >= c_end) break;
+      uint32_t r[16];
+      tmem_ld16(ta + (uint32_t)(16 * j), r);
+      tmem_ld_wait_dep16(r);
+      if (!last) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sm[16 * j + i] += __uint_as_float(r[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(sm[16 * j + i] + __uint_as_float(r[i]));
+        tmem_st16(ta + (uint32_t)(16 * j), r);
+      }
+    }
+    if (last) {
+      tmem_st_wait();  // the regular epilogue reads this slot next (same thread, same lanes)
+      return;
+    }
+    tc_fence_before();
+    if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
+    if (++acc == slots) { acc = 0; acc_phase ^= 1; }
+  }
+}
+
 // BCLS: change-of-basis pattern class of the int8 epilogue. 1 = the M2(C)
 // basis of the (1,1,1) family: each lane's blades use own rows {0,0,3,3} and
 // partner rows {2,2,1,1} (compile-time picks, 2 shuffles per channel); 0 = any.
@@ -227,7 +274,8 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   constexpr bool kAOwn = kSplit;
   // epilogue warp groups: warps 4-7, plus warps 8-11 when they are not the
   // 3xTF32 splitter (each group drains half of the accumulator columns)
-  constexpr int kEpiGroups = kSplit ? 1 : (conv_threads(PREC, NB) == 640 ? 4 : 2);
+  // (3xTF32: warps 4-11, the splitter is warps 12-15)
+  constexpr int kEpiGroups = kSplit ? 2 : (conv_threads(PREC, NB) == 640 ? 4 : 2);
   // A row-group bytes: packed 16-byte groups for bf16 / int8 digits / 1-D,
   // otherwise one protocol multivector (16 B in 2-D, 32 B in 3-D)
   constexpr int RB = (PREC == kPrecBf16 || kInt8 || NB == 2) ? 16 : NB * 4;
@@ -241,14 +289,14 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)S * p.stage_bytes);
   uint64_t* empty = full + S;
   uint64_t* lo_ready = empty + S;
-  uint64_t* tfull = lo_ready + S;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* hfull = tempty + 2;   // halo buffers: loaded
-  uint64_t* hempty = hfull + 2;   //               consumed by the last tap's MMAs
-  uint64_t* hlo = hempty + 2;     //               3xTF32 split done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hlo + 2);
+  uint64_t* tfull = lo_ready + S;  // accumulator slots: 4 barriers each (3xTF32 rotates 4 slots)
+  uint64_t* tempty = tfull + 4;
+  uint64_t* hfull = tempty + 4;   // halo buffers: loaded
+  uint64_t* hempty = hfull + 4;   //               consumed by the last tap's MMAs (up to 4 slots)
+  uint64_t* hlo = hempty + 4;     //               3xTF32 split done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hlo + 4);
   constexpr int kSchedR = 8;       // tile-scheduler ring depth (> tiles the producer may lead the epilogue by)
-  uint64_t* sfull = hlo + 3;       // ring slot published
+  uint64_t* sfull = hlo + 5;       // ring slot published
   uint64_t* sempty = sfull + kSchedR;  // ring slot read by every consumer warp (on the leader)
   long long* sids = reinterpret_cast<long long*>(sempty + kSchedR);
 
@@ -266,9 +314,11 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       mbar_init(&empty[s], 1);  // one MMA commit (the pair leader's reaches both CTAs)
       mbar_init(&lo_ready[s], 128);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < 4; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128 * kEpiGroups * (PAIR ? 2 : 1));  // pair: both CTAs' epilogues, on the leader
+    }
+    for (int a = 0; a < 4; ++a) {
       mbar_init(&hfull[a], 1);
       mbar_init(&hempty[a], 1);
       mbar_init(&hlo[a], 128 * (PAIR ? 2 : 1));
@@ -514,105 +564,89 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       // stage and phase value to vector registers (R2UR before each MMA)
       if (__reduce_min_sync(0xffffffffu, sched_read(it, false) < 0 ? -1 : 0) < 0) break;
       group_begin();
-      if constexpr (!kInt8 && !kSplit) {
+      if constexpr (!kInt8) {
         if (p.halo) {
-          // bf16 / tf32 halo mode: lean warp-converged issue. Every lane runs
-          // the loop on warp-uniform values, `issuer` guards the tcgen05
-          // instructions (no per-stage elect / divergence), one accumulation
-          // group per tile. The per-stage MMA-warp cost bounded the N = 128
-          // stages of these modes (cfg4 bf16: ~110 SASS instructions, ~650
-          // cycles per 4-MMA stage of 256 tensor cycles; tensor pipe 44 %).
+          // bf16 / tf32 / 3xTF32 halo mode: lean warp-converged issue. All
+          // lanes run the loop on warp-uniform values; elect.sync inside the
+          // MMA / commit asm issues (bare UTC*MMA on uniform registers). The
+          // per-stage MMA-warp cost had bounded the N = 128 stages of these
+          // modes (cfg4 bf16: ~110 SASS instructions, ~650 cycles per 4-MMA
+          // stage of 256 tensor cycles). Accumulation groups of p.drain
+          // stages (3xTF32's periodic drains) rotate the TMEM slots.
+          constexpr int CG = PAIR ? 2 : 1;
           const uint32_t a_hi = (uint32_t)(h_tmpl >> 32), b_hi = (uint32_t)(b_tmpl >> 32);
           const uint32_t stg4 = p.stage_bytes >> 4, hslot4 = p.halo_slot >> 4;
           const uint32_t h_base = (uint32_t)h_tmpl + ((smem_u32(smem) & 0x3FFFFu) >> 4);
           const uint32_t b_base = (uint32_t)b_tmpl + ((smem_u32(ring) & 0x3FFFFu) >> 4);
           const uint32_t a_ks = (uint32_t)a_kstep;
-          uint32_t accf = 0;
           const long long dbg_t0 = (kDbg && p.dbg_acc) ? clock64() : 0;
-          // one tap per stage: compile-time K steps, elect inside the asm, the
-          // halo-slot / accumulator commits after the stage loop (a commit
-          // covers every earlier MMA of the issuing thread)
-          auto taps1 = [&](auto ks_c) {
+          // one filter tap's KS K steps at (a, b)
+          auto tap_mmas = [&](auto ks_c, uint32_t a, uint32_t b, uint32_t accf) {
             constexpr int KS = decltype(ks_c)::value;
-            constexpr int KIND = PREC == kPrecBf16 ? 1 : 2;
-            const uint32_t b_end = b_base + (uint32_t)S * stg4;
+            if constexpr (kSplit)
+              mma_stage_x3_e<CG, KS>(d_tmem, a, a_hi, b, b_hi, idesc, accf, a_ks, b_ks4, h_img4, b_img4);
+            else
+              mma_stage_e<PREC == kPrecBf16 ? 1 : 2, CG, KS>(d_tmem, a, a_hi, b, b_hi, idesc, accf, a_ks, b_ks4);
+          };
+          auto run = [&](auto ks_c, auto tps_c) {
+            constexpr int TPS = decltype(tps_c)::value;  // 0: runtime p.tps
+            const int tps = TPS ? TPS : p.tps;
+            uint32_t accf = 0;
             uint32_t b_cur = b_base + (uint32_t)stage * stg4;
             for (int gsi = 0; gsi < p.n_gs; ++gsi) {
               const long long dbg_h0 = (kDbg && p.dbg_acc) ? clock64() : 0;
-              mbar_wait(&hfull[hsl], hphase);
+              mbar_wait(kSplit ? &hlo[hsl] : &hfull[hsl], hphase);  // 3xTF32: A_lo written
               if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 4, (unsigned long long)(clock64() - dbg_h0));
               tc_fence_after();
               uint32_t a_cur = h_base + (uint32_t)hsl * hslot4;
               int qx = 0, qy = 0;
-              for (int q = 0; q < nQ; ++q) {
+              for (int q0 = 0; q0 < nQ; q0 += tps) {
+                const int nq = TPS == 1 ? 1 : min(tps, nQ - q0);
                 const long long dbg_s0 = (kDbg && p.dbg_acc) ? clock64() : 0;
                 mbar_wait(&full[stage], phase);
                 if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
                 tc_fence_after();
-                mma_stage_e<KIND, PAIR ? 2 : 1, KS>(d_tmem, a_cur, a_hi, b_cur, b_hi, idesc, accf, a_ks, b_ks4);
-                accf = 1u;
-                commit_e<PAIR ? 2 : 1>(&empty[stage]);
+                uint32_t b0 = b_cur;
+                for (int i = 0; i < nq; ++i) {
+                  tap_mmas(ks_c, a_cur, b0, accf);
+                  accf = 1u;
+                  b0 += b_cta4;
+                  a_cur += h_dx;
+                  if (++qx == df) {
+                    qx = 0;
+                    a_cur += h_wrap_x;
+                    if (++qy == df) { qy = 0; a_cur += h_wrap_y; }
+                  }
+                }
+                commit_e<CG>(&empty[stage]);
                 b_cur += stg4;
                 if (++stage == S) { stage = 0; phase ^= 1; b_cur = b_base; }
-                a_cur += h_dx;
-                if (++qx == df) {
-                  qx = 0;
-                  a_cur += h_wrap_x;
-                  if (++qy == df) { qy = 0; a_cur += h_wrap_y; }
+                // accumulation group ended (not the tile's last stage): hand the
+                // slot to the epilogues, open the next one
+                if (++sg == p.drain && !(gsi == p.n_gs - 1 && q0 + nq >= nQ)) {
+                  commit_e<CG>(&tfull[acc]);
+                  if (++acc == slots) { acc = 0; acc_phase ^= 1; }
+                  group_begin();
+                  sg = 0;
+                  accf = 0;
                 }
               }
-              commit_e<PAIR ? 2 : 1>(&hempty[hsl]);  // halo reusable once its last tap retires
+              commit_e<CG>(&hempty[hsl]);  // halo reusable once its last tap retires
               if (++hsl == HS) { hsl = 0; hphase ^= 1; }
             }
-            commit_e<PAIR ? 2 : 1>(&tfull[acc]);
-            (void)b_end;
+            commit_e<CG>(&tfull[acc]);
           };
-          if (p.tps == 1) {
-            switch (p.ks) {
-              case 1: taps1(std::integral_constant<int, 1>{}); break;
-              case 2: taps1(std::integral_constant<int, 2>{}); break;
-              case 4: taps1(std::integral_constant<int, 4>{}); break;
-              default: taps1(std::integral_constant<int, 8>{}); break;
-            }
-            if (++acc == slots) { acc = 0; acc_phase ^= 1; }
-            if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 8, (unsigned long long)(clock64() - dbg_t0));
-            continue;
-          }
-          for (int gsi = 0; gsi < p.n_gs; ++gsi) {
-            const long long dbg_h0 = (kDbg && p.dbg_acc) ? clock64() : 0;
-            mbar_wait(&hfull[hsl], hphase);
-            if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 4, (unsigned long long)(clock64() - dbg_h0));
-            tc_fence_after();
-            const uint32_t hA = h_base + (uint32_t)hsl * hslot4;
-            uint32_t tap4 = 0;
-            int qx = 0, qy = 0;
-            for (int q0 = 0; q0 < nQ; q0 += p.tps) {
-              const int nq = min(p.tps, nQ - q0);
-              const long long dbg_s0 = (kDbg && p.dbg_acc) ? clock64() : 0;
-              mbar_wait(&full[stage], phase);
-              if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 5, (unsigned long long)(clock64() - dbg_s0));
-              tc_fence_after();
-              uint32_t b0 = b_base + (uint32_t)stage * stg4;
-              for (int i = 0; i < nq; ++i) {
-                mma_stage<PREC, PAIR>(p.ks, issuer, d_tmem, hA + tap4, a_hi, b0, b_hi, idesc, accf, a_ks, b_ks4);
-                accf = 1u;
-                b0 += b_cta4;
-                tap4 += h_dx;
-                if (++qx == df) {
-                  qx = 0;
-                  tap4 += h_wrap_x;
-                  if (++qy == df) { qy = 0; tap4 += h_wrap_y; }
-                }
-              }
-              const bool last = q0 + nq == nQ;
-              commit_g<PAIR>(issuer, &empty[stage]);
-              if (last) commit_g<PAIR>(issuer, &hempty[hsl]);  // halo reusable once the last tap retires
-              if (last && gsi == p.n_gs - 1) commit_g<PAIR>(issuer, &tfull[acc]);
-              if (++stage == S) { stage = 0; phase ^= 1; }
-            }
-            if (++hsl == HS) { hsl = 0; hphase ^= 1; }
+          using I1 = std::integral_constant<int, 1>;
+          using I0 = std::integral_constant<int, 0>;
+          const bool t1 = p.tps == 1;
+          switch (p.ks) {
+            case 1: if (t1) run(I1{}, I1{}); else run(I1{}, I0{}); break;
+            case 2: if (t1) run(std::integral_constant<int, 2>{}, I1{}); else run(std::integral_constant<int, 2>{}, I0{}); break;
+            case 4: if (t1) run(std::integral_constant<int, 4>{}, I1{}); else run(std::integral_constant<int, 4>{}, I0{}); break;
+            default: if (t1) run(std::integral_constant<int, 8>{}, I1{}); else run(std::integral_constant<int, 8>{}, I0{}); break;
           }
           if (++acc == slots) { acc = 0; acc_phase ^= 1; }
+          sg = 0;
           if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 8, (unsigned long long)(clock64() - dbg_t0));
           continue;
         }
@@ -888,7 +922,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       if constexpr (kInt8) if (valid) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
       if constexpr (kInt8 && GROUPS)  // exact mode, several accumulation groups per tile
         drain_groups<PAIR>(p, tfull, tempty, tmem_base, ew, row, c_beg, c_end, slot_cols, slots, acc, acc_phase);
-      mbar_wait_sleep(&tfull[acc], acc_phase, 64);  // off the critical path: poll gently
+      if (kSplit && p.n_groups > 1)  // returns with the last group's slot full and complete
+        x3_drain_groups<PAIR>(p, tfull, tempty, tmem_base, ew, c_beg, c_end, slot_cols, slots, acc, acc_phase);
+      else
+        mbar_wait_sleep(&tfull[acc], acc_phase, 64);  // off the critical path: poll gently
       tc_fence_after();
       const long long dbg_t0 = (kDbg && p.dbg_acc) ? clock64() : 0;
       const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)acc * slot_cols;
@@ -1304,23 +1341,27 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       }
       if (++acc == slots) { acc = 0; acc_phase ^= 1; }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 12) {
     // ===================== 3xTF32 splitter =====================
     if constexpr (kSplit) {
-      const int tid = threadIdx.x - 256;
+      const int tid = threadIdx.x - 384;
       auto split = [&](uint8_t* buf, uint32_t bytes, uint32_t lo_off) {
         uint4* a = reinterpret_cast<uint4*>(buf);
         float4* lo = reinterpret_cast<float4*>(buf + lo_off);
         const int n4 = (int)(bytes / 16);
         for (int i = tid; i < n4; i += 128) {
+          // hi = round-to-nearest tf32, lo = the remainder rounded to tf32
+          // (both exact for the tensor core, which reads the top 19 bits; a
+          // truncated hi left |lo| up to 2^-10 |x| and lo's own truncation
+          // an error of 2^-20 |x|, 16x fp32's)
           uint4 v = a[i];
           uint4 h;
-          h.x = v.x & 0xFFFFE000u; h.y = v.y & 0xFFFFE000u; h.z = v.z & 0xFFFFE000u; h.w = v.w & 0xFFFFE000u;
+          h.x = tf32_rna_bits(v.x); h.y = tf32_rna_bits(v.y); h.z = tf32_rna_bits(v.z); h.w = tf32_rna_bits(v.w);
           float4 l;
-          l.x = __uint_as_float(v.x) - __uint_as_float(h.x);
-          l.y = __uint_as_float(v.y) - __uint_as_float(h.y);
-          l.z = __uint_as_float(v.z) - __uint_as_float(h.z);
-          l.w = __uint_as_float(v.w) - __uint_as_float(h.w);
+          l.x = __uint_as_float(tf32_rna_bits(__float_as_uint(__uint_as_float(v.x) - __uint_as_float(h.x))));
+          l.y = __uint_as_float(tf32_rna_bits(__float_as_uint(__uint_as_float(v.y) - __uint_as_float(h.y))));
+          l.z = __uint_as_float(tf32_rna_bits(__float_as_uint(__uint_as_float(v.z) - __uint_as_float(h.z))));
+          l.w = __uint_as_float(tf32_rna_bits(__float_as_uint(__uint_as_float(v.w) - __uint_as_float(h.w))));
           a[i] = h;
           lo[i] = l;
         }

@@ -94,9 +94,11 @@ __global__ void expand_img_kernel(Sig sg, const float* __restrict__ f, int C_in,
 #pragma unroll
       for (int k = 0; k < kDigitsW; ++k) *reinterpret_cast<int8_t*>(base + (size_t)k * img_stride + off) = d[k];
     } else if (pl.prec == kPrec3xTf32) {
-      const float hi = __uint_as_float(__float_as_uint(w) & 0xFFFFE000u);
+      // hi = w rounded to tf32, lo = the remainder rounded to tf32: both
+      // operands reach the tensor core exactly (it reads the top 19 bits)
+      const float hi = tf32_rna(w);
       *reinterpret_cast<float*>(base + off) = hi;
-      *reinterpret_cast<float*>(base + img_stride + off) = (float)(wv - (double)hi);
+      *reinterpret_cast<float*>(base + img_stride + off) = tf32_rna((float)(wv - (double)hi));
     } else if (pl.prec == kPrecTf32) {
       *reinterpret_cast<float*>(base + off) = tf32_rna(w);
     } else {

@@ -36,6 +36,11 @@ constexpr int kTileM = 128;          // GEMM rows per tile (= TMEM lanes)
 // (L + 1) <= 4 digit-pair products of |d_i w_j| <= 2^14 per K element, so
 // |L| <= 4 * 2^14 * K < 2^31 for K <= 32000 (s32 TMEM accumulators).
 constexpr int kMaxKGroup = 32000;
+// 3xTF32: reduction elements per accumulation group. The tensor core's fp32
+// accumulation truncates, so its error grows with the chain length; draining
+// every 64 elements into fp32 registers (round-to-nearest sums) keeps
+// max_rel_error(floor 1e-2) <= 1e-4 at K = 13824 (profiles/r02_3xtf32_drain_study.txt)
+constexpr int kX3GroupK = 64;
 
 // Change of basis (basis.cu): x' = T x splits the conv into ncol independent
 // GEMMs sharing a w x w filter; T rows = (column, component), entries +-1/0,
@@ -95,7 +100,11 @@ constexpr int kConvThreads = 384;    // 12 warps, see conv_tc.cu
 // 20 warps (four epilogue warp groups) for the int8 mode (one accumulator slot to drain) and the
 // 2-D / 1-D fp32-accumulator modes (measured faster); 12 warps (two groups) for 3-D bf16 / tf32
 // (their 3-D epilogue spills at 96 registers) and 3xTF32 (warps 8-11 split A)
-constexpr int conv_threads(int prec, int nb) { return (prec == 0 || (prec != 3 && nb <= 4)) ? 640 : kConvThreads; }
+// 3xTF32 (prec 3): 16 warps = two epilogue groups (they hold the drained
+// partial sums in registers) + the splitter group
+constexpr int conv_threads(int prec, int nb) {
+  return prec == 3 ? 512 : ((prec == 0 || nb <= 4) ? 640 : kConvThreads);
+}
 constexpr int kMaxSmem = 232448;     // 227 KB opt-in dynamic shared memory per CTA
 
 // Tiling plan of one conv layer, fixed at create time (conv.py:101-140 fixes

@@ -106,8 +106,10 @@ def test_cfg5_full_batch_sampled_oracle():
 
 
 # stated bounds of the fp32-accumulator modes, normwise:
-# max_rel_error(floor=max|ref|); the floor-1e-2 reference metric is printed too
-MODE_TOL = {"3xtf32": 5e-5, "tf32": 2e-2, "bf16": 2e-2}
+# max_rel_error(floor=max|ref|); the floor-1e-2 reference metric is printed too.
+# 3xTF32 is FP32-accurate: it must also meet the fp32 bound under the
+# reference metric (<= 1e-4, measured 5.0e-5 .. 8.6e-5 at these sizes).
+MODE_TOL = {"3xtf32": 2e-6, "tf32": 2e-2, "bf16": 2e-2}
 
 
 def _check_mode(name, y, r, prec):
@@ -115,6 +117,8 @@ def _check_mode(name, y, r, prec):
     e_ref = O.max_rel_error(y, r)
     print(f"{name} {prec} normwise {e:.3e} (reference metric, floor 1e-2: {e_ref:.3e})")
     assert e <= MODE_TOL[prec]
+    if prec == "3xtf32":
+        assert e_ref <= 1e-4, e_ref
 
 
 @pytest.mark.parametrize("prec", ["3xtf32", "tf32", "bf16"])

@@ -46,14 +46,23 @@ def run_dev(fn, x, *a):
 
 
 def assert_conv_close(y, ref, prec, K=0):
-    """K = reduction length C_in * N_B * d_f^k: the 3xTF32 bound is 1e-5 up to
-    K = 1152 and 5e-5 beyond (its truncating fp32 accumulation grows linearly
-    with K: 1.2e-5 at K = 2304)."""
+    """fp32 and 3xTF32 are the FP32-accurate modes. fp32 (exact int8-digit
+    accumulation) meets the reference metric (max_rel_error, floor 1e-2,
+    bench.py:74-88) <= 1e-4 everywhere. 3xTF32 drains its tensor-core
+    accumulator every 64 reduction elements into fp32 registers (DESIGN.md
+    "3xTF32 accumulation groups"), so its error no longer grows with K:
+    normwise <= 2e-6 (fp32-class; measured 1e-7 .. 4e-7). The floor-1e-2
+    metric is absolute near zero, so for fp32-class arithmetic it scales with
+    the output magnitude: <= 1e-4 is asserted on the BASELINE configs at full
+    size (test_gpu_configs.py, unit-scale outputs), <= 3e-4 on these small
+    cases with up to 12x-scaled channels (the reference's own fp32 path: 3.6e-4
+    at cfg4)."""
     if prec == "fp32":
         assert O.max_rel_error(y, ref) <= 1e-4, O.max_rel_error(y, ref)
     elif prec == "3xtf32":
+        e_ref = O.max_rel_error(y, ref)
         e = O.max_rel_error(y, ref, floor=float(np.abs(ref).max()) + 1e-30)
-        assert e <= (1e-5 if K <= 1152 else 5e-5), (e, K)
+        assert e_ref <= 3e-4 and e <= 2e-6, (e_ref, e, K)
     else:
         e = O.max_rel_error(y, ref, floor=float(np.abs(ref).max()) + 1e-30)
         assert e <= 2e-2, e
