@@ -651,11 +651,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           continue;
         }
       }
-      if (p.halo) {
+      if (kInt8 && p.halo) {  // (the other modes took the lean path above)
         for (int gsi = 0; gsi < p.n_gs; ++gsi) {
           const long long dbg_h0 = (kDbg && p.dbg_acc) ? clock64() : 0;
-          if (kSplit) mbar_wait(&hlo[hsl], hphase);
-          else mbar_wait(&hfull[hsl], hphase);
+          mbar_wait(&hfull[hsl], hphase);
           if (kDbg && p.dbg_acc && lane == 0) atomicAdd(p.dbg_acc + 4, (unsigned long long)(clock64() - dbg_h0));
           tc_fence_after();
           const uint32_t hA4 = (smem_u32(smem + (size_t)hsl * p.halo_slot) & 0x3FFFFu) >> 4;
@@ -672,12 +671,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               if (elect_one()) {
                 const uint32_t a_hi = (uint32_t)(h_tmpl >> 32), b_hi = (uint32_t)(b_tmpl >> 32);
                 uint32_t a0 = (uint32_t)h_tmpl + hA4 + tap4, b0 = (uint32_t)b_tmpl + sB4;
-                if constexpr (!kInt8 && !kSplit)
-                  mma_stage<PREC, PAIR>(p.ks, 1u, d_tmem, a0, a_hi, b0, b_hi, idesc, sg == 0 ? 0u : 1u,
-                                        (uint32_t)a_kstep, b_ks4);
                 #pragma unroll
                 for (int s = 0; s < 8; ++s) {  // ks <= 8, unrolled: constant per-step offsets
-                  if (kInt8 || kSplit ? s >= p.ks : true) break;
+                  if (s >= p.ks) break;
                   const uint32_t first = (sg == 0 && s == 0) ? 1u : 0u;
                   if constexpr (kInt8) {  // the K step's 10 digit-pair MMAs in one asm block
                     if constexpr (PAIR)
@@ -686,12 +682,6 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                     else
                       mma_i8_kstep(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, first ? 0u : 1u, h_img4, b_img4,
                                    (uint32_t)p.n_tile);
-                  } else if constexpr (kSplit) {
-                    mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0 + h_img4, a_hi, b0, b_hi, idesc, first ? 0u : 1u);
-                    mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0, a_hi, b0 + b_img4, b_hi, idesc, 1u);
-                    mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, 1u);
-                  } else {
-                    mma_mode_s<PREC, PAIR>(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, first ? 0u : 1u);
                   }
                   a0 += (uint32_t)a_kstep;
                   b0 += b_ks4;
@@ -721,8 +711,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               }
             }
           } else {
-            // several taps per stage: converged per-MMA issue (measured faster here
-            // than one lane issuing mma_stage blocks: cfg5 bf16 5.38 vs 5.88 ms at B = 32)
+            // several taps per stage (small int8 layers, e.g. cfg1): converged per-MMA issue
             for (int q0 = 0; q0 < nQ; q0 += p.tps) {  // tps filter taps per B stage
               const int nq = min(p.tps, nQ - q0);
               const long long dbg_s0 = (kDbg && p.dbg_acc) ? clock64() : 0;
@@ -758,12 +747,6 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                                                  a_hi, b0 + (uint32_t)j * b_img, b_hi, idesc, ii == i0 ? accf : 1u);
                         }
                       }
-                    } else if constexpr (kSplit) {
-                      mma_mode_s<kPrecTf32, PAIR>(issuer, d_tmem, a0 + a_img, a_hi, b0, b_hi, idesc, accf);  // A_lo * B_hi
-                      mma_mode_s<kPrecTf32, PAIR>(issuer, d_tmem, a0, a_hi, b0 + b_img, b_hi, idesc, 1u);   // A_hi * B_lo
-                      mma_mode_s<kPrecTf32, PAIR>(issuer, d_tmem, a0, a_hi, b0, b_hi, idesc, 1u);           // A_hi * B_hi
-                    } else {
-                      mma_mode_s<PREC, PAIR>(issuer, d_tmem, a0, a_hi, b0, b_hi, idesc, accf);
                     }
                     accf = 1u;
                     a0 += a_ks;
