@@ -293,12 +293,16 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
       }
     }
     c.stages = std::min(8, (int)((kMaxSmem - 2048 - c.ring_off) / c.stage_bytes));
-    if (x3 && pl.halo && k == 3) {
-      // 3-D 3xTF32: the most K steps per stage (fewer, longer B stages;
-      // smaller halos), then the deepest ring; measured cfg5 33.1 vs 35.3 ms
-      // (B = 32) for ks 1 x 4 taps against ks 2 x 1 tap. (2-D keeps the
-      // largest ks: cfg3 ks 4 x 1 tap 1.49 ms, 2 x 4 taps 1.70, 1 x 4 2.02.)
-      const int score = c.stages >= 4 ? 100 * c.ks * c.tps + c.stages : c.stages;
+    if (pl.halo && !i8 && k == 3) {
+      // 3-D halo mode, fp32-accumulator modes: the most K steps per stage (up
+      // to 8: fewer, longer B stages, more bytes in flight against the ~1.4 K
+      // cycle TMA latency; smaller halos), then the deepest ring. Measured
+      // kernel-only: cfg4 bf16 ks 2 x 4 taps 0.79 ms vs ks 4 x 1 tap 0.87, tf32
+      // 1.40 vs 1.58; cfg5 3xTF32 ks 1 x 4 taps 33.1 ms vs ks 2 x 1 tap 35.3
+      // (B = 32). 2-D keeps the largest ks (its halos are 3x smaller): cfg3
+      // bf16 ks 8 x 1 tap 0.43 ms vs ks 2 x 4 taps 0.49, 3xTF32 ks 4 x 1 tap
+      // 1.49 vs 1.70.
+      const int score = c.stages >= 4 ? 100 * std::min(8, c.ks * c.tps) + c.stages : c.stages;
       if (c.stages >= 2 && score > best) { bestp = c; best = score; }
       continue;
     }
