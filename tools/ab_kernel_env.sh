@@ -1,6 +1,6 @@
 #!/bin/bash
 # Kernel-only times of one conv under diagnostic-library switches (under gpurun):
-# CASE="bf16 16 4" VARS="-|CL_DBG_SKIP=4|..." tools/ab_env2.sh
+# CASE="bf16 16 4" VARS="-|CL_DBG_SKIP=4|..." tools/ab_kernel_env.sh
 cd "$(dirname "$0")/.."
 export CL_LIB_PATH=$PWD/paper_2507_01040_b200/lib/libclifford_b200_ab.so
 IFS='|' read -ra vs <<< "${VARS:--}"

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2 final measurement pass (under gpurun): the GPU suite, every bench line
+# Full measurement pass (under gpurun): the GPU suite, every bench line
 # with clock records, ncu of the current headline kernel and cfg4 16-bit modes,
 # the bench launch list and the default bench line.
 cd "$(dirname "$0")/.."
