@@ -522,6 +522,24 @@ def test_exact_mode_long_reductions(g, B, ci, co, d, df, padding):
     assert np.array_equal(yi, ri)
 
 
+@pytest.mark.parametrize("g,B,ci,co,d,df,padding", [
+    ((1, 1, 1), 1, 512, 4, 4, 3, "valid"),   # 3-D halo path: K = 55296 -> 864 accumulation groups
+    ((1, -1), 1, 1900, 3, 5, 3, "same"),     # 2-D halo path: K = 34200
+    ((1, 1), 2, 7, 5, 12, 5, "same"),        # K = 700: groups not aligned with the taps
+    ((1,), 3, 300, 4, 30, 3, "valid"),       # 1-D (per-tap A loads, 1-SM, splitter per stage)
+])
+def test_3xtf32_accumulation_groups(g, B, ci, co, d, df, padding):
+    """3xTF32 drains its TMEM accumulator every 64 reduction elements into fp32
+    registers (x3_drain_groups): the error must not grow with K (one truncating
+    accumulator reached 7e-3 under the reference metric at K = 13824)."""
+    rng = np.random.default_rng(ci + 3)
+    x, f, b, layer, pad = make_conv(rng, g, B, ci, co, d, df, "3xtf32", padding)
+    y = run_dev(M.conv_forward, x, layer)
+    ref = O.conv_ref(x, f, b, g, d, df, pad)
+    e = O.max_rel_error(y, ref, floor=float(np.abs(ref).max()))
+    assert e <= 1e-6 and O.max_rel_error(y, ref) <= 1e-4, (e, O.max_rel_error(y, ref))
+
+
 def test_linear_huge_batch_and_long_reduction():
     """linear_forward on B = 100000 samples (the per-sample absmax grid is 1-D,
     no 65535-sample limit) and a C_in whose reduction exceeds 32000."""
