@@ -43,6 +43,7 @@ static int g_force_tps = CL_ENV("CL_TPS") ? atoi(CL_ENV("CL_TPS")) : 0;  // A/B:
 static bool g_no_bcls = CL_ENV("CL_NO_BCLS") != nullptr;  // A/B: generic basis-inverse picks
 static bool g_no_fused_amax = CL_ENV("CL_NO_FUSED_AMAX") != nullptr;  // A/B: separate absmax pass over y1
 static int g_force_ks = CL_ENV("CL_KS") ? atoi(CL_ENV("CL_KS")) : 0;  // A/B: force the K steps per stage
+static int g_force_hs = CL_ENV("CL_HS") ? atoi(CL_ENV("CL_HS")) : 0;  // A/B: halo slots (2..4)
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -277,7 +278,8 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
       c.halo_bytes = (uint32_t)(pl.hx * pl.hy * pl.hz * ncol * 16 * gs);  // one plane's TMA bytes
       c.a_bytes = (c.halo_bytes + 127u) / 128u * 128u;                     // plane stride (TMA dst alignment)
       c.halo_slot = (uint32_t)(((size_t)pl.n_a * c.a_bytes + 1023) / 1024 * 1024);
-      c.ring_off = (uint32_t)pl.hs * c.halo_slot;
+      c.hs = (g_force_hs >= 2 && g_force_hs <= 4) ? g_force_hs : pl.hs;
+      c.ring_off = (uint32_t)c.hs * c.halo_slot;
       c.stage_bytes = b_cta;
       if (c.ring_off + 2048 >= (size_t)kMaxSmem) continue;
     }
@@ -287,6 +289,7 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
       // (fewer barrier round trips per MMA; bf16 / tf32 stages are short)
       for (int tps : {4, 2}) {
         if (g_force_tps && tps != g_force_tps) continue;
+        if (pl.pair && tps * b_cta / 512 > 256) continue;  // a stage's B half is one TMA box (<= 256 rows)
         if (x3 && ks * tps * 8 > kX3GroupK) continue;  // a stage must not span a 3xTF32 drain
         const int st = (int)((kMaxSmem - 2048 - c.ring_off) / (c.stage_bytes * tps));
         if (st >= (g_force_tps ? 2 : 4)) { c.tps = tps; c.stage_bytes *= tps; break; }
@@ -667,7 +670,7 @@ static int conv_create_impl(const int32_t* g, int k, int sk, int C_in, int C_out
     const cuuint64_t total = (cuuint64_t)pl.n_ntiles * pl.k_iters * pl.b_bytes;
     cuuint64_t bd[2] = {64, total / 512};
     cuuint64_t bst[1] = {512};
-    cuuint32_t bbox[2] = {64, (cuuint32_t)(pl.b_bytes / 2 / 512)};
+    cuuint32_t bbox[2] = {64, (cuuint32_t)((pl.halo ? pl.tps : 1) * pl.b_bytes / 2 / 512)};  // halo: a stage's taps
     cuuint32_t bes[2] = {1, 1};
     CUresult r = enc ? enc(&h->bmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, h->img, bd, bst, bbox, bes,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

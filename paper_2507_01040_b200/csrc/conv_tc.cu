@@ -461,8 +461,21 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               if (dbg_skip(p) & 1) {  // timing experiment: no B loads (results garbage)
                 if (arm) mbar_arrive(&full[stage]);
               } else {
-                if (arm) mbar_arrive_expect_tx(&full[stage], tx_bytes * (uint32_t)nq);
-                for (int i = 0; i < nq; ++i) load_b(nt, (q0 + i) * p.n_gs + gsi, (uint32_t)i * b_cta);
+                // halo plans store each (N tile, channel group, CTA half)'s taps
+                // contiguously (expand.cu): the stage's taps arrive in ONE request
+                // (each TMA request costs its issuing thread ~290 cycles,
+                // tools/probe/tma_rate.cu). Pairs load a fixed box of tps taps
+                // (a short last stage over-reads into the next block; unused).
+                uint8_t* sB = ring + (size_t)stage * p.stage_bytes;
+                const size_t blk = ((size_t)nt * p.n_gs + gsi) * (PAIR ? 2u : 1u) + (PAIR ? (size_t)crank : 0u);
+                const size_t off = (blk * (size_t)nQ + (size_t)q0) * b_cta;
+                if constexpr (PAIR) {
+                  if (arm) mbar_arrive_expect_tx(&full[stage], tx_bytes * (uint32_t)p.tps);
+                  tma_load_2d_cg2(sB, &bmap, &full[stage], 0, (int)(off >> 9));
+                } else {
+                  mbar_arrive_expect_tx(&full[stage], tx_bytes * (uint32_t)nq);
+                  bulk_load(sB, p.b_img + off, b_cta * (uint32_t)nq, &full[stage]);
+                }
               }
               if (++stage == S) { stage = 0; phase ^= 1; }
             }

@@ -86,7 +86,12 @@ __global__ void expand_img_kernel(Sig sg, const float* __restrict__ f, int C_in,
     const int nrow = pl.pair ? pl.n_tile / 2 : pl.n_tile;
     const int half = row / nrow, rr = row % nrow;
     const size_t img_stride = pl.pair ? pl.b_img_bytes / 2 : pl.b_img_bytes;
-    uint8_t* base = img + ((size_t)nt * pl.k_iters + kit) * pl.b_bytes + (size_t)half * (pl.b_bytes / 2);
+    // halo plans: blocks ordered (N tile, channel group, CTA half, tap), so one
+    // CTA's taps of a channel group are contiguous (one load per multi-tap
+    // stage); otherwise (N tile, k_iter) with the two halves inside
+    const size_t b_half = pl.pair ? pl.b_bytes / 2 : pl.b_bytes;
+    uint8_t* base = pl.halo ? img + ((((size_t)nt * pl.n_gs + gsi) * (pl.pair ? 2 : 1) + half) * pl.Q + q) * b_half
+                            : img + ((size_t)nt * pl.k_iters + kit) * pl.b_bytes + (size_t)half * b_half;
     const size_t off = (size_t)s * nrow * 32 + (size_t)h * nrow * 16 + (size_t)rr * 16 + (size_t)e * pl.esize;
     if (pl.prec == kPrecFp32) {
       int8_t d[kDigitsW];
