@@ -177,6 +177,19 @@ __device__ __forceinline__ bool decode_tile(const ConvKParams& p, long long t, i
   return real;
 }
 
+// An epilogue warp hands an accumulator slot back to the MMA warp: one
+// arrival per warp (the barrier counts warps of both CTAs of a pair, on the
+// leader) after every lane's TMEM loads are fenced. Per-thread arrivals had
+// sent 256 remote arrives per slot and CTA over DSMEM.
+template <bool PAIR>
+__device__ __forceinline__ void release_acc(uint64_t* bar) {
+  tc_fence_before();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    if constexpr (PAIR) mbar_arrive_leader(bar); else mbar_arrive(bar);
+  }
+}
+
 // Exact mode with several accumulation groups per tile (reductions longer
 // than kMaxKGroup): drain the first n_groups - 1 groups of this thread's TMEM
 // row into its int64 partial sums, S = L0 2^24 + L1 2^16 + L2 2^8 + L3 per
@@ -208,8 +221,7 @@ __device__ __forceinline__ void drain_groups(const ConvKParams& p, uint64_t* tfu
         scr[c0 + c] = sv;
       }
     }
-    tc_fence_before();
-    if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
+    release_acc<PAIR>(&tempty[acc]);
     if (++acc == slots) { acc = 0; acc_phase ^= 1; }
   }
 }
@@ -254,8 +266,7 @@ __device__ __forceinline__ void x3_drain_groups(const ConvKParams& p, uint64_t* 
       tmem_st_wait();  // the regular epilogue reads this slot next (same thread, same lanes)
       return;
     }
-    tc_fence_before();
-    if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
+    release_acc<PAIR>(&tempty[acc]);
     if (++acc == slots) { acc = 0; acc_phase ^= 1; }
   }
 }
@@ -316,7 +327,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
     }
     for (int a = 0; a < 4; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128 * kEpiGroups * (PAIR ? 2 : 1));  // pair: both CTAs' epilogues, on the leader
+      mbar_init(&tempty[a], 4 * kEpiGroups * (PAIR ? 2 : 1));  // one per epilogue warp of both CTAs, on the leader
     }
     for (int a = 0; a < 4; ++a) {
       mbar_init(&hfull[a], 1);
@@ -1073,8 +1084,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
             }
           }
         }
-        tc_fence_before();
-        if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
+        release_acc<PAIR>(&tempty[acc]);
         if (kDbg && p.dbg_acc && threadIdx.x == 128) {  // timing instrumentation: phase-1 cycles per tile
           atomicAdd(p.dbg_acc, (unsigned long long)(clock64() - dbg_t0));
           atomicAdd(p.dbg_acc + 1, 1ull);
@@ -1329,8 +1339,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           for (int c = 0; c < 16; ++c) cur[c] = nxt[c];
         }
       }
-      tc_fence_before();
-      if constexpr (PAIR) mbar_arrive_leader(&tempty[acc]); else mbar_arrive(&tempty[acc]);
+      release_acc<PAIR>(&tempty[acc]);
       if (kDbg && p.dbg_acc && threadIdx.x == 128) {  // timing instrumentation: epilogue cycles per tile
         atomicAdd(p.dbg_acc, (unsigned long long)(clock64() - dbg_t0));
         atomicAdd(p.dbg_acc + 1, 1ull);
