@@ -621,6 +621,14 @@ def run_ours(args):
     # sustained (power-capped, ~1.3-1.4 GHz) figure is reported beside it.
     peak_sust = exec_peak / gemm_ratio
     peak = exec_peak_burst / gemm_ratio
+    # The roofline's peak is MEASURED_PEAKS.json's dense bf16 burst figure, in
+    # this mode's ALGORITHMIC units: the bf16-dense-equivalent MMA work the kernel
+    # executes per algorithmic FLOP (x0.5 under the M2(C) change of basis; an
+    # int8 MMA runs at 2x, a tf32 MMA at 1/2x the bf16 rate; fp32 mode = 10 int8
+    # digit-pair MMAs, 3xtf32 = 3 tf32 MMAs per product) divides it.
+    work_per_alg = gemm_ratio * BF16_EQUIV[prec]
+    peak_mp = peaks["bf16_tflops"] / work_per_alg
+    peak_mp_sust = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / work_per_alg
     conv_share = (t_conv * (2 if spec.kind == "block" else 1)) / (t_step)
 
     # ---- end to end through the public API with pinned HOST buffers ----
@@ -667,13 +675,21 @@ def run_ours(args):
             "data": "synthetic (seeded, BASELINE.json distributions; inputs generated on device)",
             "config": arm_config(spec, args, world),
             "tflops": flops_per_sample * spec.B / t_step / 1e12,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(spec, prec, conv_layer.dims.B),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_mp, "unit": "TFLOP/s",
+                         "frac": achieved / peak_mp, "traffic": ncu_traffic(spec, prec, conv_layer.dims.B),
                          "kernel": ("conv_tc_kernel: the block's conv2 launch with its fused residual"
                                     if spec.kind == "block" else "conv_tc_kernel"),
-                         "peak_basis": f"{prec}: {peak_basis}" + (
-                             "; x2 algorithmic/executed (M2(C) change of basis, SURVEY 8f f4)" if basis_on else ""),
-                         "frac_of_sustained": achieved / peak_sust,
+                         "peak_basis": (f"MEASURED_PEAKS.json bf16 dense {peak_kind} burst {peaks['bf16_tflops']:.1f} "
+                                        f"TF/s / {work_per_alg:g} bf16-equivalent MMA FLOP per algorithmic FLOP "
+                                        f"({prec}" + (", x0.5 under the M2(C) change of basis" if basis_on else "")
+                                        + "); achieved = conv_flops (conv.py:384-387) / event-timed launch"),
+                         "frac_of_sustained": achieved / peak_mp_sust,
+                         # the same kernel against the measured cuBLAS peak of its own MMA kind
+                         # (profiles/r01_mode_peaks.json; the round-1 primary denominator)
+                         "vs_mode_peak": {"peak": peak, "frac": achieved / peak,
+                                          "frac_of_sustained": achieved / peak_sust,
+                                          "basis": f"{prec}: {peak_basis}" + (
+                                              "; x2 algorithmic/executed (M2(C) change of basis)" if basis_on else "")},
                          "executed_tflops": achieved * gemm_ratio, "executed_peak": exec_peak_burst,
                          "executed_frac": achieved * gemm_ratio / exec_peak_burst,
                          "executed_frac_of_nominal": achieved * gemm_ratio / NOMINAL_MODE_PEAK[prec],
