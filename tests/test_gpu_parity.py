@@ -540,6 +540,22 @@ def test_3xtf32_accumulation_groups(g, B, ci, co, d, df, padding):
     assert e <= 1e-6 and O.max_rel_error(y, ref) <= 1e-4, (e, O.max_rel_error(y, ref))
 
 
+@pytest.mark.parametrize("prec", ["bf16", "tf32", "3xtf32", "fp32"])
+@pytest.mark.parametrize("df,ci,co,d", [(5, 20, 70, 7), (2, 12, 9, 6), (3, 64, 72, 5), (4, 3, 33, 6)])
+def test_halo_multi_tap_stages(prec, df, ci, co, d):
+    """3-D halo plans store each CTA's taps of a channel group contiguously and
+    load a multi-tap B stage as ONE request (a pair's box always covers tps
+    taps; a short last stage over-reads into the next block or past the end of
+    the image, zero-filled): tap counts not divisible by the taps per stage
+    (Q = 125, 8, 27, 64), several channel groups and several N tiles."""
+    rng = np.random.default_rng(df * 100 + ci)
+    g = (1, 1, 1)
+    padding = "same" if df % 2 else "valid"  # same padding needs an odd filter (conv.py)
+    x, f, b, layer, pad = make_conv(rng, g, 2, ci, co, d, df, prec, padding)
+    y = run_dev(M.conv_forward, x, layer)
+    assert_conv_close(y, O.conv_ref(x, f, b, g, d, df, pad), prec, K=ci * 8 * df ** 3)
+
+
 def test_linear_huge_batch_and_long_reduction():
     """linear_forward on B = 100000 samples (the per-sample absmax grid is 1-D,
     no 65535-sample limit) and a C_in whose reduction exceeds 32000."""
