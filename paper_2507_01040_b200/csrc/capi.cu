@@ -21,6 +21,11 @@ namespace cl {
 
 static thread_local std::string g_last_error;
 static thread_local bool g_time_kernel_only = false;  // cl_conv_time_kernel: skip operand preparation
+// integer A/B switch (0 when unset; always 0 in the production build)
+static int env_int(const char* name) {
+  const char* v = CL_ENV(name);
+  return v ? atoi(v) : 0;
+}
 static bool g_no_pair = CL_ENV("CL_NO_PAIR") != nullptr || CL_ENV("CL_NO_CLUSTER") != nullptr;  // A/B: 1-SM MMA
 static bool g_no_basis = CL_ENV("CL_NO_BASIS") != nullptr;      // A/B: disable the change of basis
 static bool g_basis_2d = CL_ENV("CL_BASIS_2D") != nullptr;      // A/B: enable it for 2-D layers (all modes)
@@ -39,11 +44,11 @@ static bool use_basis(int sk, int k, int precision) {
 static bool g_no_halo = CL_ENV("CL_NO_HALO") != nullptr;        // A/B: disable halo reuse of the A tile
 static bool g_no_halo_i8 = CL_ENV("CL_NO_HALO_I8") != nullptr;  // A/B: halo off for the int8 mode only
 static bool g_no_tma_merge = CL_ENV("CL_NO_TMA_MERGE") != nullptr;  // A/B: one TMA line per pixel
-static int g_force_tps = CL_ENV("CL_TPS") ? atoi(CL_ENV("CL_TPS")) : 0;  // A/B: taps per stage (halo)
+static int g_force_tps = env_int("CL_TPS");  // A/B: taps per stage (halo)
 static bool g_no_bcls = CL_ENV("CL_NO_BCLS") != nullptr;  // A/B: generic basis-inverse picks
 static bool g_no_fused_amax = CL_ENV("CL_NO_FUSED_AMAX") != nullptr;  // A/B: separate absmax pass over y1
-static int g_force_ks = CL_ENV("CL_KS") ? atoi(CL_ENV("CL_KS")) : 0;  // A/B: force the K steps per stage
-static int g_force_hs = CL_ENV("CL_HS") ? atoi(CL_ENV("CL_HS")) : 0;  // A/B: halo slots (2..4)
+static int g_force_ks = env_int("CL_KS");  // A/B: force the K steps per stage
+static int g_force_hs = env_int("CL_HS");  // A/B: halo slots (2..4)
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
@@ -983,7 +988,7 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
   p.pair = pl.pair;
   p.cs = pl.pair ? 2 : 1;
   p.num_tiles = ((p.num_m_tiles + p.cs - 1) / p.cs) * p.cs * p.n_ntiles;
-  static const int dbg_skip = CL_ENV("CL_DBG_SKIP") ? atoi(CL_ENV("CL_DBG_SKIP")) : 0;
+  static const int dbg_skip = env_int("CL_DBG_SKIP");
   p.dbg_skip = dbg_skip;
   p.d_filter = h->d_filter;
   p.n_gs = pl.n_gs;

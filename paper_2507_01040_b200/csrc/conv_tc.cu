@@ -290,7 +290,6 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   // A row-group bytes: packed 16-byte groups for bf16 / int8 digits / 1-D,
   // otherwise one protocol multivector (16 B in 2-D, 32 B in 3-D)
   constexpr int RB = (PREC == kPrecBf16 || kInt8 || NB == 2) ? 16 : NB * 4;
-  constexpr uint32_t kLayoutA = (RB == 32) ? kSwizzle32B : kSwizzleNone;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
