@@ -1072,9 +1072,10 @@ static int conv_run(const cl_conv* h, const float* x, const __nv_bfloat16* xbf, 
     fprintf(stderr,
             "[CL_DBG_CLK] epilogue phase-1 %.0f cyc/tile (%llu tiles); MMA warp per tile: %.0f cyc, waits: accumulator "
             "%.0f, halo %.0f, operand stages %.0f; producer per tile: empty-stage waits %.0f, halo-slot waits %.0f; "
-            "CTA finish spread %.1f us\n",
+            "CTA finish spread %.1f us; 3xTF32 drain %.0f cyc/group\n",
             h[1] ? (double)h[0] / h[1] : 0.0, h[1], h[8] / mt, h[2] / mt, h[4] / mt, h[5] / mt,
-            h[9] / (2.0 * mt), h[10] / (2.0 * mt), (double)(h[6] - ~h[7]) * 1e-3);
+            h[9] / (2.0 * mt), h[10] / (2.0 * mt), (double)(h[6] - ~h[7]) * 1e-3,
+            h[12] ? (double)h[11] / h[12] : 0.0);
   }
   if (e != cudaSuccess) return cuda_fail(e, "conv_tc launch");
   if (pl.prec == kPrecFp32 && prep && y && x) {

@@ -245,6 +245,7 @@ __device__ __forceinline__ void x3_drain_groups(const ConvKParams& p, uint64_t* 
   for (int grp = 0; grp < p.n_groups; ++grp) {
     mbar_wait_sleep(&tfull[acc], acc_phase, 20);
     tc_fence_after();
+    const long long dbg_d0 = (kDbg && p.dbg_acc) ? clock64() : 0;
     const uint32_t ta = lane_base + (uint32_t)acc * slot_cols;
     const bool last = grp + 1 == p.n_groups;
 #pragma unroll
@@ -267,6 +268,10 @@ __device__ __forceinline__ void x3_drain_groups(const ConvKParams& p, uint64_t* 
       return;
     }
     release_acc<PAIR>(&tempty[acc]);
+    if (kDbg && p.dbg_acc && threadIdx.x == 128) {  // timing instrumentation: drain cycles per group
+      atomicAdd(p.dbg_acc + 11, (unsigned long long)(clock64() - dbg_d0));
+      atomicAdd(p.dbg_acc + 12, 1ull);
+    }
     if (++acc == slots) { acc = 0; acc_phase ^= 1; }
   }
 }
