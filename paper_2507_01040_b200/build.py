@@ -32,6 +32,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", f"-I{ROOT}/include", "-Xptxas", "-v"]
+# extra -D switches for A/B builds of tools/ (e.g. CL_NVCC_DEFS="-DCL_X3_EPI_GROUPS=3"); empty in the product build
+FLAGS += os.environ.get("CL_NVCC_DEFS", "").split()
 
 
 def sources():

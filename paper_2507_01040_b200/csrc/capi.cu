@@ -235,10 +235,11 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
   pl.n_a = i8 ? kDigitsA : pl.n_img;
   pl.n_tma_a = i8 ? kDigitsA : 1;
   pl.levels = i8 ? kLevels : 1;
-  // 3xTF32 drains its accumulator every kX3GroupK reduction elements into
-  // fp32 registers (accumulation groups): 4 rotating 128-column slots
+  // 3xTF32 drains its A_hi*B_hi accumulator every kX3GroupK reduction elements
+  // into fp32 registers (accumulation groups): kX3HiSlots rotating 128-column
+  // slots, then the tile-long accumulator of the cross terms
   const bool x3 = prec == kPrec3xTf32;
-  pl.acc_slots = i8 ? 1 : (x3 ? 4 : 2);
+  pl.acc_slots = i8 ? 1 : (x3 ? kX3HiSlots : 2);  // 3xTF32: + the lo accumulator behind them
   const int max_tile = (i8 || x3) ? 128 : 256;  // levels x n_tile x slots <= 512 TMEM columns
   pl.N = C_out * wk;
   pl.n_ntiles = (pl.N + max_tile - 1) / max_tile;
@@ -331,7 +332,7 @@ static bool plan_conv_impl(int k, int nb, int prec, int C_in, int C_out, int d_o
     pl.drain = std::max(1, kX3GroupK / k_stage);
   }
   pl.n_groups = (pl.stages_per_tile + pl.drain - 1) / pl.drain;
-  pl.tmem_cols = (uint32_t)std::max(32, pow2_at_least(pl.levels * pl.n_tile * pl.acc_slots));
+  pl.tmem_cols = (uint32_t)std::max(32, pow2_at_least(pl.levels * pl.n_tile * (pl.acc_slots + (x3 ? 1 : 0))));
   // + 1024 alignment slack + the barrier area (3 x 8 stage barriers, 10 accumulator / halo
   // barriers, the TMEM slot, the 8-deep tile ring: 472 B; within the 2048 B reserve above)
   pl.smem_bytes = (size_t)pl.ring_off + (size_t)pl.stages * pl.stage_bytes + 1024 + 768;

@@ -748,44 +748,51 @@ __device__ __forceinline__ void mma_stage_e(uint32_t d, uint32_t a_lo, uint32_t 
     else asm volatile(CL_MMA_E_HEAD "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n\t" CL_MMA_E_NEXT "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, 1;\n}" CL_MMA_E_ARGS);
   }
 }
-// 3xTF32: KS K steps of 3 tf32 MMAs each, D += A_lo*B_hi + A_hi*B_lo + A_hi*B_hi
-// (the lo images sit a_img / b_img 16-byte units after the hi ones); same
-// issue conventions as mma_stage_e. acc0 applies to the first MMA only.
+// 3xTF32: KS K steps of 3 tf32 MMAs each: the cross terms A_lo*B_hi + A_hi*B_lo
+// go to the tile-long lo accumulator d_lo, A_hi*B_hi to the group slot d
+// (kX3GroupK, internal.h; the lo images sit a_img / b_img 16-byte units after
+// the hi ones); same issue conventions as mma_stage_e. acc0 / acc_lo0 = the
+// accumulate flags of the first hi / first lo MMA.
 #define CL_X3_HEAD                                                                                       \
-  "{\n\t.reg .pred e, p;\n\t.reg .b32 al, bl, t;\n\t.reg .b64 da, db, dl;\n\t"                           \
-  "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %6, 0;\n\tmov.b32 al, %1;\n\tmov.b32 bl, %3;\n\t"
-#define CL_X3_STEP(CGS, ACC)                                                                             \
+  "{\n\t.reg .pred e, p, q;\n\t.reg .b32 al, bl, t;\n\t.reg .b64 da, db, dl;\n\t"                        \
+  "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %6, 0;\n\tsetp.ne.b32 q, %12, 0;\n\t"                   \
+  "mov.b32 al, %1;\n\tmov.b32 bl, %3;\n\t"
+#define CL_X3_STEP(CGS, ACC, ACCL)                                                                       \
   "add.u32 t, al, %9;\n\tmov.b64 dl, {t, %2};\n\tmov.b64 db, {bl, %4};\n\t"                                \
-  "@e tcgen05.mma.cta_group::" CGS ".kind::tf32 [%0], dl, db, %5, " ACC ";\n\t"                             \
+  "@e tcgen05.mma.cta_group::" CGS ".kind::tf32 [%11], dl, db, %5, " ACCL ";\n\t"                          \
   "add.u32 t, bl, %10;\n\tmov.b64 da, {al, %2};\n\tmov.b64 dl, {t, %4};\n\t"                               \
-  "@e tcgen05.mma.cta_group::" CGS ".kind::tf32 [%0], da, dl, %5, 1;\n\t"                                   \
-  "@e tcgen05.mma.cta_group::" CGS ".kind::tf32 [%0], da, db, %5, 1;\n\t"                                   \
+  "@e tcgen05.mma.cta_group::" CGS ".kind::tf32 [%11], da, dl, %5, 1;\n\t"                                  \
+  "@e tcgen05.mma.cta_group::" CGS ".kind::tf32 [%0], da, db, %5, " ACC ";\n\t"                             \
   "add.u32 al, al, %7;\n\tadd.u32 bl, bl, %8;\n\t"
 #define CL_X3_ARGS                                                                                        \
   ::"r"(d), "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc0), "r"(a_step), "r"(b_step), \
-      "r"(a_img), "r"(b_img)                                                                               \
+      "r"(a_img), "r"(b_img), "r"(d_lo), "r"(acc_lo0)                                                      \
       : "memory"
 template <int CG, int KS>
-__device__ __forceinline__ void mma_stage_x3_e(uint32_t d, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
-                                               uint32_t idesc, uint32_t acc0, uint32_t a_step, uint32_t b_step,
-                                               uint32_t a_img, uint32_t b_img) {
+__device__ __forceinline__ void mma_stage_x3_e(uint32_t d, uint32_t d_lo, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                               uint32_t b_hi, uint32_t idesc, uint32_t acc0, uint32_t acc_lo0,
+                                               uint32_t a_step, uint32_t b_step, uint32_t a_img, uint32_t b_img) {
   static_assert(KS == 1 || KS == 2 || KS == 4 || KS == 8, "K steps per stage");
   if constexpr (CG == 2) {
-    if constexpr (KS == 1) asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p") "}" CL_X3_ARGS);
-    else if constexpr (KS == 2) asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p") CL_X3_STEP("2", "1") "}" CL_X3_ARGS);
+    if constexpr (KS == 1) asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p", "q") "}" CL_X3_ARGS);
+    else if constexpr (KS == 2) asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p", "q") CL_X3_STEP("2", "1", "1") "}" CL_X3_ARGS);
     else if constexpr (KS == 4)
-      asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") "}" CL_X3_ARGS);
+      asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p", "q") CL_X3_STEP("2", "1", "1") CL_X3_STEP("2", "1", "1")
+                       CL_X3_STEP("2", "1", "1") "}" CL_X3_ARGS);
     else
-      asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1")
-                       CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") CL_X3_STEP("2", "1") "}" CL_X3_ARGS);
+      asm volatile(CL_X3_HEAD CL_X3_STEP("2", "p", "q") CL_X3_STEP("2", "1", "1") CL_X3_STEP("2", "1", "1")
+                       CL_X3_STEP("2", "1", "1") CL_X3_STEP("2", "1", "1") CL_X3_STEP("2", "1", "1")
+                       CL_X3_STEP("2", "1", "1") CL_X3_STEP("2", "1", "1") "}" CL_X3_ARGS);
   } else {
-    if constexpr (KS == 1) asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p") "}" CL_X3_ARGS);
-    else if constexpr (KS == 2) asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p") CL_X3_STEP("1", "1") "}" CL_X3_ARGS);
+    if constexpr (KS == 1) asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p", "q") "}" CL_X3_ARGS);
+    else if constexpr (KS == 2) asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p", "q") CL_X3_STEP("1", "1", "1") "}" CL_X3_ARGS);
     else if constexpr (KS == 4)
-      asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") "}" CL_X3_ARGS);
+      asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p", "q") CL_X3_STEP("1", "1", "1") CL_X3_STEP("1", "1", "1")
+                       CL_X3_STEP("1", "1", "1") "}" CL_X3_ARGS);
     else
-      asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1")
-                       CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") CL_X3_STEP("1", "1") "}" CL_X3_ARGS);
+      asm volatile(CL_X3_HEAD CL_X3_STEP("1", "p", "q") CL_X3_STEP("1", "1", "1") CL_X3_STEP("1", "1", "1")
+                       CL_X3_STEP("1", "1", "1") CL_X3_STEP("1", "1", "1") CL_X3_STEP("1", "1", "1")
+                       CL_X3_STEP("1", "1", "1") CL_X3_STEP("1", "1", "1") "}" CL_X3_ARGS);
   }
 }
 #undef CL_X3_HEAD

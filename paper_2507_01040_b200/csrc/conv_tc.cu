@@ -22,8 +22,10 @@
 //   warps 12-15 3xTF32 splitter: A -> (A_hi, A_lo) in shared memory (the
 //               3xTF32 kernel has 512 threads: epilogue warps 4-11)
 //
-// 3xTF32: D += A_lo*B_hi + A_hi*B_lo + A_hi*B_hi with hi = fp32 with the 13
-// low mantissa bits cleared (exactly representable in tf32) and lo = x - hi.
+// 3xTF32: D = (A_lo*B_hi + A_hi*B_lo) + A_hi*B_hi with hi = x rounded to
+// nearest tf32 and lo = x - hi rounded to tf32. The cross terms accumulate in
+// their own TMEM accumulator over the whole tile; A_hi*B_hi in rotating
+// group slots drained into fp32 registers (x3_drain_groups, kX3GroupK).
 #include <type_traits>
 
 #include "common.cuh"
@@ -227,20 +229,23 @@ __device__ __forceinline__ void drain_groups(const ConvKParams& p, uint64_t* tfu
 }
 
 // 3xTF32 accumulation groups: the MMA warp rotates `slots` TMEM slots, one
-// group of kX3GroupK reduction elements each. This thread drains the first
-// n_groups - 1 groups of its row (columns [c_beg, c_end), <= 64) into fp32
-// registers with round-to-nearest adds, then adds the sums into the last
-// group's slot in TMEM (tcgen05.st) and returns with that slot full, so the
-// regular epilogue reads the complete accumulator. (The tensor core's fp32
+// group of kX3GroupK reduction elements of A_hi*B_hi each, and accumulates the
+// cross terms of the whole tile in the lo accumulator behind them. This thread
+// drains the first n_groups - 1 groups of its row (columns [c_beg, c_end))
+// into fp32 registers with round-to-nearest adds, then adds the sums and the
+// lo accumulator into the last group's slot in TMEM (tcgen05.st), hands the
+// lo accumulator back and returns with that slot full, so the regular
+// epilogue reads the complete accumulator. (The tensor core's fp32
 // accumulation truncates; over K = 13824 its error reached 7e-3 under the
 // reference metric, profiles/r02_3xtf32_drain_study.txt.)
 template <bool PAIR>
 __device__ __forceinline__ void x3_drain_groups(const ConvKParams& p, uint64_t* tfull, uint64_t* tempty,
                                                 uint32_t tmem_base, int ew, int c_beg, int c_end, uint32_t slot_cols,
                                                 int slots, int& acc, uint32_t& acc_phase) {
-  float sm[64];
+  constexpr int kCh = (128 / kX3EpiGroups + 15) / 16;  // 16-column chunks of this thread's share
+  float sm[16 * kCh];
 #pragma unroll
-  for (int i = 0; i < 64; ++i) sm[i] = 0.f;
+  for (int i = 0; i < 16 * kCh; ++i) sm[i] = 0.f;
   const uint32_t lane_base = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)c_beg;
   for (int grp = 0; grp < p.n_groups; ++grp) {
     mbar_wait_sleep(&tfull[acc], acc_phase, 20);
@@ -249,9 +254,15 @@ __device__ __forceinline__ void x3_drain_groups(const ConvKParams& p, uint64_t* 
     const uint32_t ta = lane_base + (uint32_t)acc * slot_cols;
     const bool last = grp + 1 == p.n_groups;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kCh; ++j) {
       if (c_beg + 16 * j >= c_end) break;
       uint32_t r[16];
+      if (last) {  // the tile's cross terms first (one register buffer: two in flight spilled)
+        tmem_ld16(lane_base + (uint32_t)kX3HiSlots * slot_cols + (uint32_t)(16 * j), r);
+        tmem_ld_wait_dep16(r);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sm[16 * j + i] += __uint_as_float(r[i]);
+      }
       tmem_ld16(ta + (uint32_t)(16 * j), r);
       tmem_ld_wait_dep16(r);
       if (!last) {
@@ -264,6 +275,7 @@ __device__ __forceinline__ void x3_drain_groups(const ConvKParams& p, uint64_t* 
       }
     }
     if (last) {
+      release_acc<PAIR>(&tempty[kX3HiSlots]);  // lo accumulator read: the next tile may overwrite it
       tmem_st_wait();  // the regular epilogue reads this slot next (same thread, same lanes)
       return;
     }
@@ -291,7 +303,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   // epilogue warp groups: warps 4-7, plus warps 8-11 when they are not the
   // 3xTF32 splitter (each group drains half of the accumulator columns)
   // (3xTF32: warps 4-11, the splitter is warps 12-15)
-  constexpr int kEpiGroups = kSplit ? 2 : (conv_threads(PREC, NB) == 640 ? 4 : 2);
+  constexpr int kEpiGroups = kSplit ? kX3EpiGroups : (conv_threads(PREC, NB) == 640 ? 4 : 2);
   // A row-group bytes: packed 16-byte groups for bf16 / int8 digits / 1-D,
   // otherwise one protocol multivector (16 B in 2-D, 32 B in 3-D)
   constexpr int RB = (PREC == kPrecBf16 || kInt8 || NB == 2) ? 16 : NB * 4;
@@ -565,6 +577,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
     // reductions (ConvPlan::drain).
     uint32_t d_tmem = 0;
     int sg = 0;  // stage index inside the current group
+    // 3xTF32: the tile-long accumulator of the cross terms (behind the hi slots)
+    const uint32_t d_lo = tmem_base + (uint32_t)kX3HiSlots * slot_cols;
+    uint32_t lo_phase = 0;
     auto group_begin = [&]() {
       const long long dbg_w0 = (kDbg && p.dbg_acc) ? clock64() : 0;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -592,6 +607,11 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       // stage and phase value to vector registers (R2UR before each MMA)
       if (__reduce_min_sync(0xffffffffu, sched_read(it, false) < 0 ? -1 : 0) < 0) break;
       group_begin();
+      if constexpr (kSplit) {  // the previous tile's lo accumulator has been read by every epilogue warp
+        mbar_wait(&tempty[kX3HiSlots], lo_phase ^ 1);
+        tc_fence_after();
+        lo_phase ^= 1;
+      }
       if constexpr (!kInt8) {
         if (p.halo) {
           // bf16 / tf32 / 3xTF32 halo mode: lean warp-converged issue. All
@@ -609,17 +629,17 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           const uint32_t a_ks = (uint32_t)a_kstep;
           const long long dbg_t0 = (kDbg && p.dbg_acc) ? clock64() : 0;
           // one filter tap's KS K steps at (a, b)
-          auto tap_mmas = [&](auto ks_c, uint32_t a, uint32_t b, uint32_t accf) {
+          auto tap_mmas = [&](auto ks_c, uint32_t a, uint32_t b, uint32_t accf, uint32_t accl) {
             constexpr int KS = decltype(ks_c)::value;
             if constexpr (kSplit)
-              mma_stage_x3_e<CG, KS>(d_tmem, a, a_hi, b, b_hi, idesc, accf, a_ks, b_ks4, h_img4, b_img4);
+              mma_stage_x3_e<CG, KS>(d_tmem, d_lo, a, a_hi, b, b_hi, idesc, accf, accl, a_ks, b_ks4, h_img4, b_img4);
             else
               mma_stage_e<PREC == kPrecBf16 ? 1 : 2, CG, KS>(d_tmem, a, a_hi, b, b_hi, idesc, accf, a_ks, b_ks4);
           };
           auto run = [&](auto ks_c, auto tps_c) {
             constexpr int TPS = decltype(tps_c)::value;  // 0: runtime p.tps
             const int tps = TPS ? TPS : p.tps;
-            uint32_t accf = 0;
+            uint32_t accf = 0, accl = 0;  // accumulate flags: hi slot (per group), lo accumulator (per tile)
             uint32_t b_cur = b_base + (uint32_t)stage * stg4;
             for (int gsi = 0; gsi < p.n_gs; ++gsi) {
               const long long dbg_h0 = (kDbg && p.dbg_acc) ? clock64() : 0;
@@ -636,8 +656,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 tc_fence_after();
                 uint32_t b0 = b_cur;
                 for (int i = 0; i < nq; ++i) {
-                  tap_mmas(ks_c, a_cur, b0, accf);
+                  tap_mmas(ks_c, a_cur, b0, accf, accl);
                   accf = 1u;
+                  accl = 1u;
                   b0 += b_cta4;
                   a_cur += h_dx;
                   if (++qx == df) {
@@ -845,9 +866,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 mma_i8_kstep(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, first ? 0u : 1u, a_img4, b_img4,
                              (uint32_t)p.n_tile);
             } else if constexpr (kSplit) {
-              mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0 + a_img4, a_hi, b0, b_hi, idesc, first ? 0u : 1u);  // A_lo * B_hi
-              mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0, a_hi, b0 + b_img4, b_hi, idesc, 1u);              // A_hi * B_lo
-              mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, 1u);                       // A_hi * B_hi
+              const uint32_t lo_first = (kit == 0 && s == 0) ? 0u : 1u;  // the tile's first cross-term MMA overwrites
+              mma_mode_s<kPrecTf32, PAIR>(1u, d_lo, a0 + a_img4, a_hi, b0, b_hi, idesc, lo_first);         // A_lo * B_hi
+              mma_mode_s<kPrecTf32, PAIR>(1u, d_lo, a0, a_hi, b0 + b_img4, b_hi, idesc, 1u);               // A_hi * B_lo
+              mma_mode_s<kPrecTf32, PAIR>(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, first ? 0u : 1u);         // A_hi * B_hi
             } else {
               mma_mode_s<PREC, PAIR>(1u, d_tmem, a0, a_hi, b0, b_hi, idesc, first ? 0u : 1u);
             }
@@ -933,7 +955,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       if constexpr (kInt8) if (valid) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
       if constexpr (kInt8 && GROUPS)  // exact mode, several accumulation groups per tile
         drain_groups<PAIR>(p, tfull, tempty, tmem_base, ew, row, c_beg, c_end, slot_cols, slots, acc, acc_phase);
-      if (kSplit && p.n_groups > 1)  // returns with the last group's slot full and complete
+      if constexpr (kSplit)  // returns with the last group's slot full and complete (lo accumulator added)
         x3_drain_groups<PAIR>(p, tfull, tempty, tmem_base, ew, c_beg, c_end, slot_cols, slots, acc, acc_phase);
       else
         mbar_wait_sleep(&tfull[acc], acc_phase, 64);  // off the critical path: poll gently
@@ -1350,10 +1372,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       }
       if (++acc == slots) { acc = 0; acc_phase ^= 1; }
     }
-  } else if (warp >= 12) {
+  } else if (warp >= 4 + 4 * kEpiGroups) {
     // ===================== 3xTF32 splitter =====================
     if constexpr (kSplit) {
-      const int tid = threadIdx.x - 384;
+      const int tid = threadIdx.x - 32 * (4 + 4 * kEpiGroups);
       auto split = [&](uint8_t* buf, uint32_t bytes, uint32_t lo_off) {
         uint4* a = reinterpret_cast<uint4*>(buf);
         float4* lo = reinterpret_cast<float4*>(buf + lo_off);

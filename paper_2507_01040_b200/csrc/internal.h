@@ -37,10 +37,19 @@ constexpr int kTileM = 128;          // GEMM rows per tile (= TMEM lanes)
 // |L| <= 4 * 2^14 * K < 2^31 for K <= 32000 (s32 TMEM accumulators).
 constexpr int kMaxKGroup = 32000;
 // 3xTF32: reduction elements per accumulation group. The tensor core's fp32
-// accumulation truncates, so its error grows with the chain length; draining
-// every 64 elements into fp32 registers (round-to-nearest sums) keeps
-// max_rel_error(floor 1e-2) <= 1e-4 at K = 13824 (profiles/r02_3xtf32_drain_study.txt)
-constexpr int kX3GroupK = 64;
+// accumulation truncates, so its error grows with the number of MMAs chained
+// into one accumulator. Two measures keep max_rel_error(floor 1e-2) <= 1e-4
+// at K = 13824 (profiles/r02_3xtf32_drain_study.txt):
+//  * the cross terms A_lo*B_hi + A_hi*B_lo (2^-11 of the product) accumulate
+//    over the whole tile in their OWN TMEM accumulator (the "lo" slot), so
+//    their truncation is 2^-11 smaller and they never truncate the main sum;
+//  * the A_hi*B_hi accumulator is drained every kX3GroupK elements
+//    (kX3GroupK / 8 chained MMAs) into fp32 registers (round-to-nearest sums).
+#ifndef CL_X3_GROUP_K
+#define CL_X3_GROUP_K 192
+#endif
+constexpr int kX3GroupK = CL_X3_GROUP_K;
+constexpr int kX3HiSlots = 3;  // rotating A_hi*B_hi slots; the 4th 128-column slot is the lo accumulator
 
 // Change of basis (basis.cu): x' = T x splits the conv into ncol independent
 // GEMMs sharing a w x w filter; T rows = (column, component), entries +-1/0,
@@ -102,8 +111,12 @@ constexpr int kConvThreads = 384;    // 12 warps, see conv_tc.cu
 // (their 3-D epilogue spills at 96 registers) and 3xTF32 (warps 8-11 split A)
 // 3xTF32 (prec 3): 16 warps = two epilogue groups (they hold the drained
 // partial sums in registers) + the splitter group
+#ifndef CL_X3_EPI_GROUPS
+#define CL_X3_EPI_GROUPS 2
+#endif
+constexpr int kX3EpiGroups = CL_X3_EPI_GROUPS;  // 3xTF32 epilogue warp groups (each drains 128 / groups columns)
 constexpr int conv_threads(int prec, int nb) {
-  return prec == 3 ? 512 : ((prec == 0 || nb <= 4) ? 640 : kConvThreads);
+  return prec == 3 ? 128 * (2 + kX3EpiGroups) : ((prec == 0 || nb <= 4) ? 640 : kConvThreads);
 }
 constexpr int kMaxSmem = 232448;     // 227 KB opt-in dynamic shared memory per CTA
 

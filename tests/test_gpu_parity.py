@@ -49,7 +49,7 @@ def assert_conv_close(y, ref, prec, K=0):
     """fp32 and 3xTF32 are the FP32-accurate modes. fp32 (exact int8-digit
     accumulation) meets the reference metric (max_rel_error, floor 1e-2,
     bench.py:74-88) <= 1e-4 everywhere. 3xTF32 drains its tensor-core
-    accumulator every 64 reduction elements into fp32 registers (DESIGN.md
+    A_hi*B_hi accumulator every 192 reduction elements into fp32 registers (DESIGN.md
     "3xTF32 accumulation groups"), so its error no longer grows with K:
     normwise <= 2e-6 (fp32-class; measured 1e-7 .. 4e-7). The floor-1e-2
     metric is absolute near zero, so for fp32-class arithmetic it scales with
@@ -529,8 +529,9 @@ def test_exact_mode_long_reductions(g, B, ci, co, d, df, padding):
     ((1,), 3, 300, 4, 30, 3, "valid"),       # 1-D (per-tap A loads, 1-SM, splitter per stage)
 ])
 def test_3xtf32_accumulation_groups(g, B, ci, co, d, df, padding):
-    """3xTF32 drains its TMEM accumulator every 64 reduction elements into fp32
-    registers (x3_drain_groups): the error must not grow with K (one truncating
+    """3xTF32 drains its A_hi*B_hi TMEM accumulator every 192 reduction elements
+    into fp32 registers and keeps the cross terms in their own tile-long
+    accumulator (x3_drain_groups): the error must not grow with K (one truncating
     accumulator reached 7e-3 under the reference metric at K = 13824)."""
     rng = np.random.default_rng(ci + 3)
     x, f, b, layer, pad = make_conv(rng, g, B, ci, co, d, df, "3xtf32", padding)
