@@ -922,6 +922,13 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       inv_os[j] = first_own ? p.bs.inv_sgn[t % 8][0] : p.bs.inv_sgn[t % 8][1];
       inv_ps[j] = first_own ? p.bs.inv_sgn[t % 8][1] : p.bs.inv_sgn[t % 8][0];
     }
+    // the same signs as +-1 multipliers (fp32-accumulator epilogue: one FMUL / FFMA per term)
+    float sgn_o[WL], sgn_p[WL];
+#pragma unroll
+    for (int j = 0; j < WL; ++j) {
+      sgn_o[j] = inv_os[j] > 0 ? 1.f : -1.f;
+      sgn_p[j] = inv_ps[j] > 0 ? 1.f : -1.f;
+    }
     const int lx = prow % p.tx, ly = (prow / p.tx) % p.ty, lz = prow / (p.tx * p.ty);
     const int d_out = p.d_out;
     const long long P_out = (p.k == 3) ? (long long)d_out * d_out * d_out
@@ -1252,28 +1259,73 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         if (p.bs.on) {
           if constexpr (NB >= 4) {
             // change of basis: lane (column bcol) produces blades bcol*W + j as
-            // (s_o own[o_j] + s_p partner[p_j]) / 2; the gate sums over both lanes
+            // (s_o own[o_j] + s_p partner[p_j]) / 2; the gate sums over both lanes.
+            // This loop had been instruction bound (ncu: ~640 issued instructions per
+            // 16-column chunk and warp, 13.6 K cycles per cfg4 bf16 tile against 13.8 K
+            // of MMAs): the signs are +-1 multipliers held in registers, bias and gate
+            // weights one vector load per channel, the gate code sits behind one
+            // warp-uniform branch, and the (1,1,1) / degenerate basis families take
+            // compile-time picks (BCLS, as in the int8 epilogue).
             constexpr int W = NB / 2;
+            const bool act = p.act_mode >= 0;
 #pragma unroll
             for (int cc = 0; cc < 16 / W; ++cc) {
               const int co = n0 / W + cc;
               const int cq = min(co, p.C_out - 1);
               float own[W], oth[W];
+              float recvA = 0.f, recvB = 0.f;
 #pragma unroll
               for (int r = 0; r < W; ++r) {
                 own[r] = __uint_as_float(cur[cc * W + r]);
-                oth[r] = __shfl_xor_sync(0xffffffffu, own[r], 1);
+                oth[r] = 0.f;
+                if constexpr (BCLS == 2) continue;
+                // BCLS 1: the partner only needs rows 1 and 2
+                if (BCLS == 0 || r == 1 || r == 2) oth[r] = __shfl_xor_sync(0xffffffffu, own[r], 1);
+              }
+              if constexpr (BCLS == 2 && W == 4) {
+                // degenerate (1,-1,0) family: lane 0 sends rows 2, 3, lane 1 rows 0, 1
+                recvA = __shfl_xor_sync(0xffffffffu, bcol ? own[0] : own[2], 1);
+                recvB = __shfl_xor_sync(0xffffffffu, bcol ? own[1] : own[3 % W], 1);
+              }
+              float bw[W];
+              if constexpr (W == 4) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias_t + cq * NB + bcol * W));
+                bw[0] = b4.x; bw[1 % W] = b4.y; bw[2 % W] = b4.z; bw[3 % W] = b4.w;
+              } else {
+                const float2 b2 = __ldg(reinterpret_cast<const float2*>(p.bias_t + cq * NB + bcol * W));
+                bw[0] = b2.x; bw[1 % W] = b2.y;
               }
               float h[W];
-              float part = 0.f;
 #pragma unroll
               for (int j = 0; j < W; ++j) {
-                const float a = pick_wf<W>(own, inv_o[j]), bq = pick_wf<W>(oth, inv_p[j]);
-                const int t = bcol * W + j;
-                h[j] = 0.5f * ((inv_os[j] > 0 ? a : -a) + (inv_ps[j] > 0 ? bq : -bq)) + __ldg(p.bias + t * p.C_out + cq);
-                if (p.act_mode >= 0 && ((p.act_kmask >> t) & 1u)) part = fmaf(h[j], __ldg(p.act_w + cq * NB + t), part);
+                float a, bq;
+                if constexpr (BCLS == 1 && W == 4) {
+                  a = own[(j >> 1) * 3];   // rows 0, 0, 3, 3
+                  bq = oth[2 - (j >> 1)];  // rows 2, 2, 1, 1
+                } else if constexpr (BCLS == 2 && W == 4) {
+                  constexpr int kQ[4] = {0, 1, 1, 0};
+                  a = bcol ? own[3 - kQ[j]] : own[kQ[j]];  // rows 0,1,1,0 / 3,2,2,3
+                  bq = (((j == 0) || (j == 3)) != (bcol != 0)) ? recvB : recvA;
+                } else {
+                  a = pick_wf<W>(own, inv_o[j]);
+                  bq = pick_wf<W>(oth, inv_p[j]);
+                }
+                // (+-a) + (+-bq) rounded once (the +-1 products are exact), then / 2 + bias
+                h[j] = fmaf(fmaf(sgn_o[j], a, sgn_p[j] * bq), 0.5f, bw[j]);
               }
-              if (p.act_mode >= 0) {
+              if (act) {
+                float aw[W];
+                if constexpr (W == 4) {
+                  const float4 a4 = __ldg(reinterpret_cast<const float4*>(p.act_w + cq * NB + bcol * W));
+                  aw[0] = a4.x; aw[1 % W] = a4.y; aw[2 % W] = a4.z; aw[3 % W] = a4.w;
+                } else {
+                  const float2 a2 = __ldg(reinterpret_cast<const float2*>(p.act_w + cq * NB + bcol * W));
+                  aw[0] = a2.x; aw[1 % W] = a2.y;
+                }
+                float part = 0.f;
+#pragma unroll
+                for (int j = 0; j < W; ++j)
+                  if ((p.act_kmask >> (bcol * W + j)) & 1u) part = fmaf(h[j], aw[j], part);
                 float sg = part + __shfl_xor_sync(0xffffffffu, part, 1);
                 if (p.act_mode == 0) sg += __ldg(p.act_b + cq);
                 else if (p.act_mode == 2) sg = sg / p.act_K;
@@ -1478,9 +1530,24 @@ static cudaError_t launch_nb(const ConvPlan& plan, const CUtensorMap& tmap, cons
           if (p.bcls == 2) return launch_t<NB, kPrecFp32, true, 2>(plan, tmap, bmap, p, grid, s);
         }
         return launch_t<NB, kPrecFp32, true>(plan, tmap, bmap, p, grid, s);
-      case kPrecTf32: return launch_t<NB, kPrecTf32, true>(plan, tmap, bmap, p, grid, s);
-      case kPrecBf16: return launch_t<NB, kPrecBf16, true>(plan, tmap, bmap, p, grid, s);
-      default: return launch_t<NB, kPrec3xTf32, true>(plan, tmap, bmap, p, grid, s);
+      case kPrecTf32:
+        if constexpr (NB == 8) {
+          if (p.bcls == 1) return launch_t<NB, kPrecTf32, true, 1>(plan, tmap, bmap, p, grid, s);
+          if (p.bcls == 2) return launch_t<NB, kPrecTf32, true, 2>(plan, tmap, bmap, p, grid, s);
+        }
+        return launch_t<NB, kPrecTf32, true>(plan, tmap, bmap, p, grid, s);
+      case kPrecBf16:
+        if constexpr (NB == 8) {
+          if (p.bcls == 1) return launch_t<NB, kPrecBf16, true, 1>(plan, tmap, bmap, p, grid, s);
+          if (p.bcls == 2) return launch_t<NB, kPrecBf16, true, 2>(plan, tmap, bmap, p, grid, s);
+        }
+        return launch_t<NB, kPrecBf16, true>(plan, tmap, bmap, p, grid, s);
+      default:
+        if constexpr (NB == 8) {
+          if (p.bcls == 1) return launch_t<NB, kPrec3xTf32, true, 1>(plan, tmap, bmap, p, grid, s);
+          if (p.bcls == 2) return launch_t<NB, kPrec3xTf32, true, 2>(plan, tmap, bmap, p, grid, s);
+        }
+        return launch_t<NB, kPrec3xTf32, true>(plan, tmap, bmap, p, grid, s);
     }
   }
   switch (plan.prec) {
