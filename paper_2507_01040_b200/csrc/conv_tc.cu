@@ -48,10 +48,21 @@ __device__ __forceinline__ int dbg_skip(const ConvKParams& p) { return kDbg ? p.
 template <int NB>
 __device__ __forceinline__ float act_gate(const float (&v)[NB], int mode, const float* __restrict__ w,
                                           float bias, float Kf, unsigned kmask) {
+  float wv[NB];  // the channel's NB gate weights: vector loads (w = act_w + channel * NB is 8 / 16-byte aligned)
+  if constexpr (NB == 2) {
+    const float2 w2 = __ldg(reinterpret_cast<const float2*>(w));
+    wv[0] = w2.x; wv[1] = w2.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < NB / 4; ++j) {
+      const float4 w4 = __ldg(reinterpret_cast<const float4*>(w) + j);
+      wv[4 * j] = w4.x; wv[(4 * j + 1) % NB] = w4.y; wv[(4 * j + 2) % NB] = w4.z; wv[(4 * j + 3) % NB] = w4.w;
+    }
+  }
   float s = 0.f;
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
-    const float t = fmaf(v[j], __ldg(w + j), s);
+    const float t = fmaf(v[j], wv[j], s);
     s = ((kmask >> j) & 1u) ? t : s;
   }
   if (mode == 0) s += bias;
@@ -1358,8 +1369,21 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
             const int co = n0 / NB + cc;
             const int cq = min(co, p.C_out - 1);
             float v[NB];
+            {  // the channel's NB biases: vector loads from the (C_out, NB) copy
+              float bw[NB];
+              if constexpr (NB == 2) {
+                const float2 b2 = __ldg(reinterpret_cast<const float2*>(p.bias_t + cq * NB));
+                bw[0] = b2.x; bw[1] = b2.y;
+              } else {
 #pragma unroll
-            for (int j = 0; j < NB; ++j) v[j] = __uint_as_float(cur[cc * NB + j]) + __ldg(p.bias + j * p.C_out + cq);
+                for (int j = 0; j < NB / 4; ++j) {
+                  const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias_t + cq * NB) + j);
+                  bw[4 * j] = b4.x; bw[(4 * j + 1) % NB] = b4.y; bw[(4 * j + 2) % NB] = b4.z; bw[(4 * j + 3) % NB] = b4.w;
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < NB; ++j) v[j] = __uint_as_float(cur[cc * NB + j]) + bw[j];
+            }
             if (!valid || co >= p.C_out) continue;
             if (p.act_mode >= 0) {
               const float gte = act_gate<NB>(v, p.act_mode, p.act_w + co * NB,

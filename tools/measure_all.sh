@@ -9,7 +9,7 @@ tail -3 gpurun_out/m2_pytest.log >> gpurun_out/m2_status.txt
 bash tools/round_numbers.sh
 cp gpurun_out/numbers.jsonl gpurun_out/m2_numbers.jsonl
 rm -f gpurun_out/ncu/status.txt
-SOURCE=1 JOBS="cfg4bf16 cfg4tf32 blk2full" bash tools/prof_all.sh
+JOBS="cfg4bf16 cfg4tf32 x3 bf16 blk2full" bash tools/prof_all.sh
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/m2_launches_cfg5_fp32.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e \
   > gpurun_out/m2_launches.log 2>&1
