@@ -851,6 +851,10 @@ __device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t u) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(__uint_as_float(u)));
   return r;
 }
+// Start the cache line of a global address towards L2 (no register, no wait).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 // 16 columns of this thread's TMEM lane (32x32b shape, like tmem_ld16)
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(

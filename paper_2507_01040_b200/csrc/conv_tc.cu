@@ -971,6 +971,23 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
       }
       double a_sc = 0.0;
       if constexpr (kInt8) if (valid) a_sc = (double)__ldg(p.a_scale + b) * (1.0 / 16384.0);  // 2^-14: two leading digits
+      if constexpr (!kInt8) {
+        // fused residual (block conv2): start this thread's residual lines towards
+        // L2 now, while the tile's MMAs still run. The epilogue loads them chunk
+        // by chunk right before use and had waited a DRAM round trip per chunk
+        // (CL_DBG_CLK, cfg3 bf16 conv2: 28.5 K cycles per tile against 16.9 K for
+        // conv1, and the MMA warp waited 12.4 K of its 18 K cycles per tile for a
+        // free accumulator). The int8 mode adds the residual in its phase 2, off
+        // the critical path.
+        if (p.resid != nullptr && valid) {
+          const int wv = p.bs.on ? NB / 2 : NB;  // floats of one channel in this lane
+          const float* rbase = p.resid + ((long long)b * p.C_out * P_res + pres) * NB + (p.bs.on ? bcol * wv : 0);
+          for (int c = c_beg; c < c_end; c += wv) {
+            const int co = (nt * p.n_tile + c) / wv;
+            if (co < p.C_out) prefetch_l2(rbase + (long long)co * P_res * NB);
+          }
+        }
+      }
       if constexpr (kInt8 && GROUPS)  // exact mode, several accumulation groups per tile
         drain_groups<PAIR>(p, tfull, tempty, tmem_base, ew, row, c_beg, c_end, slot_cols, slots, acc, acc_phase);
       if constexpr (kSplit)  // returns with the last group's slot full and complete (lo accumulator added)
@@ -1017,7 +1034,6 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 // lane (column bcol) produces blades bcol*W + j: x = (s_o own[o_j] + s_p partner[p_j]) / 2,
                 // combined exactly in int64 (one weight scale per channel), rounded once
                 constexpr int W = NB / 2;
-                float part[CH / W];  // gate pre-activations, finished for all channels together (ILP)
 #pragma unroll
                 for (int cc = 0; cc < CH / W; ++cc) {
                   const int co = n0 / W + cc;
@@ -1047,8 +1063,8 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                     }
                   }
                   const double sc = a_sc * (0.5 / 16777216.0) * (double)__ldg(p.w_scale + nt * p.n_tile + cc * W + c0);
-                  // this lane's W biases / activation weights: one vector load each
-                  float bw[W], aw[W];
+                  // this lane's W biases: one vector load
+                  float bw[W];
                   if constexpr (W == 4) {
                     const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias_t + cq * NB + bcol * W));
                     bw[0] = b4.x; bw[1 % W] = b4.y; bw[2 % W] = b4.z; bw[3 % W] = b4.w;
@@ -1056,17 +1072,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                     const float2 b2 = __ldg(reinterpret_cast<const float2*>(p.bias_t + cq * NB + bcol * W));
                     bw[0] = b2.x; bw[1 % W] = b2.y;
                   }
-                  if (p.act_mode >= 0) {
-                    if constexpr (W == 4) {
-                      const float4 a4 = __ldg(reinterpret_cast<const float4*>(p.act_w + cq * NB + bcol * W));
-                      aw[0] = a4.x; aw[1 % W] = a4.y; aw[2 % W] = a4.z; aw[3 % W] = a4.w;
-                    } else {
-                      const float2 a2 = __ldg(reinterpret_cast<const float2*>(p.act_w + cq * NB + bcol * W));
-                      aw[0] = a2.x; aw[1 % W] = a2.y;
-                    }
-                  }
                   float v[W];
-                  part[cc] = 0.f;
 #pragma unroll
                   for (int j = 0; j < W; ++j) {
                     long long a, bq;
@@ -1083,26 +1089,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                     }
                     const long long xs = (inv_os[j] > 0 ? a : -a) + (inv_ps[j] > 0 ? bq : -bq);
                     v[j] = (float)fma((double)xs, sc, (double)bw[j]);
-                    if (p.act_mode >= 0 && ((p.act_kmask >> (bcol * W + j)) & 1u)) part[cc] = fmaf(v[j], aw[j], part[cc]);
                   }
 #pragma unroll
                   for (int j = 0; j < W; ++j) hv[ci * CH + cc * W + j] = v[j];
-                }
-                if (p.act_mode >= 0) {  // the chunk's gates: other lane's partial sums, sigmoid, scale
-                  const float inv_K = 1.f / p.act_K;
-                  float sg[CH / W];
-#pragma unroll
-                  for (int cc = 0; cc < CH / W; ++cc) sg[cc] = part[cc] + __shfl_xor_sync(0xffffffffu, part[cc], 1);
-#pragma unroll
-                  for (int cc = 0; cc < CH / W; ++cc) {
-                    const int cq = min(n0 / W + cc, p.C_out - 1);
-                    if (p.act_mode == 0) sg[cc] += __ldg(p.act_b + cq);
-                    else if (p.act_mode == 2) sg[cc] = sg[cc] * inv_K;
-                    // fast exp / reciprocal: ~1e-7 relative on the gate, far inside the block's 1e-4 bound
-                    const float gte = __frcp_rn(1.f + __expf(-sg[cc]));
-#pragma unroll
-                    for (int j = 0; j < W; ++j) hv[ci * CH + cc * W + j] *= gte;
-                  }
                 }
               }
             } else {
@@ -1134,6 +1123,52 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           atomicAdd(p.dbg_acc + 1, 1ull);
         }
         if (++acc == slots) { acc = 0; acc_phase ^= 1; }
+        // The fused activation gate of the change-of-basis path (block conv1) runs
+        // here, after the accumulator went back to the MMA warp: it only needs the
+        // held values (CL_DBG_CLK: inside phase 1 it had cost 7 K of cfg3's 19.6 K
+        // cycles per tile, all of them waited for by the next tile's MMAs). All
+        // lanes take part (the partner-lane shuffle), valid or not.
+        if (p.act_mode >= 0 && p.bs.on && !(dbg_skip(p) & 4)) {
+          if constexpr (NB >= 4) {
+            constexpr int W = NB / 2;
+            const float inv_K = 1.f / p.act_K;
+#pragma unroll
+            for (int ci = 0; ci < kHold / CH; ++ci) {
+              const int c0 = c_beg + ci * CH;
+              const int n0 = nt * p.n_tile + c0;
+              if (c0 < c_end && n0 < p.N) {
+                float sg[CH / W];  // gate pre-activations, finished for the chunk's channels together (ILP)
+#pragma unroll
+                for (int cc = 0; cc < CH / W; ++cc) {
+                  const int cq = min(n0 / W + cc, p.C_out - 1);
+                  float aw[W];
+                  if constexpr (W == 4) {
+                    const float4 a4 = __ldg(reinterpret_cast<const float4*>(p.act_w + cq * NB + bcol * W));
+                    aw[0] = a4.x; aw[1 % W] = a4.y; aw[2 % W] = a4.z; aw[3 % W] = a4.w;
+                  } else {
+                    const float2 a2 = __ldg(reinterpret_cast<const float2*>(p.act_w + cq * NB + bcol * W));
+                    aw[0] = a2.x; aw[1 % W] = a2.y;
+                  }
+                  float part = 0.f;
+#pragma unroll
+                  for (int j = 0; j < W; ++j)
+                    if ((p.act_kmask >> (bcol * W + j)) & 1u) part = fmaf(hv[ci * CH + cc * W + j], aw[j], part);
+                  sg[cc] = part + __shfl_xor_sync(0xffffffffu, part, 1);
+                }
+#pragma unroll
+                for (int cc = 0; cc < CH / W; ++cc) {
+                  const int cq = min(n0 / W + cc, p.C_out - 1);
+                  if (p.act_mode == 0) sg[cc] += __ldg(p.act_b + cq);
+                  else if (p.act_mode == 2) sg[cc] = sg[cc] * inv_K;
+                  // fast exp / reciprocal: ~1e-7 relative on the gate, far inside the block's 1e-4 bound
+                  const float gte = __frcp_rn(1.f + __expf(-sg[cc]));
+#pragma unroll
+                  for (int j = 0; j < W; ++j) hv[ci * CH + cc * W + j] *= gte;
+                }
+              }
+            }
+          }
+        }
         // fused absmax for the next conv: max finite |stored value| (float bits) and a
         // non-finite marker (NaN-sticky max of |value| bits), see finite_abs_bits
         unsigned ymax = 0, yany = 0;
