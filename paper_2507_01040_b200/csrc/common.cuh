@@ -161,6 +161,16 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* ma
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader_addr(bar)) : "memory");
 }
+// The same arrival without release semantics: for hand-offs that publish no
+// memory (an epilogue warp returning a TMEM slot: its tcgen05.ld results are
+// in registers after tcgen05.wait::ld, ordered by tcgen05.fence::before_thread_sync).
+// The release form makes the thread wait for ALL its outstanding global stores
+// first (ERRBAR / MEMBAR in the SASS) -- the previous tile's output, a DRAM
+// write round trip per returned slot (ncu, cfg3 3xTF32 conv1: 15 % of the
+// epilogue warps' samples sat on that fence).
+__device__ __forceinline__ void mbar_arrive_leader_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader_addr(bar)) : "memory");
+}
 __device__ __forceinline__ void tmem_alloc_cg2(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
                "r"(ncols)

@@ -66,8 +66,10 @@ __device__ __forceinline__ float act_gate(const float (&v)[NB], int mode, const 
     s = ((kmask >> j) & 1u) ? t : s;
   }
   if (mode == 0) s += bias;
-  else if (mode == 2) s = s / Kf;
-  return 1.f / (1.f + expf(-s));
+  else if (mode == 2) s = s * (1.f / Kf);
+  // fast exp / reciprocal (~1e-7 relative on the gate, far inside the block's bounds): the
+  // precise forms' slow-path CALLs serialised the channels of an epilogue chunk
+  return __frcp_rn(1.f + __expf(-s));
 }
 
 // MMA of the precision mode, 1-SM or 2-SM (pair leader).
@@ -199,7 +201,7 @@ __device__ __forceinline__ void release_acc(uint64_t* bar) {
   tc_fence_before();
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {
-    if constexpr (PAIR) mbar_arrive_leader(bar); else mbar_arrive(bar);
+    if constexpr (PAIR) mbar_arrive_leader_relaxed(bar); else mbar_arrive(bar);
   }
 }
 
@@ -1314,6 +1316,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
             // compile-time picks (BCLS, as in the int8 epilogue).
             constexpr int W = NB / 2;
             const bool act = p.act_mode >= 0;
+            const float act_inv_K = 1.f / p.act_K;
 #pragma unroll
             for (int cc = 0; cc < 16 / W; ++cc) {
               const int co = n0 / W + cc;
@@ -1374,8 +1377,11 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                   if ((p.act_kmask >> (bcol * W + j)) & 1u) part = fmaf(h[j], aw[j], part);
                 float sg = part + __shfl_xor_sync(0xffffffffu, part, 1);
                 if (p.act_mode == 0) sg += __ldg(p.act_b + cq);
-                else if (p.act_mode == 2) sg = sg / p.act_K;
-                const float gte = 1.f / (1.f + expf(-sg));
+                else if (p.act_mode == 2) sg = sg * act_inv_K;
+                // fast exp / reciprocal, as in the int8 epilogue (~1e-7 relative on the gate): the
+                // precise forms' slow-path CALLs kept the chunk's channels from overlapping
+                // (CL_DBG_CLK, cfg3 3xTF32 conv1: the gate cost 14.6 K of 30.4 K cycles per tile)
+                const float gte = __frcp_rn(1.f + __expf(-sg));
 #pragma unroll
                 for (int j = 0; j < W; ++j) h[j] *= gte;
               }

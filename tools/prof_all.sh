@@ -31,6 +31,10 @@ for job in ${JOBS:-act bf16 tf32 x3 cfg4 cfg3 cfg1}; do
     # the block's conv2 (fused residual): skip conv1, capture the second conv_tc launch
     blk2) NCU_EXTRA="--launch-skip 1" run block_cfg5_fp32_B64_conv2 conv_tc tools/prof_block.py --config 5 --B 64 --precision fp32 ;;
     blk2full) NCU_EXTRA="--launch-skip 1" run block_cfg5_fp32_B256_conv2 conv_tc tools/prof_block.py --config 5 --B 256 --precision fp32 ;;
+    # cfg3 block convs (2-D): conv1 with the fused gate, conv2 (--launch-skip 1) with the fused residual
+    blk3x3c1) run block_cfg3_3xtf32_conv1 conv_tc tools/prof_block.py --config 3 --B 32 --precision 3xtf32 ;;
+    blk3x3c2) NCU_EXTRA="--launch-skip 1" run block_cfg3_3xtf32_conv2 conv_tc tools/prof_block.py --config 3 --B 32 --precision 3xtf32 ;;
+    blk3bf16c2) NCU_EXTRA="--launch-skip 1" run block_cfg3_bf16_conv2 conv_tc tools/prof_block.py --config 3 --B 32 --precision bf16 ;;
     cfg4bf16) run conv_cfg4_bf16_B16 conv_tc tools/prof_conv.py --config 4 --B 16 --precision bf16 --reps 1 ;;
     cfg4tf32) run conv_cfg4_tf32_B16 conv_tc tools/prof_conv.py --config 4 --B 16 --precision tf32 --reps 1 ;;
   esac
