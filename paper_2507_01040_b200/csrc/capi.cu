@@ -28,18 +28,18 @@ static int env_int(const char* name) {
 }
 static bool g_no_pair = CL_ENV("CL_NO_PAIR") != nullptr || CL_ENV("CL_NO_CLUSTER") != nullptr;  // A/B: 1-SM MMA
 static bool g_no_basis = CL_ENV("CL_NO_BASIS") != nullptr;      // A/B: disable the change of basis
-static bool g_basis_2d = CL_ENV("CL_BASIS_2D") != nullptr;      // A/B: enable it for 2-D layers (all modes)
 static bool g_no_basis_2d = CL_ENV("CL_NO_BASIS_2D") != nullptr;  // A/B: disable it for 2-D layers
 
 // The change of basis for a layer of spatial rank sk: always in 3-D; in 2-D
 // for the fp32 (int8) and 3xTF32 modes, where it measured faster (cfg3 block
 // 4.25 -> 3.16 ms / 3.97 -> 3.05 ms); the bf16 / tf32 2-D epilogues measured
-// slower with it (and bf16 loses the block's bf16 hand-off).
+// slower with it (and bf16 loses the block's bf16 hand-off): those kernels are
+// compiled without the basis epilogue (conv_tc.cu kBasisEpi).
 static bool use_basis(int sk, int k, int precision) {
   if (g_no_basis || sk != k) return false;
   if (sk == 3) return true;
   if (sk != 2 || g_no_basis_2d) return false;
-  return g_basis_2d || precision == CL_PREC_FP32 || precision == CL_PREC_3XTF32;
+  return precision == CL_PREC_FP32 || precision == CL_PREC_3XTF32;
 }
 static bool g_no_halo = CL_ENV("CL_NO_HALO") != nullptr;        // A/B: disable halo reuse of the A tile
 static bool g_no_halo_i8 = CL_ENV("CL_NO_HALO_I8") != nullptr;  // A/B: halo off for the int8 mode only

@@ -313,6 +313,9 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
   // 3xTF32 pairs (halo mode only): each CTA's A halo lands on its OWN barrier
   // for its splitter, whose "split done" arrivals go to the leader's barrier
   constexpr bool kAOwn = kSplit;
+  // 2-D bf16 / tf32 layers never change basis (capi.cu use_basis): their
+  // kernels carry no basis epilogue
+  constexpr bool kBasisEpi = !(NB == 4 && (PREC == kPrecTf32 || PREC == kPrecBf16));
   // epilogue warp groups: warps 4-7, plus warps 8-11 when they are not the
   // 3xTF32 splitter (each group drains half of the accumulator columns)
   // (3xTF32: warps 4-11, the splitter is warps 12-15)
@@ -912,8 +915,10 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
     const int c_beg = eg * c_half, c_end = min(p.n_tile, c_beg + c_half);
     const int row = ew * 32 + lane;
     // with a change of basis a pixel owns ncol = 2 adjacent rows (lanes), one per matrix column
-    const int bcol = p.bs.on ? (row & 1) : 0;
-    const int prow = p.bs.on ? (row >> 1) : row;
+    // (2-D bf16 / tf32 kernels: compile-time false, see kBasisEpi)
+    const bool bs_on = kBasisEpi && p.bs.on;
+    const int bcol = bs_on ? (row & 1) : 0;
+    const int prow = bs_on ? (row >> 1) : row;
     int inv_i0[NB], inv_i1[NB], inv_s0[NB], inv_s1[NB];  // two-term inverse transform (registers)
 #pragma unroll
     for (int t2 = 0; t2 < NB; ++t2) {
@@ -982,8 +987,8 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         // free accumulator). The int8 mode adds the residual in its phase 2, off
         // the critical path.
         if (p.resid != nullptr && valid) {
-          const int wv = p.bs.on ? NB / 2 : NB;  // floats of one channel in this lane
-          const float* rbase = p.resid + ((long long)b * p.C_out * P_res + pres) * NB + (p.bs.on ? bcol * wv : 0);
+          const int wv = bs_on ? NB / 2 : NB;  // floats of one channel in this lane
+          const float* rbase = p.resid + ((long long)b * p.C_out * P_res + pres) * NB + (bs_on ? bcol * wv : 0);
           for (int c = c_beg; c < c_end; c += wv) {
             const int co = (nt * p.n_tile + c) / wv;
             if (co < p.C_out) prefetch_l2(rbase + (long long)co * P_res * NB);
@@ -1031,7 +1036,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 for (int c = 0; c < CH; ++c) sv[c] += scr[c];
               }
             }
-            if (p.bs.on) {
+            if (bs_on) {
               if constexpr (NB >= 4) {
                 // lane (column bcol) produces blades bcol*W + j: x = (s_o own[o_j] + s_p partner[p_j]) / 2,
                 // combined exactly in int64 (one weight scale per channel), rounded once
@@ -1130,7 +1135,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         // held values (CL_DBG_CLK: inside phase 1 it had cost 7 K of cfg3's 19.6 K
         // cycles per tile, all of them waited for by the next tile's MMAs). All
         // lanes take part (the partner-lane shuffle), valid or not.
-        if (p.act_mode >= 0 && p.bs.on && !(dbg_skip(p) & 4)) {
+        if (p.act_mode >= 0 && bs_on && !(dbg_skip(p) & 4)) {
           if constexpr (NB >= 4) {
             constexpr int W = NB / 2;
             const float inv_K = 1.f / p.act_K;
@@ -1182,14 +1187,14 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
           if (c0 < c_end && n0 < p.N) {
             // W blades of one channel per store: the lane's half (change of basis) or all N_B
             constexpr int W = (NB >= 4) ? NB / 2 : NB;
-            const int wv = p.bs.on ? W : NB;
+            const int wv = bs_on ? W : NB;
 #pragma unroll
             for (int cc = 0; cc < CH / W; ++cc) {
               if (cc * wv >= CH) break;
               const int co = n0 / wv + cc;
               if (co >= p.C_out) break;
-              const long long off = p.bs.on ? (long long)bcol * W : 0;
-              if (p.bs.on) {
+              const long long off = bs_on ? (long long)bcol * W : 0;
+              if (bs_on) {
                 float h[W];
 #pragma unroll
                 for (int j = 0; j < W; ++j) h[j] = hv[ci * CH + cc * W + j];
@@ -1286,14 +1291,14 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
         const bool use_res = p.resid != nullptr && valid;
 #pragma unroll
         for (int r = 0; r < 4; ++r) rq[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (use_res && (p.bs.on || NB == 4)) {  // NB = 8 / NB = 2 without a basis: loaded in place below
-          const int wv = p.bs.on ? NB / 2 : NB;  // floats of one channel this lane adds
+        if (use_res && (bs_on || NB == 4)) {  // NB = 8 / NB = 2 without a basis: loaded in place below
+          const int wv = bs_on ? NB / 2 : NB;  // floats of one channel this lane adds
           const int nch = 16 / wv;
 #pragma unroll
           for (int cc = 0; cc < 8; ++cc) {
             const int co = n0 / wv + cc;
             if (cc < nch && co < p.C_out) {
-              const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB + (p.bs.on ? bcol * wv : 0);
+              const float* rp = p.resid + (((long long)b * p.C_out + co) * P_res + pres) * NB + (bs_on ? bcol * wv : 0);
               if (wv == 2) {
                 const float2 q2 = __ldg(reinterpret_cast<const float2*>(rp));
                 if (cc & 1) { rq[cc >> 1].z = q2.x; rq[cc >> 1].w = q2.y; }
@@ -1304,8 +1309,32 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
             }
           }
         }
-        if (p.bs.on) {
-          if constexpr (NB >= 4) {
+        if (bs_on) {
+          if constexpr (NB >= 4 && kBasisEpi) {
+            // The chunk's biases, and its gate weights when no residual occupies rq
+            // (block conv1), loaded for all channels up front like the residual: loaded
+            // per channel right before use, each first use waited a full L1 round trip
+            // (ncu, cfg3 3xTF32 conv1: long_sb 38 % of the epilogue's samples).
+            constexpr int WB = NB / 2;
+            float4 bq[4];
+            const bool aw_in_rq = p.act_mode >= 0 && !use_res;
+#pragma unroll
+            for (int cc = 0; cc < 16 / WB; ++cc) {
+              const int cq = min(n0 / WB + cc, p.C_out - 1);
+              if constexpr (WB == 4) {
+                bq[cc % 4] = __ldg(reinterpret_cast<const float4*>(p.bias_t + cq * NB + bcol * WB));
+                if (aw_in_rq) rq[cc % 4] = __ldg(reinterpret_cast<const float4*>(p.act_w + cq * NB + bcol * WB));
+              } else {
+                const float2 b2 = __ldg(reinterpret_cast<const float2*>(p.bias_t + cq * NB + bcol * WB));
+                if (cc & 1) { bq[(cc >> 1) % 4].z = b2.x; bq[(cc >> 1) % 4].w = b2.y; }
+                else { bq[(cc >> 1) % 4].x = b2.x; bq[(cc >> 1) % 4].y = b2.y; }
+                if (aw_in_rq) {
+                  const float2 a2 = __ldg(reinterpret_cast<const float2*>(p.act_w + cq * NB + bcol * WB));
+                  if (cc & 1) { rq[(cc >> 1) % 4].z = a2.x; rq[(cc >> 1) % 4].w = a2.y; }
+                  else { rq[(cc >> 1) % 4].x = a2.x; rq[(cc >> 1) % 4].y = a2.y; }
+                }
+              }
+            }
             // change of basis: lane (column bcol) produces blades bcol*W + j as
             // (s_o own[o_j] + s_p partner[p_j]) / 2; the gate sums over both lanes.
             // This loop had been instruction bound (ncu: ~640 issued instructions per
@@ -1338,11 +1367,12 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               }
               float bw[W];
               if constexpr (W == 4) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias_t + cq * NB + bcol * W));
+                const float4 b4 = bq[cc % 4];
                 bw[0] = b4.x; bw[1 % W] = b4.y; bw[2 % W] = b4.z; bw[3 % W] = b4.w;
               } else {
-                const float2 b2 = __ldg(reinterpret_cast<const float2*>(p.bias_t + cq * NB + bcol * W));
-                bw[0] = b2.x; bw[1 % W] = b2.y;
+                const float4 b4 = bq[(cc >> 1) % 4];
+                bw[0] = (cc & 1) ? b4.z : b4.x;
+                bw[1 % W] = (cc & 1) ? b4.w : b4.y;
               }
               float h[W];
 #pragma unroll
@@ -1365,10 +1395,17 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
               if (act) {
                 float aw[W];
                 if constexpr (W == 4) {
-                  const float4 a4 = __ldg(reinterpret_cast<const float4*>(p.act_w + cq * NB + bcol * W));
+                  const float4 a4 = aw_in_rq ? rq[cc % 4]
+                                             : __ldg(reinterpret_cast<const float4*>(p.act_w + cq * NB + bcol * W));
                   aw[0] = a4.x; aw[1 % W] = a4.y; aw[2 % W] = a4.z; aw[3 % W] = a4.w;
                 } else {
-                  const float2 a2 = __ldg(reinterpret_cast<const float2*>(p.act_w + cq * NB + bcol * W));
+                  float2 a2;
+                  if (aw_in_rq) {
+                    const float4 a4 = rq[(cc >> 1) % 4];
+                    a2 = (cc & 1) ? make_float2(a4.z, a4.w) : make_float2(a4.x, a4.y);
+                  } else {
+                    a2 = __ldg(reinterpret_cast<const float2*>(p.act_w + cq * NB + bcol * W));
+                  }
                   aw[0] = a2.x; aw[1 % W] = a2.y;
                 }
                 float part = 0.f;

@@ -67,7 +67,7 @@ def _run(env_extra):
 
 
 @pytest.mark.parametrize("flags", [{"CL_NO_PAIR": "1"}, {"CL_NO_HALO": "1"}, {"CL_NO_TMA_MERGE": "1"},
-                                   {"CL_TPS": "1"}, {"CL_BASIS_2D": "1"}, {"CL_NO_BASIS": "1"}, {"CL_NO_BASIS_2D": "1"},
+                                   {"CL_TPS": "1"}, {"CL_NO_BASIS": "1"}, {"CL_NO_BASIS_2D": "1"},
                                    {"CL_NO_BCLS": "1", "CL_NO_FUSED_AMAX": "1", "CL_NO_SLICE_FIXED": "1"},
                                    {"CL_NO_FUSED_PREP": "1", "CL_NO_GRAPH": "1"},
                                    {"CL_DYN_TILES": "1"}, {"CL_DYN_TILES": "1", "CL_NO_PAIR": "1"}],
