@@ -1346,6 +1346,14 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
             constexpr int W = NB / 2;
             const bool act = p.act_mode >= 0;
             const float act_inv_K = 1.f / p.act_K;
+            // the chunk's first output address; channels step by one (P_out, N_B) plane
+            float* const y_chunk = p.y ? p.y + (((long long)b * p.C_out + n0 / W) * P_out + pix) * NB + bcol * W : nullptr;
+            const long long y_step = P_out * NB;
+            // Linear gates: the chunk's gate biases up front, like the weights
+            float ab[16 / W];
+#pragma unroll
+            for (int cc = 0; cc < 16 / W; ++cc)
+              ab[cc] = p.act_mode == 0 ? __ldg(p.act_b + min(n0 / W + cc, p.C_out - 1)) : 0.f;
 #pragma unroll
             for (int cc = 0; cc < 16 / W; ++cc) {
               const int co = n0 / W + cc;
@@ -1413,7 +1421,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 for (int j = 0; j < W; ++j)
                   if ((p.act_kmask >> (bcol * W + j)) & 1u) part = fmaf(h[j], aw[j], part);
                 float sg = part + __shfl_xor_sync(0xffffffffu, part, 1);
-                if (p.act_mode == 0) sg += __ldg(p.act_b + cq);
+                if (p.act_mode == 0) sg += ab[cc];
                 else if (p.act_mode == 2) sg = sg * act_inv_K;
                 // fast exp / reciprocal, as in the int8 epilogue (~1e-7 relative on the gate): the
                 // precise forms' slow-path CALLs kept the chunk's channels from overlapping
@@ -1433,8 +1441,8 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                     h[1 % W] += (cc & 1) ? q4.w : q4.y;
                   }
                 }
-                if (p.y) {
-                  float* yp = p.y + (((long long)b * p.C_out + co) * P_out + pix) * NB + bcol * W;
+                if (y_chunk) {
+                  float* yp = y_chunk + cc * y_step;
                   if constexpr (W == 2) *reinterpret_cast<float2*>(yp) = make_float2(h[0], h[1 % W]);
                   else *reinterpret_cast<float4*>(yp) = make_float4(h[0], h[1 % W], h[2 % W], h[3 % W]);
                 }
