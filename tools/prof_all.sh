@@ -35,6 +35,7 @@ for job in ${JOBS:-act bf16 tf32 x3 cfg4 cfg3 cfg1}; do
     blk3x3c1) run block_cfg3_3xtf32_conv1 conv_tc tools/prof_block.py --config 3 --B 32 --precision 3xtf32 ;;
     blk3x3c2) NCU_EXTRA="--launch-skip 1" run block_cfg3_3xtf32_conv2 conv_tc tools/prof_block.py --config 3 --B 32 --precision 3xtf32 ;;
     blk3bf16c2) NCU_EXTRA="--launch-skip 1" run block_cfg3_bf16_conv2 conv_tc tools/prof_block.py --config 3 --B 32 --precision bf16 ;;
+    cfg3fp32) run conv_cfg3_fp32_B32 conv_tc tools/prof_conv.py --config 3 --B 32 --precision fp32 --reps 1 ;;
     cfg4bf16) run conv_cfg4_bf16_B16 conv_tc tools/prof_conv.py --config 4 --B 16 --precision bf16 --reps 1 ;;
     cfg4tf32) run conv_cfg4_tf32_B16 conv_tc tools/prof_conv.py --config 4 --B 16 --precision tf32 --reps 1 ;;
   esac
