@@ -64,8 +64,9 @@ typedef enum {
                          (max_rel_error <= 1e-4 vs the fp64 oracle) */
   CL_PREC_TF32 = 1,   /* single TF32 pass */
   CL_PREC_BF16 = 2,   /* BF16 operands, fp32 accumulate */
-  CL_PREC_3XTF32 = 3  /* 3xTF32 split (hi/lo rounded to nearest tf32), fp32 tensor-core
-                         accumulation drained every 64 reduction elements into fp32
+  CL_PREC_3XTF32 = 3  /* 3xTF32 split (hi/lo rounded to nearest tf32): the cross terms
+                         accumulate in their own tensor-core accumulator, the hi*hi
+                         accumulator is drained every 192 reduction elements into fp32
                          sums: fp32-accurate (max_rel_error <= 1e-4 at the BASELINE
                          configs, normwise ~1e-7) */
 } cl_precision;
