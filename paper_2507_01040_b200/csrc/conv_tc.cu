@@ -942,6 +942,7 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
     }
     // the same signs as +-1 multipliers (fp32-accumulator epilogue: one FMUL / FFMA per term)
     float sgn_o[WL], sgn_p[WL];
+    const unsigned act_kml = (p.act_kmask >> (bcol * WL)) & ((1u << WL) - 1u);  // this lane's kernel blades
 #pragma unroll
     for (int j = 0; j < WL; ++j) {
       sgn_o[j] = inv_os[j] > 0 ? 1.f : -1.f;
@@ -1354,10 +1355,13 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
 #pragma unroll
             for (int cc = 0; cc < 16 / W; ++cc)
               ab[cc] = p.act_mode == 0 ? __ldg(p.act_b + min(n0 / W + cc, p.C_out - 1)) : 0.f;
+            // Three passes over the chunk's channels -- combine, gate, residual + store --
+            // so that each warp-uniform condition (gate on? residual? output?) is tested
+            // once per chunk instead of once per channel (ncu: 55 BRA, 133 ISETP and 73
+            // LDC / LDCU of ~1000 issued instructions per 8-channel chunk).
+            float hq[16];
 #pragma unroll
             for (int cc = 0; cc < 16 / W; ++cc) {
-              const int co = n0 / W + cc;
-              const int cq = min(co, p.C_out - 1);
               float own[W], oth[W];
               float recvA = 0.f, recvB = 0.f;
 #pragma unroll
@@ -1382,7 +1386,6 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 bw[0] = (cc & 1) ? b4.z : b4.x;
                 bw[1 % W] = (cc & 1) ? b4.w : b4.y;
               }
-              float h[W];
 #pragma unroll
               for (int j = 0; j < W; ++j) {
                 float a, bq;
@@ -1398,9 +1401,14 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                   bq = pick_wf<W>(oth, inv_p[j]);
                 }
                 // (+-a) + (+-bq) rounded once (the +-1 products are exact), then / 2 + bias
-                h[j] = fmaf(fmaf(sgn_o[j], a, sgn_p[j] * bq), 0.5f, bw[j]);
+                hq[cc * W + j] = fmaf(fmaf(sgn_o[j], a, sgn_p[j] * bq), 0.5f, bw[j]);
               }
-              if (act) {
+            }
+            if (act) {
+              float sg[16 / W];
+#pragma unroll
+              for (int cc = 0; cc < 16 / W; ++cc) {
+                const int cq = min(n0 / W + cc, p.C_out - 1);
                 float aw[W];
                 if constexpr (W == 4) {
                   const float4 a4 = aw_in_rq ? rq[cc % 4]
@@ -1419,32 +1427,42 @@ __global__ void __launch_bounds__(conv_threads(PREC, NB), 1)
                 float part = 0.f;
 #pragma unroll
                 for (int j = 0; j < W; ++j)
-                  if ((p.act_kmask >> (bcol * W + j)) & 1u) part = fmaf(h[j], aw[j], part);
-                float sg = part + __shfl_xor_sync(0xffffffffu, part, 1);
-                if (p.act_mode == 0) sg += ab[cc];
-                else if (p.act_mode == 2) sg = sg * act_inv_K;
-                // fast exp / reciprocal, as in the int8 epilogue (~1e-7 relative on the gate): the
-                // precise forms' slow-path CALLs kept the chunk's channels from overlapping
-                // (CL_DBG_CLK, cfg3 3xTF32 conv1: the gate cost 14.6 K of 30.4 K cycles per tile)
-                const float gte = __frcp_rn(1.f + __expf(-sg));
-#pragma unroll
-                for (int j = 0; j < W; ++j) h[j] *= gte;
+                  if ((act_kml >> j) & 1u) part = fmaf(hq[cc * W + j], aw[j], part);
+                sg[cc] = part + __shfl_xor_sync(0xffffffffu, part, 1);
               }
-              if (valid && co < p.C_out) {
-                if (use_res) {
+#pragma unroll
+              for (int cc = 0; cc < 16 / W; ++cc) {
+                if (p.act_mode == 0) sg[cc] += ab[cc];
+                else if (p.act_mode == 2) sg[cc] = sg[cc] * act_inv_K;
+                // fast exp / reciprocal, as in the int8 epilogue (~1e-7 relative on the gate)
+                const float gte = __frcp_rn(1.f + __expf(-sg[cc]));
+#pragma unroll
+                for (int j = 0; j < W; ++j) hq[cc * W + j] *= gte;
+              }
+            }
+            if (valid) {
+              const int nch = min(16 / W, p.C_out - n0 / W);  // channels of this chunk that exist
+              if (use_res) {  // (rq is zero for channels that do not exist)
+#pragma unroll
+                for (int cc = 0; cc < 16 / W; ++cc) {
                   if constexpr (W == 4) {
                     const float4 q4 = rq[cc % 4];
-                    h[0] += q4.x; h[1 % W] += q4.y; h[2 % W] += q4.z; h[3 % W] += q4.w;
+                    hq[cc * W] += q4.x; hq[cc * W + 1 % W] += q4.y; hq[cc * W + 2 % W] += q4.z; hq[cc * W + 3 % W] += q4.w;
                   } else {  // W == 2: channel cc is rq[cc / 2].xy (even) or .zw (odd)
                     const float4 q4 = rq[(cc >> 1) % 4];
-                    h[0] += (cc & 1) ? q4.z : q4.x;
-                    h[1 % W] += (cc & 1) ? q4.w : q4.y;
+                    hq[cc * W] += (cc & 1) ? q4.z : q4.x;
+                    hq[cc * W + 1 % W] += (cc & 1) ? q4.w : q4.y;
                   }
                 }
-                if (y_chunk) {
-                  float* yp = y_chunk + cc * y_step;
-                  if constexpr (W == 2) *reinterpret_cast<float2*>(yp) = make_float2(h[0], h[1 % W]);
-                  else *reinterpret_cast<float4*>(yp) = make_float4(h[0], h[1 % W], h[2 % W], h[3 % W]);
+              }
+              if (y_chunk) {
+#pragma unroll
+                for (int cc = 0; cc < 16 / W; ++cc) {
+                  if (cc < nch) {
+                    float* yp = y_chunk + cc * y_step;
+                    if constexpr (W == 2) *reinterpret_cast<float2*>(yp) = make_float2(hq[cc * W], hq[cc * W + 1 % W]);
+                    else *reinterpret_cast<float4*>(yp) = make_float4(hq[cc * W], hq[cc * W + 1 % W], hq[cc * W + 2 % W], hq[cc * W + 3 % W]);
+                  }
                 }
               }
             }
